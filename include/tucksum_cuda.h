@@ -1,0 +1,147 @@
+/*
+ * tucksum_cuda.h — C ABI of the B200-native KRP sketched Tucker summation.
+ *
+ * Drop-in boundary for the reference's `krp_sum` hot path (arXiv 2603.13532,
+ * reference /root/reference/proj).  Eigen-free, plain pointers and sizes; the
+ * C++/Python adapters that restore the reference signatures live above it
+ * (paper_2603_13532_b200/tucksum.py).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   ts_tucker_view        ← tucksum::TuckerTensor / CoreBlock storage
+ *                           (include/tucksum/tucker.hpp:13-48, src/tucker.cpp:16-79)
+ *   ts_batch_upload       ← SumRequest::summands (include/tucksum/sketch.hpp:43-50); the
+ *                           device copy uses the formal-sum layout of formal_sum
+ *                           (src/tucker.cpp:183-226): per mode one stacked factor matrix
+ *   ts_omega_prepare      ← gaussian_matrix(dims[n], s, seed.substream(n))
+ *                           (src/kernels.cpp:88-101, src/sketch.cpp:91-95)
+ *   ts_krp_sum            ← krp_sum(req, plan, stats) → sketched_sum(krp=true)
+ *                           (include/tucksum/sketch.hpp:85-86, src/sketch.cpp:66-181,360-362)
+ *   ts_effective_subrank  ← effective_subrank(..., Strategy::Krp, ...) (src/sketch.cpp:272-349)
+ *   ts_substream          ← RngSeed::substream (include/tucksum/types.hpp:17-24, src/kernels.cpp:23-25)
+ *   ts_gaussian_matrix    ← gaussian_matrix (src/kernels.cpp:88-101)
+ *   status codes          ← std::invalid_argument / std::runtime_error thrown by
+ *                           src/sketch.cpp:16-30,69-71,80-85 (adapters rethrow the same types)
+ */
+#ifndef TUCKSUM_CUDA_H
+#define TUCKSUM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. */
+#define TS_OK 0
+#define TS_INVALID_ARGUMENT 1 /* reference: std::invalid_argument */
+#define TS_RUNTIME 2          /* reference: std::runtime_error */
+#define TS_CUDA 3
+#define TS_NCCL 4
+#define TS_OOM 5
+#define TS_UNSUPPORTED 6
+
+#define TS_MAX_ORDER 8
+
+typedef struct ts_ctx ts_ctx;
+typedef struct ts_batch ts_batch;
+typedef struct ts_result ts_result;
+
+/* Borrowed host view of one Tucker tensor (reference TuckerTensor).
+ * factors[k]: column-major dims[k] × ranks[k] (ld = dims[k]).
+ * Core: num_blocks super-diagonal blocks; block b has offsets
+ * block_offsets[b*order + k], extents block_shapes[b*order + k] and
+ * column-major data block_data[b] (first index fastest).  A dense core is one
+ * block at zero offsets spanning the rank box. */
+typedef struct ts_tucker_view {
+    int64_t order;
+    const int64_t* dims;
+    const int64_t* ranks;
+    const double* const* factors;
+    int64_t num_blocks;
+    const int64_t* block_offsets;
+    const int64_t* block_shapes;
+    const double* const* block_data;
+} ts_tucker_view;
+
+/* Last error message of the calling thread (valid until the next call). */
+const char* ts_last_error(void);
+
+/* Library version string. */
+const char* ts_version(void);
+
+/* ---- context: one per GPU (one CUDA stream, workspace arena, Ω cache) ---- */
+int ts_ctx_create(int device, ts_ctx** out);
+int ts_ctx_destroy(ts_ctx* ctx);
+/* Multi-GPU: join an NCCL communicator of `nranks` ranks (one ctx per GPU).
+ * `unique_id` is the 128-byte ncclUniqueId produced by ts_nccl_unique_id on
+ * rank 0 and shared by the host (e.g. torch.distributed broadcast).  With a
+ * communicator, ts_krp_sum all-reduces the partial sketches Y and the partial
+ * projected core h over the ranks; each rank passes its own shard of summands. */
+int ts_nccl_unique_id(void* unique_id_128);
+int ts_ctx_init_nccl(ts_ctx* ctx, const void* unique_id_128, int nranks, int rank);
+/* The CUDA stream (cudaStream_t) the context launches on. */
+void* ts_ctx_stream(ts_ctx* ctx);
+/* Number of kernels the context launched so far (for the bench's gpu_launches). */
+int64_t ts_ctx_launch_count(ts_ctx* ctx);
+
+/* ---- device-resident summand storage ---- */
+/* Copies K summands (host memory) to the device in the stacked formal-sum layout. */
+int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* summands, int64_t count, ts_batch** out);
+int ts_batch_free(ts_batch* batch);
+int64_t ts_batch_count(const ts_batch* batch);
+/* Device bytes held by the batch (factors + cores + atom table). */
+int64_t ts_batch_bytes(const ts_batch* batch);
+
+/* ---- RNG (bit-identical to the reference's libstdc++ stream) ---- */
+void ts_substream(uint64_t seed, uint64_t stream, uint64_t salt, uint64_t* out_seed, uint64_t* out_stream);
+int ts_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out_colmajor);
+/* Generates Ω_n = gaussian_matrix(dims[n], width, {seed, stream}.substream(n)) for
+ * n < order on the host and caches them on the device (keyed by seed, stream, dims,
+ * width).  ts_krp_sum calls this implicitly; calling it first keeps host Ω
+ * generation out of a timed region. */
+int ts_omega_prepare(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t width, uint64_t seed,
+                     uint64_t stream);
+
+/* ---- the hot path ---- */
+/* krp_sum with the plan given: widths[n] = plan.mode_sketch_dims (uniform width
+ * s = max(widths) is used, src/sketch.cpp:86-87).  weights[count] belong to the
+ * batch's summands.  eps >= 0 is the st_hosvd tolerance (src/tucker.cpp:239-283).
+ * max_rank (nullable, [order], entries <= 0 mean "no cap") is the optional
+ * per-mode rank cap of SURVEY.md §8(d); NULL reproduces the reference exactly. */
+int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
+               uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
+/* Plan stage for Strategy::Krp (src/sketch.cpp:272-349): effective ranks,
+ * targets and the uniform widths.  oversampling[order] >= 0. */
+int ts_effective_subrank(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps,
+                         const int64_t* oversampling, int64_t* effective_ranks, int64_t* targets, int64_t* widths);
+
+/* ---- result: a dense-core Tucker tensor owned by the library ---- */
+int64_t ts_result_order(const ts_result* r);
+void ts_result_dims(const ts_result* r, int64_t* dims);
+void ts_result_ranks(const ts_result* r, int64_t* ranks);
+/* Copies (device → host) factor `mode` (dims × ranks, column-major) / the core. */
+int ts_result_factor(const ts_result* r, int64_t mode, double* out_host);
+int ts_result_core(const ts_result* r, double* out_host);
+/* Device pointers (valid until ts_result_free). */
+const double* ts_result_factor_device(const ts_result* r, int64_t mode);
+const double* ts_result_core_device(const ts_result* r);
+/* Stage intermediates kept by the last call when the context has debug capture
+ * on (ts_ctx_set_debug): which = 0 Ω_n, 1 Y_n, 2 Û_n, 3 h. Returns element count;
+ * rows/cols receive the shape (h: rows = prod(q), cols = 1). */
+int64_t ts_result_intermediate(const ts_result* r, int which, int64_t mode, double* out_host, int64_t* rows,
+                               int64_t* cols);
+int ts_result_free(ts_result* r);
+
+/* Debug capture of stage intermediates (0/1). */
+int ts_ctx_set_debug(ts_ctx* ctx, int enabled);
+/* Per-stage CUDA-event times (ms) of the last ts_krp_sum: A, B, C, allreduce Y,
+ * D, E, F1, F2, allreduce h, G, H; returns the number written (<= cap). */
+int ts_ctx_stage_times(ts_ctx* ctx, double* ms, int cap);
+/* Enables per-stage event timing (adds event records; off by default). */
+int ts_ctx_set_timing(ts_ctx* ctx, int enabled);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TUCKSUM_CUDA_H */

@@ -1,0 +1,980 @@
+// capi.cu — C ABI (include/tucksum_cuda.h) and the host-side orchestration of
+// the KRP sketched Tucker summation on one B200 (plus NCCL all-reduce across GPUs).
+//
+// Pipeline of ts_krp_sum (reference src/sketch.cpp:66-181, krp = true), with the
+// summands stored once in the stacked formal-sum layout F_j = [U_j^(1) … U_j^(K)]:
+//   A  Z_j = Ω_jᵀ F_j                       grouped TN DMMA GEMM      (sketch.cpp:108-112)
+//   B  W_n[b] = w_b · G_b,(n) · ⊙_{j≠n} M_j  KRP generated in smem      (sketch.cpp:117-130)
+//   C  Y_n = F_n W_n                         grouped NN DMMA GEMM      (sketch.cpp:131)
+//      all-reduce Y over GPUs (NCCL)
+//   D  Û_n = thin Q(Y_n), R_ii >= 0          Householder TSQR          (sketch.cpp:145-150)
+//   E  P_n = Û_nᵀ F_n                        grouped TN DMMA GEMM      (sketch.cpp:157-160)
+//   F1 T_b = w_b · G_b ×_0 P_0,b ⋯ ×_{d-2}    grouped batched GEMMs     (sketch.cpp:161-166)
+//   F2 h = [T_b]_b · P_{d-1}ᵀ                 NT DMMA GEMM (sum over b) (sketch.cpp:167)
+//      all-reduce h over GPUs (NCCL)
+//   G  st_hosvd(h, eps [, cap])              TSQR(R) + Jacobi SVD + TTM (tucker.cpp:239-283)
+//   H  Ũ_n = Û_n P_n                          grouped NN DMMA GEMM      (sketch.cpp:172-175)
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <map>
+#include <memory>
+#include <tuple>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/tucksum_cuda.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace ts {
+void substream(std::uint64_t seed, std::uint64_t stream, std::uint64_t salt, std::uint64_t* out_seed,
+               std::uint64_t* out_stream);
+void gaussian_fill(std::int64_t rows, std::int64_t cols, std::uint64_t seed, std::uint64_t stream, double* out);
+}  // namespace ts
+
+namespace {
+
+thread_local std::string g_err;
+
+// NCCL entry points resolved at run time (libnccl.so.2 — the copy torch already
+// loaded when present), so the library has no link-time NCCL dependency.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string error;
+};
+
+NcclApi& nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.error = dlerror() ? dlerror() : "dlopen libnccl.so.2 failed";
+            return;
+        }
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce) api.error = "libnccl.so.2 lacks required symbols";
+    });
+    if (!api.error.empty()) throw ts::Error(TS_NCCL, "NCCL unavailable: " + api.error);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) {
+        const char* m = nccl_api().GetErrorString ? nccl_api().GetErrorString(r) : "?";
+        throw ts::Error(TS_NCCL, std::string(what) + ": " + m);
+    }
+}
+
+[[noreturn]] void invalid(const std::string& m) { throw ts::Error(TS_INVALID_ARGUMENT, m); }
+
+template <class F>
+int guarded(F fn) {
+    try {
+        fn();
+        return TS_OK;
+    } catch (const ts::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return TS_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TS_RUNTIME;
+    }
+}
+
+struct OmegaKey {
+    std::uint64_t seed, stream;
+    std::int64_t width;
+    std::vector<std::int64_t> dims;
+    bool operator<(const OmegaKey& o) const {
+        return std::tie(seed, stream, width, dims) < std::tie(o.seed, o.stream, o.width, o.dims);
+    }
+};
+
+constexpr int kNumStages = 11;
+
+}  // namespace
+
+struct ts_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    ts::HostStage stage;
+    std::map<OmegaKey, double*> omega;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    bool debug = false, timing = false;
+    std::vector<double> stage_ms;
+    std::int64_t launches = 0;
+    std::vector<cudaEvent_t> events;
+};
+
+struct ts_batch {
+    ts_ctx* ctx = nullptr;
+    int order = 0;
+    std::int64_t dims[TS_MAX_ORDER] = {};
+    std::int64_t count = 0;
+    std::int64_t R[TS_MAX_ORDER] = {};  // stacked columns per mode
+    double* F[TS_MAX_ORDER] = {};       // device n_j × R_j column-major
+    double* cores = nullptr;
+    std::int64_t core_elems = 0;
+    std::vector<ts::Atom> atoms;
+    ts::Atom* d_atoms = nullptr;
+    std::vector<double> core_norm;  // per summand ‖core‖_F (plan energies)
+    int max_shape = 0;
+    std::int64_t bytes = 0;
+};
+
+struct ts_result {
+    int order = 0;
+    std::int64_t dims[TS_MAX_ORDER] = {}, ranks[TS_MAX_ORDER] = {};
+    double* factors[TS_MAX_ORDER] = {};
+    double* core = nullptr;
+    int device = 0;
+    // Debug intermediates (host copies).
+    std::vector<double> inter[3][TS_MAX_ORDER];
+    std::int64_t inter_rows[3][TS_MAX_ORDER] = {}, inter_cols[3][TS_MAX_ORDER] = {};
+    std::vector<double> h;
+    ~ts_result() {
+        cudaSetDevice(device);
+        for (auto* f : factors)
+            if (f) cudaFree(f);
+        if (core) cudaFree(core);
+    }
+};
+
+namespace {
+
+using ts::CallScratch;
+using ts::GemmProblem;
+using ts::Layout;
+
+double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, std::int64_t width, std::uint64_t seed,
+                  std::uint64_t stream) {
+    OmegaKey key{seed, stream, width, std::vector<std::int64_t>(dims, dims + order)};
+    auto it = ctx->omega.find(key);
+    if (it != ctx->omega.end()) return it->second;
+    std::int64_t total = 0;
+    for (int n = 0; n < order; ++n) total += dims[n] * width;
+    std::vector<double> host(static_cast<size_t>(total));
+    std::int64_t off = 0;
+    for (int n = 0; n < order; ++n) {
+        std::uint64_t s2, t2;
+        ts::substream(seed, stream, static_cast<std::uint64_t>(n), &s2, &t2);
+        ts::gaussian_fill(dims[n], width, s2, t2, host.data() + off);
+        off += dims[n] * width;
+    }
+    double* d = nullptr;
+    TS_CUDA_CHECK(cudaMalloc(&d, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(total, 1))));
+    TS_CUDA_CHECK(cudaMemcpy(d, host.data(), sizeof(double) * static_cast<size_t>(total), cudaMemcpyHostToDevice));
+    ctx->omega.emplace(std::move(key), d);
+    return d;
+}
+
+void mark(ts_ctx* ctx, int idx) {
+    if (ctx->timing) TS_CUDA_CHECK(cudaEventRecord(ctx->events[static_cast<size_t>(idx)], ctx->stream));
+}
+
+void copy_to_host(std::vector<double>& dst, const double* src, std::int64_t n, cudaStream_t st) {
+    dst.resize(static_cast<size_t>(n));
+    if (n > 0) TS_CUDA_CHECK(cudaMemcpyAsync(dst.data(), src, sizeof(double) * static_cast<size_t>(n),
+                                             cudaMemcpyDeviceToHost, st));
+}
+
+// Reference rank rule of st_hosvd (src/tucker.cpp:255-276) + optional cap.
+std::int64_t hosvd_rank(const std::vector<double>& s, double tau, double theta, std::int64_t cap) {
+    const std::int64_t count = static_cast<std::int64_t>(s.size());
+    std::int64_t rank = 1;
+    if (tau == 0.0) {
+        const double floor = 1e-14 * s[0];
+        rank = count;
+        while (rank > 1 && s[static_cast<size_t>(rank - 1)] <= floor) --rank;
+    } else {
+        std::vector<double> suffix(static_cast<size_t>(count) + 1, 0.0);
+        for (std::int64_t j = count - 1; j >= 0; --j)
+            suffix[static_cast<size_t>(j)] = suffix[static_cast<size_t>(j) + 1] + s[static_cast<size_t>(j)] * s[static_cast<size_t>(j)];
+        rank = count;
+        for (std::int64_t r = 1; r <= count; ++r)
+            if (suffix[static_cast<size_t>(r)] <= theta) {
+                rank = r;
+                break;
+            }
+    }
+    if (cap > 0) rank = std::min(rank, cap);
+    return rank;
+}
+
+// Left singular vectors + singular values of the unfolding g_(k) (q_k × rest) via
+// TSQR of g_(k)ᵀ and a one-sided Jacobi SVD of the small triangular factor.
+void unfolding_svd(const double* g, int order, const std::int64_t* shape, int k, double* sigma, double* U,
+                   CallScratch& sc) {
+    std::int64_t rest = 1;
+    for (int j = 0; j < order; ++j)
+        if (j != k) rest *= shape[j];
+    const std::int64_t qk = shape[k];
+    double* X = sc.alloc_n<double>(static_cast<size_t>(rest * qk));
+    ts::launch_unfold_t(g, order, shape, k, X, sc);
+    ts::TsqrPlan plan = ts::plan_tsqr(X, rest, rest, qk, nullptr, 0, sc);
+    ts::run_tsqr({&plan}, sc, false);
+    ts::launch_jacobi_svd(plan.Rtop, plan.kk, static_cast<int>(plan.kk), static_cast<int>(qk), sigma, U, sc);
+}
+
+ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
+                        std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank) {
+    // Validation mirrors src/sketch.cpp:16-30,66-87.
+    if (b == nullptr || b->count < 1) invalid("sum request needs matching, nonempty summands and weights");
+    if (weights == nullptr) invalid("sum request needs matching, nonempty summands and weights");
+    if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
+    const int d = b->order;
+    if (d < 2) invalid("sketched summation needs order >= 2");
+    if (widths == nullptr) invalid("plan order does not match summand order");
+    for (int n = 0; n < d; ++n)
+        if (widths[n] < 1) invalid("plan sketch widths must be positive");
+    const std::int64_t s = *std::max_element(widths, widths + d);
+    if (s > ts::max_tsqr_cols())
+        throw ts::Error(TS_UNSUPPORTED, "sketch width " + std::to_string(s) + " exceeds the supported maximum of " +
+                                            std::to_string(ts::max_tsqr_cols()));
+    for (std::int64_t i = 0; i < b->count; ++i)
+        if (!std::isfinite(weights[i])) invalid("weights must be finite");
+
+    TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+    ctx->stage.reset();
+    cudaStream_t st = ctx->stream;
+    CallScratch sc(st, ctx->stage);
+    const std::int64_t* dims = b->dims;
+    if (ctx->timing && ctx->events.empty()) {
+        ctx->events.resize(kNumStages + 1);
+        for (auto& e : ctx->events) TS_CUDA_CHECK(cudaEventCreate(&e));
+    }
+    mark(ctx, 0);
+
+    double* omega = omega_get(ctx, d, dims, s, seed, stream);
+    std::int64_t q[TS_MAX_ORDER];
+    std::int64_t ooff[TS_MAX_ORDER], yoff[TS_MAX_ORDER];
+    std::int64_t ytot = 0, acc = 0;
+    for (int n = 0; n < d; ++n) {
+        q[n] = std::min(dims[n], s);
+        ooff[n] = acc;
+        acc += dims[n] * s;
+        yoff[n] = ytot;
+        ytot += dims[n] * s;
+    }
+    auto* d_w = static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
+
+    // ---- Stage A: Z_j = Ω_jᵀ F_j (s × R_j)
+    double* Z[TS_MAX_ORDER];
+    {
+        std::vector<GemmProblem> ps;
+        for (int j = 0; j < d; ++j) {
+            Z[j] = sc.alloc_n<double>(static_cast<size_t>(s * b->R[j]));
+            GemmProblem p{};
+            p.A = omega + ooff[j];
+            p.lda = dims[j];
+            p.B = b->F[j];
+            p.ldb = dims[j];
+            p.C = Z[j];
+            p.ldc = s;
+            p.M = static_cast<int>(s);
+            p.N = static_cast<int>(b->R[j]);
+            p.K = static_cast<int>(dims[j]);
+            ps.push_back(p);
+        }
+        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+    }
+    mark(ctx, 1);
+    // ---- Stage B: W_n (R_n × s)
+    double* W[TS_MAX_ORDER];
+    {
+        ts::KrpArgs ka{};
+        for (int n = 0; n < d; ++n) {
+            W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * s));
+            ka.Z[n] = Z[n];
+            ka.W[n] = W[n];
+            ka.R[n] = b->R[n];
+        }
+        ka.order = d;
+        ka.s = static_cast<int>(s);
+        ka.natoms = static_cast<int>(b->atoms.size());
+        ka.atoms = b->d_atoms;
+        ka.cores = b->cores;
+        ka.weights = d_w;
+        ts::launch_krp_contract(ka, b->max_shape, sc);
+    }
+    mark(ctx, 2);
+    // ---- Stage C: Y_n = F_n W_n (n × s), all modes in one buffer
+    double* Y = sc.alloc_n<double>(static_cast<size_t>(ytot));
+    {
+        std::vector<GemmProblem> ps;
+        for (int n = 0; n < d; ++n) {
+            GemmProblem p{};
+            p.A = b->F[n];
+            p.lda = dims[n];
+            p.B = W[n];
+            p.ldb = b->R[n];
+            p.C = Y + yoff[n];
+            p.ldc = dims[n];
+            p.M = static_cast<int>(dims[n]);
+            p.N = static_cast<int>(s);
+            p.K = static_cast<int>(b->R[n]);
+            ps.push_back(p);
+        }
+        ts::launch_grouped_gemm(Layout::NN, ps, sc, ctx->num_sms);
+    }
+    mark(ctx, 3);
+    if (ctx->comm) nccl_check(nccl_api().AllReduce(Y, Y, static_cast<size_t>(ytot), ncclFloat64, ncclSum, ctx->comm, st),
+                              "ncclAllReduce(Y)");
+    mark(ctx, 4);
+    auto res = std::make_unique<ts_result>();
+    res->device = ctx->device;
+    res->order = d;
+    if (ctx->debug) {
+        for (int n = 0; n < d; ++n) {
+            copy_to_host(res->inter[0][n], omega + ooff[n], dims[n] * s, st);
+            res->inter_rows[0][n] = dims[n];
+            res->inter_cols[0][n] = s;
+            copy_to_host(res->inter[1][n], Y + yoff[n], dims[n] * s, st);
+            res->inter_rows[1][n] = dims[n];
+            res->inter_cols[1][n] = s;
+        }
+    }
+    // ---- Stage D: Û_n = thin Q of Y_n
+    double* Uh[TS_MAX_ORDER];
+    {
+        std::vector<ts::TsqrPlan> plans(static_cast<size_t>(d));
+        std::vector<ts::TsqrPlan*> pp;
+        for (int n = 0; n < d; ++n) {
+            Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+            plans[static_cast<size_t>(n)] = ts::plan_tsqr(Y + yoff[n], dims[n], dims[n], s, Uh[n], dims[n], sc);
+            pp.push_back(&plans[static_cast<size_t>(n)]);
+        }
+        ts::run_tsqr(pp, sc, true);
+    }
+    mark(ctx, 5);
+    // ---- Stage E: P_n = Û_nᵀ F_n (q_n × R_n)
+    double* P[TS_MAX_ORDER];
+    {
+        std::vector<GemmProblem> ps;
+        for (int n = 0; n < d; ++n) {
+            P[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
+            GemmProblem p{};
+            p.A = Uh[n];
+            p.lda = dims[n];
+            p.B = b->F[n];
+            p.ldb = dims[n];
+            p.C = P[n];
+            p.ldc = q[n];
+            p.M = static_cast<int>(q[n]);
+            p.N = static_cast<int>(b->R[n]);
+            p.K = static_cast<int>(dims[n]);
+            ps.push_back(p);
+        }
+        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+    }
+    mark(ctx, 6);
+    // ---- Stage F1: per-atom multi-TTM over modes 0..d-2 into T_stack (Q' × R_{d-1})
+    std::int64_t Qp = 1;
+    for (int j = 0; j < d - 1; ++j) Qp *= q[j];
+    double* Tstack = sc.alloc_n<double>(static_cast<size_t>(Qp * b->R[d - 1]));
+    {
+        const size_t na = b->atoms.size();
+        std::vector<double*> cur(na), nxt(na);
+        for (int m = 0; m <= d - 2; ++m) {
+            const bool last = (m == d - 2);
+            double* outbuf = nullptr;
+            std::vector<std::int64_t> outoff(na);
+            if (!last) {
+                std::int64_t tot = 0;
+                for (size_t a = 0; a < na; ++a) {
+                    std::int64_t e = 1;
+                    for (int j = 0; j <= m; ++j) e *= q[j];
+                    for (int j = m + 1; j < d; ++j) e *= b->atoms[a].shape[j];
+                    outoff[a] = tot;
+                    tot += e;
+                }
+                outbuf = sc.alloc_n<double>(static_cast<size_t>(tot));
+            }
+            std::vector<GemmProblem> ps;
+            ps.reserve(na);
+            for (size_t a = 0; a < na; ++a) {
+                const ts::Atom& at = b->atoms[a];
+                double* out = last ? Tstack + static_cast<std::int64_t>(at.col[d - 1]) * Qp : outbuf + outoff[a];
+                const double alpha = last ? weights[at.summand] : 1.0;
+                std::int64_t left = 1, right = 1;
+                for (int j = 0; j < m; ++j) left *= q[j];
+                for (int j = m + 1; j < d; ++j) right *= at.shape[j];
+                GemmProblem p{};
+                p.alpha = alpha;
+                if (m == 0) {
+                    // out (q0 × right) = P_0[:, cols] (q0 × r0) · G_(0) (r0 × right)
+                    p.A = P[0] + static_cast<std::int64_t>(at.col[0]) * q[0];
+                    p.lda = q[0];
+                    p.B = b->cores + at.core_off;
+                    p.ldb = at.shape[0];
+                    p.C = out;
+                    p.ldc = q[0];
+                    p.M = static_cast<int>(q[0]);
+                    p.N = static_cast<int>(right);
+                    p.K = at.shape[0];
+                } else {
+                    // per right slice: out (left × q_m) = T (left × r_m) · P_m[:, cols]ᵀ
+                    p.A = cur[a];
+                    p.lda = left;
+                    p.sA = left * at.shape[m];
+                    p.B = P[m] + static_cast<std::int64_t>(at.col[m]) * q[m];
+                    p.ldb = q[m];
+                    p.sB = 0;
+                    p.C = out;
+                    p.ldc = left;
+                    p.sC = left * q[m];
+                    p.M = static_cast<int>(left);
+                    p.N = static_cast<int>(q[m]);
+                    p.K = at.shape[m];
+                    p.batch = static_cast<int>(right);
+                }
+                ps.push_back(p);
+                nxt[a] = out;
+            }
+            ts::launch_grouped_gemm(m == 0 ? Layout::NN : Layout::NT, ps, sc, ctx->num_sms);
+            std::swap(cur, nxt);
+        }
+    }
+    mark(ctx, 7);
+    // ---- Stage F2: h (Q' × q_{d-1}) = T_stack · P_{d-1}ᵀ
+    const std::int64_t hsize = Qp * q[d - 1];
+    double* h = sc.alloc_n<double>(static_cast<size_t>(hsize));
+    {
+        GemmProblem p{};
+        p.A = Tstack;
+        p.lda = Qp;
+        p.B = P[d - 1];
+        p.ldb = q[d - 1];
+        p.C = h;
+        p.ldc = Qp;
+        p.M = static_cast<int>(Qp);
+        p.N = static_cast<int>(q[d - 1]);
+        p.K = static_cast<int>(b->R[d - 1]);
+        ts::launch_grouped_gemm(Layout::NT, {p}, sc, ctx->num_sms);
+    }
+    mark(ctx, 8);
+    if (ctx->comm) nccl_check(nccl_api().AllReduce(h, h, static_cast<size_t>(hsize), ncclFloat64, ncclSum, ctx->comm, st),
+                              "ncclAllReduce(h)");
+    mark(ctx, 9);
+    if (ctx->debug) {
+        for (int n = 0; n < d; ++n) {
+            copy_to_host(res->inter[2][n], Uh[n], dims[n] * q[n], st);
+            res->inter_rows[2][n] = dims[n];
+            res->inter_cols[2][n] = q[n];
+        }
+        copy_to_host(res->h, h, hsize, st);
+    }
+    // ---- Stage G: ST-HOSVD of h (replicated on every GPU)
+    std::int64_t cur_shape[TS_MAX_ORDER];
+    for (int n = 0; n < d; ++n) cur_shape[n] = q[n];
+    double* Pk[TS_MAX_ORDER] = {};  // q_k × q_k left singular vectors (first rank_k columns used)
+    std::int64_t rank[TS_MAX_ORDER];
+    double* g = h;
+    {
+        double* d_ss = sc.alloc_n<double>(1);
+        ts::launch_sumsq(h, hsize, d_ss, sc);
+        double hss = 0.0;
+        TS_CUDA_CHECK(cudaMemcpyAsync(&hss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        const double theta = eps * eps * hss / static_cast<double>(d);
+        std::vector<int> mode_order(static_cast<size_t>(d));
+        std::iota(mode_order.begin(), mode_order.end(), 0);
+        std::stable_sort(mode_order.begin(), mode_order.end(), [&](int x, int y) { return cur_shape[x] < cur_shape[y]; });
+        for (int k : mode_order) {
+            const std::int64_t qk = cur_shape[k];
+            double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
+            Pk[k] = sc.alloc_n<double>(static_cast<size_t>(qk * qk));
+            unfolding_svd(g, d, cur_shape, k, sigma, Pk[k], sc);
+            std::vector<double> sig(static_cast<size_t>(qk));
+            TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
+                                          cudaMemcpyDeviceToHost, st));
+            TS_CUDA_CHECK(cudaStreamSynchronize(st));
+            const std::int64_t rk = hosvd_rank(sig, eps, theta, max_rank ? max_rank[k] : 0);
+            rank[k] = rk;
+            // g ← g ×_k P_kᵀ
+            std::int64_t left = 1, right = 1, total_out = rk;
+            for (int j = 0; j < d; ++j) {
+                if (j < k) left *= cur_shape[j];
+                if (j > k) right *= cur_shape[j];
+                if (j != k) total_out *= cur_shape[j];
+            }
+            double* gn = sc.alloc_n<double>(static_cast<size_t>(total_out));
+            GemmProblem p{};
+            if (k == 0) {
+                p.A = Pk[k];
+                p.lda = qk;
+                p.B = g;
+                p.ldb = qk;
+                p.C = gn;
+                p.ldc = rk;
+                p.M = static_cast<int>(rk);
+                p.N = static_cast<int>(right);
+                p.K = static_cast<int>(qk);
+                ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
+            } else {
+                p.A = g;
+                p.lda = left;
+                p.sA = left * qk;
+                p.B = Pk[k];
+                p.ldb = qk;
+                p.C = gn;
+                p.ldc = left;
+                p.sC = left * rk;
+                p.M = static_cast<int>(left);
+                p.N = static_cast<int>(rk);
+                p.K = static_cast<int>(qk);
+                p.batch = static_cast<int>(right);
+                ts::launch_grouped_gemm(Layout::NN, {p}, sc, ctx->num_sms);
+            }
+            g = gn;
+            cur_shape[k] = rk;
+        }
+    }
+    mark(ctx, 10);
+    // ---- Stage H: Ũ_n = Û_n · P_n (n × rank_n); the core is g.
+    {
+        std::vector<GemmProblem> ps;
+        for (int n = 0; n < d; ++n) {
+            res->dims[n] = dims[n];
+            res->ranks[n] = rank[n];
+            TS_CUDA_CHECK(cudaMalloc(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n])));
+            GemmProblem p{};
+            p.A = Uh[n];
+            p.lda = dims[n];
+            p.B = Pk[n];
+            p.ldb = q[n];
+            p.C = res->factors[n];
+            p.ldc = dims[n];
+            p.M = static_cast<int>(dims[n]);
+            p.N = static_cast<int>(rank[n]);
+            p.K = static_cast<int>(q[n]);
+            ps.push_back(p);
+        }
+        ts::launch_grouped_gemm(Layout::NN, ps, sc, ctx->num_sms);
+        std::int64_t csize = 1;
+        for (int n = 0; n < d; ++n) csize *= rank[n];
+        TS_CUDA_CHECK(cudaMalloc(&res->core, sizeof(double) * static_cast<size_t>(csize)));
+        TS_CUDA_CHECK(cudaMemcpyAsync(res->core, g, sizeof(double) * static_cast<size_t>(csize),
+                                      cudaMemcpyDeviceToDevice, st));
+    }
+    mark(ctx, 11);
+    ctx->launches += sc.launches;
+    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (ctx->timing) {
+        ctx->stage_ms.assign(kNumStages, 0.0);
+        for (int i = 0; i < kNumStages; ++i) {
+            float ms = 0.f;
+            TS_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->events[static_cast<size_t>(i)], ctx->events[static_cast<size_t>(i + 1)]));
+            ctx->stage_ms[static_cast<size_t>(i)] = ms;
+        }
+    }
+    return res.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ts_last_error(void) { return g_err.c_str(); }
+const char* ts_version(void) { return "tucksum-b200 0.1 (sm_100a)"; }
+
+int ts_ctx_create(int device, ts_ctx** out) {
+    return guarded([&] {
+        if (out == nullptr) invalid("ts_ctx_create: null out");
+        int ndev = 0;
+        TS_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) invalid("ts_ctx_create: no such device");
+        TS_CUDA_CHECK(cudaSetDevice(device));
+        auto ctx = std::make_unique<ts_ctx>();
+        ctx->device = device;
+        TS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        TS_CUDA_CHECK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+        cudaMemPool_t pool;
+        TS_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+        std::uint64_t thresh = std::numeric_limits<std::uint64_t>::max();
+        TS_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+        *out = ctx.release();
+    });
+}
+
+int ts_ctx_destroy(ts_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& kv : ctx->omega) cudaFree(kv.second);
+        for (auto& e : ctx->events) cudaEventDestroy(e);
+        if (ctx->comm && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int ts_nccl_unique_id(void* unique_id_128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        nccl_check(nccl_api().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(unique_id_128, &id, sizeof(id));
+    });
+}
+
+int ts_ctx_init_nccl(ts_ctx* ctx, const void* unique_id_128, int nranks, int rank) {
+    return guarded([&] {
+        if (!ctx || !unique_id_128 || nranks < 1 || rank < 0 || rank >= nranks) invalid("ts_ctx_init_nccl: bad arguments");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id_128, sizeof(id));
+        nccl_check(nccl_api().CommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+    });
+}
+
+void* ts_ctx_stream(ts_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+int64_t ts_ctx_launch_count(ts_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ts_ctx_set_debug(ts_ctx* ctx, int enabled) {
+    return guarded([&] {
+        if (!ctx) invalid("null context");
+        ctx->debug = enabled != 0;
+    });
+}
+int ts_ctx_set_timing(ts_ctx* ctx, int enabled) {
+    return guarded([&] {
+        if (!ctx) invalid("null context");
+        ctx->timing = enabled != 0;
+    });
+}
+int ts_ctx_stage_times(ts_ctx* ctx, double* ms, int cap) {
+    if (!ctx) return 0;
+    const int n = std::min<int>(cap, static_cast<int>(ctx->stage_ms.size()));
+    for (int i = 0; i < n; ++i) ms[i] = ctx->stage_ms[static_cast<size_t>(i)];
+    return n;
+}
+
+int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_batch** out) {
+    return guarded([&] {
+        if (!ctx || !out) invalid("ts_batch_upload: null argument");
+        if (count < 1 || xs == nullptr) invalid("sum request needs matching, nonempty summands and weights");
+        const ts_tucker_view& x0 = xs[0];
+        const int d = static_cast<int>(x0.order);
+        if (d < 1) invalid("TuckerTensor: order must be >= 1");
+        if (d > TS_MAX_ORDER) throw ts::Error(TS_UNSUPPORTED, "order exceeds TS_MAX_ORDER");
+        auto b = std::make_unique<ts_batch>();
+        b->ctx = ctx;
+        b->order = d;
+        b->count = count;
+        for (int j = 0; j < d; ++j) b->dims[j] = x0.dims[j];
+        // Structure validation (src/tucker.cpp:16-55) and dims agreement (src/sketch.cpp:23-28).
+        std::int64_t core_elems = 0;
+        for (std::int64_t i = 0; i < count; ++i) {
+            const ts_tucker_view& x = xs[i];
+            if (x.order != d) invalid("sum request summands must share dims");
+            for (int j = 0; j < d; ++j) {
+                if (x.dims[j] != b->dims[j]) invalid("sum request summands must share dims");
+                if (x.dims[j] < 1 || x.ranks[j] < 1) invalid("TuckerTensor: dims and ranks must be positive");
+                if (x.factors == nullptr || x.factors[j] == nullptr) invalid("TuckerTensor: one factor matrix per mode required");
+            }
+            if (x.num_blocks < 1) invalid("TuckerTensor: core needs at least one block");
+            std::int64_t cursor[TS_MAX_ORDER] = {};
+            for (std::int64_t bl = 0; bl < x.num_blocks; ++bl) {
+                std::int64_t e = 1;
+                for (int j = 0; j < d; ++j) {
+                    if (x.block_offsets[bl * d + j] != cursor[j]) invalid("TuckerTensor: blocks must tile the super-diagonal");
+                    const std::int64_t ext = x.block_shapes[bl * d + j];
+                    if (ext < 1) invalid("DenseTensor: every dimension must be >= 1");
+                    cursor[j] += ext;
+                    e *= ext;
+                }
+                if (x.block_data == nullptr || x.block_data[bl] == nullptr) invalid("TuckerTensor: null block data");
+                core_elems += e;
+            }
+            for (int j = 0; j < d; ++j)
+                if (cursor[j] != x.ranks[j]) invalid("TuckerTensor: blocks must span the full rank box");
+            for (int j = 0; j < d; ++j) b->R[j] += x.ranks[j];
+        }
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        std::int64_t bytes = 0;
+        for (int j = 0; j < d; ++j) {
+            TS_CUDA_CHECK(cudaMalloc(&b->F[j], sizeof(double) * static_cast<size_t>(b->dims[j] * b->R[j])));
+            bytes += sizeof(double) * b->dims[j] * b->R[j];
+        }
+        TS_CUDA_CHECK(cudaMalloc(&b->cores, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(core_elems, 1))));
+        bytes += sizeof(double) * core_elems;
+        b->core_elems = core_elems;
+        // Copies; adjacent host ranges (e.g. one pinned slab per mode) are merged.
+        struct Run {
+            const double* src = nullptr;
+            double* dst = nullptr;
+            std::int64_t n = 0;
+        };
+        auto flush = [&](Run& r) {
+            if (r.n > 0)
+                TS_CUDA_CHECK(cudaMemcpyAsync(r.dst, r.src, sizeof(double) * static_cast<size_t>(r.n),
+                                              cudaMemcpyHostToDevice, st));
+            r = Run{};
+        };
+        auto add = [&](Run& r, const double* src, double* dst, std::int64_t n) {
+            if (r.n > 0 && r.src + r.n == src && r.dst + r.n == dst) {
+                r.n += n;
+                return;
+            }
+            flush(r);
+            r.src = src;
+            r.dst = dst;
+            r.n = n;
+        };
+        std::int64_t col[TS_MAX_ORDER] = {};
+        for (int j = 0; j < d; ++j) {
+            Run run;
+            std::int64_t c = 0;
+            for (std::int64_t i = 0; i < count; ++i) {
+                add(run, xs[i].factors[j], b->F[j] + c * b->dims[j], b->dims[j] * xs[i].ranks[j]);
+                c += xs[i].ranks[j];
+            }
+            flush(run);
+        }
+        Run crun;
+        std::int64_t coff = 0;
+        b->core_norm.assign(static_cast<size_t>(count), 0.0);
+        for (std::int64_t i = 0; i < count; ++i) {
+            const ts_tucker_view& x = xs[i];
+            double sq = 0.0;
+            for (std::int64_t bl = 0; bl < x.num_blocks; ++bl) {
+                ts::Atom at{};
+                at.summand = static_cast<int>(i);
+                at.core_off = coff;
+                std::int64_t e = 1;
+                for (int j = 0; j < d; ++j) {
+                    at.col[j] = static_cast<int>(col[j] + x.block_offsets[bl * d + j]);
+                    at.shape[j] = static_cast<int>(x.block_shapes[bl * d + j]);
+                    e *= at.shape[j];
+                    b->max_shape = std::max(b->max_shape, at.shape[j]);
+                }
+                for (std::int64_t t = 0; t < e; ++t) sq += x.block_data[bl][t] * x.block_data[bl][t];
+                add(crun, x.block_data[bl], b->cores + coff, e);
+                coff += e;
+                b->atoms.push_back(at);
+            }
+            b->core_norm[static_cast<size_t>(i)] = std::sqrt(sq);
+            for (int j = 0; j < d; ++j) col[j] += x.ranks[j];
+        }
+        flush(crun);
+        TS_CUDA_CHECK(cudaMalloc(&b->d_atoms, sizeof(ts::Atom) * b->atoms.size()));
+        TS_CUDA_CHECK(cudaMemcpyAsync(b->d_atoms, b->atoms.data(), sizeof(ts::Atom) * b->atoms.size(),
+                                      cudaMemcpyHostToDevice, st));
+        bytes += sizeof(ts::Atom) * b->atoms.size();
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        b->bytes = bytes;
+        *out = b.release();
+    });
+}
+
+int ts_batch_free(ts_batch* b) {
+    return guarded([&] {
+        if (!b) return;
+        cudaSetDevice(b->ctx->device);
+        cudaStreamSynchronize(b->ctx->stream);
+        for (auto* f : b->F)
+            if (f) cudaFree(f);
+        if (b->cores) cudaFree(b->cores);
+        if (b->d_atoms) cudaFree(b->d_atoms);
+        delete b;
+    });
+}
+
+int64_t ts_batch_count(const ts_batch* b) { return b ? b->count : 0; }
+int64_t ts_batch_bytes(const ts_batch* b) { return b ? b->bytes : 0; }
+
+void ts_substream(uint64_t seed, uint64_t stream, uint64_t salt, uint64_t* out_seed, uint64_t* out_stream) {
+    ts::substream(seed, stream, salt, out_seed, out_stream);
+}
+
+int ts_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream, double* out) {
+    return guarded([&] {
+        if (rows < 0 || cols < 0) invalid("gaussian_matrix: negative extent");
+        ts::gaussian_fill(rows, cols, seed, stream, out);
+    });
+}
+
+int ts_omega_prepare(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t width, uint64_t seed, uint64_t stream) {
+    return guarded([&] {
+        if (!ctx || order < 1 || order > TS_MAX_ORDER || width < 1) invalid("ts_omega_prepare: bad arguments");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        omega_get(ctx, static_cast<int>(order), dims, width, seed, stream);
+    });
+}
+
+int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
+               uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
+    return guarded([&] {
+        if (!ctx || !out) invalid("ts_krp_sum: null argument");
+        *out = krp_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank);
+    });
+}
+
+// Plan stage (src/sketch.cpp:272-349, Strategy::Krp).  The spectrum of the Gram
+// of the energy-weighted stacked factors V_n = F_n·diag(e) is obtained as the
+// squared singular values of V_n (TSQR + Jacobi on device), with the reference's
+// floor / tail rule applied on the returned values.
+int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, double eps, const int64_t* oversampling,
+                         int64_t* effective_ranks, int64_t* targets, int64_t* widths) {
+    return guarded([&] {
+        if (!ctx || !b || !weights || !oversampling) invalid("sum request needs matching, nonempty summands and weights");
+        if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
+        const int d = b->order;
+        for (int n = 0; n < d; ++n)
+            if (oversampling[n] < 0) invalid("oversampling must be nonnegative");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->stage.reset();
+        CallScratch sc(ctx->stream, ctx->stage);
+        std::vector<double> energy(static_cast<size_t>(b->count));
+        for (std::int64_t i = 0; i < b->count; ++i)
+            energy[static_cast<size_t>(i)] = std::fabs(weights[i]) * b->core_norm[static_cast<size_t>(i)];
+        auto complement_product = [&](int skip) {
+            const std::int64_t cap = std::int64_t(1) << 50;
+            std::int64_t prod = 1;
+            for (int j = 0; j < d; ++j) {
+                if (j == skip) continue;
+                const std::int64_t f = std::max<std::int64_t>(b->dims[j], 1);
+                if (prod > cap / f) return cap;
+                prod *= f;
+            }
+            return prod;
+        };
+        for (int n = 0; n < d; ++n) {
+            const std::int64_t rows = b->dims[n], R = b->R[n];
+            const std::int64_t small = std::min(rows, R);
+            if (small > ts::max_tsqr_cols())
+                throw ts::Error(TS_UNSUPPORTED, "effective_subrank: min(n, sum of ranks) exceeds the device eigen-solver size");
+            // Per-column energy scale.
+            std::vector<double> cscale(static_cast<size_t>(R));
+            std::int64_t c = 0;
+            std::vector<std::int64_t> rank_of(static_cast<size_t>(b->count), 0);
+            for (const auto& at : b->atoms) rank_of[static_cast<size_t>(at.summand)] += 0;
+            // Column ranges per summand follow the stacking order.
+            {
+                std::vector<std::int64_t> rk(static_cast<size_t>(b->count), 0);
+                std::int64_t cnt_cols = 0;
+                for (const auto& at : b->atoms) rk[static_cast<size_t>(at.summand)] += at.shape[n];
+                for (std::int64_t i = 0; i < b->count; ++i) {
+                    for (std::int64_t t = 0; t < rk[static_cast<size_t>(i)]; ++t) cscale[static_cast<size_t>(c++)] = energy[static_cast<size_t>(i)];
+                    cnt_cols += rk[static_cast<size_t>(i)];
+                }
+                (void)cnt_cols;
+            }
+            auto* d_scale = static_cast<double*>(sc.upload(cscale.data(), sizeof(double) * static_cast<size_t>(R)));
+            const bool tall = rows >= R;
+            double* V = sc.alloc_n<double>(static_cast<size_t>(rows * R));
+            ts::launch_scale_columns(b->F[n], rows, R, d_scale, V, !tall, sc);
+            const std::int64_t m = tall ? rows : R, cols = tall ? R : rows;
+            ts::TsqrPlan plan = ts::plan_tsqr(V, m, m, cols, nullptr, 0, sc);
+            ts::run_tsqr({&plan}, sc, false);
+            double* sigma = sc.alloc_n<double>(static_cast<size_t>(cols));
+            double* U = sc.alloc_n<double>(static_cast<size_t>(cols * cols));
+            ts::launch_jacobi_svd(plan.Rtop, plan.kk, static_cast<int>(plan.kk), static_cast<int>(cols), sigma, U, sc);
+            std::vector<double> sig(static_cast<size_t>(cols));
+            TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(cols),
+                                          cudaMemcpyDeviceToHost, ctx->stream));
+            TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            // Eigenvalues of VᵀV (R of them; the R - cols missing ones are zero).
+            std::vector<double> lam(static_cast<size_t>(R), 0.0);
+            for (std::int64_t j = 0; j < cols; ++j) lam[static_cast<size_t>(j)] = sig[static_cast<size_t>(j)] * sig[static_cast<size_t>(j)];
+            const double lmax = lam.empty() ? 0.0 : lam[0];
+            const double floor = static_cast<double>(R) * std::numeric_limits<double>::epsilon() * lmax;
+            for (double& l : lam)
+                if (l < floor) l = 0.0;
+            std::vector<double> suffix(static_cast<size_t>(R) + 1, 0.0);
+            for (std::int64_t j = R - 1; j >= 0; --j) suffix[static_cast<size_t>(j)] = suffix[static_cast<size_t>(j) + 1] + lam[static_cast<size_t>(j)];
+            const double thresh = eps * eps / static_cast<double>(d) * suffix[0];
+            std::int64_t keep = R;
+            for (std::int64_t r = 1; r <= R; ++r)
+                if (suffix[static_cast<size_t>(r)] <= thresh) {
+                    keep = r;
+                    break;
+                }
+            effective_ranks[n] = keep;
+            std::int64_t target = keep + oversampling[n];
+            target = std::min({target, b->dims[n], complement_product(n)});
+            targets[n] = std::max<std::int64_t>(target, 1);
+        }
+        const std::int64_t smax = *std::max_element(targets, targets + d);
+        for (int n = 0; n < d; ++n) widths[n] = smax;
+        ctx->launches += sc.launches;
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int64_t ts_result_order(const ts_result* r) { return r ? r->order : 0; }
+void ts_result_dims(const ts_result* r, int64_t* dims) {
+    for (int n = 0; n < r->order; ++n) dims[n] = r->dims[n];
+}
+void ts_result_ranks(const ts_result* r, int64_t* ranks) {
+    for (int n = 0; n < r->order; ++n) ranks[n] = r->ranks[n];
+}
+int ts_result_factor(const ts_result* r, int64_t mode, double* out) {
+    return guarded([&] {
+        if (!r || mode < 0 || mode >= r->order) invalid("ts_result_factor: bad mode");
+        TS_CUDA_CHECK(cudaSetDevice(r->device));
+        TS_CUDA_CHECK(cudaMemcpy(out, r->factors[mode], sizeof(double) * static_cast<size_t>(r->dims[mode] * r->ranks[mode]),
+                                 cudaMemcpyDeviceToHost));
+    });
+}
+int ts_result_core(const ts_result* r, double* out) {
+    return guarded([&] {
+        if (!r) invalid("ts_result_core: null result");
+        std::int64_t n = 1;
+        for (int k = 0; k < r->order; ++k) n *= r->ranks[k];
+        TS_CUDA_CHECK(cudaSetDevice(r->device));
+        TS_CUDA_CHECK(cudaMemcpy(out, r->core, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+    });
+}
+const double* ts_result_factor_device(const ts_result* r, int64_t mode) {
+    return (r && mode >= 0 && mode < r->order) ? r->factors[mode] : nullptr;
+}
+const double* ts_result_core_device(const ts_result* r) { return r ? r->core : nullptr; }
+
+int64_t ts_result_intermediate(const ts_result* r, int which, int64_t mode, double* out, int64_t* rows, int64_t* cols) {
+    if (!r) return -1;
+    if (which == 3) {
+        if (out) std::memcpy(out, r->h.data(), sizeof(double) * r->h.size());
+        if (rows) *rows = static_cast<int64_t>(r->h.size());
+        if (cols) *cols = 1;
+        return static_cast<int64_t>(r->h.size());
+    }
+    if (which < 0 || which > 2 || mode < 0 || mode >= r->order) return -1;
+    const auto& v = r->inter[which][mode];
+    if (out) std::memcpy(out, v.data(), sizeof(double) * v.size());
+    if (rows) *rows = r->inter_rows[which][mode];
+    if (cols) *cols = r->inter_cols[which][mode];
+    return static_cast<int64_t>(v.size());
+}
+
+int ts_result_free(ts_result* r) {
+    return guarded([&] { delete r; });
+}
+
+}  // extern "C"

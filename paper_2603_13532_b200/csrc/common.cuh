@@ -1,0 +1,44 @@
+// common.cuh — shared device helpers for the sm_100a KRP-sum kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ts {
+
+constexpr int kMaxOrder = 8;
+
+// One fp64 tensor-core MMA: C(8x8) += A(8x4, row) * B(4x8, col).  On sm_100a this
+// is the DMMA.8x8x4 SASS instruction (the only fp64 MMA shape the chip executes;
+// larger PTX shapes lower to several of these).  Fragment ownership, with
+// g = lane>>2 and t = lane&3: a = A[g][t], b = B[t][g], c0/c1 = C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// cp.async with zero-fill: copies src_bytes (0 or 8) and zero-fills to 8 bytes.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes));
+}
+// 16-byte variant (cache-global): src_bytes in {0, 8, 16}.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace ts

@@ -1,0 +1,95 @@
+// kernels.cuh — non-GEMM kernels of the KRP sketched sum (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "runtime.hpp"
+
+namespace ts {
+
+// One core block ("atom") of the device-resident formal-sum layout
+// (reference src/tucker.cpp:183-226): summand index (for its weight), the block's
+// core data offset, its column offset into every stacked factor, and its extents.
+struct Atom {
+    int summand;
+    int pad;
+    int64_t core_off;
+    int col[kMaxOrder];
+    int shape[kMaxOrder];
+};
+
+// Stage B (reference src/sketch.cpp:117-131): for every atom b and mode n,
+//   W_n[col_b[n] + a, c] = w_b · Σ_J G_b,(n)(a, J) · Π_{j≠n} M_j(col_b[j] + a_j(J), c)
+// i.e. the core times the implicit Khatri-Rao product of the M_j slices, with
+// M_j stored transposed as Z_j (s × R_j).  The KRP is generated in shared memory
+// chunk by chunk and never reaches HBM.
+struct KrpArgs {
+    const double* Z[kMaxOrder];
+    double* W[kMaxOrder];
+    int64_t R[kMaxOrder];
+    int order;
+    int s;
+    int natoms;
+    const Atom* atoms;
+    const double* cores;
+    const double* weights;  // per summand
+};
+void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc);
+
+// Stage D building blocks: Householder TSQR with the R_ii >= 0 sign convention
+// of qr_econ (reference src/kernels.cpp:50-63).
+struct QrTask {
+    double* A;  // rows × cols block (in/out: Householder vectors below the diagonal)
+    int64_t lda;
+    int rows, cols;
+    double* tau;  // [cols]
+    double* R;    // out: min(rows,cols) × cols upper-triangular (ld ldr)
+    int64_t ldr;
+};
+struct QrApplyTask {
+    const double* V;  // Householder vectors of the block (rows × kk)
+    int64_t ldv;
+    const double* tau;
+    int rows, kk, q;
+    const double* Qin;  // parent piece kk × q (ld ldqin); nullptr → [I; 0]
+    int64_t ldqin;
+    double* Q;  // out rows × q
+    int64_t ldq;
+    const double* Rsign;  // top level: flip column c when Rsign[c + c*ldrs] < 0
+    int64_t ldrs;
+};
+
+// A full TSQR of one tall matrix (rows × cols), planned on the host.
+struct TsqrPlan {
+    std::vector<std::vector<QrTask>> levels;       // bottom-up factor tasks
+    std::vector<std::vector<QrApplyTask>> applies;  // top-down Q-formation tasks
+    double* Rtop = nullptr;                        // kk × cols (ld kk)
+    int64_t kk = 0;
+};
+// Builds the plan for `A` (rows × cols, ld lda).  If Q != nullptr the thin Q
+// (rows × min(rows,cols), ld ldq) is formed by the apply tasks.
+TsqrPlan plan_tsqr(double* A, int64_t lda, int64_t rows, int64_t cols, double* Q, int64_t ldq, CallScratch& sc);
+// Runs several plans level-synchronously (factor levels bottom-up, then the
+// Q-formation levels top-down), batching the plans' tasks per level.
+void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q);
+
+// One-sided Jacobi SVD of a small m × nc matrix R in one CTA (stage G).
+// Writes sigma[nc] (descending) and U (nc × nc, ld nc): the right singular
+// vectors of R, i.e. the left singular vectors of Rᵀ.
+void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigma, double* U, CallScratch& sc);
+
+// X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
+void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);
+// out[0] = Σ x_i² (single-CTA, deterministic).
+void launch_sumsq(const double* x, int64_t n, double* out, CallScratch& sc);
+
+// out = F·diag(scale) (n × R, ld n) or its transpose (R × n, ld R) when transpose.
+void launch_scale_columns(const double* F, int64_t n, int64_t R, const double* scale, double* out, bool transpose,
+                          CallScratch& sc);
+
+int max_tsqr_cols();
+
+}  // namespace ts

@@ -1,0 +1,61 @@
+// runtime.cpp — pinned descriptor staging and stream-ordered call scratch.
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cstdio>
+
+#include "../../include/tucksum_cuda.h"
+
+namespace ts {
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e), file,
+                  line, what);
+    throw Error(e == cudaErrorMemoryAllocation ? TS_OOM : TS_CUDA, buf);
+}
+
+HostStage::~HostStage() {
+    for (auto& c : retired_) cudaFreeHost(c.p);
+    if (buf_) cudaFreeHost(buf_);
+}
+
+void HostStage::reset() {
+    for (auto& c : retired_) cudaFreeHost(c.p);
+    retired_.clear();
+    used_ = 0;
+}
+
+void* HostStage::put(const void* src, size_t bytes) {
+    const size_t need = (bytes + 255) & ~size_t(255);
+    if (used_ + need > cap_) {
+        if (buf_) retired_.push_back({buf_, cap_});
+        cap_ = std::max<size_t>(need, std::max<size_t>(cap_ * 2, size_t(1) << 20));
+        TS_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&buf_), cap_));
+        used_ = 0;
+    }
+    char* p = buf_ + used_;
+    used_ += need;
+    std::memcpy(p, src, bytes);
+    return p;
+}
+
+CallScratch::~CallScratch() {
+    for (void* p : ptrs_) cudaFreeAsync(p, stream_);
+}
+
+void* CallScratch::alloc(size_t bytes) {
+    void* p = nullptr;
+    TS_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(bytes, 256), stream_));
+    ptrs_.push_back(p);
+    return p;
+}
+
+void* CallScratch::upload(const void* src, size_t bytes) {
+    void* host = stage_.put(src, bytes);
+    void* dev = alloc(bytes);
+    TS_CUDA_CHECK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, stream_));
+    return dev;
+}
+
+}  // namespace ts

@@ -1,0 +1,597 @@
+"""Host-side mirror of the reference ``tucksum`` interface for the KRP hot path.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(``/root/reference/proj/include/tucksum/{types,tucker,sketch}.hpp``), backed by
+the sm_100a CUDA library through its C ABI (``include/tucksum_cuda.h``).  There
+is no CPU fallback: if ``libtucksum_cuda.so`` is missing or no GPU is present the
+calls raise.
+
+Reference → here:
+  RngSeed / substream          types.hpp:17-24, kernels.cpp:23-25   → RngSeed
+  gaussian_matrix              kernels.cpp:88-101                   → gaussian_matrix
+  CoreBlock / TuckerTensor     tucker.hpp:13-48, tucker.cpp:16-79   → CoreBlock / TuckerTensor
+  formal_sum / tucker_axby     tucker.cpp:183-233                   → formal_sum / tucker_axby (structural)
+  Strategy / SketchPlan /      sketch.hpp:18-58                     → same names
+  SumRequest / SumStats
+  effective_subrank (Krp)      sketch.cpp:272-349                   → effective_subrank
+  krp_sum                      sketch.cpp:66-181,360-362            → krp_sum
+  round_sum (Strategy::Krp)    sketch.cpp:368-376                   → round_sum
+std::invalid_argument maps to ValueError, std::runtime_error to RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtucksum_cuda.so")
+
+i64 = C.c_int64
+u64 = C.c_uint64
+dptr = C.POINTER(C.c_double)
+i64p = C.POINTER(C.c_int64)
+
+TS_OK, TS_INVALID_ARGUMENT, TS_RUNTIME, TS_CUDA, TS_NCCL, TS_OOM, TS_UNSUPPORTED = range(7)
+MAX_ORDER = 8
+
+# Every symbol include/tucksum_cuda.h declares (checked by the CPU test suite).
+EXPORTED_SYMBOLS = [
+    "ts_last_error", "ts_version", "ts_ctx_create", "ts_ctx_destroy", "ts_nccl_unique_id", "ts_ctx_init_nccl",
+    "ts_ctx_stream", "ts_ctx_launch_count", "ts_batch_upload", "ts_batch_free", "ts_batch_count", "ts_batch_bytes",
+    "ts_substream", "ts_gaussian_matrix", "ts_omega_prepare", "ts_krp_sum", "ts_effective_subrank",
+    "ts_result_order", "ts_result_dims", "ts_result_ranks", "ts_result_factor", "ts_result_core",
+    "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
+    "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing",
+]
+
+
+class TucksumCudaError(RuntimeError):
+    """CUDA / NCCL / out-of-memory / unsupported-shape failures of the device path."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class TsTuckerView(C.Structure):
+    _fields_ = [
+        ("order", i64),
+        ("dims", i64p),
+        ("ranks", i64p),
+        ("factors", C.POINTER(dptr)),
+        ("num_blocks", i64),
+        ("block_offsets", i64p),
+        ("block_shapes", i64p),
+        ("block_data", C.POINTER(dptr)),
+    ]
+
+
+_lib_handle = None
+
+
+def lib():
+    """Loads libtucksum_cuda.so (raises if it was not built — no fallback)."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run paper_2603_13532_b200/build.py (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.ts_last_error.restype = C.c_char_p
+        L.ts_version.restype = C.c_char_p
+        L.ts_ctx_stream.restype = C.c_void_p
+        L.ts_ctx_stream.argtypes = [C.c_void_p]
+        L.ts_ctx_launch_count.restype = i64
+        L.ts_ctx_launch_count.argtypes = [C.c_void_p]
+        L.ts_batch_count.restype = i64
+        L.ts_batch_bytes.restype = i64
+        L.ts_batch_bytes.argtypes = [C.c_void_p]
+        L.ts_result_order.restype = i64
+        L.ts_result_order.argtypes = [C.c_void_p]
+        L.ts_result_intermediate.restype = i64
+        L.ts_result_factor_device.restype = C.c_void_p
+        L.ts_result_core_device.restype = C.c_void_p
+        L.ts_krp_sum.argtypes = [C.c_void_p, C.c_void_p, dptr, i64p, u64, u64, C.c_double, i64p,
+                                 C.POINTER(C.c_void_p)]
+        L.ts_effective_subrank.argtypes = [C.c_void_p, C.c_void_p, dptr, C.c_double, i64p, i64p, i64p, i64p]
+        L.ts_batch_upload.argtypes = [C.c_void_p, C.POINTER(TsTuckerView), i64, C.POINTER(C.c_void_p)]
+        L.ts_omega_prepare.argtypes = [C.c_void_p, i64, i64p, i64, u64, u64]
+        for name in ("ts_result_factor", "ts_result_core", "ts_result_free", "ts_result_dims", "ts_result_ranks",
+                     "ts_batch_free", "ts_ctx_destroy", "ts_ctx_set_debug", "ts_ctx_set_timing",
+                     "ts_ctx_stage_times", "ts_result_intermediate"):
+            getattr(L, name).restype = C.c_int if name not in ("ts_result_dims", "ts_result_ranks") else None
+        L.ts_result_intermediate.restype = i64
+        _lib_handle = L
+    return _lib_handle
+
+
+def _check(rc: int):
+    if rc != TS_OK:
+        msg = lib().ts_last_error().decode()
+        if rc == TS_INVALID_ARGUMENT:
+            raise ValueError(msg)
+        if rc == TS_RUNTIME:
+            raise RuntimeError(msg)
+        raise TucksumCudaError(rc, msg)
+
+
+def _f64(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(dptr)
+
+
+# ---------------------------------------------------------------------------- RNG
+@dataclass(frozen=True)
+class RngSeed:
+    """Seed plus stream index (reference include/tucksum/types.hpp:17-24)."""
+
+    seed: int = 0
+    stream: int = 0
+
+    def substream(self, salt: int) -> "RngSeed":
+        s, t = u64(), u64()
+        lib().ts_substream(u64(self.seed), u64(self.stream), u64(salt), C.byref(s), C.byref(t))
+        return RngSeed(int(s.value), int(t.value))
+
+
+def gaussian_matrix(rows: int, cols: int, seed: RngSeed) -> np.ndarray:
+    """iid N(0,1) rows×cols, column-major fill, bit-identical to the reference stream."""
+    out = np.zeros((rows, cols), dtype=np.float64, order="F")
+    _check(lib().ts_gaussian_matrix(i64(rows), i64(cols), u64(seed.seed), u64(seed.stream), _p(out)))
+    return out
+
+
+# ---------------------------------------------------------------------------- Tucker
+@dataclass
+class CoreBlock:
+    """Dense sub-core at per-mode offsets (reference include/tucksum/tucker.hpp:13-16)."""
+
+    offsets: List[int]
+    data: np.ndarray
+
+
+class TuckerTensor:
+    """Tucker tensor with a (block super-diagonal) core (reference tucker.hpp:22-48).
+
+    ``TuckerTensor(core, factors)`` builds a dense-core tensor;
+    ``TuckerTensor(ranks=..., blocks=..., factors=...)`` a block-core one.
+    Factors are column-major n_k × r_k float64 arrays; cores are Fortran-ordered
+    (first index fastest), matching the reference's DenseTensor buffer.
+    """
+
+    def __init__(self, core=None, factors=None, *, ranks=None, blocks=None):
+        if factors is None:
+            raise ValueError("TuckerTensor: one factor matrix per mode required")
+        self.factors = [_f64(f) for f in factors]
+        if blocks is None:
+            core = _f64(core)
+            self.ranks = [int(x) for x in core.shape]
+            self.blocks = [CoreBlock([0] * core.ndim, core)]
+        else:
+            self.ranks = [int(x) for x in ranks]
+            self.blocks = [CoreBlock([int(o) for o in b.offsets], _f64(b.data)) for b in blocks]
+        self.dims = [int(f.shape[0]) for f in self.factors]
+        self._validate()
+
+    def _validate(self):  # reference src/tucker.cpp:16-55
+        order = len(self.ranks)
+        if order == 0:
+            raise ValueError("TuckerTensor: order must be >= 1")
+        if len(self.factors) != order:
+            raise ValueError("TuckerTensor: one factor matrix per mode required")
+        for k in range(order):
+            if self.factors[k].ndim != 2 or self.factors[k].shape[1] != self.ranks[k]:
+                raise ValueError("TuckerTensor: factor shape must be dims[k] x ranks[k]")
+            if self.dims[k] < 1 or self.ranks[k] < 1:
+                raise ValueError("TuckerTensor: dims and ranks must be positive")
+        if not self.blocks:
+            raise ValueError("TuckerTensor: core needs at least one block")
+        cursor = [0] * order
+        for b in self.blocks:
+            if len(b.offsets) != order or b.data.ndim != order:
+                raise ValueError("TuckerTensor: block order mismatch")
+            for k in range(order):
+                if b.offsets[k] != cursor[k]:
+                    raise ValueError("TuckerTensor: blocks must tile the super-diagonal")
+                cursor[k] += b.data.shape[k]
+        if cursor != self.ranks:
+            raise ValueError("TuckerTensor: blocks must span the full rank box")
+
+    def order(self) -> int:
+        return len(self.ranks)
+
+    def has_dense_core(self) -> bool:
+        return len(self.blocks) == 1 and list(self.blocks[0].data.shape) == self.ranks
+
+    def dense_core(self) -> np.ndarray:
+        if not self.has_dense_core():
+            raise RuntimeError("TuckerTensor::dense_core: core is block-diagonal")
+        return self.blocks[0].data
+
+    def core_norm(self) -> float:
+        return float(np.sqrt(sum(float(np.sum(b.data * b.data)) for b in self.blocks)))
+
+    def max_rank(self) -> int:
+        return max(self.ranks)
+
+
+def formal_sum(xs: Sequence[TuckerTensor], weights: Sequence[float]) -> TuckerTensor:
+    """Concatenate factors, stack scaled cores on the super-diagonal (tucker.cpp:183-226)."""
+    if len(xs) == 0 or len(xs) != len(weights):
+        raise ValueError("formal_sum: need matching, nonempty summands and weights")
+    if any(x is None for x in xs):
+        raise ValueError("formal_sum: null summand")
+    dims = xs[0].dims
+    if any(x.dims != dims for x in xs):
+        raise ValueError("formal_sum: all summands must share dims")
+    order = len(dims)
+    factors = [np.concatenate([x.factors[k] for x in xs], axis=1) for k in range(order)]
+    ranks = [sum(x.ranks[k] for x in xs) for k in range(order)]
+    blocks, shift = [], [0] * order
+    for x, w in zip(xs, weights):
+        for b in x.blocks:
+            blocks.append(CoreBlock([shift[k] + b.offsets[k] for k in range(order)], b.data * float(w)))
+        shift = [shift[k] + x.ranks[k] for k in range(order)]
+    return TuckerTensor(ranks=ranks, blocks=blocks, factors=factors)
+
+
+def tucker_axby(alpha: float, x: TuckerTensor, beta: float, y: TuckerTensor) -> TuckerTensor:
+    return formal_sum([x, y], [alpha, beta])
+
+
+# ---------------------------------------------------------------------------- sketch API
+class Strategy(enum.Enum):
+    Lazy = 0
+    Eager = 1
+    Krp = 2
+    Kron = 3
+
+
+def strategy_name(s: Strategy) -> str:
+    return s.name.lower()
+
+
+def strategy_from_name(name: str) -> Strategy:
+    for s in Strategy:
+        if s.name.lower() == name:
+            return s
+    raise ValueError("unknown strategy name: " + name)
+
+
+@dataclass
+class SketchPlan:
+    """Per-mode sketch widths (reference include/tucksum/sketch.hpp:26-39)."""
+
+    strategy: Strategy = Strategy.Krp
+    effective_ranks: List[int] = field(default_factory=list)
+    oversampling: List[int] = field(default_factory=list)
+    targets: List[int] = field(default_factory=list)
+    mode_sketch_dims: List[int] = field(default_factory=list)
+    eps: float = 0.0
+    seed: RngSeed = RngSeed()
+
+    def report(self) -> str:  # reference src/sketch.cpp:203-220 (Krp fields)
+        def fld(v, i):
+            return str(v[i]) if i < len(v) else "-"
+
+        lines = [f"summation plan ({strategy_name(self.strategy)}): eps={self.eps:g}, seed=({self.seed.seed},{self.seed.stream})"]
+        for n in range(len(self.mode_sketch_dims)):
+            lines.append(f"  mode {n + 1}: effective_rank={fld(self.effective_ranks, n)} oversample="
+                         f"{fld(self.oversampling, n)} target={fld(self.targets, n)} sketch_dim={self.mode_sketch_dims[n]}")
+        return "\n".join(lines) + "\n"
+
+
+@dataclass
+class SumRequest:
+    """sum_i weights[i] * summands[i] at tolerance eps (reference sketch.hpp:43-50).
+
+    ``max_rank`` is this build's optional per-mode output-rank cap (SURVEY.md
+    §8(d)); ``None`` reproduces the reference semantics exactly.
+    """
+
+    summands: List[TuckerTensor] = field(default_factory=list)
+    weights: List[float] = field(default_factory=list)
+    eps: float = 1e-8
+    oversampling: int = 5
+    strategy: Strategy = Strategy.Lazy
+    seed: RngSeed = RngSeed()
+    max_rank: Optional[List[int]] = None
+
+
+@dataclass
+class SumStats:
+    eager_rank_trace: List[List[int]] = field(default_factory=list)
+    plan: SketchPlan = field(default_factory=SketchPlan)
+    has_plan: bool = False
+
+
+# ---------------------------------------------------------------------------- device engine
+class _Views:
+    """Marshals TuckerTensors into ts_tucker_view structs (keeps buffers alive)."""
+
+    def __init__(self, tensors: Sequence[TuckerTensor]):
+        self.keep = []
+        self.arr = (TsTuckerView * max(1, len(tensors)))()
+        for i, t in enumerate(tensors):
+            if t is None:
+                raise ValueError("sum request holds a null summand")
+            self.arr[i] = self._view(t)
+
+    def _view(self, t: TuckerTensor) -> TsTuckerView:
+        order = len(t.dims)
+        if order > MAX_ORDER:
+            raise TucksumCudaError(TS_UNSUPPORTED, "order exceeds TS_MAX_ORDER")
+        dims = np.asarray(t.dims, dtype=np.int64)
+        ranks = np.asarray(t.ranks, dtype=np.int64)
+        facs = [_f64(f) for f in t.factors]
+        fptrs = (dptr * order)(*[_p(f) for f in facs])
+        offs = np.asarray([b.offsets for b in t.blocks], dtype=np.int64).reshape(-1)
+        shps = np.asarray([list(b.data.shape) for b in t.blocks], dtype=np.int64).reshape(-1)
+        datas = [_f64(b.data) for b in t.blocks]
+        bptrs = (dptr * len(datas))(*[_p(x) for x in datas])
+        self.keep += [dims, ranks, facs, fptrs, offs, shps, datas, bptrs]
+        return TsTuckerView(order, dims.ctypes.data_as(i64p), ranks.ctypes.data_as(i64p), fptrs, len(datas),
+                            offs.ctypes.data_as(i64p), shps.ctypes.data_as(i64p), bptrs)
+
+
+class DeviceBatch:
+    """Summands resident in HBM in the stacked formal-sum layout (ts_batch)."""
+
+    def __init__(self, engine: "Engine", handle: C.c_void_p, count: int, order: int, dims):
+        self.engine, self.handle, self.count, self.order, self.dims = engine, handle, count, order, list(dims)
+
+    @property
+    def nbytes(self) -> int:
+        return int(lib().ts_batch_bytes(self.handle))
+
+    def free(self):
+        if self.handle:
+            lib().ts_batch_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class DeviceResult:
+    """A dense-core Tucker tensor in device memory (ts_result)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.handle = handle
+        L = lib()
+        order = int(L.ts_result_order(handle))
+        dims = np.zeros(order, dtype=np.int64)
+        ranks = np.zeros(order, dtype=np.int64)
+        L.ts_result_dims(handle, dims.ctypes.data_as(i64p))
+        L.ts_result_ranks(handle, ranks.ctypes.data_as(i64p))
+        self.order, self.dims, self.ranks = order, [int(x) for x in dims], [int(x) for x in ranks]
+
+    def to_tucker(self) -> TuckerTensor:
+        L = lib()
+        factors = []
+        for k in range(self.order):
+            f = np.zeros((self.dims[k], self.ranks[k]), order="F")
+            _check(L.ts_result_factor(self.handle, i64(k), _p(f)))
+            factors.append(f)
+        core = np.zeros(tuple(self.ranks), order="F")
+        _check(L.ts_result_core(self.handle, _p(core)))
+        return TuckerTensor(core, factors)
+
+    def intermediates(self) -> dict:
+        """Stage intermediates captured in debug mode: omega, y, uhat (per mode) and h."""
+        L = lib()
+        out = {}
+        rows, cols = i64(), i64()
+        for name, which in (("omega", 0), ("y", 1), ("uhat", 2)):
+            mats = []
+            for k in range(self.order):
+                n = L.ts_result_intermediate(self.handle, C.c_int(which), i64(k), None, C.byref(rows), C.byref(cols))
+                m = np.zeros((rows.value, cols.value), order="F")
+                if n > 0:
+                    L.ts_result_intermediate(self.handle, C.c_int(which), i64(k), _p(m), None, None)
+                mats.append(m)
+            out[name] = mats
+        n = L.ts_result_intermediate(self.handle, C.c_int(3), i64(0), None, C.byref(rows), C.byref(cols))
+        h = np.zeros(max(n, 0))
+        if n > 0:
+            L.ts_result_intermediate(self.handle, C.c_int(3), i64(0), _p(h), None, None)
+        qd = tuple(m.shape[1] for m in out["uhat"])
+        out["h"] = h.reshape(qd, order="F") if n > 0 else h
+        return out
+
+    def free(self):
+        if self.handle:
+            lib().ts_result_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Engine:
+    """One CUDA device context (stream, scratch pool, Ω cache, optional NCCL comm)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        _check(lib().ts_ctx_create(C.c_int(device), C.byref(h)))
+        self.handle = h
+
+    # -- multi-GPU
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().ts_nccl_unique_id(buf))
+        return buf.raw
+
+    def init_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(unique_id, 128)
+        _check(lib().ts_ctx_init_nccl(self.handle, buf, C.c_int(nranks), C.c_int(rank)))
+
+    @property
+    def stream(self) -> int:
+        return int(lib().ts_ctx_stream(self.handle) or 0)
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().ts_ctx_launch_count(self.handle))
+
+    def set_debug(self, on: bool):
+        _check(lib().ts_ctx_set_debug(self.handle, C.c_int(1 if on else 0)))
+
+    def set_timing(self, on: bool):
+        _check(lib().ts_ctx_set_timing(self.handle, C.c_int(1 if on else 0)))
+
+    def stage_times(self) -> List[float]:
+        buf = (C.c_double * 16)()
+        n = lib().ts_ctx_stage_times(self.handle, buf, C.c_int(16))
+        return [buf[i] for i in range(n)]
+
+    # -- data
+    def upload(self, summands: Sequence[TuckerTensor]) -> DeviceBatch:
+        if len(summands) == 0:
+            raise ValueError("sum request needs matching, nonempty summands and weights")
+        views = _Views(summands)
+        h = C.c_void_p()
+        _check(lib().ts_batch_upload(self.handle, views.arr, i64(len(summands)), C.byref(h)))
+        return DeviceBatch(self, h, len(summands), len(summands[0].dims), summands[0].dims)
+
+    def upload_views(self, views: "C.Array", count: int, order: int, dims) -> DeviceBatch:
+        h = C.c_void_p()
+        _check(lib().ts_batch_upload(self.handle, views, i64(count), C.byref(h)))
+        return DeviceBatch(self, h, count, order, dims)
+
+    def prepare_omega(self, dims, width: int, seed: RngSeed):
+        d = np.asarray(dims, dtype=np.int64)
+        _check(lib().ts_omega_prepare(self.handle, i64(len(d)), d.ctypes.data_as(i64p), i64(width), u64(seed.seed),
+                                      u64(seed.stream)))
+
+    def krp_sum(self, batch: DeviceBatch, weights, widths, seed: RngSeed, eps: float,
+                max_rank=None) -> DeviceResult:
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        if len(w) != batch.count:
+            raise ValueError("sum request needs matching, nonempty summands and weights")
+        wd = np.ascontiguousarray(np.asarray(widths, dtype=np.int64))
+        if len(wd) != batch.order:
+            raise ValueError("plan order does not match summand order")
+        cap = None if max_rank is None else np.ascontiguousarray(np.asarray(max_rank, dtype=np.int64))
+        h = C.c_void_p()
+        _check(lib().ts_krp_sum(self.handle, batch.handle, _p(w), wd.ctypes.data_as(i64p), u64(seed.seed),
+                                u64(seed.stream), C.c_double(eps),
+                                cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
+        return DeviceResult(h)
+
+    def effective_subrank(self, batch: DeviceBatch, weights, eps: float, oversampling):
+        order = batch.order
+        ov = np.asarray(oversampling if np.ndim(oversampling) else [oversampling] * order, dtype=np.int64)
+        if len(ov) != order:
+            raise ValueError("oversampling vector must have one entry per mode")
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        eff, tg, wd = (np.zeros(order, dtype=np.int64) for _ in range(3))
+        _check(lib().ts_effective_subrank(self.handle, batch.handle, _p(w), C.c_double(eps), ov.ctypes.data_as(i64p),
+                                          eff.ctypes.data_as(i64p), tg.ctypes.data_as(i64p), wd.ctypes.data_as(i64p)))
+        return [int(x) for x in eff], [int(x) for x in tg], [int(x) for x in wd]
+
+    def close(self):
+        if self.handle:
+            lib().ts_ctx_destroy(self.handle)
+            self.handle = None
+
+
+_default_engine: Optional[Engine] = None
+
+
+def default_engine() -> Engine:
+    global _default_engine
+    if _default_engine is None:
+        _default_engine = Engine(int(os.environ.get("TUCKSUM_DEVICE", "0")))
+    return _default_engine
+
+
+# ---------------------------------------------------------------------------- reference entry points
+def _validate_request(summands, weights):  # reference src/sketch.cpp:16-30
+    if len(summands) == 0 or len(summands) != len(weights):
+        raise ValueError("sum request needs matching, nonempty summands and weights")
+    if any(x is None for x in summands):
+        raise ValueError("sum request holds a null summand")
+    dims = summands[0].dims
+    if any(x.dims != dims for x in summands):
+        raise ValueError("sum request summands must share dims")
+
+
+def effective_subrank(summands, weights, eps, oversampling, strategy=Strategy.Krp, seed=RngSeed(),
+                      engine: Optional[Engine] = None) -> SketchPlan:
+    """Plan stage for Strategy.Krp (reference src/sketch.cpp:272-358), on the GPU."""
+    _validate_request(summands, weights)
+    if eps < 0:
+        raise ValueError("tolerance must be nonnegative")
+    order = len(summands[0].dims)
+    ov = list(oversampling) if np.ndim(oversampling) else [int(oversampling)] * order
+    if len(ov) != order:
+        raise ValueError("oversampling vector must have one entry per mode")
+    if any(p < 0 for p in ov):
+        raise ValueError("oversampling must be nonnegative")
+    if strategy != Strategy.Krp:
+        raise NotImplementedError("only Strategy.Krp plans are on the B200 hot path")
+    eng = engine or default_engine()
+    batch = eng.upload(summands)
+    try:
+        eff, tg, wd = eng.effective_subrank(batch, weights, eps, ov)
+    finally:
+        batch.free()
+    return SketchPlan(Strategy.Krp, eff, ov, tg, wd, eps, seed)
+
+
+def krp_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[SumStats] = None,
+            engine: Optional[Engine] = None) -> TuckerTensor:
+    """KRP sketched summation (reference src/sketch.cpp:66-181 via krp_sum, :360-362)."""
+    _validate_request(req.summands, req.weights)
+    if req.eps < 0:
+        raise ValueError("tolerance must be nonnegative")
+    order = len(req.summands[0].dims)
+    if order < 2:
+        raise ValueError("sketched summation needs order >= 2")
+    eng = engine or default_engine()
+    batch = eng.upload(req.summands)
+    try:
+        if plan is None:
+            ov = [int(req.oversampling)] * order
+            if any(p < 0 for p in ov):
+                raise ValueError("oversampling must be nonnegative")
+            eff, tg, wd = eng.effective_subrank(batch, req.weights, req.eps, ov)
+            plan = SketchPlan(Strategy.Krp, eff, ov, tg, wd, req.eps, req.seed)
+        if len(plan.mode_sketch_dims) != order:
+            raise ValueError("plan order does not match summand order")
+        if any(s < 1 for s in plan.mode_sketch_dims):
+            raise ValueError("plan sketch widths must be positive")
+        res = eng.krp_sum(batch, req.weights, plan.mode_sketch_dims, req.seed, req.eps, req.max_rank)
+        out = res.to_tucker()
+        res.free()
+    finally:
+        batch.free()
+    if stats is not None:
+        stats.plan = plan
+        stats.has_plan = True
+    return out
+
+
+def round_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[SumStats] = None,
+              engine: Optional[Engine] = None) -> TuckerTensor:
+    """Strategy dispatcher (reference src/sketch.cpp:368-376); only Krp is on the B200 path."""
+    if req.strategy == Strategy.Krp:
+        return krp_sum(req, plan, stats, engine)
+    _validate_request(req.summands, req.weights)
+    raise NotImplementedError(f"strategy {strategy_name(req.strategy)} is outside the B200 hot path (SURVEY.md §8)")

@@ -1,0 +1,279 @@
+"""Parity of the sm_100a CUDA path (through the C ABI) with the CPU oracle.
+
+Tolerances (BASELINE.json north_star): the returned factors × core within 1e-10
+relative Frobenius error of the oracle's on identical inputs and identical Ω,
+and the same approximation error to the exact sum to 3 significant digits.
+Factors are never compared directly (SVD sign / rank-deficient QR freedom,
+SURVEY.md §8(c)); reconstructions are compared through the reference's
+orthogonalized-difference norm (tucker_rel_error, src/tucker.cpp:298-303).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import (cancellation_instance, dense_rel_error, dense_weighted_sum, random_tucker, shared_subspace,
+                     sub)
+from paper_2603_13532_b200 import tucksum as T
+from paper_2603_13532_b200.workloads import make_workload
+
+pytestmark = pytest.mark.gpu
+
+PARITY = 1e-10  # relative Frobenius error of factors × core vs the oracle
+
+
+def gpu_sum(engine, xs, ws, widths, seed, eps, cap=None, debug=False):
+    engine.set_debug(debug)
+    batch = engine.upload(xs)
+    try:
+        res = engine.krp_sum(batch, ws, widths, T.RngSeed(*seed), eps, cap)
+        out = res.to_tucker()
+        inter = res.intermediates() if debug else None
+        res.free()
+    finally:
+        batch.free()
+        engine.set_debug(False)
+    return out, inter
+
+
+def rel_diff(a, b):
+    return O.rel_error_to_sum(a, [b], [1.0])
+
+
+def check_pair(engine, xs, ws, widths, seed, eps, cap=None, err_digits=True, gram=False):
+    ref, _ = O.krp_sum(xs, ws, widths, seed, eps, cap=cap, threads=8)
+    out, _ = gpu_sum(engine, xs, ws, widths, seed, eps, cap)
+    assert out.ranks == ref.ranks
+    assert rel_diff(out, ref) <= PARITY
+    if err_digits:
+        if gram:
+            e_gpu, e_ref = O.rel_error_gram(out, xs, ws, 8), O.rel_error_gram(ref, xs, ws, 8)
+        else:
+            e_gpu, e_ref = O.rel_error_to_sum(out, xs, ws), O.rel_error_to_sum(ref, xs, ws)
+        assert abs(e_gpu - e_ref) <= 5e-4 * max(e_ref, 1e-300) or abs(e_gpu - e_ref) <= 1e-13
+    return out, ref
+
+
+# ------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_baseline_config_parity(engine, cfg):
+    wl = make_workload(cfg)
+    check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), wl.eps, wl.cap)
+
+
+def test_baseline_cfg4_parity(engine):
+    wl = make_workload(4)
+    check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), wl.eps, wl.cap, gram=True)
+
+
+def test_baseline_cfg5_reduced_parity(engine):
+    """Config 5 shapes (n = 8192, r = 32, s = 64, cap 48) at K = 16 summands."""
+    wl = make_workload(5, K=16)
+    check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), wl.eps, wl.cap, gram=True)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_reference_semantics_eps(engine, cfg):
+    """Pure reference semantics (eps > 0, no rank cap) on the same inputs."""
+    wl = make_workload(cfg)
+    check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), 1e-6, None)
+
+
+def test_stage_intermediates_cfg1(engine):
+    """Ω bitwise; Y, Û, h against the oracle's intermediates."""
+    wl = make_workload(1)
+    seed = (wl.seed.seed, wl.seed.stream)
+    ref, info = O.krp_sum(wl.summands, wl.weights, wl.widths, seed, 0.0, cap=wl.cap, intermediates=True)
+    _, inter = gpu_sum(engine, wl.summands, wl.weights, wl.widths, seed, 0.0, wl.cap, debug=True)
+    for n in range(3):
+        assert np.array_equal(inter["omega"][n], info["omega"][n])
+        y, yr = inter["y"][n], info["y"][n]
+        assert np.linalg.norm(y - yr) <= 1e-13 * np.linalg.norm(yr)
+        u, ur = inter["uhat"][n], info["uhat"][n]
+        assert np.linalg.norm(u - ur) <= 1e-11
+    assert np.linalg.norm(inter["h"] - info["h"]) <= 1e-11 * np.linalg.norm(info["h"])
+
+
+# ------------------------------------------------------------ reference test assertions through the C ABI
+def test_opposite_summands_annihilate(engine):
+    """test_sketch_sum.cpp:186-198."""
+    x = random_tucker([12, 10, 8], [3, 4, 2], (21, 3))
+    req = T.SumRequest([x, x], [1.0, -1.0], 1e-6, 5, T.Strategy.Krp, T.RngSeed(21, 4))
+    out = T.krp_sum(req, engine=engine)
+    assert O.tucker_norm(out) <= 1e-12 * O.tucker_norm(x)
+
+
+def test_single_summand_passes_through(engine):
+    """test_sketch_sum.cpp:200-219."""
+    x = random_tucker([15, 12, 18], [4, 3, 5], (31, 0))
+    ref = O.reconstruct(x)
+    req = T.SumRequest([x], [1.0], 1e-10, 2, T.Strategy.Krp, T.RngSeed(31, 1))
+    out = T.krp_sum(req, engine=engine)
+    assert out.dims == x.dims
+    assert O.rel_error_to_sum(out, [x], [1.0]) <= 1e-10
+    assert dense_rel_error(out, ref) <= 1e-10
+
+
+def test_shared_subspace_recovers_latent_ranks(engine):
+    """test_sketch_sum.cpp:221-264."""
+    seed = (51, 0)
+    xs = shared_subspace(60, 4, 10, 20, seed)
+    ws = [1.0] * 20
+    ref = dense_weighted_sum(xs, ws)
+    req = T.SumRequest(xs, ws, 1e-6, 2, T.Strategy.Krp, T.RngSeed(*sub(seed, 77)))
+    stats = T.SumStats()
+    out = T.krp_sum(req, None, stats, engine=engine)
+    assert out.ranks == [10] * 4
+    assert dense_rel_error(out, ref) <= 1e-10
+    assert stats.has_plan
+    assert stats.plan.effective_ranks == [10] * 4
+    assert stats.plan.mode_sketch_dims == [12] * 4
+
+
+def test_random_sums_match_dense_oracle_and_cpu_oracle(engine):
+    """test_sketch_sum.cpp:266-299 (KRP) + parity with the CPU oracle, plans included."""
+    rng = np.random.Generator(np.random.MT19937(907))
+    dims = [14, 11, 9]
+    for trial in range(20):
+        xs, ws = [], []
+        for i in range(5):
+            ranks = [int(x) for x in rng.integers(1, 4, size=3)]
+            xs.append(random_tucker(dims, ranks, (1000 + trial, i)))
+            ws.append((1.0 if rng.integers(0, 2) == 0 else -1.0) * rng.uniform(0.5, 2.0))
+        ref = dense_weighted_sum(xs, ws)
+        req = T.SumRequest(xs, ws, 1e-6, 5, T.Strategy.Krp, T.RngSeed(42, trial))
+        stats = T.SumStats()
+        out = T.round_sum(req, None, stats, engine=engine)
+        assert dense_rel_error(out, ref) <= 1e-6
+        eff, tg, wd = O.effective_subrank_krp(xs, ws, 1e-6, 5)
+        assert stats.plan.effective_ranks == eff and stats.plan.mode_sketch_dims == wd
+        oref, _ = O.krp_sum(xs, ws, wd, (42, trial), 1e-6)
+        assert out.ranks == oref.ranks
+        assert rel_diff(out, oref) <= PARITY
+
+
+def test_shared_subspaces_across_seeds(engine):
+    """test_sketch_sum.cpp:301-347."""
+    rng = np.random.Generator(np.random.MT19937(1310))
+    dims = [18, 15, 12]
+    for trial in range(20):
+        seed = (2000 + trial, 0)
+        xs = shared_subspace(dims, 3, 4, 8, seed, rank=2, core_salt=True)
+        ws = list(rng.uniform(0.5, 1.5, size=8))
+        ref = dense_weighted_sum(xs, ws)
+        req = T.SumRequest(xs, ws, 1e-8, 2, T.Strategy.Krp, T.RngSeed(*sub(seed, 9000)))
+        stats = T.SumStats()
+        out = T.krp_sum(req, None, stats, engine=engine)
+        assert out.ranks == [4, 4, 4]
+        assert dense_rel_error(out, ref) <= 1e-8
+        assert stats.plan.effective_ranks == [4, 4, 4]
+
+
+def test_paired_cancellation_keeps_quiet_components(engine):
+    """test_sketch_sum.cpp:560-598 (block cores: every summand is a 2-block formal sum)."""
+    xs, ws, target = cancellation_instance(40, 10, (107, 0))
+    ref = O.reconstruct(target)
+    req = T.SumRequest(xs, ws, 1e-6, 2, T.Strategy.Krp, T.RngSeed(107, 1))
+    out = T.round_sum(req, engine=engine)
+    assert dense_rel_error(out, ref) <= 1e-9
+    eff, tg, wd = O.effective_subrank_krp(xs, ws, 1e-6, 2)
+    oref, _ = O.krp_sum(xs, ws, wd, (107, 1), 1e-6)
+    assert rel_diff(out, oref) <= PARITY
+
+
+def test_malformed_requests_rejected(engine):
+    """test_sketch_sum.cpp:514-547."""
+    a = random_tucker([8, 7, 6], [2, 2, 2], (91, 0))
+    b = random_tucker([8, 7, 5], [2, 2, 2], (91, 1))
+    one_d = random_tucker([9], [2], (91, 2))
+    with pytest.raises(ValueError):
+        T.krp_sum(T.SumRequest([a, b], [1.0, 1.0], strategy=T.Strategy.Krp), engine=engine)
+    with pytest.raises(ValueError):
+        T.round_sum(T.SumRequest([], []), engine=engine)
+    with pytest.raises(ValueError):
+        T.round_sum(T.SumRequest([a], [1.0, 2.0], strategy=T.Strategy.Krp), engine=engine)
+    with pytest.raises(ValueError):
+        T.round_sum(T.SumRequest([a, None], [1.0, 1.0], strategy=T.Strategy.Krp), engine=engine)
+    with pytest.raises(ValueError):
+        T.krp_sum(T.SumRequest([one_d], [1.0], strategy=T.Strategy.Krp), engine=engine)
+    with pytest.raises(ValueError):
+        T.krp_sum(T.SumRequest([a], [1.0], eps=-1.0, strategy=T.Strategy.Krp), engine=engine)
+    with pytest.raises(ValueError):
+        T.effective_subrank([a], [1.0], 1e-6, [1, 1], T.Strategy.Krp, engine=engine)
+    with pytest.raises(ValueError):
+        T.effective_subrank([a], [1.0], 1e-6, -1, T.Strategy.Krp, engine=engine)
+    # C-ABI level: mismatched batch / weights / widths.
+    batch = engine.upload([a])
+    with pytest.raises(ValueError):
+        engine.krp_sum(batch, [1.0, 2.0], [3, 3, 3], T.RngSeed(1, 1), 1e-8)
+    with pytest.raises(ValueError):
+        engine.krp_sum(batch, [1.0], [3, 0, 3], T.RngSeed(1, 1), 1e-8)
+    with pytest.raises(ValueError):
+        engine.krp_sum(batch, [1.0], [3, 3], T.RngSeed(1, 1), 1e-8)
+    batch.free()
+
+
+def test_dispatcher_bitwise_equals_entry_point(engine):
+    """test_sketch_sum.cpp:473-491 (Krp) and same-seed bitwise determinism
+    (test_ndg_transport.cpp:618-626)."""
+    xs = [random_tucker([10, 9, 8], [2, 3, 2], (81, i)) for i in range(3)]
+    req = T.SumRequest(xs, [1.0, -0.5, 2.0], 1e-8, 3, T.Strategy.Krp, T.RngSeed(81, 9))
+    a = T.round_sum(req, engine=engine)
+    b = T.krp_sum(req, engine=engine)
+    assert a.ranks == b.ranks
+    for fa, fb in zip(a.factors, b.factors):
+        assert np.array_equal(fa, fb)
+    assert np.array_equal(a.dense_core(), b.dense_core())
+
+
+def test_plan_matches_oracle_plan(engine):
+    """Device effective_subrank == oracle effective_subrank on skewed random instances
+    (test_sketch_sum.cpp:372-404 style)."""
+    rng = np.random.Generator(np.random.MT19937(4242))
+    for it in range(30):
+        order = 2 + it % 3
+        dims = [2 + int(rng.integers(0, 23)) for _ in range(order)]
+        count = 1 + int(rng.integers(0, 5))
+        xs, ws = [], []
+        for i in range(count):
+            ranks = [1 + int(rng.integers(0, min(dims[k], 4))) for k in range(order)]
+            xs.append(random_tucker(dims, ranks, (7000 + it, i)))
+            ws.append(float(int(rng.integers(0, 5)) - 2.0))
+        if all(w == 0 for w in ws):
+            ws[0] = 1.0
+        eps = 1e-4 if it % 2 == 0 else 1e-8
+        p = (it % 3) * 2
+        eff, tg, wd = O.effective_subrank_krp(xs, ws, eps, p)
+        plan = T.effective_subrank(xs, ws, eps, p, T.Strategy.Krp, engine=engine)
+        assert plan.effective_ranks == eff and plan.targets == tg and plan.mode_sketch_dims == wd
+
+
+def test_general_orders_and_block_cores(engine):
+    """d = 2 and d = 5, mixed ranks, block-core summands, n < s."""
+    cases = [([30, 25], [4, 3], 5, 9), ([7, 6, 5, 4, 6], [2, 2, 1, 2, 2], 3, 8), ([9, 40, 11], [3, 5, 2], 4, 12)]
+    for t, (dims, r, K, s) in enumerate(cases):
+        xs = [random_tucker(dims, r, (800 + t, i)) for i in range(K)]
+        xs.append(T.tucker_axby(0.5, xs[0], -1.5, xs[1]))
+        ws = [1.0, -0.75, 0.5, 2.0, 1.25, 0.3][:len(xs)]
+        check_pair(engine, xs, ws, [s] * len(dims), (800 + t, 5), 1e-9, None)
+
+
+# ------------------------------------------------------------ full-size config 5 properties
+def test_cfg5_full_properties(engine):
+    """K = 256 at n = 8192: linearity in the weights, bitwise determinism, orthonormal factors."""
+    wl = make_workload(5)
+    seed = wl.seed
+    batch = engine.upload(wl.summands)
+    try:
+        r1 = engine.krp_sum(batch, wl.weights, wl.widths, seed, 0.0, wl.cap).to_tucker()
+        r2 = engine.krp_sum(batch, wl.weights, wl.widths, seed, 0.0, wl.cap).to_tucker()
+        r3 = engine.krp_sum(batch, 2.0 * wl.weights, wl.widths, seed, 0.0, wl.cap).to_tucker()
+    finally:
+        batch.free()
+    assert r1.ranks == [48, 48, 48]
+    for a, b in zip(r1.factors, r2.factors):
+        assert np.array_equal(a, b)
+    assert np.array_equal(r1.dense_core(), r2.dense_core())
+    for f in r1.factors:
+        assert np.linalg.norm(f.T @ f - np.eye(f.shape[1])) <= 1e-12
+    # 2·sum → 2·result (sketch, QR and truncation are scale-equivariant).
+    assert O.rel_error_to_sum(r3, [r1], [2.0]) <= 1e-12
