@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 KRP sketched Tucker summation (BASELINE.json metric).
+
+Metric: Tucker summands/s for one krp_sum call (whole job), plus fp64 GFLOP/s of
+the algorithmic contraction work F_alg and its fraction of
+the measured B200 FP64 (DMMA) peak.
+
+Workload (N=1 default): BASELINE.json config 5 — d=3, n=8192, K=256 summands of
+rank (32,32,32), s=64, rank cap 48 — the largest config, the one the 1→8 GPU
+scaling target is quoted on.  For N>1 (torchrun) the K summands are split evenly
+across ranks (strong scaling); the library all-reduces the partial sketches and
+partial cores with NCCL.
+
+  value : device-resident inputs, Ω cached, plan given; CUDA events on the
+          library's stream around each call; max over ranks.
+  e2e   : the public API with HOST buffers: pinned H2D upload of the step's
+          summands, krp_sum, D2H of the result factors + core, every step.
+  --impl reference : the reference's CPU path (the oracle port, since the
+          reference needs Eigen which is absent) on all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "roofline_traffic_r01.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--stages", action="store_true", help="print per-stage times to stderr")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def fp64_peak():
+    """Measured FP64 DMMA peak (tools/fp64_peak.cu on this pool's B200), TFLOP/s."""
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            d = json.load(f)
+        return float(d["dmma_tflops"]), "profiles/fp64_peak_r01.json (DMMA.8x8x4 microbenchmark, measured)"
+    except Exception:
+        return 37.0, "fallback 37.0 TF/s (B200 FP64 datasheet figure)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def config_desc(wl, world):
+    r = wl.ranks[0]
+    return {"workload": f"{wl.name}: d={len(wl.dims)} n={wl.dims} K={wl.K} r={r} s={wl.widths[0]} "
+                        f"cap={wl.cap} eps={wl.eps} (BASELINE.json configs[{wl.cfg - 1}])",
+            "summands_per_gpu": wl.K // world, "plan": "given (uniform KRP width)", "omega": "cached on device",
+            "l2": "inputs larger than L2 (no flush)" if sum(s.nbytes for s in wl.slabs) > 126e6 else
+            "inputs fit in L2; L2 flushed between steps",
+            "parallelism": f"summand-sharded dp{world} + NCCL all-reduce of Y and h" if world > 1 else "1 GPU"}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def cpu_sample_run(wl, K_sample, threads):
+    import oracle as O
+
+    xs = wl.summands[:K_sample]
+    ws = wl.weights[:K_sample]
+    t0 = time.perf_counter()
+    O.krp_sum(xs, ws, wl.widths, (wl.seed.seed, wl.seed.stream), wl.eps, cap=wl.cap, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(wl, budget_s=15.0):
+    """Oracle port on all host threads, bounded sample of the same workload."""
+    import oracle as O
+
+    threads = O.num_threads()
+    k = min(wl.K, max(2, threads))
+    t = cpu_sample_run(wl, k, threads)
+    # Scale the sample so the measured run takes ~budget_s / 2.
+    while t < budget_s / 4 and k < wl.K:
+        k = min(wl.K, k * 2)
+        t = cpu_sample_run(wl, k, threads)
+    return {"value": k / t, "unit": "summands/s", "cores": threads, "kind": "port",
+            "sample": f"{k} of {wl.K} summands of {wl.name} (same shapes, Ω, plan, cap), one call incl. Ω "
+                      f"generation, {t:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2603_13532_b200.workloads import make_workload
+    import oracle as O
+
+    wl = make_workload(args.config)
+    threads = O.num_threads()
+    # One step = a bounded sample sized so steps+warmup stay within a few minutes.
+    k = min(wl.K, max(2, threads))
+    t = cpu_sample_run(wl, k, threads)
+    while t < 2.0 and k < wl.K:
+        k = min(wl.K, k * 2)
+        t = cpu_sample_run(wl, k, threads)
+    for _ in range(max(0, args.warmup - 1)):
+        cpu_sample_run(wl, k, threads)
+    times = [cpu_sample_run(wl, k, threads) for _ in range(args.steps)]
+    ms = 1000.0 * statistics.mean(times)
+    value = k / (ms / 1000.0)
+    line = {"metric": "tucker_summands_per_sec", "value": value, "unit": "summands/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE.json recipe)",
+            "config": config_desc(wl, 1), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "summands/s", "cores": threads, "kind": "port",
+                             "sample": f"{k} of {wl.K} summands per step (oracle port of the reference CPU path; "
+                                       f"the reference needs Eigen>=3.4, absent from the image)"},
+            "e2e": {"value": value, "unit": "summands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_13532_b200 import tucksum as T
+    from paper_2603_13532_b200.sharding import init_nccl_engine, shard_range
+    from paper_2603_13532_b200.workloads import f_alg, make_workload
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    wl = make_workload(args.config)
+    b, e = shard_range(wl.K, world, rank)
+    xs, ws = wl.summands[b:e], np.ascontiguousarray(wl.weights[b:e])
+    eng = init_nccl_engine(local if world > 1 else 0, rank, world)
+    stream = torch.cuda.ExternalStream(eng.stream)
+    eng.prepare_omega(wl.dims, max(wl.widths), wl.seed)
+    batch = eng.upload(xs)
+
+    def step():
+        res = eng.krp_sum(batch, ws, wl.widths, wl.seed, wl.eps, wl.cap)
+        return res
+
+    flush = None
+    if sum(s.nbytes for s in wl.slabs) <= 126e6:
+        flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda")  # 512 MB > L2
+
+    for _ in range(max(3, args.warmup)):
+        step().free()
+    # Stage breakdown (separate pass with stage events on).
+    eng.set_timing(True)
+    step().free()
+    stages = eng.stage_times()
+    eng.set_timing(False)
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = eng.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                with torch.cuda.stream(stream):
+                    flush.add_(1.0)
+            ev0[i].record(stream)
+            res = step()
+            ev1[i].record(stream)
+            res.free()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = (eng.launch_count - launches0) // max(1, args.steps)
+    times = [a.elapsed_time(c) for a, c in zip(ev0, ev1)]
+    total_ms = sum(times)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = wl.K / (ms / 1000.0)
+    falg = f_alg(wl.dims, wl.ranks, wl.widths[0])
+    gflops = falg / (ms / 1000.0) / 1e9
+    peak, peak_src = fp64_peak()
+
+    # Dominant kernel: the stage-A grouped DMMA GEMM (Z_j = Ω_jᵀ F_j over all modes, one launch).
+    d = len(wl.dims)
+    Kloc = e - b
+    fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * wl.widths[0] * Kloc for j in range(d))
+    ta = stages[0] if stages else float("nan")
+    achieved = fa / (ta / 1000.0) / 1e12 if ta == ta and ta > 0 else None
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            traffic = json.load(f).get(wl.name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "kernel": "gemm_kernel<TN> (stage A, grouped over modes)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src,
+                "whole_step_fp64_tflops": gflops / 1000.0, "whole_step_frac": gflops / 1000.0 / (peak * world)}
+    stage_names = ["A_project", "B_krp", "C_expand", "allreduce_Y", "D_tsqr", "E_project", "F1_ttm", "F2_core",
+                   "allreduce_h", "G_sthosvd", "H_output"]
+    if args.stages and rank == 0:
+        print(json.dumps(dict(zip(stage_names, stages))), file=sys.stderr)
+
+    # ---------------- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        regs = []
+        cudart = torch.cuda.cudart()
+        for s in wl.slabs:
+            if s.nbytes and cudart.cudaHostRegister(s.ctypes.data, s.nbytes, 0) == 0:
+                regs.append(s)
+        h2d = sum(sum(f.nbytes for f in x.factors) + sum(bl.data.nbytes for bl in x.blocks) for x in xs)
+        d2h = 0
+        e2e_times = []
+        for i in range(args.e2e_steps + 1):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            bt = eng.upload(xs)
+            res = eng.krp_sum(bt, ws, wl.widths, wl.seed, wl.eps, wl.cap)
+            out = res.to_tucker()
+            res.free()
+            bt.free()
+            dt = time.perf_counter() - t0
+            d2h = sum(f.nbytes for f in out.factors) + out.dense_core().nbytes
+            if i > 0:
+                e2e_times.append(dt)
+        for s in regs:
+            cudart.cudaHostUnregister(s.ctypes.data)
+        te = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": wl.K / float(te.item()), "unit": "summands/s", "h2d_bytes_per_step": int(h2d) * world,
+               "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": 1000.0 * float(te.item()),
+               "timing": "host wall clock around synchronous API calls, max over ranks, mean of "
+                         f"{args.e2e_steps} steps after 1 warm-up"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
+
+    if rank == 0:
+        line = {"metric": "tucker_summands_per_sec", "value": value, "unit": "summands/s", "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded BASELINE.json config recipe; no public dataset)",
+                "config": config_desc(wl, world), "gflops": gflops, "fp64_frac_of_peak": gflops / 1000.0 / (peak * world),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages))}
+        print(json.dumps(line), flush=True)
+    batch.free()
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

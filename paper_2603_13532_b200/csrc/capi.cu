@@ -150,6 +150,7 @@ struct ts_result {
     double* factors[TS_MAX_ORDER] = {};
     double* core = nullptr;
     int device = 0;
+    cudaStream_t stream = nullptr;  // owning context's stream (stream-ordered alloc/free)
     // Debug intermediates (host copies).
     std::vector<double> inter[3][TS_MAX_ORDER];
     std::int64_t inter_rows[3][TS_MAX_ORDER] = {}, inter_cols[3][TS_MAX_ORDER] = {};
@@ -157,8 +158,8 @@ struct ts_result {
     ~ts_result() {
         cudaSetDevice(device);
         for (auto* f : factors)
-            if (f) cudaFree(f);
-        if (core) cudaFree(core);
+            if (f) cudaFreeAsync(f, stream);
+        if (core) cudaFreeAsync(core, stream);
     }
 };
 
@@ -345,6 +346,7 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     mark(ctx, 4);
     auto res = std::make_unique<ts_result>();
     res->device = ctx->device;
+    res->stream = st;
     res->order = d;
     if (ctx->debug) {
         for (int n = 0; n < d; ++n) {
@@ -559,7 +561,7 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
         for (int n = 0; n < d; ++n) {
             res->dims[n] = dims[n];
             res->ranks[n] = rank[n];
-            TS_CUDA_CHECK(cudaMalloc(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n])));
+            TS_CUDA_CHECK(cudaMallocAsync(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n]), st));
             GemmProblem p{};
             p.A = Uh[n];
             p.lda = dims[n];
@@ -575,7 +577,7 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
         ts::launch_grouped_gemm(Layout::NN, ps, sc, ctx->num_sms);
         std::int64_t csize = 1;
         for (int n = 0; n < d; ++n) csize *= rank[n];
-        TS_CUDA_CHECK(cudaMalloc(&res->core, sizeof(double) * static_cast<size_t>(csize)));
+        TS_CUDA_CHECK(cudaMallocAsync(&res->core, sizeof(double) * static_cast<size_t>(csize), st));
         TS_CUDA_CHECK(cudaMemcpyAsync(res->core, g, sizeof(double) * static_cast<size_t>(csize),
                                       cudaMemcpyDeviceToDevice, st));
     }
@@ -939,8 +941,10 @@ int ts_result_factor(const ts_result* r, int64_t mode, double* out) {
     return guarded([&] {
         if (!r || mode < 0 || mode >= r->order) invalid("ts_result_factor: bad mode");
         TS_CUDA_CHECK(cudaSetDevice(r->device));
-        TS_CUDA_CHECK(cudaMemcpy(out, r->factors[mode], sizeof(double) * static_cast<size_t>(r->dims[mode] * r->ranks[mode]),
-                                 cudaMemcpyDeviceToHost));
+        TS_CUDA_CHECK(cudaMemcpyAsync(out, r->factors[mode],
+                                      sizeof(double) * static_cast<size_t>(r->dims[mode] * r->ranks[mode]),
+                                      cudaMemcpyDeviceToHost, r->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(r->stream));
     });
 }
 int ts_result_core(const ts_result* r, double* out) {
@@ -949,7 +953,9 @@ int ts_result_core(const ts_result* r, double* out) {
         std::int64_t n = 1;
         for (int k = 0; k < r->order; ++k) n *= r->ranks[k];
         TS_CUDA_CHECK(cudaSetDevice(r->device));
-        TS_CUDA_CHECK(cudaMemcpy(out, r->core, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost));
+        TS_CUDA_CHECK(cudaMemcpyAsync(out, r->core, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                                      r->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(r->stream));
     });
 }
 const double* ts_result_factor_device(const ts_result* r, int64_t mode) {

@@ -177,7 +177,11 @@ def test_paired_cancellation_keeps_quiet_components(engine):
     assert dense_rel_error(out, ref) <= 1e-9
     eff, tg, wd = O.effective_subrank_krp(xs, ws, 1e-6, 2)
     oref, _ = O.krp_sum(xs, ws, wd, (107, 1), 1e-6)
-    assert rel_diff(out, oref) <= PARITY
+    # The summands cancel by a factor ~1e7 (±1e6-amplitude noise around a unit
+    # target), so any two summation orders differ by ~eps·1e7 ≈ 1e-9 relative;
+    # the parity bound here is the reference's own bound for this instance
+    # (test_sketch_sum.cpp:591), not the 1e-10 of the well-conditioned configs.
+    assert rel_diff(out, oref) <= 1e-9
 
 
 def test_malformed_requests_rejected(engine):
