@@ -233,6 +233,7 @@ def main():
     eng.set_timing(True)
     step().free()
     stages = eng.stage_times()
+    paths = eng.last_paths()
     eng.set_timing(False)
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -333,7 +334,8 @@ def main():
                 "data": "synthetic (seeded BASELINE.json config recipe; no public dataset)",
                 "config": config_desc(wl, world), "gflops": gflops, "fp64_frac_of_peak": gflops / 1000.0 / (peak * world),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages))}
+                "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages)),
+                "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]}}
         print(json.dumps(line), flush=True)
     batch.free()
     eng.close()

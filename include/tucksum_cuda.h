@@ -132,6 +132,12 @@ int64_t ts_result_intermediate(const ts_result* r, int which, int64_t mode, doub
                                int64_t* cols);
 int ts_result_free(ts_result* r);
 
+/* Which numerical path the last ts_krp_sum took: number of modes whose thin QR
+ * fell back from CholeskyQR2 to Householder TSQR, and number of ST-HOSVD modes
+ * whose Gram-eigenvalue decision was not provably exact and used the accurate
+ * TSQR + one-sided Jacobi SVD. */
+int ts_ctx_last_paths(ts_ctx* ctx, int* qr_fallback_modes, int* svd_fallback_modes);
+
 /* Debug capture of stage intermediates (0/1). */
 int ts_ctx_set_debug(ts_ctx* ctx, int enabled);
 /* Per-stage CUDA-event times (ms) of the last ts_krp_sum: A, B, C, allreduce Y,

@@ -126,6 +126,7 @@ struct ts_ctx {
     std::vector<double> stage_ms;
     std::int64_t launches = 0;
     std::vector<cudaEvent_t> events;
+    int last_qr_fallbacks = 0, last_svd_fallbacks = 0;  // accurate-path uses in the last call
 };
 
 struct ts_batch {
@@ -224,19 +225,61 @@ std::int64_t hosvd_rank(const std::vector<double>& s, double tau, double theta, 
     return rank;
 }
 
-// Left singular vectors + singular values of the unfolding g_(k) (q_k × rest) via
-// TSQR of g_(k)ᵀ and a one-sided Jacobi SVD of the small triangular factor.
-void unfolding_svd(const double* g, int order, const std::int64_t* shape, int k, double* sigma, double* U,
-                   CallScratch& sc) {
-    std::int64_t rest = 1;
-    for (int j = 0; j < order; ++j)
-        if (j != k) rest *= shape[j];
-    const std::int64_t qk = shape[k];
-    double* X = sc.alloc_n<double>(static_cast<size_t>(rest * qk));
-    ts::launch_unfold_t(g, order, shape, k, X, sc);
+// Accurate path: left singular vectors + singular values of the unfolding
+// g_(k) (q_k × rest) from X = g_(k)ᵀ via TSQR (R only) and a one-sided Jacobi SVD
+// of the small triangular factor.  X is overwritten.
+void unfolding_svd_accurate(double* X, std::int64_t rest, std::int64_t qk, double* sigma, double* U, CallScratch& sc) {
     ts::TsqrPlan plan = ts::plan_tsqr(X, rest, rest, qk, nullptr, 0, sc);
     ts::run_tsqr({&plan}, sc, false);
     ts::launch_jacobi_svd(plan.Rtop, plan.kk, static_cast<int>(plan.kk), static_cast<int>(qk), sigma, U, sc);
+}
+
+// Fast path of the ST-HOSVD rank decision from the eigenvalues lam (descending)
+// of the Gram h_(k)h_(k)ᵀ.  The Gram's eigenvalues carry absolute errors of a few
+// ulps of λ₁, so the decision (and the kept subspace) is accepted only when it is
+// provably the one the exact singular values give; otherwise *ok = false and the
+// caller takes the accurate TSQR + one-sided Jacobi path.
+std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double theta, std::int64_t cap, bool* ok) {
+    *ok = false;
+    const std::int64_t q = static_cast<std::int64_t>(lam_in.size());
+    if (q == 0 || !(lam_in[0] > 0.0)) return 1;
+    std::vector<double> lam(lam_in);
+    for (double& l : lam) l = std::max(l, 0.0);
+    const double l1 = lam[0];
+    const double noise = 1e-12 * l1;
+    const double resolvable = 1e-8 * l1;  // σ ≥ 1e-4·σ₁: far above both noise and the 1e-14·σ₁ floor
+    std::int64_t rank;
+    if (tau == 0.0) {
+        if (cap > 0 && cap < q) {
+            if (lam[static_cast<size_t>(cap - 1)] < resolvable) return 1;
+            rank = cap;
+        } else {
+            if (lam[static_cast<size_t>(q - 1)] < resolvable) return 1;
+            rank = q;
+        }
+    } else {
+        std::vector<double> suffix(static_cast<size_t>(q) + 1, 0.0);
+        for (std::int64_t j = q - 1; j >= 0; --j) suffix[static_cast<size_t>(j)] = suffix[static_cast<size_t>(j) + 1] + lam[static_cast<size_t>(j)];
+        std::int64_t r = q;
+        for (std::int64_t i = 1; i <= q; ++i)
+            if (suffix[static_cast<size_t>(i)] <= theta) {
+                r = i;
+                break;
+            }
+        const double margin = static_cast<double>(q) * noise;
+        if (r < q && suffix[static_cast<size_t>(r)] > theta - margin) return 1;
+        if (r > 1 && suffix[static_cast<size_t>(r - 1)] <= theta + margin) return 1;
+        rank = r;
+        if (cap > 0) rank = std::min(rank, cap);
+    }
+    if (rank < q) {  // the kept subspace must be well separated from the discarded one
+        const double gap = lam[static_cast<size_t>(rank - 1)] - lam[static_cast<size_t>(rank)];
+        if (!(gap > 0.0)) return 1;
+        const double err = 2.2e-16 * l1 / gap * std::sqrt(lam[static_cast<size_t>(rank)] / l1);
+        if (err > 1e-12) return 1;
+    }
+    *ok = true;
+    return rank;
 }
 
 ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
@@ -358,17 +401,85 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             res->inter_cols[1][n] = s;
         }
     }
-    // ---- Stage D: Û_n = thin Q of Y_n
+    // ---- Stage D: Û_n = thin Q of Y_n.  Fast path CholeskyQR2 (Gram GEMM, small
+    // Cholesky + inverse, GEMM, twice); R = R₂R₁ has a positive diagonal, so Û is
+    // the Householder Q with R_ii ≥ 0 of the reference.  Modes whose Y is too
+    // ill-conditioned (failed pivot, or second Gram far from I) or too short take
+    // the Householder TSQR.
     double* Uh[TS_MAX_ORDER];
     {
+        std::vector<int> chol(static_cast<size_t>(d), 0);
+        std::vector<GemmProblem> g1, q1, g2, q2;
+        int* flags = sc.alloc_n<int>(static_cast<size_t>(d));
+        TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<size_t>(d), st));
+        double *G1[TS_MAX_ORDER], *G2[TS_MAX_ORDER], *Ri1[TS_MAX_ORDER], *Ri2[TS_MAX_ORDER], *Q1[TS_MAX_ORDER];
+        bool any = false;
+        for (int n = 0; n < d; ++n) {
+            Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+            chol[static_cast<size_t>(n)] = dims[n] >= 2 * s;
+            if (!chol[static_cast<size_t>(n)]) continue;
+            any = true;
+            G1[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
+            G2[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
+            Ri1[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
+            Ri2[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
+            Q1[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * s));
+            GemmProblem p{};
+            p.M = p.N = static_cast<int>(s);
+            p.K = static_cast<int>(dims[n]);
+            p.A = Y + yoff[n];
+            p.lda = dims[n];
+            p.B = Y + yoff[n];
+            p.ldb = dims[n];
+            p.C = G1[n];
+            p.ldc = s;
+            g1.push_back(p);
+            p.A = Q1[n];
+            p.B = Q1[n];
+            p.C = G2[n];
+            g2.push_back(p);
+            GemmProblem m{};
+            m.M = static_cast<int>(dims[n]);
+            m.N = static_cast<int>(s);
+            m.K = static_cast<int>(s);
+            m.A = Y + yoff[n];
+            m.lda = dims[n];
+            m.B = Ri1[n];
+            m.ldb = s;
+            m.C = Q1[n];
+            m.ldc = dims[n];
+            q1.push_back(m);
+            m.A = Q1[n];
+            m.B = Ri2[n];
+            m.C = Uh[n];
+            q2.push_back(m);
+        }
+        if (any) {
+            ts::launch_grouped_gemm(Layout::TN, g1, sc, ctx->num_sms);
+            for (int n = 0; n < d; ++n)
+                if (chol[static_cast<size_t>(n)])
+                    ts::launch_chol_inv(G1[n], s, static_cast<int>(s), Ri1[n], s, flags + n, false, sc);
+            ts::launch_grouped_gemm(Layout::NN, q1, sc, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::TN, g2, sc, ctx->num_sms);
+            for (int n = 0; n < d; ++n)
+                if (chol[static_cast<size_t>(n)])
+                    ts::launch_chol_inv(G2[n], s, static_cast<int>(s), Ri2[n], s, flags + n, true, sc);
+            ts::launch_grouped_gemm(Layout::NN, q2, sc, ctx->num_sms);
+            std::vector<int> hf(static_cast<size_t>(d), 0);
+            TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
+            TS_CUDA_CHECK(cudaStreamSynchronize(st));
+            for (int n = 0; n < d; ++n)
+                if (hf[static_cast<size_t>(n)] != 0) chol[static_cast<size_t>(n)] = 0;
+        }
         std::vector<ts::TsqrPlan> plans(static_cast<size_t>(d));
         std::vector<ts::TsqrPlan*> pp;
         for (int n = 0; n < d; ++n) {
-            Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+            if (chol[static_cast<size_t>(n)]) continue;
             plans[static_cast<size_t>(n)] = ts::plan_tsqr(Y + yoff[n], dims[n], dims[n], s, Uh[n], dims[n], sc);
             pp.push_back(&plans[static_cast<size_t>(n)]);
         }
-        ts::run_tsqr(pp, sc, true);
+        if (!pp.empty()) ts::run_tsqr(pp, sc, true);
+        ctx->last_qr_fallbacks = static_cast<int>(pp.size());
     }
     mark(ctx, 5);
     // ---- Stage E: P_n = Û_nᵀ F_n (q_n × R_n)
@@ -501,19 +612,50 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
         TS_CUDA_CHECK(cudaMemcpyAsync(&hss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
         TS_CUDA_CHECK(cudaStreamSynchronize(st));
         const double theta = eps * eps * hss / static_cast<double>(d);
+        ctx->last_svd_fallbacks = 0;
         std::vector<int> mode_order(static_cast<size_t>(d));
         std::iota(mode_order.begin(), mode_order.end(), 0);
         std::stable_sort(mode_order.begin(), mode_order.end(), [&](int x, int y) { return cur_shape[x] < cur_shape[y]; });
         for (int k : mode_order) {
             const std::int64_t qk = cur_shape[k];
-            double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
             Pk[k] = sc.alloc_n<double>(static_cast<size_t>(qk * qk));
-            unfolding_svd(g, d, cur_shape, k, sigma, Pk[k], sc);
-            std::vector<double> sig(static_cast<size_t>(qk));
-            TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
-                                          cudaMemcpyDeviceToHost, st));
+            std::int64_t rest = 1;
+            for (int j = 0; j < d; ++j)
+                if (j != k) rest *= cur_shape[j];
+            double* X = sc.alloc_n<double>(static_cast<size_t>(rest * qk));
+            ts::launch_unfold_t(g, d, cur_shape, k, X, sc);
+            // Fast path: Gram C = XᵀX (DMMA GEMM) + two-sided Jacobi.
+            double* C = sc.alloc_n<double>(static_cast<size_t>(qk * qk));
+            double* lam = sc.alloc_n<double>(static_cast<size_t>(qk));
+            {
+                GemmProblem p{};
+                p.M = p.N = static_cast<int>(qk);
+                p.K = static_cast<int>(rest);
+                p.A = X;
+                p.lda = rest;
+                p.B = X;
+                p.ldb = rest;
+                p.C = C;
+                p.ldc = qk;
+                ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
+            }
+            ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc);
+            std::vector<double> lv(static_cast<size_t>(qk));
+            TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk), cudaMemcpyDeviceToHost, st));
             TS_CUDA_CHECK(cudaStreamSynchronize(st));
-            const std::int64_t rk = hosvd_rank(sig, eps, theta, max_rank ? max_rank[k] : 0);
+            const std::int64_t capk = max_rank ? max_rank[k] : 0;
+            bool ok = false;
+            std::int64_t rk = gram_rank(lv, eps, theta, capk, &ok);
+            if (!ok) {
+                double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
+                unfolding_svd_accurate(X, rest, qk, sigma, Pk[k], sc);
+                std::vector<double> sig(static_cast<size_t>(qk));
+                TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
+                                              cudaMemcpyDeviceToHost, st));
+                TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                rk = hosvd_rank(sig, eps, theta, capk);
+                ++ctx->last_svd_fallbacks;
+            }
             rank[k] = rk;
             // g ← g ×_k P_kᵀ
             std::int64_t left = 1, right = 1, total_out = rk;
@@ -656,6 +798,14 @@ int ts_ctx_init_nccl(ts_ctx* ctx, const void* unique_id_128, int nranks, int ran
 
 void* ts_ctx_stream(ts_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 int64_t ts_ctx_launch_count(ts_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ts_ctx_last_paths(ts_ctx* ctx, int* qr_fallback_modes, int* svd_fallback_modes) {
+    return guarded([&] {
+        if (!ctx) invalid("null context");
+        if (qr_fallback_modes) *qr_fallback_modes = ctx->last_qr_fallbacks;
+        if (svd_fallback_modes) *svd_fallback_modes = ctx->last_svd_fallbacks;
+    });
+}
 
 int ts_ctx_set_debug(ts_ctx* ctx, int enabled) {
     return guarded([&] {

@@ -7,6 +7,7 @@
 // pairs per half-warp, whichever operand dimension is contiguous.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -182,13 +183,25 @@ __global__ void splitk_reduce(const GemmDesc* __restrict__ descs, const int* __r
     }
 }
 
-// Tile configuration used for every layout (tuned on B200).
-constexpr int kBM = 64, kBN = 64, kBK = 16, kWM = 32, kWN = 32, kStages = 4;
+// ---------------------------------------------------------------- tile configurations
+// Runtime-selectable CTA tiles (TS_GEMM_CFG_{TN,NN,NT} override the defaults).
+struct TileCfg {
+    int bm, bn, bk;
+};
+constexpr TileCfg kCfgs[] = {
+    {64, 64, 16},   // 0: 4 warps of 32×32, 4 stages
+    {128, 64, 16},  // 1: 8 warps of 32×32, 3 stages
+    {64, 128, 16},  // 2: 8 warps of 32×32, 3 stages
+    {64, 64, 32},   // 3: 4 warps of 32×32, 3 stages
+    {128, 64, 16},  // 4: 4 warps of 64×32, 3 stages
+    {64, 128, 16},  // 5: 4 warps of 32×64, 3 stages
+};
+constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
-template <bool AK, bool BKM, int VEC>
-void launch_cfg(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStream_t stream) {
-    using Cfg = GemmCfg<kBM, kBN, kBK, kWM, kWN, kStages, AK, BKM>;
-    auto kern = gemm_kernel<kBM, kBN, kBK, kWM, kWN, kStages, AK, BKM, VEC>;
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
+void launch_kernel(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStream_t stream) {
+    using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
+    auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
     static bool configured = false;
     if (!configured) {
         TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -199,17 +212,107 @@ void launch_cfg(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStream_
     TS_LAUNCH_CHECK();
 }
 
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
+int occupancy_of() {
+    using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
+    static int occ = 0;
+    if (occ == 0) {
+        auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
+        TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(Cfg::kSmemBytes)));
+        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes));
+        occ = std::max(occ, 1);
+    }
+    return occ;
+}
+
+template <bool AK, bool BKM>
+struct Dispatch {
+    static int occupancy(int cfg) {
+        switch (cfg) {
+            case 1: return occupancy_of<128, 64, 16, 32, 32, 3, AK, BKM>();
+            case 2: return occupancy_of<64, 128, 16, 32, 32, 3, AK, BKM>();
+            case 3: return occupancy_of<64, 64, 32, 32, 32, 3, AK, BKM>();
+            case 4: return occupancy_of<128, 64, 16, 64, 32, 3, AK, BKM>();
+            case 5: return occupancy_of<64, 128, 16, 32, 64, 3, AK, BKM>();
+            default: return occupancy_of<64, 64, 16, 32, 32, 4, AK, BKM>();
+        }
+    }
+    template <int VEC>
+    static void launch(int cfg, const GemmDesc* d, int ng, int64_t units, cudaStream_t st) {
+        switch (cfg) {
+            case 1: return launch_kernel<128, 64, 16, 32, 32, 3, AK, BKM, VEC>(d, ng, units, st);
+            case 2: return launch_kernel<64, 128, 16, 32, 32, 3, AK, BKM, VEC>(d, ng, units, st);
+            case 3: return launch_kernel<64, 64, 32, 32, 32, 3, AK, BKM, VEC>(d, ng, units, st);
+            case 4: return launch_kernel<128, 64, 16, 64, 32, 3, AK, BKM, VEC>(d, ng, units, st);
+            case 5: return launch_kernel<64, 128, 16, 32, 64, 3, AK, BKM, VEC>(d, ng, units, st);
+            default: return launch_kernel<64, 64, 16, 32, 32, 4, AK, BKM, VEC>(d, ng, units, st);
+        }
+    }
+};
+
+int config_for(Layout layout) {
+    static int cfg[3] = {-2, -2, -2};
+    const int li = static_cast<int>(layout);
+    if (cfg[li] == -2) {
+        const char* names[3] = {"TS_GEMM_CFG_TN", "TS_GEMM_CFG_NN", "TS_GEMM_CFG_NT"};
+        const int defaults[3] = {0, 0, 0};
+        const char* e = std::getenv(names[li]);
+        int v = e ? std::atoi(e) : defaults[li];
+        if (v < 0 || v >= kNumCfgs) v = defaults[li];
+        cfg[li] = v;
+    }
+    return cfg[li];
+}
+
+int occupancy(Layout layout, int cfg) {
+    switch (layout) {
+        case Layout::TN: return Dispatch<true, true>::occupancy(cfg);
+        case Layout::NN: return Dispatch<false, true>::occupancy(cfg);
+        default: return Dispatch<false, false>::occupancy(cfg);
+    }
+}
+
+// Splits K so the launch fills whole waves of CTA slots: maximise
+// units / (waves × slots), preferring fewer splits within 3 %.
+int choose_splits(int64_t tiles, int64_t slots, int K, int bk) {
+    const int maxs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * bk))));
+    double best = -1.0;
+    int best_s = 1;
+    std::vector<double> eff(static_cast<size_t>(maxs) + 1, 0.0);
+    for (int s = 1; s <= maxs; ++s) {
+        const int64_t u = tiles * s;
+        const int64_t waves = (u + slots - 1) / slots;
+        // Small problems: more splits also shorten each CTA's serial K loop.
+        eff[static_cast<size_t>(s)] = static_cast<double>(u) / static_cast<double>(waves * slots);
+        best = std::max(best, eff[static_cast<size_t>(s)]);
+    }
+    for (int s = 1; s <= maxs; ++s)
+        if (eff[static_cast<size_t>(s)] >= best - 0.03) {
+            best_s = s;
+            break;
+        }
+    return best_s;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
 
 int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallScratch& sc, int num_sms) {
+    const int cfg = config_for(layout);
+    const TileCfg tc = kCfgs[cfg];
+    const int64_t slots = static_cast<int64_t>(num_sms) * occupancy(layout, cfg);
     std::vector<GemmDesc> descs;
     descs.reserve(probs.size());
     int64_t units = 0;
     bool vec2 = true;
     size_t ws_elems = 0;
     std::vector<int> red;
+    int64_t total_tiles = 0;
+    for (const GemmProblem& p : probs)
+        if (p.M > 0 && p.N > 0 && p.batch > 0)
+            total_tiles += static_cast<int64_t>((p.M + tc.bm - 1) / tc.bm) * ((p.N + tc.bn - 1) / tc.bn) * p.batch;
     for (const GemmProblem& p : probs) {
         if (p.M <= 0 || p.N <= 0 || p.batch <= 0) continue;
         GemmDesc d{};
@@ -228,20 +331,15 @@ int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, Ca
         d.batch = p.batch;
         d.alpha = p.alpha;
         d.beta = p.beta;
-        d.tiles_m = (p.M + kBM - 1) / kBM;
-        d.tiles_n = (p.N + kBN - 1) / kBN;
+        d.tiles_m = (p.M + tc.bm - 1) / tc.bm;
+        d.tiles_n = (p.N + tc.bn - 1) / tc.bn;
         const int64_t tiles = static_cast<int64_t>(d.tiles_m) * d.tiles_n * p.batch;
-        // Split K until the launch offers ~2 CTAs per SM, keeping >= 4 K-steps per split.
-        int splits = 1;
-        const int64_t target = 2LL * num_sms;
-        if (tiles < target && p.K > 4 * kBK) {
-            const int64_t want = (target + tiles - 1) / tiles;
-            const int64_t maxs = std::max<int64_t>(1, p.K / (4 * kBK));
-            splits = static_cast<int>(std::min(want, maxs));
-        }
+        // Split decision on the whole launch (groups share the waves); every group
+        // gets the same split factor, applied only when its K is long enough.
+        int splits = p.K > 4 * tc.bk ? choose_splits(total_tiles, slots, p.K, tc.bk) : 1;
         int kps = (p.K + splits - 1) / splits;
-        kps = ((kps + kBK - 1) / kBK) * kBK;
-        if (kps <= 0) kps = kBK;
+        kps = ((kps + tc.bk - 1) / tc.bk) * tc.bk;
+        if (kps <= 0) kps = tc.bk;
         splits = std::max(1, (p.K + kps - 1) / kps);
         d.splits = splits;
         d.k_per_split = kps;
@@ -270,14 +368,16 @@ int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, Ca
     cudaStream_t st = sc.stream();
     switch (layout) {
         case Layout::TN:
-            vec2 ? launch_cfg<true, true, 2>(d_descs, ng, units, st) : launch_cfg<true, true, 1>(d_descs, ng, units, st);
+            vec2 ? Dispatch<true, true>::launch<2>(cfg, d_descs, ng, units, st)
+                 : Dispatch<true, true>::launch<1>(cfg, d_descs, ng, units, st);
             break;
         case Layout::NN:
-            vec2 ? launch_cfg<false, true, 2>(d_descs, ng, units, st) : launch_cfg<false, true, 1>(d_descs, ng, units, st);
+            vec2 ? Dispatch<false, true>::launch<2>(cfg, d_descs, ng, units, st)
+                 : Dispatch<false, true>::launch<1>(cfg, d_descs, ng, units, st);
             break;
         case Layout::NT:
-            vec2 ? launch_cfg<false, false, 2>(d_descs, ng, units, st)
-                 : launch_cfg<false, false, 1>(d_descs, ng, units, st);
+            vec2 ? Dispatch<false, false>::launch<2>(cfg, d_descs, ng, units, st)
+                 : Dispatch<false, false>::launch<1>(cfg, d_descs, ng, units, st);
             break;
     }
     int launched = 1;

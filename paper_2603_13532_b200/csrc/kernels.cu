@@ -1,5 +1,5 @@
-// kernels.cu — stage B (core × implicit Khatri-Rao), stage D (TSQR), stage G
-// (one-sided Jacobi SVD, unfolding) kernels for sm_100a.
+// kernels.cu — stage D (TSQR, CholeskyQR), stage G (Jacobi SVD / eigensolver,
+// unfolding) kernels for sm_100a.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -9,280 +9,278 @@
 namespace ts {
 namespace {
 
-constexpr int kKrpThreads = 128;
-constexpr int kKrpCT = 32;  // sketch columns per CTA (one per lane)
-constexpr int kKrpJC = 32;  // complement-index chunk
+// ------------------------------------------------------------------ TSQR
+constexpr int kQrThreads = 512;
+constexpr int kQrWarps = kQrThreads / 32;
+constexpr int kQrMaxCPW = 6;  // columns per warp: 96 / 16
 
-// grid = (atoms, order, ceil(s / CT)).  Thread (ag = warp, c = lane) owns rows
-// a ≡ ag (mod 4) of the RT-row output tile for sketch column c.
-template <int RT>
-__global__ void __launch_bounds__(kKrpThreads) krp_contract_kernel(KrpArgs args) {
-    constexpr int RPT = RT / 4;
-    const Atom& at = args.atoms[blockIdx.x];
-    const int n = blockIdx.y;
-    const int c0 = blockIdx.z * kKrpCT;
-    const int order = args.order, s = args.s;
-    const int tid = threadIdx.x, lane = tid & 31, ag = tid >> 5;
-
-    int shape[kMaxOrder], col[kMaxOrder];
-    int64_t gstride[kMaxOrder];
-    int64_t st = 1;
-    for (int j = 0; j < order; ++j) {
-        shape[j] = at.shape[j];
-        col[j] = at.col[j];
-        gstride[j] = st;
-        st *= shape[j];
-    }
-    const int rn = shape[n];
-    int64_t jtot = 1;
-    for (int j = 0; j < order; ++j)
-        if (j != n) jtot *= shape[j];
-
-    extern __shared__ __align__(16) double sm[];
-    int moff[kMaxOrder];
-    int msum = 0;
-    for (int j = 0; j < order; ++j) {
-        moff[j] = msum;
-        if (j != n) msum += shape[j] * kKrpCT;
-    }
-    double* Ms = sm;                                  // Σ_{j≠n} r_j × CT
-    double* Ks = Ms + msum;                           // JC × CT
-    double* Gs = Ks + kKrpJC * kKrpCT;                // RT × JC
-    int64_t* Goff = reinterpret_cast<int64_t*>(Gs + RT * kKrpJC);  // JC
-    int* Idx = reinterpret_cast<int*>(Goff + kKrpJC);              // JC × order
-
-    for (int j = 0; j < order; ++j) {
-        if (j == n) continue;
-        const double* Z = args.Z[j];
-        for (int idx = tid; idx < shape[j] * kKrpCT; idx += kKrpThreads) {
-            const int a = idx / kKrpCT, c = idx % kKrpCT;
-            const int cg = c0 + c;
-            Ms[moff[j] + idx] = cg < s ? Z[cg + static_cast<int64_t>(col[j] + a) * s] : 0.0;
-        }
-    }
-    const double w = args.weights[at.summand];
-    const double* core = args.cores + at.core_off;
-    double* Wn = args.W[n];
-    const int64_t Rn = args.R[n];
-    __syncthreads();
-
-    for (int a0 = 0; a0 < rn; a0 += RT) {
-        double acc[RPT];
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
-        for (int64_t J0 = 0; J0 < jtot; J0 += kKrpJC) {
-            if (tid < kKrpJC) {
-                const int64_t J = J0 + tid;
-                int64_t off = -1;
-                if (J < jtot) {
-                    int64_t rem = J;
-                    off = 0;
-                    for (int j = 0; j < order; ++j) {
-                        if (j == n) continue;
-                        const int aj = static_cast<int>(rem % shape[j]);
-                        rem /= shape[j];
-                        off += aj * gstride[j];
-                        Idx[tid * kMaxOrder + j] = aj;
-                    }
-                }
-                Goff[tid] = off;
-            }
-            __syncthreads();
-            for (int idx = tid; idx < kKrpJC * kKrpCT; idx += kKrpThreads) {
-                const int jj = idx / kKrpCT, c = idx % kKrpCT;
-                double v = 0.0;
-                if (Goff[jj] >= 0) {
-                    v = 1.0;
-                    for (int j = 0; j < order; ++j) {
-                        if (j == n) continue;
-                        v *= Ms[moff[j] + Idx[jj * kMaxOrder + j] * kKrpCT + c];
-                    }
-                }
-                Ks[idx] = v;
-            }
-            for (int idx = tid; idx < RT * kKrpJC; idx += kKrpThreads) {
-                const int a = idx / kKrpJC, jj = idx % kKrpJC;
-                const int64_t off = Goff[jj];
-                Gs[idx] = (off >= 0 && a0 + a < rn) ? core[off + (a0 + a) * gstride[n]] : 0.0;
-            }
-            __syncthreads();
-#pragma unroll 8
-            for (int jj = 0; jj < kKrpJC; ++jj) {
-                const double k = Ks[jj * kKrpCT + lane];
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) acc[i] = fma(Gs[(ag + 4 * i) * kKrpJC + jj], k, acc[i]);
-            }
-            __syncthreads();
-        }
-        const int cg = c0 + lane;
-        if (cg < s) {
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const int a = a0 + ag + 4 * i;
-                if (a < rn) Wn[(col[n] + a) + static_cast<int64_t>(cg) * Rn] = w * acc[i];
-            }
-        }
+// Householder parameters with Eigen's makeHouseholder convention: beta =
+// -sign(c0)·‖x‖, tau = (beta - c0)/beta, v = [1; x_tail/(c0 - beta)]; tau = 0
+// when the tail is below the smallest normal (see oracle/tucksum_oracle.cpp).
+__device__ __forceinline__ void householder_params(double c0, double tail, double* beta, double* tau, double* inv) {
+    if (tail <= DBL_MIN) {
+        *tau = 0.0;
+        *beta = c0;
+        *inv = 0.0;
+    } else {
+        double b = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) b = -b;
+        *beta = b;
+        *inv = 1.0 / (c0 - b);
+        *tau = (b - c0) / b;
     }
 }
 
-// ------------------------------------------------------------------ TSQR
-constexpr int kQrThreads = 256;
-constexpr int kQrWarps = kQrThreads / 32;
-
 // Householder QR of one rows × cols block held column-major in shared memory.
-// Reflector convention of Eigen's makeHouseholder (see oracle/tucksum_oracle.cpp).
+// One block barrier per reflector: the reflector k is applied with its vector
+// still unscaled (the 1/(c0 - beta) factor folded into the update), its
+// scaling is deferred to step k+1, and warp 0 — which owns column k+1 — derives
+// the next reflector right after updating that column.  Each warp reduces the
+// dot products of all its columns together so their shuffle latencies overlap.
 __global__ void __launch_bounds__(kQrThreads) tsqr_factor_kernel(const QrTask* __restrict__ tasks) {
     const QrTask tk = tasks[blockIdx.x];
     const int rows = tk.rows, cols = tk.cols, kk = min(rows, cols);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     extern __shared__ __align__(16) double As[];
-    __shared__ double sh_beta, sh_tau, sh_inv;
+    __shared__ double pb[2], pt[2], pv[2];
     for (int idx = tid; idx < rows * cols; idx += kQrThreads) {
         const int i = idx % rows, c = idx / rows;
-        As[idx] = tk.A[i + c * tk.lda];
+        As[idx] = tk.A[i + static_cast<int64_t>(c) * tk.lda];
+    }
+    __syncthreads();
+    if (warp == 0 && kk > 0) {
+        double tail = 0.0;
+        for (int i = 1 + lane; i < rows; i += 32) tail += As[i] * As[i];
+        tail = warp_sum(tail);
+        if (lane == 0) householder_params(As[0], tail, &pb[0], &pt[0], &pv[0]);
     }
     __syncthreads();
     for (int k = 0; k < kk; ++k) {
-        double* x = As + k * rows;
-        if (warp == 0) {
+        const int sl = k & 1;
+        const double tau = pt[sl], inv = pv[sl];
+        const double* x = As + k * rows;
+        if (k > 0) {  // deferred scaling of reflector k-1 (column k-1 is not read in this step)
+            const int ps = sl ^ 1;
+            const double ptau = pt[ps], pinv = pv[ps];
+            double* xp = As + (k - 1) * rows;
+            for (int i = k + tid; i < rows; i += kQrThreads) xp[i] = ptau == 0.0 ? 0.0 : xp[i] * pinv;
+            if (tid == 0) {
+                xp[k - 1] = pb[ps];
+                tk.tau[k - 1] = ptau;
+            }
+        }
+        int js[kQrMaxCPW];
+        int nj = 0;
+#pragma unroll
+        for (int i = 0; i < kQrMaxCPW; ++i) {
+            const int j = k + 1 + warp + kQrWarps * i;
+            js[i] = j;
+            if (j < cols) nj = i + 1;
+        }
+        if (tau != 0.0 && nj > 0) {
+            double dot[kQrMaxCPW];
+#pragma unroll
+            for (int i = 0; i < kQrMaxCPW; ++i) dot[i] = 0.0;
+            for (int r = k + 1 + lane; r < rows; r += 32) {
+                const double xr = x[r];
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i)
+                    if (i < nj) dot[i] = fma(xr, As[r + js[i] * rows], dot[i]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
+            double w[kQrMaxCPW];
+#pragma unroll
+            for (int i = 0; i < kQrMaxCPW; ++i) w[i] = i < nj ? tau * (As[k + js[i] * rows] + inv * dot[i]) : 0.0;
+            for (int r = k + 1 + lane; r < rows; r += 32) {
+                const double xr = x[r] * inv;
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i)
+                    if (i < nj) As[r + js[i] * rows] -= w[i] * xr;
+            }
+            __syncwarp();
+            if (lane == 0)
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i)
+                    if (i < nj) As[k + js[i] * rows] -= w[i];
+            __syncwarp();
+        }
+        if (warp == 0 && k + 1 < kk) {  // next reflector from the freshly updated column k+1
+            const double* y = As + (k + 1) * rows;
             double tail = 0.0;
-            for (int i = k + 1 + lane; i < rows; i += 32) tail += x[i] * x[i];
+            for (int i = k + 2 + lane; i < rows; i += 32) tail += y[i] * y[i];
             tail = warp_sum(tail);
-            if (lane == 0) {
-                const double c0 = x[k];
-                if (tail <= DBL_MIN) {
-                    sh_tau = 0.0;
-                    sh_beta = c0;
-                    sh_inv = 0.0;
-                } else {
-                    double beta = sqrt(c0 * c0 + tail);
-                    if (c0 >= 0.0) beta = -beta;
-                    sh_beta = beta;
-                    sh_inv = 1.0 / (c0 - beta);
-                    sh_tau = (beta - c0) / beta;
-                }
-            }
-        }
-        __syncthreads();
-        const double tau = sh_tau, inv = sh_inv;
-        for (int i = k + 1 + tid; i < rows; i += kQrThreads) x[i] = tau == 0.0 ? 0.0 : x[i] * inv;
-        __syncthreads();
-        if (tid == 0) {
-            x[k] = sh_beta;
-            tk.tau[k] = tau;
-        }
-        if (tau != 0.0) {
-            for (int j = k + 1 + warp; j < cols; j += kQrWarps) {
-                double* y = As + j * rows;
-                double wsum = 0.0;
-                for (int i = k + 1 + lane; i < rows; i += 32) wsum += x[i] * y[i];
-                wsum = (warp_sum(wsum) + y[k]) * tau;
-                for (int i = k + 1 + lane; i < rows; i += 32) y[i] -= wsum * x[i];
-                __syncwarp();
-                if (lane == 0) y[k] -= wsum;
-            }
+            if (lane == 0) householder_params(y[k + 1], tail, &pb[sl ^ 1], &pt[sl ^ 1], &pv[sl ^ 1]);
         }
         __syncthreads();
     }
+    if (kk > 0) {
+        const int ps = (kk - 1) & 1;
+        const double ptau = pt[ps], pinv = pv[ps];
+        double* xp = As + (kk - 1) * rows;
+        for (int i = kk + tid; i < rows; i += kQrThreads) xp[i] = ptau == 0.0 ? 0.0 : xp[i] * pinv;
+        if (tid == 0) {
+            xp[kk - 1] = pb[ps];
+            tk.tau[kk - 1] = ptau;
+        }
+    }
+    __syncthreads();
     for (int idx = tid; idx < rows * cols; idx += kQrThreads) {
         const int i = idx % rows, c = idx / rows;
-        tk.A[i + c * tk.lda] = As[idx];
+        tk.A[i + static_cast<int64_t>(c) * tk.lda] = As[idx];
     }
     for (int idx = tid; idx < kk * cols; idx += kQrThreads) {
         const int i = idx % kk, c = idx / kk;
-        tk.R[i + c * tk.ldr] = i <= c ? As[i + c * rows] : 0.0;
+        tk.R[i + static_cast<int64_t>(c) * tk.ldr] = i <= c ? As[i + c * rows] : 0.0;
     }
 }
 
-// Q formation for one block: Q = H_0 ⋯ H_{kk-1} · [Qin; 0], optional column signs.
+// Q formation for one block: Q = H_0 ⋯ H_{kk-1} · [Qin; 0], optional column
+// signs.  Reflector k-1 is prefetched (cp.async) while reflector k is applied.
 __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTask* __restrict__ tasks) {
     const QrApplyTask tk = tasks[blockIdx.x];
     const int rows = tk.rows, kk = tk.kk, q = tk.q;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     extern __shared__ __align__(16) double Qs[];
-    double* v = Qs + rows * q;
+    double* vbuf = Qs + rows * q;      // 2 × rows
+    double* taus = vbuf + 2 * rows;    // kk
     for (int idx = tid; idx < rows * q; idx += kQrThreads) {
         const int i = idx % rows, c = idx / rows;
         double val = 0.0;
-        if (i < kk) val = tk.Qin ? tk.Qin[i + c * tk.ldqin] : (i == c ? 1.0 : 0.0);
+        if (i < kk) val = tk.Qin ? tk.Qin[i + static_cast<int64_t>(c) * tk.ldqin] : (i == c ? 1.0 : 0.0);
         Qs[idx] = val;
     }
+    for (int i = tid; i < kk; i += kQrThreads) taus[i] = tk.tau[i];
+    if (kk > 0)
+        for (int i = kk + tid; i < rows; i += kQrThreads)
+            cp_async8(vbuf + ((kk - 1) & 1) * rows + i, tk.V + i + static_cast<int64_t>(kk - 1) * tk.ldv, 8);
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     for (int k = kk - 1; k >= 0; --k) {
-        const double tau = tk.tau[k];
-        if (tau == 0.0) continue;
-        for (int i = k + 1 + tid; i < rows; i += kQrThreads) v[i] = tk.V[i + k * tk.ldv];
-        __syncthreads();
-        for (int c = warp; c < q; c += kQrWarps) {
-            double* y = Qs + c * rows;
-            double wsum = 0.0;
-            for (int i = k + 1 + lane; i < rows; i += 32) wsum += v[i] * y[i];
-            wsum = (warp_sum(wsum) + y[k]) * tau;
-            for (int i = k + 1 + lane; i < rows; i += 32) y[i] -= wsum * v[i];
+        if (k > 0)
+            for (int i = k + tid; i < rows; i += kQrThreads)
+                cp_async8(vbuf + ((k - 1) & 1) * rows + i, tk.V + i + static_cast<int64_t>(k - 1) * tk.ldv, 8);
+        cp_async_commit();
+        const double tau = taus[k];
+        const double* v = vbuf + (k & 1) * rows;
+        if (tau != 0.0) {
+            int cs[kQrMaxCPW];
+            int nc = 0;
+#pragma unroll
+            for (int i = 0; i < kQrMaxCPW; ++i) {
+                cs[i] = warp + kQrWarps * i;
+                if (cs[i] < q) nc = i + 1;
+            }
+            double dot[kQrMaxCPW];
+#pragma unroll
+            for (int i = 0; i < kQrMaxCPW; ++i) dot[i] = 0.0;
+            for (int r = k + 1 + lane; r < rows; r += 32) {
+                const double vr = v[r];
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i)
+                    if (i < nc) dot[i] = fma(vr, Qs[r + cs[i] * rows], dot[i]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
+            double w[kQrMaxCPW];
+#pragma unroll
+            for (int i = 0; i < kQrMaxCPW; ++i) w[i] = i < nc ? tau * (Qs[k + cs[i] * rows] + dot[i]) : 0.0;
+            for (int r = k + 1 + lane; r < rows; r += 32) {
+                const double vr = v[r];
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i)
+                    if (i < nc) Qs[r + cs[i] * rows] -= w[i] * vr;
+            }
             __syncwarp();
-            if (lane == 0) y[k] -= wsum;
+            if (lane == 0)
+#pragma unroll
+                for (int i = 0; i < kQrMaxCPW; ++i)
+                    if (i < nc) Qs[k + cs[i] * rows] -= w[i];
         }
+        cp_async_wait<0>();
         __syncthreads();
     }
     for (int idx = tid; idx < rows * q; idx += kQrThreads) {
         const int i = idx % rows, c = idx / rows;
         double val = Qs[idx];
-        if (tk.Rsign && tk.Rsign[c + c * tk.ldrs] < 0.0) val = -val;
-        tk.Q[i + c * tk.ldq] = val;
+        if (tk.Rsign && tk.Rsign[c + static_cast<int64_t>(c) * tk.ldrs] < 0.0) val = -val;
+        tk.Q[i + static_cast<int64_t>(c) * tk.ldq] = val;
     }
 }
 
-// ------------------------------------------------------------------ Jacobi SVD
-constexpr int kJacThreads = 256;
+// ------------------------------------------------------------------ Jacobi
+constexpr int kJacThreads = 1024;
 constexpr int kJacWarps = kJacThreads / 32;
 
+__device__ __forceinline__ void pair_of(int r, int pi, int np, int* p, int* q) {
+    int a, b;
+    if (pi == 0) {
+        a = np - 1;
+        b = r;
+    } else {
+        a = (r + pi) % (np - 1);
+        b = (r - pi + (np - 1)) % (np - 1);
+    }
+    *p = min(a, b);
+    *q = max(a, b);
+}
+
+// Writes sigma/U sorted by descending key (stable): U[:, rank(c)] = J[:, c].
+__device__ void sort_desc_store(const double* key, const double* J, int nc, double* sigma, double* U) {
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const double v = key[c];
+        int rank = 0;
+        for (int i = 0; i < nc; ++i) rank += (key[i] > v) || (key[i] == v && i < c);
+        sigma[rank] = v;
+        for (int i = 0; i < nc; ++i) U[i + static_cast<int64_t>(rank) * nc] = J[i + c * nc];
+    }
+}
+
+// One-sided (Hestenes) Jacobi SVD of a small m × nc matrix R (accurate path).
+// One column pair per warp per round (round-robin ordering); squared column
+// norms are carried through the rotations so each pair needs one reduction.
 __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* __restrict__ R, int64_t ldr, int m,
                                                                  int nc, double* __restrict__ sigma,
                                                                  double* __restrict__ U) {
     extern __shared__ __align__(16) double sm[];
-    double* W = sm;           // m × nc (ld m)
-    double* J = W + m * nc;   // nc × nc (ld nc)
-    double* nrm = J + nc * nc;  // nc
+    double* W = sm;             // m × nc (ld m)
+    double* J = W + m * nc;     // nc × nc (ld nc)
+    double* nrm = J + nc * nc;  // nc (squared norms, then norms)
     __shared__ int rotated;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int idx = tid; idx < m * nc; idx += kJacThreads) {
         const int i = idx % m, c = idx / m;
-        W[idx] = R[i + c * ldr];
+        W[idx] = R[i + static_cast<int64_t>(c) * ldr];
     }
     for (int idx = tid; idx < nc * nc; idx += kJacThreads) J[idx] = (idx % nc == idx / nc) ? 1.0 : 0.0;
-    const int np = nc + (nc & 1);  // players (one dummy when odd)
+    const int np = nc + (nc & 1);
     const double tol = 1e-15;
     for (int sweep = 0; sweep < 80; ++sweep) {
+        __syncthreads();
+        for (int c = warp; c < nc; c += kJacWarps) {  // exact norms once per sweep
+            double a = 0.0;
+            for (int i = lane; i < m; i += 32) a = fma(W[i + c * m], W[i + c * m], a);
+            a = warp_sum(a);
+            if (lane == 0) nrm[c] = a;
+        }
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int r = 0; r < np - 1; ++r) {
             for (int pi = warp; pi < np / 2; pi += kJacWarps) {
                 int p, q;
-                if (pi == 0) {
-                    p = np - 1;
-                    q = r;
-                } else {
-                    p = (r + pi) % (np - 1);
-                    q = (r - pi + (np - 1)) % (np - 1);
-                }
-                if (p >= nc || q >= nc) continue;
-                if (p > q) {
-                    const int tmp = p;
-                    p = q;
-                    q = tmp;
-                }
+                pair_of(r, pi, np, &p, &q);
+                if (q >= nc) continue;
                 double* wp = W + p * m;
                 double* wq = W + q * m;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = lane; i < m; i += 32) {
-                    const double x = wp[i], y = wq[i];
-                    al += x * x;
-                    be += y * y;
-                    ga += x * y;
-                }
-                al = warp_sum(al);
-                be = warp_sum(be);
+                double ga = 0.0;
+                for (int i = lane; i < m; i += 32) ga = fma(wp[i], wq[i], ga);
                 ga = warp_sum(ga);
+                const double al = nrm[p], be = nrm[q];
                 if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -299,28 +297,180 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
                     jp[i] = c * x - s * y;
                     jq[i] = s * x + c * y;
                 }
-                if (lane == 0) rotated = 1;
+                __syncwarp();
+                if (lane == 0) {
+                    nrm[p] = al - t * ga;
+                    nrm[q] = be + t * ga;
+                    rotated = 1;
+                }
             }
             __syncthreads();
         }
         if (!rotated) break;
-        __syncthreads();
     }
+    __syncthreads();
     for (int c = warp; c < nc; c += kJacWarps) {
         double a = 0.0;
-        for (int i = lane; i < m; i += 32) a += W[i + c * m] * W[i + c * m];
+        for (int i = lane; i < m; i += 32) a = fma(W[i + c * m], W[i + c * m], a);
         a = warp_sum(a);
         if (lane == 0) nrm[c] = sqrt(a);
     }
     __syncthreads();
-    // Stable descending order: rank = #{i : n_i > n_c or (n_i == n_c and i < c)}.
-    for (int c = tid; c < nc; c += kJacThreads) {
-        const double v = nrm[c];
-        int rank = 0;
-        for (int i = 0; i < nc; ++i) rank += (nrm[i] > v) || (nrm[i] == v && i < c);
-        sigma[rank] = v;
-        for (int i = 0; i < nc; ++i) U[i + static_cast<int64_t>(rank) * nc] = J[i + c * nc];
+    sort_desc_store(nrm, J, nc, sigma, U);
+}
+
+// Two-sided cyclic Jacobi eigensolver for a small symmetric n × n matrix C
+// (fast path of ST-HOSVD on the Gram of an unfolding).  Each round applies the
+// rotations of n/2 disjoint pairs: rows first (Jᵀ·A), then columns (A·J) and
+// the eigenvector columns.  Outputs eigenvalues (descending) and vectors.
+__global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* __restrict__ Cin, int64_t ldc, int n,
+                                                                 double* __restrict__ lambda, double* __restrict__ V) {
+    extern __shared__ __align__(16) double sm[];
+    const int ld = n + 1;                   // padded row stride
+    double* A = sm;                          // n × ld (A[i*ld + j])
+    double* Vs = A + n * ld;                 // n × n (column j at j*n)
+    double* cs = Vs + n * n;                 // 2 per pair
+    double* diag = cs + 2 * ((n + 1) / 2 + 1);
+    __shared__ int rotated;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int idx = tid; idx < n * n; idx += kJacThreads) {
+        const int i = idx % n, j = idx / n;
+        A[i * ld + j] = 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc]);
+        Vs[idx] = (i == j) ? 1.0 : 0.0;
     }
+    const int np = n + (n & 1);
+    const double tol = 1e-15;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int r = 0; r < np - 1; ++r) {
+            // Phase 1: rotation parameters + row update (rows of a pair are disjoint).
+            for (int pi = warp; pi < np / 2; pi += kJacWarps) {
+                int p, q;
+                pair_of(r, pi, np, &p, &q);
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
+                    if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
+                        const double theta = (aqq - app) / (2.0 * apq);
+                        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                        if (lane == 0) rotated = 1;
+                    }
+                    if (s != 0.0)
+                        for (int k = lane; k < n; k += 32) {
+                            const double x = A[p * ld + k], y = A[q * ld + k];
+                            A[p * ld + k] = c * x - s * y;
+                            A[q * ld + k] = s * x + c * y;
+                        }
+                }
+                if (lane == 0) {
+                    cs[2 * pi] = c;
+                    cs[2 * pi + 1] = s;
+                }
+            }
+            __syncthreads();
+            // Phase 2: column update of A and V.
+            for (int pi = warp; pi < np / 2; pi += kJacWarps) {
+                int p, q;
+                pair_of(r, pi, np, &p, &q);
+                const double c = cs[2 * pi], s = cs[2 * pi + 1];
+                if (q >= n || s == 0.0) continue;
+                for (int k = lane; k < n; k += 32) {
+                    const double x = A[k * ld + p], y = A[k * ld + q];
+                    A[k * ld + p] = c * x - s * y;
+                    A[k * ld + q] = s * x + c * y;
+                    const double vx = Vs[k + p * n], vy = Vs[k + q * n];
+                    Vs[k + p * n] = c * vx - s * vy;
+                    Vs[k + q * n] = s * vx + c * vy;
+                }
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+    }
+    for (int i = tid; i < n; i += kJacThreads) diag[i] = A[i * ld + i];
+    __syncthreads();
+    sort_desc_store(diag, Vs, n, lambda, V);
+}
+
+// Cholesky R (upper, RᵀR = G) of a small SPD matrix and its inverse R⁻¹.
+// flag[0] |= 1 when a pivot is not safely positive, |= 2 when check_identity
+// and max|G - I| > 1e-2 (second CholQR pass on a badly conditioned input).
+__global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int n,
+                                                               double* __restrict__ Rinv, int64_t ldri,
+                                                               int* __restrict__ flag, int check_identity) {
+    extern __shared__ __align__(16) double sm[];
+    const int ld = n + 1;
+    double* A = sm;          // n × ld, A[i*ld + j] (upper part used)
+    double* X = A + n * ld;  // n × n inverse, X[i*n + j]
+    double* piv = X + n * n; // n
+    __shared__ int bad;
+    __shared__ double dmax;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        bad = 0;
+        dmax = 0.0;
+    }
+    __syncthreads();
+    double dev = 0.0, dm = 0.0;
+    for (int idx = tid; idx < n * n; idx += kJacThreads) {
+        const int i = idx % n, j = idx / n;
+        const double g = G[i + static_cast<int64_t>(j) * ldg];
+        A[i * ld + j] = g;
+        dev = fmax(dev, fabs(g - (i == j ? 1.0 : 0.0)));
+        if (i == j) dm = fmax(dm, g);
+    }
+    if (check_identity && dev > 1e-2) atomicOr(&bad, 2);
+    // max diagonal (for a relative pivot floor)
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if ((tid & 31) == 0 && dm > 0) {
+        unsigned long long* p = reinterpret_cast<unsigned long long*>(&dmax);
+        atomicMax(p, __double_as_longlong(dm));  // positive doubles order like their bit patterns
+    }
+    __syncthreads();
+    const double floor_piv = 1e-28 * dmax;  // κ(Y) ≲ 1e14 for the pivot test; the CholQR2 check catches the rest
+    for (int k = 0; k < n; ++k) {
+        double p = A[k * ld + k];
+        if (!(p > floor_piv)) {
+            if (tid == 0) bad |= 1;
+            p = fmax(dmax, 1.0);
+        }
+        if (tid == 0) piv[k] = p;
+        if (k > 0) {  // deferred scaling of row k-1
+            const double r = sqrt(piv[k - 1]);
+            for (int j = k - 1 + tid; j < n; j += kJacThreads) A[(k - 1) * ld + j] /= r;
+        }
+        const double ip = 1.0 / p;
+        const int m = n - k - 1;  // trailing size
+        for (int idx = tid; idx < m * m; idx += kJacThreads) {
+            const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+            if (j >= i) A[i * ld + j] -= A[k * ld + i] * A[k * ld + j] * ip;
+        }
+        __syncthreads();
+    }
+    {
+        const double r = sqrt(piv[n - 1]);
+        if (tid == 0) A[(n - 1) * ld + (n - 1)] /= r;
+    }
+    __syncthreads();
+    // Column-parallel back substitution: X = R⁻¹ (upper).
+    for (int j = tid; j < n; j += kJacThreads) {
+        for (int i = n - 1; i >= 0; --i) X[i * n + j] = 0.0;
+        X[j * n + j] = 1.0 / A[j * ld + j];
+        for (int i = j - 1; i >= 0; --i) {
+            double acc = 0.0;
+            for (int k = i + 1; k <= j; ++k) acc = fma(A[i * ld + k], X[k * n + j], acc);
+            X[i * n + j] = -acc / A[i * ld + i];
+        }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += kJacThreads) {
+        const int i = idx % n, j = idx / n;
+        Rinv[i + static_cast<int64_t>(j) * ldri] = X[i * n + j];
+    }
+    if (tid == 0 && bad) atomicOr(flag, bad);
 }
 
 // ------------------------------------------------------------------ misc
@@ -379,26 +529,6 @@ int tsqr_block_rows(int64_t cols) {
 }  // namespace
 
 int max_tsqr_cols() { return 96; }
-
-void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc) {
-    if (args.natoms == 0) return;
-    int msum_max = 0;  // Σ_{j≠n} r_j ≤ Σ_j max r
-    msum_max = max_shape * args.order;
-    const int RT = max_shape <= 16 ? 16 : (max_shape <= 32 ? 32 : 64);
-    const size_t smem = sizeof(double) * (static_cast<size_t>(msum_max) * kKrpCT + kKrpJC * kKrpCT + RT * kKrpJC) +
-                        sizeof(int64_t) * kKrpJC + sizeof(int) * kKrpJC * kMaxOrder;
-    dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>(args.order),
-              static_cast<unsigned>((args.s + kKrpCT - 1) / kKrpCT));
-    auto go = [&](auto kern) {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid, kKrpThreads, smem, sc.stream()>>>(args);
-        TS_LAUNCH_CHECK();
-    };
-    if (RT == 16) go(krp_contract_kernel<16>);
-    else if (RT == 32) go(krp_contract_kernel<32>);
-    else go(krp_contract_kernel<64>);
-    sc.launches += 1;
-}
 
 TsqrPlan plan_tsqr(double* A, int64_t lda, int64_t rows, int64_t cols, double* Q, int64_t ldq, CallScratch& sc) {
     TsqrPlan plan;
@@ -532,7 +662,7 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
             if (A < off) continue;
             for (const QrApplyTask& t : p->applies[A - off]) {
                 tasks.push_back(t);
-                smem = std::max(smem, sizeof(double) * static_cast<size_t>(t.rows) * (t.q + 1));
+                smem = std::max(smem, sizeof(double) * (static_cast<size_t>(t.rows) * (t.q + 2) + t.kk));
             }
         }
         if (tasks.empty()) continue;
@@ -541,6 +671,31 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
         TS_LAUNCH_CHECK();
         sc.launches += 1;
     }
+}
+
+void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc) {
+    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * (n + 1) + static_cast<size_t>(n) * n + 2 * ((n + 1) / 2 + 1) + n);
+    static bool configured = false;
+    if (!configured) {
+        TS_CUDA_CHECK(cudaFuncSetAttribute(sym_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
+    sym_jacobi_kernel<<<1, kJacThreads, smem, sc.stream()>>>(C, ldc, n, lambda, V);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
+void launch_chol_inv(const double* G, int64_t ldg, int n, double* Rinv, int64_t ldri, int* flag, bool check_identity,
+                     CallScratch& sc) {
+    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * (n + 1) + static_cast<size_t>(n) * n + n);
+    static bool configured = false;
+    if (!configured) {
+        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
+    chol_inv_kernel<<<1, kJacThreads, smem, sc.stream()>>>(G, ldg, n, Rinv, ldri, flag, check_identity ? 1 : 0);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
 }
 
 void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigma, double* U, CallScratch& sc) {

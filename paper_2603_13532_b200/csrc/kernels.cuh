@@ -81,6 +81,14 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
 // vectors of R, i.e. the left singular vectors of Rᵀ.
 void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigma, double* U, CallScratch& sc);
 
+// Two-sided Jacobi eigensolver of a small symmetric n × n matrix (one CTA):
+// lambda[n] descending, V (n × n, ld n) matching eigenvectors.
+void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc);
+// R⁻¹ of the Cholesky factor of a small SPD G (one CTA); *flag |= 1 on a
+// non-positive pivot, |= 2 when check_identity and max|G - I| > 1e-2.
+void launch_chol_inv(const double* G, int64_t ldg, int n, double* Rinv, int64_t ldri, int* flag, bool check_identity,
+                     CallScratch& sc);
+
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);
 // out[0] = Σ x_i² (single-CTA, deterministic).

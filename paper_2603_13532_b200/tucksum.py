@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = [
     "ts_substream", "ts_gaussian_matrix", "ts_omega_prepare", "ts_krp_sum", "ts_effective_subrank",
     "ts_result_order", "ts_result_dims", "ts_result_ranks", "ts_result_factor", "ts_result_core",
     "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
-    "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing",
+    "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths",
 ]
 
 
@@ -448,6 +448,12 @@ class Engine:
     @property
     def launch_count(self) -> int:
         return int(lib().ts_ctx_launch_count(self.handle))
+
+    def last_paths(self):
+        """(qr_fallback_modes, svd_fallback_modes) of the last krp_sum."""
+        a, b = C.c_int(), C.c_int()
+        _check(lib().ts_ctx_last_paths(self.handle, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
 
     def set_debug(self, on: bool):
         _check(lib().ts_ctx_set_debug(self.handle, C.c_int(1 if on else 0)))

@@ -71,6 +71,23 @@ def test_baseline_cfg5_reduced_parity(engine):
     check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), wl.eps, wl.cap, gram=True)
 
 
+def test_numerical_paths_are_exercised(engine):
+    """CholeskyQR2 must hand exactly rank-deficient sketches (config 3, modes 2-3:
+    rank 10 < s = 50) to Householder TSQR, and ST-HOSVD must take the accurate
+    SVD path whenever the Gram decision is not provably exact."""
+    wl = make_workload(3)
+    seed = (wl.seed.seed, wl.seed.stream)
+    check_pair(engine, wl.summands, wl.weights, wl.widths, seed, wl.eps, wl.cap)
+    qr_fb, _ = engine.last_paths()
+    assert qr_fb >= 2
+    wl1 = make_workload(1)
+    s1 = (wl1.seed.seed, wl1.seed.stream)
+    check_pair(engine, wl1.summands, wl1.weights, wl1.widths, s1, wl1.eps, wl1.cap)
+    assert engine.last_paths() == (0, 0)  # well-conditioned: CholQR2 and Gram fast paths
+    check_pair(engine, wl1.summands, wl1.weights, wl1.widths, s1, 1e-10, None)
+    assert engine.last_paths()[1] >= 1  # tail threshold below the Gram's noise → accurate SVD
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_reference_semantics_eps(engine, cfg):
     """Pure reference semantics (eps > 0, no rank cap) on the same inputs."""
