@@ -5,7 +5,7 @@
 // summands stored once in the stacked formal-sum layout F_j = [U_j^(1) … U_j^(K)]:
 //   A  Z_j = Ω_jᵀ F_j                       grouped TN DMMA GEMM      (sketch.cpp:108-112)
 //   B  W_n[b] = w_b · G_b,(n) · ⊙_{j≠n} M_j  KRP generated in smem      (sketch.cpp:117-130)
-//   C  Y_n = F_n W_n                         grouped NN DMMA GEMM      (sketch.cpp:131)
+//   C  Y_n = F_n W_n                         grouped NT DMMA GEMM (W stored transposed) (sketch.cpp:131)
 //      all-reduce Y over GPUs (NCCL)
 //   D  Û_n = thin Q(Y_n), R_ii >= 0          Householder TSQR          (sketch.cpp:145-150)
 //   E  P_n = Û_nᵀ F_n                        grouped TN DMMA GEMM      (sketch.cpp:157-160)
@@ -275,8 +275,11 @@ std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double the
     if (rank < q) {  // the kept subspace must be well separated from the discarded one
         const double gap = lam[static_cast<size_t>(rank - 1)] - lam[static_cast<size_t>(rank)];
         if (!(gap > 0.0)) return 1;
-        const double err = 2.2e-16 * l1 / gap * std::sqrt(lam[static_cast<size_t>(rank)] / l1);
-        if (err > 1e-12) return 1;
+        // Eigenvector error of the kept subspace ≲ residual / gap with the Jacobi
+        // residual off(C) ≤ 1e-14·‖C‖; its effect on the truncated tensor is damped
+        // by σ_{r+1}/σ₁.  Require it 10× below the 1e-10 parity bar.
+        const double err = 1e-14 * l1 / gap * std::sqrt(lam[static_cast<size_t>(rank)] / l1);
+        if (err > 1e-11) return 1;
     }
     *ok = true;
     return rank;
@@ -372,8 +375,8 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             GemmProblem p{};
             p.A = b->F[n];
             p.lda = dims[n];
-            p.B = W[n];
-            p.ldb = b->R[n];
+            p.B = W[n];  // stored transposed: Wt_n (s × R_n)
+            p.ldb = s;
             p.C = Y + yoff[n];
             p.ldc = dims[n];
             p.M = static_cast<int>(dims[n]);
@@ -381,7 +384,7 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             p.K = static_cast<int>(b->R[n]);
             ps.push_back(p);
         }
-        ts::launch_grouped_gemm(Layout::NN, ps, sc, ctx->num_sms);
+        ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
     }
     mark(ctx, 3);
     if (ctx->comm) nccl_check(nccl_api().AllReduce(Y, Y, static_cast<size_t>(ytot), ncclFloat64, ncclSum, ctx->comm, st),
@@ -455,15 +458,27 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             q2.push_back(m);
         }
         if (any) {
+            ts::CholBatch cb1{}, cb2{};
+            int nb = 0;
+            for (int n = 0; n < d; ++n) {
+                if (!chol[static_cast<size_t>(n)]) continue;
+                cb1.G[nb] = G1[n];
+                cb1.Rinv[nb] = Ri1[n];
+                cb1.flag[nb] = flags + n;
+                cb2.G[nb] = G2[n];
+                cb2.Rinv[nb] = Ri2[n];
+                cb2.flag[nb] = flags + n;
+                ++nb;
+            }
+            cb1.ldg = cb1.ldri = cb2.ldg = cb2.ldri = s;
+            cb1.n = cb2.n = static_cast<int>(s);
+            cb1.check_identity = 0;
+            cb2.check_identity = 1;
             ts::launch_grouped_gemm(Layout::TN, g1, sc, ctx->num_sms);
-            for (int n = 0; n < d; ++n)
-                if (chol[static_cast<size_t>(n)])
-                    ts::launch_chol_inv(G1[n], s, static_cast<int>(s), Ri1[n], s, flags + n, false, sc);
+            ts::launch_chol_inv(cb1, nb, sc);
             ts::launch_grouped_gemm(Layout::NN, q1, sc, ctx->num_sms);
             ts::launch_grouped_gemm(Layout::TN, g2, sc, ctx->num_sms);
-            for (int n = 0; n < d; ++n)
-                if (chol[static_cast<size_t>(n)])
-                    ts::launch_chol_inv(G2[n], s, static_cast<int>(s), Ri2[n], s, flags + n, true, sc);
+            ts::launch_chol_inv(cb2, nb, sc);
             ts::launch_grouped_gemm(Layout::NN, q2, sc, ctx->num_sms);
             std::vector<int> hf(static_cast<size_t>(d), 0);
             TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
@@ -871,10 +886,10 @@ int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_bat
         cudaStream_t st = ctx->stream;
         std::int64_t bytes = 0;
         for (int j = 0; j < d; ++j) {
-            TS_CUDA_CHECK(cudaMalloc(&b->F[j], sizeof(double) * static_cast<size_t>(b->dims[j] * b->R[j])));
+            TS_CUDA_CHECK(cudaMallocAsync(&b->F[j], sizeof(double) * static_cast<size_t>(b->dims[j] * b->R[j]), st));
             bytes += sizeof(double) * b->dims[j] * b->R[j];
         }
-        TS_CUDA_CHECK(cudaMalloc(&b->cores, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(core_elems, 1))));
+        TS_CUDA_CHECK(cudaMallocAsync(&b->cores, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(core_elems, 1)), st));
         bytes += sizeof(double) * core_elems;
         b->core_elems = core_elems;
         // Copies; adjacent host ranges (e.g. one pinned slab per mode) are merged.
@@ -911,10 +926,8 @@ int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_bat
         }
         Run crun;
         std::int64_t coff = 0;
-        b->core_norm.assign(static_cast<size_t>(count), 0.0);
         for (std::int64_t i = 0; i < count; ++i) {
             const ts_tucker_view& x = xs[i];
-            double sq = 0.0;
             for (std::int64_t bl = 0; bl < x.num_blocks; ++bl) {
                 ts::Atom at{};
                 at.summand = static_cast<int>(i);
@@ -926,16 +939,14 @@ int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_bat
                     e *= at.shape[j];
                     b->max_shape = std::max(b->max_shape, at.shape[j]);
                 }
-                for (std::int64_t t = 0; t < e; ++t) sq += x.block_data[bl][t] * x.block_data[bl][t];
                 add(crun, x.block_data[bl], b->cores + coff, e);
                 coff += e;
                 b->atoms.push_back(at);
             }
-            b->core_norm[static_cast<size_t>(i)] = std::sqrt(sq);
             for (int j = 0; j < d; ++j) col[j] += x.ranks[j];
         }
         flush(crun);
-        TS_CUDA_CHECK(cudaMalloc(&b->d_atoms, sizeof(ts::Atom) * b->atoms.size()));
+        TS_CUDA_CHECK(cudaMallocAsync(&b->d_atoms, sizeof(ts::Atom) * b->atoms.size(), st));
         TS_CUDA_CHECK(cudaMemcpyAsync(b->d_atoms, b->atoms.data(), sizeof(ts::Atom) * b->atoms.size(),
                                       cudaMemcpyHostToDevice, st));
         bytes += sizeof(ts::Atom) * b->atoms.size();
@@ -949,11 +960,11 @@ int ts_batch_free(ts_batch* b) {
     return guarded([&] {
         if (!b) return;
         cudaSetDevice(b->ctx->device);
-        cudaStreamSynchronize(b->ctx->stream);
+        cudaStream_t st = b->ctx->stream;  // stream-ordered: safe while kernels are still queued
         for (auto* f : b->F)
-            if (f) cudaFree(f);
-        if (b->cores) cudaFree(b->cores);
-        if (b->d_atoms) cudaFree(b->d_atoms);
+            if (f) cudaFreeAsync(f, st);
+        if (b->cores) cudaFreeAsync(b->cores, st);
+        if (b->d_atoms) cudaFreeAsync(b->d_atoms, st);
         delete b;
     });
 }
@@ -1003,6 +1014,17 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
         ctx->stage.reset();
         CallScratch sc(ctx->stream, ctx->stage);
+        if (b->core_norm.empty()) {  // per-summand ‖core‖_F, computed once on the device
+            double* d_sq = sc.alloc_n<double>(b->atoms.size());
+            ts::launch_atom_sumsq(b->cores, b->d_atoms, static_cast<int>(b->atoms.size()), d, d_sq, sc);
+            std::vector<double> sq(b->atoms.size());
+            TS_CUDA_CHECK(cudaMemcpyAsync(sq.data(), d_sq, sizeof(double) * sq.size(), cudaMemcpyDeviceToHost, ctx->stream));
+            TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            auto* bm = const_cast<ts_batch*>(b);
+            bm->core_norm.assign(static_cast<size_t>(b->count), 0.0);
+            for (size_t a = 0; a < b->atoms.size(); ++a) bm->core_norm[static_cast<size_t>(b->atoms[a].summand)] += sq[a];
+            for (double& v : bm->core_norm) v = std::sqrt(v);
+        }
         std::vector<double> energy(static_cast<size_t>(b->count));
         for (std::int64_t i = 0; i < b->count; ++i)
             energy[static_cast<size_t>(i)] = std::fabs(weights[i]) * b->core_norm[static_cast<size_t>(i)];

@@ -300,6 +300,10 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 }  // namespace
 
 int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallScratch& sc, int num_sms) {
+    {
+        int launched = 0;
+        if (probs.size() <= 16 && launch_tma_gemm(layout, probs, sc, num_sms, &launched)) return launched;
+    }
     const int cfg = config_for(layout);
     const TileCfg tc = kCfgs[cfg];
     const int64_t slots = static_cast<int64_t>(num_sms) * occupancy(layout, cfg);

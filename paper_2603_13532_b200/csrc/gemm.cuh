@@ -48,6 +48,13 @@ struct GemmProblem {
 // Plans tiles/splits, uploads descriptors and launches the grouped GEMM (+ the
 // split-K reduction when needed) on the scratch's stream.  `scratch` provides device memory
 // for descriptors and split-K partials.  Returns the number of kernels launched.
+// TMA + mbarrier warp-specialised path (gemm_tma.cu) for TN / NT problems with
+// 16-byte aligned operands, even leading dimensions and batch 1.  Returns false
+// without launching anything when the problems do not qualify.
+bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallScratch& sc, int num_sms,
+                     int* launched);
+bool tma_gemm_enabled();
+
 int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallScratch& scratch,
                         int num_sms);
 

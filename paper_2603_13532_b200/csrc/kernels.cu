@@ -217,6 +217,17 @@ __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTas
 constexpr int kJacThreads = 1024;
 constexpr int kJacWarps = kJacThreads / 32;
 
+// Jacobi rotation (c, s) zeroing the off-diagonal of [[a, g], [g, b]] (the
+// reference formula of oracle sym_eig / one-sided Jacobi): θ = (b - a)/(2g),
+// t = sign(θ)/(|θ| + sqrt(1 + θ²)), c = 1/sqrt(1 + t²), s = t·c — written with
+// reciprocal / rsqrt so the dependent chain of slow fp64 ops stays short.
+__device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& c, double& s, double& t) {
+    const double theta = (b - a) * __drcp_rn(2.0 * g);
+    t = copysign(__drcp_rn(fabs(theta) + sqrt(fma(theta, theta, 1.0))), theta);
+    c = rsqrt(fma(t, t, 1.0));
+    s = t * c;
+}
+
 __device__ __forceinline__ void pair_of(int r, int pi, int np, int* p, int* q) {
     int a, b;
     if (pi == 0) {
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
     for (int idx = tid; idx < nc * nc; idx += kJacThreads) J[idx] = (idx % nc == idx / nc) ? 1.0 : 0.0;
     const int np = nc + (nc & 1);
     const double tol = 1e-15;
-    for (int sweep = 0; sweep < 80; ++sweep) {
+    for (int sweep = 0; sweep < 30; ++sweep) {  // LAPACK dgesvj caps at 30 sweeps
         __syncthreads();
         for (int c = warp; c < nc; c += kJacWarps) {  // exact norms once per sweep
             double a = 0.0;
@@ -282,9 +293,8 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
                 ga = warp_sum(ga);
                 const double al = nrm[p], be = nrm[q];
                 if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
-                const double zeta = (be - al) / (2.0 * ga);
-                const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                double c, s, t;
+                jacobi_rotation(al, be, ga, c, s, t);
                 for (int i = lane; i < m; i += 32) {
                     const double x = wp[i], y = wq[i];
                     wp[i] = c * x - s * y;
@@ -340,6 +350,27 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
     }
     const int np = n + (n & 1);
     const double tol = 1e-15;
+    // Absolute floor: off-diagonal entries below 1e-16·max|a_ii| sit under the
+    // Gram's own rounding noise; rotating them only burns sweeps.
+    __shared__ double amax_s;
+    if (tid == 0) amax_s = 0.0;
+    __syncthreads();
+    {
+        double m = 0.0;
+        for (int i = tid; i < n; i += kJacThreads) m = fmax(m, fabs(A[i * ld + i]));
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((tid & 31) == 0 && m > 0.0)
+            atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(m));
+    }
+    __syncthreads();
+    const double abs_floor = 1e-16 * amax_s;
+    __shared__ double red[2 * kJacWarps];
+    __shared__ double prev_off;
+    __shared__ int stop;
+    if (tid == 0) {
+        prev_off = 0.0;
+        stop = 0;
+    }
     for (int sweep = 0; sweep < 60; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
@@ -351,11 +382,9 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
                 double c = 1.0, s = 0.0;
                 if (q < n) {
                     const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
-                    if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
-                        const double theta = (aqq - app) / (2.0 * apq);
-                        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
+                    if (fabs(apq) > abs_floor && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
+                        double t;
+                        jacobi_rotation(app, aqq, apq, c, s, t);
                         if (lane == 0) rotated = 1;
                     }
                     if (s != 0.0)
@@ -389,23 +418,56 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
             __syncthreads();
         }
         if (!rotated) break;
+        // Stop at working precision: off(A) ≤ n·1e-16·‖A‖_F, or once the
+        // (asymptotically quadratic) decrease stalls on rounding noise.
+        {
+            double off = 0.0, tot = 0.0;
+            for (int idx = tid; idx < n * n; idx += kJacThreads) {
+                const int i = idx % n, j = idx / n;
+                const double a = A[i * ld + j];
+                tot = fma(a, a, tot);
+                if (i != j) off = fma(a, a, off);
+            }
+            off = warp_sum(off);
+            tot = warp_sum(tot);
+            if (lane == 0) {
+                red[2 * warp] = off;
+                red[2 * warp + 1] = tot;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double o = 0.0, t = 0.0;
+                for (int w = 0; w < kJacWarps; ++w) {
+                    o += red[2 * w];
+                    t += red[2 * w + 1];
+                }
+                stop = (o <= 1e-28 * t) || (sweep >= 2 && o > 0.25 * prev_off);  // off(A) ≤ 1e-14·‖A‖_F
+                prev_off = o;
+            }
+            __syncthreads();
+            if (stop) break;
+        }
     }
     for (int i = tid; i < n; i += kJacThreads) diag[i] = A[i * ld + i];
     __syncthreads();
     sort_desc_store(diag, Vs, n, lambda, V);
 }
 
-// Cholesky R (upper, RᵀR = G) of a small SPD matrix and its inverse R⁻¹.
-// flag[0] |= 1 when a pivot is not safely positive, |= 2 when check_identity
-// and max|G - I| > 1e-2 (second CholQR pass on a badly conditioned input).
-__global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int n,
-                                                               double* __restrict__ Rinv, int64_t ldri,
-                                                               int* __restrict__ flag, int check_identity) {
+// Cholesky R (upper, RᵀR = G) of small SPD matrices and their inverses R⁻¹, one
+// CTA per matrix (blockIdx.x indexes the batch).  flag[b] |= 1 when a pivot is
+// not safely positive, |= 2 when check_identity and max|G - I| > 1e-2 (second
+// CholQR pass on a badly conditioned input).  The inverse is formed by recursive
+// 2×2 block doubling (X12 = -X11·R12·X22), i.e. log2(n) parallel levels instead
+// of an n-step back substitution.
+__global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(CholBatch cb) {
+    const int b = blockIdx.x;
+    const int n = cb.n;
+    const double* __restrict__ G = cb.G[b];
     extern __shared__ __align__(16) double sm[];
     const int ld = n + 1;
-    double* A = sm;          // n × ld, A[i*ld + j] (upper part used)
-    double* X = A + n * ld;  // n × n inverse, X[i*n + j]
-    double* piv = X + n * n; // n
+    double* A = sm;              // n × ld, A[i*ld + j]: R (upper)
+    double* X = A + n * ld;      // n × ld: R⁻¹ in the upper part, level scratch T (transposed) below
+    double* piv = X + n * ld;    // n
     __shared__ int bad;
     __shared__ double dmax;
     const int tid = threadIdx.x;
@@ -417,20 +479,19 @@ __global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(const double* __r
     double dev = 0.0, dm = 0.0;
     for (int idx = tid; idx < n * n; idx += kJacThreads) {
         const int i = idx % n, j = idx / n;
-        const double g = G[i + static_cast<int64_t>(j) * ldg];
-        A[i * ld + j] = g;
+        const double g = G[i + static_cast<int64_t>(j) * cb.ldg];
         dev = fmax(dev, fabs(g - (i == j ? 1.0 : 0.0)));
         if (i == j) dm = fmax(dm, g);
+        A[i * ld + j] = g;
+        X[i * ld + j] = 0.0;
     }
-    if (check_identity && dev > 1e-2) atomicOr(&bad, 2);
-    // max diagonal (for a relative pivot floor)
+    if (cb.check_identity && dev > 1e-2) atomicOr(&bad, 2);
     for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-    if ((tid & 31) == 0 && dm > 0) {
-        unsigned long long* p = reinterpret_cast<unsigned long long*>(&dmax);
-        atomicMax(p, __double_as_longlong(dm));  // positive doubles order like their bit patterns
-    }
+    if ((tid & 31) == 0 && dm > 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(&dmax), __double_as_longlong(dm));
     __syncthreads();
-    const double floor_piv = 1e-28 * dmax;  // κ(Y) ≲ 1e14 for the pivot test; the CholQR2 check catches the rest
+    const double floor_piv = 1e-28 * dmax;
+    // Right-looking Cholesky; the scaling of row k-1 is deferred into step k.
     for (int k = 0; k < n; ++k) {
         double p = A[k * ld + k];
         if (!(p > floor_piv)) {
@@ -438,39 +499,53 @@ __global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(const double* __r
             p = fmax(dmax, 1.0);
         }
         if (tid == 0) piv[k] = p;
-        if (k > 0) {  // deferred scaling of row k-1
+        if (k > 0) {
             const double r = sqrt(piv[k - 1]);
             for (int j = k - 1 + tid; j < n; j += kJacThreads) A[(k - 1) * ld + j] /= r;
         }
         const double ip = 1.0 / p;
-        const int m = n - k - 1;  // trailing size
+        const int m = n - k - 1;
         for (int idx = tid; idx < m * m; idx += kJacThreads) {
             const int i = k + 1 + idx / m, j = k + 1 + idx % m;
             if (j >= i) A[i * ld + j] -= A[k * ld + i] * A[k * ld + j] * ip;
         }
         __syncthreads();
     }
-    {
-        const double r = sqrt(piv[n - 1]);
-        if (tid == 0) A[(n - 1) * ld + (n - 1)] /= r;
-    }
+    if (tid == 0) A[(n - 1) * ld + (n - 1)] /= sqrt(piv[n - 1]);
     __syncthreads();
-    // Column-parallel back substitution: X = R⁻¹ (upper).
-    for (int j = tid; j < n; j += kJacThreads) {
-        for (int i = n - 1; i >= 0; --i) X[i * n + j] = 0.0;
-        X[j * n + j] = 1.0 / A[j * ld + j];
-        for (int i = j - 1; i >= 0; --i) {
+    for (int i = tid; i < n; i += kJacThreads) X[i * ld + i] = 1.0 / A[i * ld + i];
+    __syncthreads();
+    // Block doubling: for diagonal pairs (o, o+bs), X12 = -X11 · (R12 · X22).
+    for (int bs = 1; bs < n; bs <<= 1) {
+        const int pairs = (n + 2 * bs - 1) / (2 * bs);
+        const int per = bs * bs;
+        for (int idx = tid; idx < pairs * per; idx += kJacThreads) {
+            const int pr = idx / per, e = idx % per;
+            const int o = pr * 2 * bs, i = e % bs, j = e / bs;
+            const int r = o + i, c = o + bs + j;
+            if (c >= n) continue;
             double acc = 0.0;
-            for (int k = i + 1; k <= j; ++k) acc = fma(A[i * ld + k], X[k * n + j], acc);
-            X[i * n + j] = -acc / A[i * ld + i];
+            for (int k = o + bs; k <= c; ++k) acc = fma(A[r * ld + k], X[k * ld + c], acc);
+            X[c * ld + r] = acc;  // T(r, c) kept transposed in the free lower triangle
         }
+        __syncthreads();
+        for (int idx = tid; idx < pairs * per; idx += kJacThreads) {
+            const int pr = idx / per, e = idx % per;
+            const int o = pr * 2 * bs, i = e % bs, j = e / bs;
+            const int r = o + i, c = o + bs + j;
+            if (c >= n) continue;
+            double acc = 0.0;
+            for (int k = r; k < o + bs; ++k) acc = fma(X[r * ld + k], X[c * ld + k], acc);
+            X[r * ld + c] = -acc;
+        }
+        __syncthreads();
     }
-    __syncthreads();
+    double* Rinv = cb.Rinv[b];
     for (int idx = tid; idx < n * n; idx += kJacThreads) {
         const int i = idx % n, j = idx / n;
-        Rinv[i + static_cast<int64_t>(j) * ldri] = X[i * n + j];
+        Rinv[i + static_cast<int64_t>(j) * cb.ldri] = i <= j ? X[i * ld + j] : 0.0;
     }
-    if (tid == 0 && bad) atomicOr(flag, bad);
+    if (tid == 0 && bad) atomicOr(cb.flag[b], bad);
 }
 
 // ------------------------------------------------------------------ misc
@@ -529,6 +604,34 @@ int tsqr_block_rows(int64_t cols) {
 }  // namespace
 
 int max_tsqr_cols() { return 96; }
+
+namespace {
+__global__ void atom_sumsq_kernel(const double* __restrict__ cores, const Atom* __restrict__ atoms, int order,
+                                  double* __restrict__ out) {
+    const Atom& at = atoms[blockIdx.x];
+    int64_t e = 1;
+    for (int j = 0; j < order; ++j) e *= at.shape[j];
+    const double* c = cores + at.core_off;
+    __shared__ double part[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < e; i += blockDim.x) s = fma(c[i], c[i], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < blockDim.x / 32 ? part[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) out[blockIdx.x] = v;
+    }
+}
+}  // namespace
+
+void launch_atom_sumsq(const double* cores, const Atom* atoms, int natoms, int order, double* out, CallScratch& sc) {
+    if (natoms <= 0) return;
+    atom_sumsq_kernel<<<natoms, 256, 0, sc.stream()>>>(cores, atoms, order, out);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
 
 TsqrPlan plan_tsqr(double* A, int64_t lda, int64_t rows, int64_t cols, double* Q, int64_t ldq, CallScratch& sc) {
     TsqrPlan plan;
@@ -685,15 +788,15 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
     sc.launches += 1;
 }
 
-void launch_chol_inv(const double* G, int64_t ldg, int n, double* Rinv, int64_t ldri, int* flag, bool check_identity,
-                     CallScratch& sc) {
-    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * (n + 1) + static_cast<size_t>(n) * n + n);
+void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
+    if (count <= 0) return;
+    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(cb.n) * (cb.n + 1) + cb.n);
     static bool configured = false;
     if (!configured) {
         TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    chol_inv_kernel<<<1, kJacThreads, smem, sc.stream()>>>(G, ldg, n, Rinv, ldri, flag, check_identity ? 1 : 0);
+    chol_inv_kernel<<<count, kJacThreads, smem, sc.stream()>>>(cb);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }

@@ -28,7 +28,7 @@ struct Atom {
 // chunk by chunk and never reaches HBM.
 struct KrpArgs {
     const double* Z[kMaxOrder];
-    double* W[kMaxOrder];
+    double* W[kMaxOrder];  // Wt_n: s × R_n column-major (transposed W_n)
     int64_t R[kMaxOrder];
     int order;
     int s;
@@ -84,10 +84,18 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigm
 // Two-sided Jacobi eigensolver of a small symmetric n × n matrix (one CTA):
 // lambda[n] descending, V (n × n, ld n) matching eigenvectors.
 void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc);
-// R⁻¹ of the Cholesky factor of a small SPD G (one CTA); *flag |= 1 on a
-// non-positive pivot, |= 2 when check_identity and max|G - I| > 1e-2.
-void launch_chol_inv(const double* G, int64_t ldg, int n, double* Rinv, int64_t ldri, int* flag, bool check_identity,
-                     CallScratch& sc);
+// R⁻¹ of the Cholesky factor of small SPD matrices G[b] (n ≤ 96, one CTA each);
+// *flag[b] |= 1 on a non-positive pivot, |= 2 when check_identity and
+// max|G - I| > 1e-2.
+struct CholBatch {
+    const double* G[kMaxOrder];
+    double* Rinv[kMaxOrder];
+    int* flag[kMaxOrder];
+    int64_t ldg, ldri;
+    int n;
+    int check_identity;
+};
+void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc);
 
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);
@@ -97,6 +105,9 @@ void launch_sumsq(const double* x, int64_t n, double* out, CallScratch& sc);
 // out = F·diag(scale) (n × R, ld n) or its transpose (R × n, ld R) when transpose.
 void launch_scale_columns(const double* F, int64_t n, int64_t R, const double* scale, double* out, bool transpose,
                           CallScratch& sc);
+
+// out[a] = Σ core(atom a)² (one CTA per atom, deterministic).
+void launch_atom_sumsq(const double* cores, const Atom* atoms, int natoms, int order, double* out, CallScratch& sc);
 
 int max_tsqr_cols();
 

@@ -8,7 +8,9 @@
 // One CTA per (atom, mode, 64 sketch columns): the M_j slices sit in shared
 // memory, each 16-row chunk of K_n is generated there (never in HBM), the
 // matching 16 columns of G_(n) are gathered from the core (prefetched into
-// registers one chunk ahead), and the product runs on DMMA.8x8x4.
+// registers one chunk ahead), and the product runs on DMMA.8x8x4.  The result
+// is stored transposed, Wt_n (s × R_n), so stage C reads both of its operands
+// along their non-reduction dimension (gemm_tma.cu MN scheme).
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -82,7 +84,6 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
     const double w = args.weights[at.summand];
     const double* __restrict__ core = args.cores + at.core_off;
     double* Wn = args.W[n];
-    const int64_t Rn = args.R[n];
 
     auto decode = [&](int64_t chunk, int buf) {
         if (tid < kJC) {
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
                 for (int h = 0; h < 2; ++h) {
                     const int a = a0 + wm * WM + i * 8 + g;
                     const int cg = c0 + wn * WN + j * 8 + 2 * t + h;
-                    if (a < rn && cg < s) Wn[(col[n] + a) + static_cast<int64_t>(cg) * Rn] = w * acc[i][j][h];
+                    if (a < rn && cg < s) Wn[cg + static_cast<int64_t>(col[n] + a) * s] = w * acc[i][j][h];
                 }
     }
 }
