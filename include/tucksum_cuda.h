@@ -115,6 +115,12 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
 int ts_effective_subrank(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps,
                          const int64_t* oversampling, int64_t* effective_ranks, int64_t* targets, int64_t* widths);
 
+/* Small symmetric eigensolver used by ST-HOSVD's fast path (reference sym_eig,
+ * src/kernels.cpp:70-86): a (n × n, column-major, host), n <= 96 → values
+ * (descending) and column eigenvectors (host).  sweeps / ms (nullable) report
+ * the Jacobi sweeps and the kernel time. */
+int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms);
+
 /* ---- result: a dense-core Tucker tensor owned by the library ---- */
 int64_t ts_result_order(const ts_result* r);
 void ts_result_dims(const ts_result* r, int64_t* dims);

@@ -1102,6 +1102,38 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
     });
 }
 
+// Symmetric eigensolver of the ST-HOSVD fast path (reference sym_eig,
+// src/kernels.cpp:70-86): host in / host out; also reports sweeps and kernel ms.
+int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms) {
+    return guarded([&] {
+        if (!ctx || n < 1 || n > ts::max_tsqr_cols()) invalid("ts_sym_eig: need 1 <= n <= 96");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->stage.reset();
+        CallScratch sc(ctx->stream, ctx->stage);
+        auto* dA = static_cast<double*>(sc.upload(a, sizeof(double) * static_cast<size_t>(n * n)));
+        double* dl = sc.alloc_n<double>(static_cast<size_t>(n));
+        double* dV = sc.alloc_n<double>(static_cast<size_t>(n * n));
+        int* dsw = sc.alloc_n<int>(1);
+        cudaEvent_t e0, e1;
+        TS_CUDA_CHECK(cudaEventCreate(&e0));
+        TS_CUDA_CHECK(cudaEventCreate(&e1));
+        TS_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        ts::launch_sym_jacobi(dA, n, static_cast<int>(n), dl, dV, sc, dsw);
+        TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        int hs = 0;
+        TS_CUDA_CHECK(cudaMemcpyAsync(values, dl, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(vectors, dV, sizeof(double) * static_cast<size_t>(n * n), cudaMemcpyDeviceToHost, ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(&hs, dsw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        float t = 0.f;
+        TS_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (sweeps) *sweeps = hs;
+        if (ms) *ms = t;
+    });
+}
+
 int64_t ts_result_order(const ts_result* r) { return r ? r->order : 0; }
 void ts_result_dims(const ts_result* r, int64_t* dims) {
     for (int n = 0; n < r->order; ++n) dims[n] = r->dims[n];

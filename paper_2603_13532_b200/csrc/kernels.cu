@@ -217,14 +217,39 @@ __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTas
 constexpr int kJacThreads = 1024;
 constexpr int kJacWarps = kJacThreads / 32;
 
-// Jacobi rotation (c, s) zeroing the off-diagonal of [[a, g], [g, b]] (the
-// reference formula of oracle sym_eig / one-sided Jacobi): θ = (b - a)/(2g),
-// t = sign(θ)/(|θ| + sqrt(1 + θ²)), c = 1/sqrt(1 + t²), s = t·c — written with
-// reciprocal / rsqrt so the dependent chain of slow fp64 ops stays short.
+__device__ __forceinline__ double rcp_approx(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+__device__ __forceinline__ double rsqrt_approx(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
+// Jacobi rotation (c, s) for [[a, g], [g, b]] (the reference formula of the
+// oracle's sym_eig / one-sided Jacobi): θ = (b - a)/(2g), t = sign(θ)/(|θ| +
+// sqrt(1 + θ²)), c = 1/sqrt(1 + t²), s = t·c.  The rounds of a Jacobi sweep are
+// sequential, so this chain is the solver's critical path: t is formed with the
+// ~20-bit MUFU approximations (an angle that annihilates g to ~1e-6 relative is
+// all the iteration needs), while c is Newton-refined to full precision so every
+// applied rotation is orthogonal to working accuracy (c² + s² = 1 ± 1 ulp).
 __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, double& c, double& s, double& t) {
-    const double theta = (b - a) * __drcp_rn(2.0 * g);
-    t = copysign(__drcp_rn(fabs(theta) + sqrt(fma(theta, theta, 1.0))), theta);
-    c = rsqrt(fma(t, t, 1.0));
+    const double theta = (b - a) * rcp_approx(2.0 * g);
+    const double at = fabs(theta);
+    if (at > 1e150) {
+        t = 0.5 * rcp_approx(theta);
+    } else {
+        const double u = fma(theta, theta, 1.0);
+        const double sq = u * rsqrt_approx(u);
+        t = copysign(rcp_approx(at + sq), theta);
+    }
+    const double w = fma(t, t, 1.0);
+    double r = rsqrt_approx(w);
+    r = r * fma(-0.5 * w, r * r, 1.5);
+    r = r * fma(-0.5 * w, r * r, 1.5);
+    c = r;
     s = t * c;
 }
 
@@ -330,127 +355,202 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
 }
 
 // Two-sided cyclic Jacobi eigensolver for a small symmetric n × n matrix C
-// (fast path of ST-HOSVD on the Gram of an unfolding).  Each round applies the
-// rotations of n/2 disjoint pairs: rows first (Jᵀ·A), then columns (A·J) and
-// the eigenvector columns.  Outputs eigenvalues (descending) and vectors.
+// (fast path of ST-HOSVD on the Gram of an unfolding), one CTA.
+//
+// The matrix is padded to an even order np (a zero row/column for odd n) and
+// each round rotates np/2 disjoint pairs at once.  Instead of a row pass and a
+// column pass, the round is applied block-wise: with pairs P_i = (p_i, q_i) and
+// their 2×2 rotations R_i, every 2×2 block A[P_i, P_j] becomes R_iᵀ·A[P_i,P_j]·R_j.
+// One thread owns one block (np = 64: 32×32 blocks = the 1024 threads), so a
+// round is: rotation parameters (one thread per pair) → barrier → all blocks
+// and the eigenvector columns updated in one pass → barrier.
 __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* __restrict__ Cin, int64_t ldc, int n,
-                                                                 double* __restrict__ lambda, double* __restrict__ V) {
+                                                                 double* __restrict__ lambda, double* __restrict__ V,
+                                                                 int* __restrict__ sweeps_out) {
     extern __shared__ __align__(16) double sm[];
-    const int ld = n + 1;                   // padded row stride
-    double* A = sm;                          // n × ld (A[i*ld + j])
-    double* Vs = A + n * ld;                 // n × n (column j at j*n)
-    double* cs = Vs + n * n;                 // 2 per pair
-    double* diag = cs + 2 * ((n + 1) / 2 + 1);
-    __shared__ int rotated;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int idx = tid; idx < n * n; idx += kJacThreads) {
-        const int i = idx % n, j = idx / n;
-        A[i * ld + j] = 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc]);
-        Vs[idx] = (i == j) ? 1.0 : 0.0;
-    }
     const int np = n + (n & 1);
-    const double tol = 1e-15;
-    // Absolute floor: off-diagonal entries below 1e-16·max|a_ii| sit under the
-    // Gram's own rounding noise; rotating them only burns sweeps.
-    __shared__ double amax_s;
-    if (tid == 0) amax_s = 0.0;
+    const int npair = np / 2;
+    const int ld = np + 1;                        // padded row stride
+    double* A = sm;                               // np × ld
+    double* Vs = A + np * ld;                     // np × ld, Vs[k*ld + j] = V(k, j)
+    double* csv = Vs + np * ld;                   // 2 per pair
+    double* diag = csv + 2 * npair;               // np
+    int* sched = reinterpret_cast<int*>(diag + np);  // (np-1) × npair packed (p | q << 16)
+    __shared__ int rotated, stop;
+    __shared__ double red[2 * kJacWarps];
+    __shared__ double prev_off, amax_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int idx = tid; idx < np * np; idx += kJacThreads) {
+        const int i = idx % np, j = idx / np;
+        double v = 0.0;
+        if (i < n && j < n) v = 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc]);
+        A[i * ld + j] = v;
+        Vs[i * ld + j] = (i == j) ? 1.0 : 0.0;
+    }
+    for (int idx = tid; idx < (np - 1) * npair; idx += kJacThreads) {
+        const int r = idx / npair, pi = idx % npair;
+        int p, q;
+        pair_of(r, pi, np, &p, &q);
+        sched[idx] = p | (q << 16);
+    }
+    if (tid == 0) {
+        amax_s = 0.0;
+        prev_off = 0.0;
+        stop = 0;
+    }
     __syncthreads();
     {
         double m = 0.0;
         for (int i = tid; i < n; i += kJacThreads) m = fmax(m, fabs(A[i * ld + i]));
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if ((tid & 31) == 0 && m > 0.0)
-            atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(m));
+        if (lane == 0 && m > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(m));
     }
     __syncthreads();
-    const double abs_floor = 1e-16 * amax_s;
-    __shared__ double red[2 * kJacWarps];
-    __shared__ double prev_off;
-    __shared__ int stop;
-    if (tid == 0) {
-        prev_off = 0.0;
-        stop = 0;
+    // Entries below 1e-15·max|a_ii| sit under the Gram's own rounding noise (the
+    // fast path needs absolute accuracy only); rotating them only burns sweeps.
+    const double abs_floor = 1e-15 * amax_s;
+    const double tol = 1e-15;
+    // Per-thread work list fixed for the whole solve (no divisions in the loop):
+    // upper-triangular blocks (bi ≤ bj) of the pair grid, and (row, pair) items of V.
+    constexpr int kMaxBlk = 2, kMaxV = 5;  // np ≤ 96: 1176 blocks, 4608 V items
+    int blk_i[kMaxBlk], blk_j[kMaxBlk], vk[kMaxV], vp[kMaxV];
+    int nb = 0, nv = 0;
+    {
+        const int nub = npair * (npair + 1) / 2;
+        for (int b = tid; b < nub && nb < kMaxBlk; b += kJacThreads) {
+            int bi = 0, rem = b;
+            while (rem >= npair - bi) {
+                rem -= npair - bi;
+                ++bi;
+            }
+            blk_i[nb] = bi;
+            blk_j[nb] = bi + rem;
+            ++nb;
+        }
+        for (int e = tid; e < np * npair && nv < kMaxV; e += kJacThreads) {
+            vk[nv] = e % np;
+            vp[nv] = e / np;
+            ++nv;
+        }
     }
-    for (int sweep = 0; sweep < 60; ++sweep) {
+    const int m = np - 1;
+    // Round-robin pairing of round r, pair i (cf. pair_of) without divisions.
+    auto pair_at = [m](int r, int i, int& p, int& q) {
+        int a, b;
+        if (i == 0) {
+            a = m;
+            b = r;
+        } else {
+            a = r + i;
+            a -= (a >= m) ? m : 0;
+            b = r - i;
+            b += (b < 0) ? m : 0;
+        }
+        p = min(a, b);
+        q = max(a, b);
+    };
+    double2* cs2 = reinterpret_cast<double2*>(csv);
+    int sweeps_done = 0;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        sweeps_done = sweep + 1;
         if (tid == 0) rotated = 0;
-        __syncthreads();
-        for (int r = 0; r < np - 1; ++r) {
-            // Phase 1: rotation parameters + row update (rows of a pair are disjoint).
-            for (int pi = warp; pi < np / 2; pi += kJacWarps) {
+        for (int r = 0; r < m; ++r) {
+            if (tid < npair) {
                 int p, q;
-                pair_of(r, pi, np, &p, &q);
+                pair_at(r, tid, p, q);
+                const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
                 double c = 1.0, s = 0.0;
-                if (q < n) {
-                    const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
-                    if (fabs(apq) > abs_floor && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
-                        double t;
-                        jacobi_rotation(app, aqq, apq, c, s, t);
-                        if (lane == 0) rotated = 1;
-                    }
-                    if (s != 0.0)
-                        for (int k = lane; k < n; k += 32) {
-                            const double x = A[p * ld + k], y = A[q * ld + k];
-                            A[p * ld + k] = c * x - s * y;
-                            A[q * ld + k] = s * x + c * y;
-                        }
+                if (fabs(apq) > abs_floor && apq * apq > tol * tol * fabs(app * aqq)) {
+                    double t;
+                    jacobi_rotation(app, aqq, apq, c, s, t);
+                    rotated = 1;
                 }
-                if (lane == 0) {
-                    cs[2 * pi] = c;
-                    cs[2 * pi + 1] = s;
-                }
+                cs2[tid] = make_double2(c, s);
             }
             __syncthreads();
-            // Phase 2: column update of A and V.
-            for (int pi = warp; pi < np / 2; pi += kJacWarps) {
-                int p, q;
-                pair_of(r, pi, np, &p, &q);
-                const double c = cs[2 * pi], s = cs[2 * pi + 1];
-                if (q >= n || s == 0.0) continue;
-                for (int k = lane; k < n; k += 32) {
-                    const double x = A[k * ld + p], y = A[k * ld + q];
-                    A[k * ld + p] = c * x - s * y;
-                    A[k * ld + q] = s * x + c * y;
-                    const double vx = Vs[k + p * n], vy = Vs[k + q * n];
-                    Vs[k + p * n] = c * vx - s * vy;
-                    Vs[k + q * n] = s * vx + c * vy;
+            for (int u = 0; u < nb; ++u) {
+                const int bi = blk_i[u], bj = blk_j[u];
+                const double2 r1 = cs2[bi], r2 = cs2[bj];
+                if (r1.y == 0.0 && r2.y == 0.0) continue;
+                int p1, q1, p2, q2;
+                pair_at(r, bi, p1, q1);
+                pair_at(r, bj, p2, q2);
+                const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
+                const double a11 = A[p1 * ld + p2], a12 = A[p1 * ld + q2];
+                const double a21 = A[q1 * ld + p2], a22 = A[q1 * ld + q2];
+                // rows: Rᵀ·B with R = [[c, s], [-s, c]], then columns: ·R
+                const double b11 = c1 * a11 - s1 * a21, b12 = c1 * a12 - s1 * a22;
+                const double b21 = s1 * a11 + c1 * a21, b22 = s1 * a12 + c1 * a22;
+                const double d11 = c2 * b11 - s2 * b12, d12 = s2 * b11 + c2 * b12;
+                const double d21 = c2 * b21 - s2 * b22, d22 = s2 * b21 + c2 * b22;
+                if (bi == bj) {  // diagonal block: keep the (tiny) residual of the approximate angle
+                    const double off = 0.5 * (d12 + d21);
+                    A[p1 * ld + p1] = d11;
+                    A[q1 * ld + q1] = d22;
+                    A[p1 * ld + q1] = off;
+                    A[q1 * ld + p1] = off;
+                } else {  // block and its mirror image
+                    A[p1 * ld + p2] = d11;
+                    A[p1 * ld + q2] = d12;
+                    A[q1 * ld + p2] = d21;
+                    A[q1 * ld + q2] = d22;
+                    A[p2 * ld + p1] = d11;
+                    A[q2 * ld + p1] = d12;
+                    A[p2 * ld + q1] = d21;
+                    A[q2 * ld + q1] = d22;
                 }
+            }
+            for (int u = 0; u < nv; ++u) {  // eigenvector columns: V·R
+                const double2 rr = cs2[vp[u]];
+                if (rr.y == 0.0) continue;
+                int p, q;
+                pair_at(r, vp[u], p, q);
+                const int k = vk[u];
+                const double x = Vs[k * ld + p], y = Vs[k * ld + q];
+                Vs[k * ld + p] = rr.x * x - rr.y * y;
+                Vs[k * ld + q] = rr.y * x + rr.x * y;
             }
             __syncthreads();
         }
         if (!rotated) break;
-        // Stop at working precision: off(A) ≤ n·1e-16·‖A‖_F, or once the
-        // (asymptotically quadratic) decrease stalls on rounding noise.
-        {
-            double off = 0.0, tot = 0.0;
-            for (int idx = tid; idx < n * n; idx += kJacThreads) {
-                const int i = idx % n, j = idx / n;
-                const double a = A[i * ld + j];
-                tot = fma(a, a, tot);
-                if (i != j) off = fma(a, a, off);
-            }
-            off = warp_sum(off);
-            tot = warp_sum(tot);
-            if (lane == 0) {
-                red[2 * warp] = off;
-                red[2 * warp + 1] = tot;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                double o = 0.0, t = 0.0;
-                for (int w = 0; w < kJacWarps; ++w) {
-                    o += red[2 * w];
-                    t += red[2 * w + 1];
-                }
-                stop = (o <= 1e-28 * t) || (sweep >= 2 && o > 0.25 * prev_off);  // off(A) ≤ 1e-14·‖A‖_F
-                prev_off = o;
-            }
-            __syncthreads();
-            if (stop) break;
+        // Stop at off(A) ≤ 1e-14·‖A‖_F, or once stalled on rounding noise ≤ 1e-12·‖A‖_F.
+        double off = 0.0, tot = 0.0;
+        for (int idx = tid; idx < np * np; idx += kJacThreads) {
+            const int i = idx % np, j = idx / np;
+            const double a = A[i * ld + j];
+            tot = fma(a, a, tot);
+            if (i != j) off = fma(a, a, off);
         }
+        off = warp_sum(off);
+        tot = warp_sum(tot);
+        if (lane == 0) {
+            red[2 * warp] = off;
+            red[2 * warp + 1] = tot;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double o = 0.0, t = 0.0;
+            for (int w = 0; w < kJacWarps; ++w) {
+                o += red[2 * w];
+                t += red[2 * w + 1];
+            }
+            stop = (o <= 1e-28 * t) || (o <= 1e-24 * t && o > 0.25 * prev_off);
+            prev_off = o;
+        }
+        __syncthreads();
+        if (stop) break;
     }
-    for (int i = tid; i < n; i += kJacThreads) diag[i] = A[i * ld + i];
+    for (int i = tid; i < np; i += kJacThreads) diag[i] = i < n ? A[i * ld + i] : -INFINITY;
+    if (tid == 0 && sweeps_out) *sweeps_out = sweeps_done;
     __syncthreads();
-    sort_desc_store(diag, Vs, n, lambda, V);
+    // Stable descending order of the n real eigenvalues (the padding sorts last).
+    for (int c = tid; c < n; c += kJacThreads) {
+        const double v = diag[c];
+        int rank = 0;
+        for (int i = 0; i < n; ++i) rank += (diag[i] > v) || (diag[i] == v && i < c);
+        lambda[rank] = v;
+        for (int i = 0; i < n; ++i) V[i + static_cast<int64_t>(rank) * n] = Vs[i * ld + c];
+    }
 }
 
 // Cholesky R (upper, RᵀR = G) of small SPD matrices and their inverses R⁻¹, one
@@ -492,26 +592,34 @@ __global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(CholBatch cb) {
     __syncthreads();
     const double floor_piv = 1e-28 * dmax;
     // Right-looking Cholesky; the scaling of row k-1 is deferred into step k.
+    // Rows of the trailing update go to warps, columns to lanes: no index
+    // divisions; one thread forms 1/p and 1/sqrt(p) per step.
+    const int warp = tid >> 5, lane = tid & 31;
+    __shared__ double s_ip, s_ir;
     for (int k = 0; k < n; ++k) {
-        double p = A[k * ld + k];
-        if (!(p > floor_piv)) {
-            if (tid == 0) bad |= 1;
-            p = fmax(dmax, 1.0);
-        }
-        if (tid == 0) piv[k] = p;
-        if (k > 0) {
-            const double r = sqrt(piv[k - 1]);
-            for (int j = k - 1 + tid; j < n; j += kJacThreads) A[(k - 1) * ld + j] /= r;
-        }
-        const double ip = 1.0 / p;
-        const int m = n - k - 1;
-        for (int idx = tid; idx < m * m; idx += kJacThreads) {
-            const int i = k + 1 + idx / m, j = k + 1 + idx % m;
-            if (j >= i) A[i * ld + j] -= A[k * ld + i] * A[k * ld + j] * ip;
+        if (tid == 0) {
+            double p = A[k * ld + k];
+            if (!(p > floor_piv)) {
+                bad |= 1;
+                p = fmax(dmax, 1.0);
+            }
+            piv[k] = p;
+            s_ip = 1.0 / p;
+            s_ir = 1.0 / sqrt(p);
         }
         __syncthreads();
+        const double ip = s_ip;
+        for (int i = k + 1 + warp; i < n; i += kJacWarps) {
+            const double aki = A[k * ld + i] * ip;
+            for (int j = i + lane; j < n; j += 32) A[i * ld + j] -= aki * A[k * ld + j];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const double ir = s_ir;
+            for (int j = k + lane; j < n; j += 32) A[k * ld + j] = (j == k) ? piv[k] * ir : A[k * ld + j] * ir;
+        }
     }
-    if (tid == 0) A[(n - 1) * ld + (n - 1)] /= sqrt(piv[n - 1]);
+    __syncthreads();
     __syncthreads();
     for (int i = tid; i < n; i += kJacThreads) X[i * ld + i] = 1.0 / A[i * ld + i];
     __syncthreads();
@@ -776,14 +884,15 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
     }
 }
 
-void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc) {
-    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * (n + 1) + static_cast<size_t>(n) * n + 2 * ((n + 1) / 2 + 1) + n);
+void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc, int* sweeps) {
+    const size_t np = static_cast<size_t>(n + (n & 1));
+    const size_t smem = sizeof(double) * (2 * np * (np + 1) + np + np) + sizeof(int) * (np - 1) * (np / 2) + 16;
     static bool configured = false;
     if (!configured) {
         TS_CUDA_CHECK(cudaFuncSetAttribute(sym_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    sym_jacobi_kernel<<<1, kJacThreads, smem, sc.stream()>>>(C, ldc, n, lambda, V);
+    sym_jacobi_kernel<<<1, kJacThreads, smem, sc.stream()>>>(C, ldc, n, lambda, V, sweeps);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }

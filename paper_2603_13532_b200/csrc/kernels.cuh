@@ -83,7 +83,8 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigm
 
 // Two-sided Jacobi eigensolver of a small symmetric n × n matrix (one CTA):
 // lambda[n] descending, V (n × n, ld n) matching eigenvectors.
-void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc);
+void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
+                       int* sweeps = nullptr);
 // R⁻¹ of the Cholesky factor of small SPD matrices G[b] (n ≤ 96, one CTA each);
 // *flag[b] |= 1 on a non-positive pivot, |= 2 when check_identity and
 // max|G - I| > 1e-2.

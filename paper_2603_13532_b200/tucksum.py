@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = [
     "ts_substream", "ts_gaussian_matrix", "ts_omega_prepare", "ts_krp_sum", "ts_effective_subrank",
     "ts_result_order", "ts_result_dims", "ts_result_ranks", "ts_result_factor", "ts_result_core",
     "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
-    "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths",
+    "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
 ]
 
 
@@ -448,6 +448,17 @@ class Engine:
     @property
     def launch_count(self) -> int:
         return int(lib().ts_ctx_launch_count(self.handle))
+
+    def sym_eig(self, a):
+        """Device symmetric eigensolver (reference sym_eig): (values desc, vectors, sweeps, ms)."""
+        a = _f64(a)
+        n = a.shape[0]
+        vals = np.zeros(n)
+        vecs = np.zeros((n, n), order="F")
+        sw = C.c_int()
+        ms = C.c_double()
+        _check(lib().ts_sym_eig(self.handle, i64(n), _p(a), _p(vals), _p(vecs), C.byref(sw), C.byref(ms)))
+        return vals, vecs, int(sw.value), float(ms.value)
 
     def last_paths(self):
         """(qr_fallback_modes, svd_fallback_modes) of the last krp_sum."""

@@ -300,3 +300,16 @@ def test_cfg5_full_properties(engine):
         assert np.linalg.norm(f.T @ f - np.eye(f.shape[1])) <= 1e-12
     # 2·sum → 2·result (sketch, QR and truncation are scale-equivariant).
     assert O.rel_error_to_sum(r3, [r1], [2.0]) <= 1e-12
+
+
+def test_sym_eig_matches_oracle(engine):
+    """Device Jacobi eigensolver vs the oracle's sym_eig (test_tensor_kernels.cpp:237-248 style)."""
+    for n, seed in [(6, 1), (26, 2), (50, 3), (64, 4), (96, 5)]:
+        a = O.gaussian_matrix(2 * n, n, (17, seed))
+        c = a.T @ a
+        vals, vecs, sweeps, ms = engine.sym_eig(c)
+        ov, _ = O.sym_eig(c)
+        assert np.max(np.abs(vals - ov)) <= 1e-12 * ov[0]
+        assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-12
+        assert np.linalg.norm(vecs @ np.diag(vals) @ vecs.T - c) <= 1e-12 * np.linalg.norm(c)
+        assert 1 <= sweeps <= 20, sweeps
