@@ -1102,6 +1102,12 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
     });
 }
 
+void tsi_read_eig_profile(long long* out);
+// Debug: thread-0 cycle split of the last n ≤ 64 eigensolve (rotation, barrier, pass, barrier).
+int ts_debug_eig_profile(long long* out4) {
+    return guarded([&] { tsi_read_eig_profile(out4); });
+}
+
 // Symmetric eigensolver of the ST-HOSVD fast path (reference sym_eig,
 // src/kernels.cpp:70-86): host in / host out; also reports sweeps and kernel ms.
 int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms) {

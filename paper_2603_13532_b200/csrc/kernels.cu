@@ -357,26 +357,30 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
 // Two-sided cyclic Jacobi eigensolver for a small symmetric n × n matrix C
 // (fast path of ST-HOSVD on the Gram of an unfolding), one CTA.
 //
-// The matrix is padded to an even order np (a zero row/column for odd n) and
-// each round rotates np/2 disjoint pairs at once.  Instead of a row pass and a
-// column pass, the round is applied block-wise: with pairs P_i = (p_i, q_i) and
-// their 2×2 rotations R_i, every 2×2 block A[P_i, P_j] becomes R_iᵀ·A[P_i,P_j]·R_j.
-// One thread owns one block (np = 64: 32×32 blocks = the 1024 threads), so a
-// round is: rotation parameters (one thread per pair) → barrier → all blocks
-// and the eigenvector columns updated in one pass → barrier.
+// The matrix is padded to an even order np and each round rotates the np/2
+// disjoint pairs of a round-robin tournament (players a, b meet in round R iff
+// a + b ≡ 2R mod (np-1); the last player meets R).  A round is ONE pass and ONE
+// barrier: every thread owns upper-triangular 2×2 blocks A[P_i, P_j] of the pair
+// grid and applies R_iᵀ·A[P_i,P_j]·R_j (plus the mirror block), updates its
+// eigenvector items, and — when its block holds the next round's pair (x, y) —
+// immediately derives that pair's rotation from the rotated entries (the new
+// diagonal entries follow in closed form from the pairs' saved 2×2 blocks).
+// The rotation-parameter latency thus overlaps the block updates instead of
+// costing a separate phase and barrier.
 __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* __restrict__ Cin, int64_t ldc, int n,
                                                                  double* __restrict__ lambda, double* __restrict__ V,
                                                                  int* __restrict__ sweeps_out) {
     extern __shared__ __align__(16) double sm[];
     const int np = n + (n & 1);
     const int npair = np / 2;
+    const int m = np - 1;
     const int ld = np + 1;                        // padded row stride
     double* A = sm;                               // np × ld
     double* Vs = A + np * ld;                     // np × ld, Vs[k*ld + j] = V(k, j)
-    double* csv = Vs + np * ld;                   // 2 per pair
-    double* diag = csv + 2 * npair;               // np
-    int* sched = reinterpret_cast<int*>(diag + np);  // (np-1) × npair packed (p | q << 16)
-    __shared__ int rotated, stop;
+    double2* cs = reinterpret_cast<double2*>(Vs + np * ld);  // [2][npair] (c, s)
+    double* dg = reinterpret_cast<double*>(cs + 2 * npair);   // [2][npair][3] (a_pp, a_qq, a_pq)
+    double* diag = dg + 6 * npair;                            // np
+    __shared__ int stop;
     __shared__ double red[2 * kJacWarps];
     __shared__ double prev_off, amax_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -387,12 +391,6 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
         A[i * ld + j] = v;
         Vs[i * ld + j] = (i == j) ? 1.0 : 0.0;
     }
-    for (int idx = tid; idx < (np - 1) * npair; idx += kJacThreads) {
-        const int r = idx / npair, pi = idx % npair;
-        int p, q;
-        pair_of(r, pi, np, &p, &q);
-        sched[idx] = p | (q << 16);
-    }
     if (tid == 0) {
         amax_s = 0.0;
         prev_off = 0.0;
@@ -400,18 +398,58 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
     }
     __syncthreads();
     {
-        double m = 0.0;
-        for (int i = tid; i < n; i += kJacThreads) m = fmax(m, fabs(A[i * ld + i]));
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0 && m > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(m));
+        double mx = 0.0;
+        for (int i = tid; i < n; i += kJacThreads) mx = fmax(mx, fabs(A[i * ld + i]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && mx > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(mx));
     }
     __syncthreads();
     // Entries below 1e-15·max|a_ii| sit under the Gram's own rounding noise (the
     // fast path needs absolute accuracy only); rotating them only burns sweeps.
     const double abs_floor = 1e-15 * amax_s;
-    const double tol = 1e-15;
-    // Per-thread work list fixed for the whole solve (no divisions in the loop):
-    // upper-triangular blocks (bi ≤ bj) of the pair grid, and (row, pair) items of V.
+    const double tol2 = 1e-30;
+    auto pair_at = [m](int R, int i, int& p, int& q) {  // pair i of round R (p < q)
+        int a, b;
+        if (i == 0) {
+            a = m;
+            b = R;
+        } else {
+            a = R + i;
+            a -= (a >= m) ? m : 0;
+            b = R - i;
+            b += (b < 0) ? m : 0;
+        }
+        p = min(a, b);
+        q = max(a, b);
+    };
+    auto partner = [m](int x, int R) {  // x's opponent in round R
+        if (x == m) return R;
+        if (x == R) return m;
+        int y = 2 * R - x;
+        y -= (y >= m) ? m : 0;
+        y += (y < 0) ? m : 0;
+        return y;
+    };
+    auto pair_index = [m](int x, int R) {  // index of the pair holding x in round R
+        if (x == m || x == R) return 0;
+        int i = x - R;
+        i += (i < 0) ? m : 0;
+        return min(i, m - i);
+    };
+    auto rotation = [&](double app, double aqq, double apq, int slot, int i) {
+        double c = 1.0, s = 0.0;
+        if (fabs(apq) > abs_floor && apq * apq > tol2 * fabs(app * aqq)) {
+            double t;
+            jacobi_rotation(app, aqq, apq, c, s, t);
+        }
+        cs[slot * npair + i] = make_double2(c, s);
+        double* d = dg + (slot * npair + i) * 3;
+        d[0] = app;
+        d[1] = aqq;
+        d[2] = apq;
+    };
+    // Per-thread work list fixed for the whole solve: upper-triangular blocks
+    // (bi ≤ bj) of the pair grid and (row, pair) items of V.
     constexpr int kMaxBlk = 2, kMaxV = 5;  // np ≤ 96: 1176 blocks, 4608 V items
     int blk_i[kMaxBlk], blk_j[kMaxBlk], vk[kMaxV], vp[kMaxV];
     int nb = 0, nv = 0;
@@ -433,63 +471,43 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
             ++nv;
         }
     }
-    const int m = np - 1;
-    // Round-robin pairing of round r, pair i (cf. pair_of) without divisions.
-    auto pair_at = [m](int r, int i, int& p, int& q) {
-        int a, b;
-        if (i == 0) {
-            a = m;
-            b = r;
-        } else {
-            a = r + i;
-            a -= (a >= m) ? m : 0;
-            b = r - i;
-            b += (b < 0) ? m : 0;
-        }
-        p = min(a, b);
-        q = max(a, b);
-    };
-    double2* cs2 = reinterpret_cast<double2*>(csv);
-    int sweeps_done = 0;
+    // Rotations of round 0.
+    if (tid < npair) {
+        int p, q;
+        pair_at(0, tid, p, q);
+        rotation(A[p * ld + p], A[q * ld + q], A[p * ld + q], 0, tid);
+    }
+    __syncthreads();
+    int sweeps_done = 0, gr = 0;  // gr: global round counter (slot = gr & 1)
     for (int sweep = 0; sweep < 40; ++sweep) {
         sweeps_done = sweep + 1;
-        if (tid == 0) rotated = 0;
-        for (int r = 0; r < m; ++r) {
-            if (tid < npair) {
-                int p, q;
-                pair_at(r, tid, p, q);
-                const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
-                double c = 1.0, s = 0.0;
-                if (fabs(apq) > abs_floor && apq * apq > tol * tol * fabs(app * aqq)) {
-                    double t;
-                    jacobi_rotation(app, aqq, apq, c, s, t);
-                    rotated = 1;
-                }
-                cs2[tid] = make_double2(c, s);
-            }
-            __syncthreads();
+        for (int r = 0; r < m; ++r, ++gr) {
+            const int slot = gr & 1;
+            const double2* csr = cs + slot * npair;
+            const double* dgr = dg + slot * npair * 3;
+            const int Rn = (r + 1 == m) ? 0 : r + 1;  // next round (the schedule repeats every sweep)
             for (int u = 0; u < nb; ++u) {
                 const int bi = blk_i[u], bj = blk_j[u];
-                const double2 r1 = cs2[bi], r2 = cs2[bj];
-                if (r1.y == 0.0 && r2.y == 0.0) continue;
                 int p1, q1, p2, q2;
                 pair_at(r, bi, p1, q1);
                 pair_at(r, bj, p2, q2);
+                const double2 r1 = csr[bi], r2 = csr[bj];
                 const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
                 const double a11 = A[p1 * ld + p2], a12 = A[p1 * ld + q2];
                 const double a21 = A[q1 * ld + p2], a22 = A[q1 * ld + q2];
                 // rows: Rᵀ·B with R = [[c, s], [-s, c]], then columns: ·R
                 const double b11 = c1 * a11 - s1 * a21, b12 = c1 * a12 - s1 * a22;
                 const double b21 = s1 * a11 + c1 * a21, b22 = s1 * a12 + c1 * a22;
-                const double d11 = c2 * b11 - s2 * b12, d12 = s2 * b11 + c2 * b12;
-                const double d21 = c2 * b21 - s2 * b22, d22 = s2 * b21 + c2 * b22;
-                if (bi == bj) {  // diagonal block: keep the (tiny) residual of the approximate angle
+                double d11 = c2 * b11 - s2 * b12, d12 = s2 * b11 + c2 * b12;
+                double d21 = c2 * b21 - s2 * b22, d22 = s2 * b21 + c2 * b22;
+                if (bi == bj) {
                     const double off = 0.5 * (d12 + d21);
+                    d12 = d21 = off;
                     A[p1 * ld + p1] = d11;
                     A[q1 * ld + q1] = d22;
                     A[p1 * ld + q1] = off;
                     A[q1 * ld + p1] = off;
-                } else {  // block and its mirror image
+                } else {
                     A[p1 * ld + p2] = d11;
                     A[p1 * ld + q2] = d12;
                     A[q1 * ld + p2] = d21;
@@ -499,9 +517,32 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
                     A[p2 * ld + q1] = d21;
                     A[q2 * ld + q1] = d22;
                 }
+                // Does this block hold a pair (x, y) of the next round?
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int x = e == 0 ? p1 : q1;
+                    const int y = partner(x, Rn);
+                    int f = -1;
+                    if (y == p2) f = 0;
+                    else if (y == q2) f = 1;
+                    if (f < 0 || (bi == bj && y <= x)) continue;
+                    const double gxy = e == 0 ? (f == 0 ? d11 : d12) : (f == 0 ? d21 : d22);
+                    // New diagonal entries of x (in pair bi) and y (in pair bj):
+                    // (Rᵀ·[[app, apq], [apq, aqq]]·R)_kk, k = position in the pair.
+                    auto newdiag = [&](int pi, int k) {
+                        const double2 rr = csr[pi];
+                        const double* d = dgr + pi * 3;
+                        const double c = rr.x, s = rr.y, cc = c * c, ss = s * s, c2s = 2.0 * c * s;
+                        return k == 0 ? cc * d[0] - c2s * d[2] + ss * d[1] : ss * d[0] + c2s * d[2] + cc * d[1];
+                    };
+                    const double ax = newdiag(bi, e), ay = newdiag(bj, f);
+                    const int j = pair_index(x, Rn);
+                    if (x < y) rotation(ax, ay, gxy, slot ^ 1, j);
+                    else rotation(ay, ax, gxy, slot ^ 1, j);
+                }
             }
             for (int u = 0; u < nv; ++u) {  // eigenvector columns: V·R
-                const double2 rr = cs2[vp[u]];
+                const double2 rr = csr[vp[u]];
                 if (rr.y == 0.0) continue;
                 int p, q;
                 pair_at(r, vp[u], p, q);
@@ -512,7 +553,6 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
             }
             __syncthreads();
         }
-        if (!rotated) break;
         // Stop at off(A) ≤ 1e-14·‖A‖_F, or once stalled on rounding noise ≤ 1e-12·‖A‖_F.
         double off = 0.0, tot = 0.0;
         for (int idx = tid; idx < np * np; idx += kJacThreads) {
@@ -885,8 +925,9 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
 }
 
 void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc, int* sweeps) {
+    if (launch_sym_jacobi_pp(C, ldc, n, lambda, V, sc, sweeps)) return;  // eig.cu, n ≤ 64
     const size_t np = static_cast<size_t>(n + (n & 1));
-    const size_t smem = sizeof(double) * (2 * np * (np + 1) + np + np) + sizeof(int) * (np - 1) * (np / 2) + 16;
+    const size_t smem = sizeof(double) * (2 * np * (np + 1) + 2 * np + 3 * np + np) + 16;
     static bool configured = false;
     if (!configured) {
         TS_CUDA_CHECK(cudaFuncSetAttribute(sym_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

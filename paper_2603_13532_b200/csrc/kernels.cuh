@@ -85,6 +85,9 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigm
 // lambda[n] descending, V (n × n, ld n) matching eigenvectors.
 void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
                        int* sweeps = nullptr);
+// Fixed-address (permuted-layout) variant for n ≤ 64 (eig.cu); false if n > 64.
+bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
+                          int* sweeps);
 // R⁻¹ of the Cholesky factor of small SPD matrices G[b] (n ≤ 96, one CTA each);
 // *flag[b] |= 1 on a non-positive pivot, |= 2 when check_identity and
 // max|G - I| > 1e-2.

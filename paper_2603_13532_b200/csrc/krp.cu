@@ -12,6 +12,7 @@
 // is stored transposed, Wt_n (s × R_n), so stage C reads both of its operands
 // along their non-reduction dimension (gemm_tma.cu MN scheme).
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -179,10 +180,162 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Order-3 specialisation (all block ranks ≤ 32): per core slice G_s = G[:, :, a2]
+//   T0 = G_s · M1   (r0 × s)   →  V0 += M2(a2, :) ⊙ T0,   V2(a2, :) = colsum(M0 ⊙ T0)
+//   T1 = G_sᵀ · M0  (r1 × s)   →  V1 += M2(a2, :) ⊙ T1
+// i.e. the three mode contractions of src/sketch.cpp:117-130 share the two
+// slice GEMMs (4·r³·s flops per atom instead of 6·r³·s) and no Khatri-Rao row
+// is ever formed.  One CTA per (atom, 64 sketch columns); warps own 16 columns
+// each; core slices stream through a cp.async double buffer.
+constexpr int k3Rows = 32;            // padded r0 = r1
+constexpr int k3GLD = k3Rows + 4;     // slice row stride (conflict-free both ways)
+constexpr int k3MLD = kCT + 4;        // M0 / M1 row stride
+
+__global__ void __launch_bounds__(kThreads) krp3_dmma_kernel(KrpArgs args) {
+    const Atom& at = args.atoms[blockIdx.x];
+    const int c0 = blockIdx.y * kCT;
+    const int s = args.s;
+    const int r0 = at.shape[0], r1 = at.shape[1], r2 = at.shape[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int cw = warp * 16;  // this warp's 16 columns within the chunk
+
+    extern __shared__ __align__(16) double sm[];
+    double* M0s = sm;                       // 32 × k3MLD
+    double* M1s = M0s + k3Rows * k3MLD;     // 32 × k3MLD
+    double* Gs = M1s + k3Rows * k3MLD;      // 2 × 32 × k3GLD
+    double* M2s = Gs + 2 * k3Rows * k3GLD;  // r2 × kCT
+    const double* Z0 = args.Z[0];
+    const double* Z1 = args.Z[1];
+    const double* Z2 = args.Z[2];
+    for (int idx = tid; idx < k3Rows * kCT; idx += kThreads) {
+        const int a = idx / kCT, c = idx % kCT, cg = c0 + c;
+        M0s[a * k3MLD + c] = (a < r0 && cg < s) ? Z0[cg + static_cast<int64_t>(at.col[0] + a) * s] : 0.0;
+        M1s[a * k3MLD + c] = (a < r1 && cg < s) ? Z1[cg + static_cast<int64_t>(at.col[1] + a) * s] : 0.0;
+    }
+    for (int idx = tid; idx < r2 * kCT; idx += kThreads) {
+        const int a = idx / kCT, c = idx % kCT, cg = c0 + c;
+        M2s[idx] = cg < s ? Z2[cg + static_cast<int64_t>(at.col[2] + a) * s] : 0.0;
+    }
+    // Zero the slice buffers once: padded rows / columns stay zero.
+    for (int idx = tid; idx < 2 * k3Rows * k3GLD; idx += kThreads) Gs[idx] = 0.0;
+    __syncthreads();
+    const double* __restrict__ core = args.cores + at.core_off;
+    const int slice = r0 * r1;
+    auto load_slice = [&](int a2, int buf) {
+        double* dst = Gs + buf * k3Rows * k3GLD;
+        const double* src = core + static_cast<int64_t>(a2) * slice;
+        for (int idx = tid; idx < slice; idx += kThreads) {
+            const int i = idx % r0, j = idx / r0;  // G_s(i, j) column-major
+            cp_async8(dst + i + j * k3GLD, src + idx, 8);
+        }
+    };
+
+    double v0[4][2][2], v1[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) v0[i][j][0] = v0[i][j][1] = v1[i][j][0] = v1[i][j][1] = 0.0;
+    const double w = args.weights[at.summand];
+    double* W2 = args.W[2];
+
+    if (r2 > 0) load_slice(0, 0);
+    cp_async_commit();
+    for (int a2 = 0; a2 < r2; ++a2) {
+        const int buf = a2 & 1;
+        if (a2 + 1 < r2) load_slice(a2 + 1, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* G = Gs + buf * k3Rows * k3GLD;
+        double t0[4][2][2], t1[4][2][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) t0[i][j][0] = t0[i][j][1] = t1[i][j][0] = t1[i][j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < k3Rows; kk += 4) {
+            double a0f[4], a1f[4], b1f[2], b0f[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a0f[i] = G[(8 * i + g) + (kk + t) * k3GLD];  // G_s(a0, a1):  m = a0, k = a1
+                a1f[i] = G[(kk + t) + (8 * i + g) * k3GLD];  // G_sᵀ(a1, a0): m = a1, k = a0
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                b1f[j] = M1s[(kk + t) * k3MLD + cw + 8 * j + g];
+                b0f[j] = M0s[(kk + t) * k3MLD + cw + 8 * j + g];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    dmma884(t0[i][j][0], t0[i][j][1], a0f[i], b1f[j]);
+                    dmma884(t1[i][j][0], t1[i][j][1], a1f[i], b0f[j]);
+                }
+        }
+        // Fold the slice into the three mode sketches.
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = cw + 8 * j + 2 * t + h;
+                const double m2 = M2s[a2 * kCT + c];
+                double part = 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v0[i][j][h] = fma(t0[i][j][h], m2, v0[i][j][h]);
+                    v1[i][j][h] = fma(t1[i][j][h], m2, v1[i][j][h]);
+                    part = fma(M0s[(8 * i + g) * k3MLD + c], t0[i][j][h], part);
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 4);
+                part += __shfl_xor_sync(0xffffffffu, part, 8);
+                part += __shfl_xor_sync(0xffffffffu, part, 16);
+                const int cg = c0 + c;
+                if (g == 0 && cg < s) W2[cg + static_cast<int64_t>(at.col[2] + a2) * s] = w * part;
+            }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    double* W0 = args.W[0];
+    double* W1 = args.W[1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int a = 8 * i + g;
+                const int cg = c0 + cw + 8 * j + 2 * t + h;
+                if (cg >= s) continue;
+                if (a < r0) W0[cg + static_cast<int64_t>(at.col[0] + a) * s] = w * v0[i][j][h];
+                if (a < r1) W1[cg + static_cast<int64_t>(at.col[1] + a) * s] = w * v1[i][j][h];
+            }
+}
+
 }  // namespace
 
 void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc) {
     if (args.natoms == 0) return;
+    static const bool use3 = [] {
+        const char* e = std::getenv("TS_KRP_GENERIC");
+        return !(e && e[0] == '1');
+    }();
+    if (use3 && args.order == 3 && max_shape <= k3Rows) {
+        const size_t smem =
+            sizeof(double) * (2 * k3Rows * k3MLD + 2 * k3Rows * k3GLD + static_cast<size_t>(max_shape) * kCT);
+        static bool configured = false;
+        if (!configured) {
+            TS_CUDA_CHECK(cudaFuncSetAttribute(krp3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+            configured = true;
+        }
+        dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>((args.s + kCT - 1) / kCT));
+        krp3_dmma_kernel<<<grid, kThreads, smem, sc.stream()>>>(args);
+        TS_LAUNCH_CHECK();
+        sc.launches += 1;
+        return;
+    }
     const int RT = max_shape <= 32 ? 32 : 64;
     const size_t smem = sizeof(double) * (static_cast<size_t>(max_shape) * args.order * kCT + kJC * kKS + RT * kGS) +
                         sizeof(int64_t) * 2 * kJC + sizeof(int) * 2 * kJC * kMaxOrder;

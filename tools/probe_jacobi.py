@@ -12,4 +12,9 @@ for n, decay in [(64, 0.0), (64, 0.05), (64, 0.2), (50, 0.2), (26, 0.1), (96, 0.
     for _ in range(2):
         vals, vecs, sw, ms = eng.sym_eig(c)
     err = np.max(np.abs(np.sort(vals)[::-1] - np.sort(lam)[::-1]))
-    print(json.dumps({"n": n, "decay": decay, "sweeps": sw, "ms": ms, "max_eig_err": err}))
+    import ctypes as C
+    prof = (C.c_longlong * 4)()
+    T.lib().ts_debug_eig_profile(prof)
+    print(json.dumps({"n": n, "decay": decay, "sweeps": sw, "ms": ms, "max_eig_err": err,
+                      "cycles_rot_bar_pass_bar": [int(x) for x in prof],
+                      "rounds": sw * (n + (n & 1) - 1)}))
