@@ -522,7 +522,24 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     std::int64_t Qp = 1;
     for (int j = 0; j < d - 1; ++j) Qp *= q[j];
     double* Tstack = sc.alloc_n<double>(static_cast<size_t>(Qp * b->R[d - 1]));
-    {
+    bool f1_done = false;
+    if (d == 3) {  // fused per-slice chain (ttm3.cu)
+        ts::Ttm3Args ta{};
+        for (int n = 0; n < d; ++n) {
+            ta.P[n] = P[n];
+            ta.q[n] = q[n];
+        }
+        ta.atoms = b->d_atoms;
+        ta.cores = b->cores;
+        ta.weights = d_w;
+        ta.Tstack = Tstack;
+        ta.Qp = Qp;
+        ta.natoms = static_cast<int>(b->atoms.size());
+        int max_r2 = 0;
+        for (const auto& at : b->atoms) max_r2 = std::max(max_r2, at.shape[2]);
+        f1_done = ts::launch_ttm3(ta, b->max_shape, max_r2, sc);
+    }
+    if (!f1_done) {
         const size_t na = b->atoms.size();
         std::vector<double*> cur(na), nxt(na);
         for (int m = 0; m <= d - 2; ++m) {

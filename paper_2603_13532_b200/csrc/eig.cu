@@ -219,24 +219,45 @@ __global__ void __launch_bounds__(128) jacobi_vectors_kernel(int n, const double
     const int k = np / 2;
     const int lane = threadIdx.x & 31;
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (row >= np) return;  // warp-uniform
     const int rounds = info[0];
     const bool vlane = lane < k;
     double f = (row == 2 * lane) ? 1.0 : 0.0;      // position 2·lane
     double g = (row == 2 * lane + 1) ? 1.0 : 0.0;  // position 2·lane + 1
-    double2 rr = (vlane && rounds > 0) ? rot[lane] : make_double2(1.0, 0.0);
-    for (int r = 0; r < rounds; ++r) {
-        const double2 nx = (vlane && r + 1 < rounds) ? rot[static_cast<int64_t>(r + 1) * k + lane] : make_double2(1.0, 0.0);
-        const double x = rr.x * f - rr.y * g;
-        const double y = rr.y * f + rr.x * g;
-        const double x_up = __shfl_up_sync(0xffffffffu, x, 1);
-        const double y_dn = __shfl_down_sync(0xffffffffu, y, 1);
-        const double y0 = __shfl_sync(0xffffffffu, y, 0);
-        const double xk = __shfl_sync(0xffffffffu, x, k - 1);
-        f = lane == 0 ? x : (lane == 1 ? y0 : x_up);
-        g = lane == k - 1 ? xk : y_dn;
-        rr = nx;
+    // The log streams through shared memory in chunks of kChunk rounds
+    // (cp.async, double-buffered, shared by the CTA's four rows) so the
+    // loop-carried chain never waits on L2.
+    constexpr int kChunk = 32;
+    __shared__ __align__(16) double2 logbuf[2][kChunk * 32];
+    auto stage = [&](int chunk, int b) {
+        const int r0 = chunk * kChunk;
+        const int nr = min(kChunk, rounds - r0);
+        for (int e = threadIdx.x; e < nr * k; e += blockDim.x)
+            cp_async16(&logbuf[b][(e / k) * 32 + (e % k)], rot + static_cast<int64_t>(r0) * k + e, 16);
+    };
+    const int nchunks = (rounds + kChunk - 1) / kChunk;
+    if (nchunks > 0) stage(0, 0);
+    cp_async_commit();
+    for (int ch = 0; ch < nchunks; ++ch) {
+        if (ch + 1 < nchunks) stage(ch + 1, (ch + 1) & 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double2* cur = logbuf[ch & 1];
+        const int nr = min(kChunk, rounds - ch * kChunk);
+        for (int ri = 0; ri < nr; ++ri) {
+            const double2 rr = vlane ? cur[ri * 32 + lane] : make_double2(1.0, 0.0);
+            const double x = rr.x * f - rr.y * g;
+            const double y = rr.y * f + rr.x * g;
+            const double x_up = __shfl_up_sync(0xffffffffu, x, 1);
+            const double y_dn = __shfl_down_sync(0xffffffffu, y, 1);
+            const double y0 = __shfl_sync(0xffffffffu, y, 0);
+            const double xk = __shfl_sync(0xffffffffu, x, k - 1);
+            f = lane == 0 ? x : (lane == 1 ? y0 : x_up);
+            g = lane == k - 1 ? xk : y_dn;
+        }
+        __syncthreads();
     }
+    cp_async_wait<0>();
     if (!vlane || row >= n) return;
     int ppad = -1;
     if (np != n) {

@@ -39,6 +39,21 @@ struct KrpArgs {
 };
 void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc);
 
+// Stage F1 fused for order 3 (ttm3.cu): T_stack[:, col_b[2] + a2] =
+// w_b · vec(P_0,b · G_b[:, :, a2] · P_1,bᵀ).  Returns false when the shapes exceed
+// the kernel's tile (ranks > 32 or q > 64); the caller then uses the GEMM chain.
+struct Ttm3Args {
+    const double* P[kMaxOrder];  // P_n (q_n × R_n)
+    int64_t q[kMaxOrder];
+    const Atom* atoms;
+    const double* cores;
+    const double* weights;
+    double* Tstack;  // Qp × R_2
+    int64_t Qp;
+    int natoms;
+};
+bool launch_ttm3(const Ttm3Args& args, int max_shape, int max_r2, CallScratch& sc);
+
 // Stage D building blocks: Householder TSQR with the R_ii >= 0 sign convention
 // of qr_econ (reference src/kernels.cpp:50-63).
 struct QrTask {
