@@ -177,7 +177,18 @@ __global__ void splitk_reduce(const GemmDesc* __restrict__ descs, const int* __r
         const int m = static_cast<int>(r % d.M), n = static_cast<int>(r / d.M);
         const double* w = d.ws + b * d.splits * mn + r;
         double s = 0.0;
-        for (int sp = 0; sp < d.splits; ++sp) s += w[sp * mn];
+        // Split order is fixed (deterministic); loads are batched 8 at a time so
+        // their L2 latencies overlap instead of serialising on the running sum.
+        const double* src = w;
+        int sp = 0;
+        for (; sp + 8 <= d.splits; sp += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = src[(sp + u) * mn];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; sp < d.splits; ++sp) s += src[sp * mn];
         double* c = d.C + b * d.sC + m + static_cast<int64_t>(n) * d.ldc;
         *c = d.beta == 0.0 ? d.alpha * s : d.alpha * s + d.beta * *c;
     }

@@ -247,7 +247,18 @@ __global__ void tma_splitk_reduce(const TmaGroup* __restrict__ groups, const int
          r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int m = static_cast<int>(r % d.M), n = static_cast<int>(r / d.M);
         double s = 0.0;
-        for (int sp = 0; sp < d.splits; ++sp) s += d.ws[sp * mn + r];
+        // Split order is fixed (deterministic); loads are batched 8 at a time so
+        // their L2 latencies overlap instead of serialising on the running sum.
+        const double* src = d.ws + r;
+        int sp = 0;
+        for (; sp + 8 <= d.splits; sp += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = src[(sp + u) * mn];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; sp < d.splits; ++sp) s += src[sp * mn];
         double* c = d.C + m + static_cast<int64_t>(n) * d.ldc;
         *c = d.beta == 0.0 ? d.alpha * s : d.alpha * s + d.beta * *c;
     }

@@ -718,18 +718,38 @@ __global__ void unfold_t_kernel(const double* __restrict__ g, UnfoldArgs a, doub
     }
 }
 
-__global__ void sumsq_kernel(const double* __restrict__ x, int64_t n, double* out) {
-    __shared__ double part[32];
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i] * x[i];
+// Σ x_i² in two deterministic passes: fixed contiguous chunks per CTA, then the
+// per-CTA partials summed in order by one CTA.
+constexpr int kSumsqBlocks = 128;
+
+__device__ __forceinline__ double block_sum(double s, double* part) {
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
     __syncthreads();
+    double v = 0.0;
     if (threadIdx.x < 32) {
-        double v = threadIdx.x < blockDim.x / 32 ? part[threadIdx.x] : 0.0;
+        v = threadIdx.x < blockDim.x / 32 ? part[threadIdx.x] : 0.0;
         v = warp_sum(v);
-        if (threadIdx.x == 0) out[0] = v;
     }
+    return v;
+}
+
+__global__ void sumsq_partial_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ partial) {
+    __shared__ double part[32];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t b = blockIdx.x * chunk, e = min(n, b + chunk);
+    double s = 0.0;
+    for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) s = fma(x[i], x[i], s);
+    const double v = block_sum(s, part);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+}
+
+__global__ void sumsq_final_kernel(const double* __restrict__ partial, int np, double* out) {
+    __shared__ double part[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) s += partial[i];
+    const double v = block_sum(s, part);
+    if (threadIdx.x == 0) out[0] = v;
 }
 
 __global__ void scale_columns_kernel(const double* __restrict__ F, int64_t n, int64_t R, const double* __restrict__ sc,
@@ -990,9 +1010,12 @@ void launch_scale_columns(const double* F, int64_t n, int64_t R, const double* s
 }
 
 void launch_sumsq(const double* x, int64_t n, double* out, CallScratch& sc) {
-    sumsq_kernel<<<1, 1024, 0, sc.stream()>>>(x, n, out);
+    double* partial = sc.alloc_n<double>(kSumsqBlocks);
+    sumsq_partial_kernel<<<kSumsqBlocks, 256, 0, sc.stream()>>>(x, n, partial);
     TS_LAUNCH_CHECK();
-    sc.launches += 1;
+    sumsq_final_kernel<<<1, 128, 0, sc.stream()>>>(partial, kSumsqBlocks, out);
+    TS_LAUNCH_CHECK();
+    sc.launches += 2;
 }
 
 }  // namespace ts
