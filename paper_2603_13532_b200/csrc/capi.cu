@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <map>
 #include <memory>
@@ -671,10 +672,16 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
                 p.ldc = qk;
                 ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
             }
-            ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc);
+            static const bool dbg_sweeps = std::getenv("TS_DEBUG_SWEEPS") != nullptr;
+            int* dsw = dbg_sweeps ? sc.alloc_n<int>(1) : nullptr;
+            ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
             std::vector<double> lv(static_cast<size_t>(qk));
             TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk), cudaMemcpyDeviceToHost, st));
+            int hsw = 0;
+            if (dsw) TS_CUDA_CHECK(cudaMemcpyAsync(&hsw, dsw, sizeof(int), cudaMemcpyDeviceToHost, st));
             TS_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (dsw) std::fprintf(stderr, "[ts] st-hosvd mode %d: n=%lld sweeps=%d lam1=%.3e lam_last=%.3e\n", k,
+                                  static_cast<long long>(qk), hsw, lv[0], lv.back());
             const std::int64_t capk = max_rank ? max_rank[k] : 0;
             bool ok = false;
             std::int64_t rk = gram_rank(lv, eps, theta, capk, &ok);
@@ -1120,9 +1127,9 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
 }
 
 void tsi_read_eig_profile(long long* out);
-// Debug: thread-0 cycle split of the last n ≤ 64 eigensolve (rotation, barrier, pass, barrier).
-int ts_debug_eig_profile(long long* out4) {
-    return guarded([&] { tsi_read_eig_profile(out4); });
+// Debug: phase clock totals of the last n ≤ 64 values-kernel run (TS_EIG_PROFILE=1).
+int ts_debug_eig_profile(long long* out5) {
+    return guarded([&] { tsi_read_eig_profile(out5); });
 }
 
 // Symmetric eigensolver of the ST-HOSVD fast path (reference sym_eig,

@@ -23,14 +23,16 @@
 //     V across many SMs (rows evolve independently; the column permutation is a
 //     pair of lane shifts), then writes the eigenpairs in descending order.
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
 namespace ts {
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kWarps = kThreads / 32;
+constexpr int kWorkWarps = 15;                 // worker warps of the values kernel (464 blocks at n = 64)
+constexpr int kValWarps = kWorkWarps + 1;      // + the pivot warp
+constexpr int kValThreads = 32 * kValWarps;
 constexpr int kMaxNp = 64;
 constexpr int kMaxSweeps = 40;
 
@@ -73,29 +75,87 @@ __device__ __forceinline__ int dest_of(int pos, int k) {
     return pos - 2;
 }
 
+// Storage of position (r, c), r ≤ c: even columns in the first half-row, odd in
+// the second, so a warp's 8-byte accesses along a row of blocks are contiguous.
+__device__ __forceinline__ int addr_of(int r, int c, int k) { return r * 2 * k + (c & 1) * k + (c >> 1); }
+__device__ __forceinline__ int addr_sym(int r, int c, int k) { return r <= c ? addr_of(r, c, k) : addr_of(c, r, k); }
+// Stored address of the element at positions (r, c) after the permutation.
+__device__ __forceinline__ int addr_next(int r, int c, int k) { return addr_sym(dest_of(r, k), dest_of(c, k), k); }
+
+// Shared-space accesses by precomputed 32-bit address (no per-round address math).
+__device__ __forceinline__ double lds64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double2 lds128(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts128(unsigned a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Rᵢᵀ·B·Rⱼ of one 2×2 block (R = [[c, s], [-s, c]]).
+__device__ __forceinline__ void rotate_block(double2 ri, double2 rj, double a11, double a12, double a21, double a22,
+                                             double& d11, double& d12, double& d21, double& d22) {
+    const double b11 = ri.x * a11 - ri.y * a21, b12 = ri.x * a12 - ri.y * a22;
+    const double b21 = ri.y * a11 + ri.x * a21, b22 = ri.y * a12 + ri.x * a22;
+    d11 = rj.x * b11 - rj.y * b12;
+    d12 = rj.y * b11 + rj.x * b12;
+    d21 = rj.x * b21 - rj.y * b22;
+    d22 = rj.y * b21 + rj.x * b22;
+}
+
+__device__ __forceinline__ double2 rotation_or_identity(double app, double aqq, double apq, double abs_floor) {
+    double c = 1.0, s = 0.0;
+    if (fabs(apq) > abs_floor && apq * apq > 1e-30 * fabs(app * aqq)) rotation(app, aqq, apq, c, s);
+    return make_double2(c, s);
+}
+
 // info[0] = rounds performed, info[1] = sweeps; diag_out[p] = A[p][p] at the end
-// (position order), rot[round * k + i] = rotation of pair i in that round.
-__global__ void __launch_bounds__(kThreads) jacobi_values_kernel(const double* __restrict__ Cin, int64_t ldc, int n,
-                                                                 double2* __restrict__ rot, double* __restrict__ diag_out,
-                                                                 int* __restrict__ info) {
+// (position order), rot[round * k + i] = rotation of pair i in that round;
+// prof (optional) = {round-loop clocks, 0, 0, 0, rounds}.
+//
+// One barrier per round.  A round is issue-bound (every block costs the same
+// few instructions), so the upper triangle's blocks are packed densely: worker
+// warp w takes row pairs w and k-2-w (k blocks together, each row a contiguous
+// lane segment) with every shared address precomputed.  The pivot warp's lane m
+// updates diagonal block m and the off-diagonal block holding the entry that
+// pairs the two players meeting in pair m NEXT round, then forms that next
+// rotation — so round r+1's rotations are ready when round r's barrier opens and
+// their latency hides behind the workers' updates of round r.
+__global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const double* __restrict__ Cin, int64_t ldc, int n,
+                                                                    double2* __restrict__ rot,
+                                                                    double* __restrict__ diag_out, int* __restrict__ info,
+                                                                    unsigned long long* __restrict__ prof) {
     extern __shared__ __align__(16) double sm[];
     const int np = n + (n & 1);
     const int k = np / 2;
-    const int ld = np + 2;    // even stride keeps column pairs 16-byte aligned
-    const int mat = np * ld;  // buffer c at sm + c·mat (arithmetic selection stays in shared space)
-    double2* cs = reinterpret_cast<double2*>(sm + 2 * mat);
+    const int mat = np * np;
+    // Layout: matrix buffers 0/1 (mat doubles each), rotations cs[2][kMaxNp/2],
+    // then the rotation log ring (2·(np-1) rounds), flushed to global once per
+    // sweep: a global store inside the round would stretch the round's barrier.
+    const int ring = 2 * (np - 1);
+    __shared__ int srcpos[kMaxNp];
+    __shared__ unsigned xmask[kMaxNp / 2];
     __shared__ int stop;
-    __shared__ double red[2 * kWarps];
+    __shared__ double red[2 * kValWarps];
     __shared__ double prev_off, amax_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int idx = tid; idx < np * ld; idx += kThreads) {
-        const int i = idx / ld, j = idx % ld;
+    for (int idx = tid; idx < np * np; idx += kValThreads) {
+        const int i = idx / np, j = idx % np;
         double v = 0.0;
         if (i < n && j < n && j >= i)
             v = 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc]);
-        sm[idx] = v;
-        sm[mat + idx] = 0.0;
+        if (j >= i) sm[addr_of(i, j, k)] = v;
     }
+    if (tid < np) srcpos[dest_of(tid, k)] = tid;
+    if (tid < kMaxNp / 2) xmask[tid] = 0u;
     if (tid == 0) {
         amax_s = 0.0;
         prev_off = 0.0;
@@ -104,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) jacobi_values_kernel(const double* _
     __syncthreads();
     {
         double mx = 0.0;
-        for (int i = tid; i < n; i += kThreads) mx = fmax(mx, fabs(sm[i * ld + i]));
+        for (int i = tid; i < n; i += kValThreads) mx = fmax(mx, fabs(sm[addr_of(i, i, k)]));
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0 && mx > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(mx));
     }
@@ -113,68 +173,181 @@ __global__ void __launch_bounds__(kThreads) jacobi_values_kernel(const double* _
     // path needs absolute accuracy only); rotating them only burns sweeps.
     const double abs_floor = 1e-15 * amax_s;
 
-    // Fixed roles: warp i → row pair (2i, 2i+1), lane j → column pair (2j, 2j+1), j ≥ i.
-    const bool active = warp < k && lane < k && lane >= warp;
-    const bool dblk = lane == warp;
-    const int i2 = 2 * warp, j2 = 2 * lane;
-    int dst[4] = {0, 0, 0, 0};
-    if (active) {
-        const int ra[2] = {i2, i2 + 1}, cb[2] = {j2, j2 + 1};
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-#pragma unroll
-            for (int y = 0; y < 2; ++y) {
-                const int da = dest_of(ra[x], k), db = dest_of(cb[y], k);
-                dst[2 * x + y] = min(da, db) * ld + max(da, db);
-            }
-    }
+    const unsigned sbase = smem_u32(sm);
+    const unsigned matb = static_cast<unsigned>(mat) * 8u;
+    const unsigned csb = sbase + 2u * matb;  // cs buffer b at csb + 512·b
+    const unsigned logb = csb + 1024u;       // ring slot s, pair m at logb + 16·(s·k + m)
 
-    int cur = 0, rounds = 0, sweeps_done = 0;
+    // Worker role: the t-th block (bi, bj), bj > bi, in row-major order among
+    // those the pivot warp does not own (xmask[i] bit j: pivot-owned), so every
+    // warp takes 32 consecutive blocks (one to three contiguous row segments).
+    if (tid < k) {
+        const int p = srcpos[2 * tid], q = srcpos[2 * tid + 1];
+        atomicOr(&xmask[min(p, q) >> 1], 1u << (max(p, q) >> 1));
+    }
+    __syncthreads();
+    bool work = false;
+    unsigned la[4] = {0, 0, 0, 0}, sa[4] = {0, 0, 0, 0}, rio = 0, rjo = 0;
+    if (warp < kWorkWarps) {
+        const unsigned kmask = k == 32 ? 0xffffffffu : ((1u << k) - 1u);
+        int t = tid, bi = -1, bj = -1;
+        for (int i = 0; i < k - 1; ++i) {
+            unsigned row = kmask & ~((2u << i) - 1u) & ~xmask[i];
+            const int c = __popc(row);
+            if (t < c) {
+                for (int u = 0; u < t; ++u) row &= row - 1u;
+                bi = i;
+                bj = __ffs(row) - 1;
+                break;
+            }
+            t -= c;
+        }
+        if (bi >= 0) {
+            work = true;
+            const int i2 = 2 * bi, j2 = 2 * bj;
+            la[0] = 8u * addr_of(i2, j2, k);
+            la[1] = 8u * addr_of(i2, j2 + 1, k);
+            la[2] = 8u * addr_of(i2 + 1, j2, k);
+            la[3] = 8u * addr_of(i2 + 1, j2 + 1, k);
+            sa[0] = 8u * addr_next(i2, j2, k);
+            sa[1] = 8u * addr_next(i2, j2 + 1, k);
+            sa[2] = 8u * addr_next(i2 + 1, j2, k);
+            sa[3] = 8u * addr_next(i2 + 1, j2 + 1, k);
+            rio = 16u * bi;
+            rjo = 16u * bj;
+        }
+    }
+    // Pivot lane m: diagonal block m, the block (ea, eb) holding A[sp][sq] (sp/sq
+    // the positions whose players form pair m next round; (ex, ey) within it), and
+    // the diagonal blocks of sp and sq, whose rotated diagonal it recomputes
+    // itself (same arithmetic as their owners) instead of exchanging it.  Lanes
+    // ≥ k mirror lane k-1 and store nothing, so the warp stays converged.
+    const bool pwarp = warp == kWorkWarps;
+    const bool plane = pwarp && lane < k;
+    unsigned dla[3] = {0, 0, 0}, dsa[3] = {0, 0, 0}, ela[4] = {0, 0, 0, 0}, esa[4] = {0, 0, 0, 0};
+    unsigned pla[3] = {0, 0, 0}, qla[3] = {0, 0, 0};
+    unsigned rmo = 0, rao = 0, rbo = 0, rpo = 0, rqo = 0;
+    int ex = 0, ey = 0, sx = 0, sy = 0;
+    if (pwarp) {
+        const int m = min(lane, k - 1);
+        const int sp = srcpos[2 * m], sq = srcpos[2 * m + 1];
+        const int lo = min(sp, sq), hi = max(sp, sq);
+        const int ea = lo >> 1, eb = hi >> 1;
+        ex = lo & 1;
+        ey = hi & 1;
+        sx = sp & 1;
+        sy = sq & 1;
+        const int m2 = 2 * m, a2 = 2 * ea, b2 = 2 * eb, p2 = 2 * (sp >> 1), q2 = 2 * (sq >> 1);
+        dla[0] = 8u * addr_of(m2, m2, k);
+        dla[1] = 8u * addr_of(m2, m2 + 1, k);
+        dla[2] = 8u * addr_of(m2 + 1, m2 + 1, k);
+        dsa[0] = 8u * addr_next(m2, m2, k);
+        dsa[1] = 8u * addr_next(m2, m2 + 1, k);
+        dsa[2] = 8u * addr_next(m2 + 1, m2 + 1, k);
+        ela[0] = 8u * addr_of(a2, b2, k);
+        ela[1] = 8u * addr_of(a2, b2 + 1, k);
+        ela[2] = 8u * addr_of(a2 + 1, b2, k);
+        ela[3] = 8u * addr_of(a2 + 1, b2 + 1, k);
+        esa[0] = 8u * addr_next(a2, b2, k);
+        esa[1] = 8u * addr_next(a2, b2 + 1, k);
+        esa[2] = 8u * addr_next(a2 + 1, b2, k);
+        esa[3] = 8u * addr_next(a2 + 1, b2 + 1, k);
+        pla[0] = 8u * addr_of(p2, p2, k);
+        pla[1] = 8u * addr_of(p2, p2 + 1, k);
+        pla[2] = 8u * addr_of(p2 + 1, p2 + 1, k);
+        qla[0] = 8u * addr_of(q2, q2, k);
+        qla[1] = 8u * addr_of(q2, q2 + 1, k);
+        qla[2] = 8u * addr_of(q2 + 1, q2 + 1, k);
+        rmo = 16u * m;
+        rao = 16u * ea;
+        rbo = 16u * eb;
+        rpo = 16u * (sp >> 1);
+        rqo = 16u * (sq >> 1);
+        if (plane) {
+            // Round 0's rotations from the input matrix.
+            const double2 v = rotation_or_identity(lds64(sbase + dla[0]), lds64(sbase + dla[2]),
+                                                   lds64(sbase + dla[1]), abs_floor);
+            sts128(csb + rmo, v);
+            sts128(logb + rmo, v);
+        }
+    }
+    __syncthreads();
+
+    unsigned cur = 0;  // byte offset of the current matrix buffer (0 or matb)
+    int rounds = 0, sweeps_done = 0, wslot = 0;
+    const long long tloop = clock64();
+    const bool probe = prof != nullptr && lane == 0 && warp == kWorkWarps;
+    unsigned long long chain = 0, sweep_tail = 0;
     for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
         sweeps_done = sweep + 1;
         for (int r = 0; r < np - 1; ++r, ++rounds) {
-            const double* A = sm + cur * mat;
-            double* An = sm + (cur ^ 1) * mat;
-            if (tid < k) {
-                const int p = 2 * tid, q = p + 1;
-                const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
-                double c = 1.0, s = 0.0;
-                if (fabs(apq) > abs_floor && apq * apq > 1e-30 * fabs(app * aqq)) rotation(app, aqq, apq, c, s);
-                const double2 v = make_double2(c, s);
-                cs[tid] = v;
-                rot[static_cast<int64_t>(rounds) * k + tid] = v;
-            }
-            __syncthreads();
-            if (active) {
-                const double2 ri = cs[warp], rj = cs[lane];
-                const double2 top = *reinterpret_cast<const double2*>(A + i2 * ld + j2);        // (2i, 2j), (2i, 2j+1)
-                const double2 bot = *reinterpret_cast<const double2*>(A + (i2 + 1) * ld + j2);  // (2i+1, 2j), (2i+1, 2j+1)
-                const double a11 = top.x, a12 = top.y, a22 = bot.y;
-                const double a21 = dblk ? top.y : bot.x;  // diagonal block: the lower entry mirrors a12
-                // rows: Rᵀ·B with R = [[c, s], [-s, c]], then columns: ·R
-                const double b11 = ri.x * a11 - ri.y * a21, b12 = ri.x * a12 - ri.y * a22;
-                const double b21 = ri.y * a11 + ri.x * a21, b22 = ri.y * a12 + ri.x * a22;
-                const double d11 = rj.x * b11 - rj.y * b12, d12 = rj.y * b11 + rj.x * b12;
-                const double d21 = rj.x * b21 - rj.y * b22, d22 = rj.y * b21 + rj.x * b22;
-                An[dst[0]] = d11;
-                An[dst[3]] = d22;
-                if (dblk) {
-                    An[dst[1]] = 0.5 * (d12 + d21);
-                } else {
-                    An[dst[1]] = d12;
-                    An[dst[2]] = d21;
+            const unsigned A = sbase + cur, An = sbase + (matb - cur);
+            const unsigned C = csb + (static_cast<unsigned>(rounds & 1) << 9);
+            wslot = wslot + 1 == ring ? 0 : wslot + 1;
+            if (!pwarp) {
+                // Workers start their shared-memory traffic only once the pivot
+                // warp's loads are queued ahead of it.
+                asm volatile("bar.sync 1, %0;" ::"n"(kValThreads) : "memory");
+                if (work) {
+                    const double2 ri = lds128(C + rio), rj = lds128(C + rjo);
+                    double d11, d12, d21, d22;
+                    rotate_block(ri, rj, lds64(A + la[0]), lds64(A + la[1]), lds64(A + la[2]), lds64(A + la[3]), d11,
+                                 d12, d21, d22);
+                    sts64(An + sa[0], d11);
+                    sts64(An + sa[1], d12);
+                    sts64(An + sa[2], d21);
+                    sts64(An + sa[3], d22);
+                }
+            } else {
+                const double2 rm = lds128(C + rmo), ra = lds128(C + rao), rb = lds128(C + rbo);
+                const double2 rp = lds128(C + rpo), rq = lds128(C + rqo);
+                const double a11 = lds64(A + dla[0]), a12 = lds64(A + dla[1]), a22 = lds64(A + dla[2]);
+                const double e11 = lds64(A + ela[0]), e12 = lds64(A + ela[1]), e21 = lds64(A + ela[2]),
+                             e22 = lds64(A + ela[3]);
+                const double p11 = lds64(A + pla[0]), p12 = lds64(A + pla[1]), p22 = lds64(A + pla[2]);
+                const double q11 = lds64(A + qla[0]), q12 = lds64(A + qla[1]), q22 = lds64(A + qla[2]);
+                asm volatile("bar.arrive 1, %0;" ::"n"(kValThreads) : "memory");
+                long long ta = 0;
+                if (probe) ta = clock64() + static_cast<long long>(rm.x == 12345.0);
+                double d11, d12, d21, d22;
+                rotate_block(rm, rm, a11, a12, a12, a22, d11, d12, d21, d22);
+                double f11, f12, f21, f22;
+                rotate_block(ra, rb, e11, e12, e21, e22, f11, f12, f21, f22);
+                double x11, x12, x21, x22, y11, y12, y21, y22;
+                rotate_block(rp, rp, p11, p12, p12, p22, x11, x12, x21, x22);
+                rotate_block(rq, rq, q11, q12, q12, q22, y11, y12, y21, y22);
+                const double e = ex ? (ey ? f22 : f21) : (ey ? f12 : f11);
+                const double2 v = rotation_or_identity(sx ? x22 : x11, sy ? y22 : y11, e, abs_floor);
+                if (probe) chain += clock64() + static_cast<long long>(v.x == 12345.0) - ta;
+                if (plane) {
+                    sts128(csb + (static_cast<unsigned>((rounds + 1) & 1) << 9) + rmo, v);
+                    sts128(logb + 16u * static_cast<unsigned>(wslot * k) + rmo, v);
+                    sts64(An + dsa[0], d11);
+                    sts64(An + dsa[1], 0.5 * (d12 + d21));
+                    sts64(An + dsa[2], d22);
+                    sts64(An + esa[0], f11);
+                    sts64(An + esa[1], f12);
+                    sts64(An + esa[2], f21);
+                    sts64(An + esa[3], f22);
                 }
             }
-            cur ^= 1;
+            cur = matb - cur;
             __syncthreads();
         }
+        const long long ttail = clock64();
+        {
+            const int r0 = sweep * (np - 1);
+            const double2* logs = reinterpret_cast<const double2*>(sm + 2 * mat + 2 * kMaxNp);
+            for (int e = tid; e < (np - 1) * k; e += kValThreads)
+                rot[static_cast<int64_t>(r0) * k + e] = logs[((r0 + e / k) % ring) * k + e % k];
+        }
         // Stop at off(A) ≤ 1e-14·‖A‖_F, or once stalled on rounding noise ≤ 1e-12·‖A‖_F.
-        const double* A = sm + cur * mat;
+        const double* A = sm + cur / 8;
         double off = 0.0, tot = 0.0;
-        for (int idx = tid; idx < np * np; idx += kThreads) {
+        for (int idx = tid; idx < np * np; idx += kValThreads) {
             const int i = idx / np, j = idx % np;
             if (j < i) continue;
-            const double a = A[i * ld + j];
+            const double a = A[addr_of(i, j, k)];
             const double w2 = (i == j) ? 1.0 : 2.0;
             tot = fma(w2 * a, a, tot);
             if (i != j) off = fma(w2 * a, a, off);
@@ -188,7 +361,7 @@ __global__ void __launch_bounds__(kThreads) jacobi_values_kernel(const double* _
         __syncthreads();
         if (tid == 0) {
             double o = 0.0, t = 0.0;
-            for (int w = 0; w < kWarps; ++w) {
+            for (int w = 0; w < kValWarps; ++w) {
                 o += red[2 * w];
                 t += red[2 * w + 1];
             }
@@ -196,15 +369,26 @@ __global__ void __launch_bounds__(kThreads) jacobi_values_kernel(const double* _
             prev_off = o;
         }
         __syncthreads();
+        if (probe) sweep_tail += clock64() - ttail;
         if (stop) break;
     }
-    const double* A = sm + cur * mat;
-    for (int p = tid; p < np; p += kThreads) diag_out[p] = A[p * ld + p];
+    if (probe) {
+        prof[1] = chain;
+        prof[3] = sweep_tail;
+    }
+    const double* A = sm + cur / 8;
+    for (int p = tid; p < np; p += kValThreads) diag_out[p] = A[addr_of(p, p, k)];
     if (tid == 0) {
         info[0] = rounds;
         info[1] = sweeps_done;
+        if (prof) {
+            prof[0] = static_cast<unsigned long long>(clock64() - tloop);
+            prof[2] = 0;
+            prof[4] = static_cast<unsigned long long>(rounds);
+        }
     }
 }
+
 
 // One warp per row of V (row = original index 0..np-1): replay the rotation log
 // on e_row with the same position permutation, then place each eigenvector
@@ -281,12 +465,27 @@ __global__ void __launch_bounds__(128) jacobi_vectors_kernel(int n, const double
 
 }  // namespace
 
+unsigned long long* eig_probe_buffer() {
+    static unsigned long long* buf = nullptr;
+    static bool init = false;
+    if (!init) {
+        init = true;
+        if (std::getenv("TS_EIG_PROFILE")) {
+            TS_CUDA_CHECK(cudaMalloc(&buf, 8 * sizeof(unsigned long long)));
+            const unsigned long long mode[8] = {0, 0, 0, 0, 0, 0, 0,
+                                                static_cast<unsigned long long>(std::atoi(std::getenv("TS_EIG_PROFILE")))};
+            TS_CUDA_CHECK(cudaMemcpy(buf, mode, sizeof(mode), cudaMemcpyHostToDevice));
+        }
+    }
+    return buf;
+}
+
 bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
                           int* sweeps) {
     const int np = n + (n & 1);
     if (np > kMaxNp || np < 4) return false;
     const int k = np / 2;
-    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(np) * (np + 2) + 2 * k) + 16;
+    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(np) * np + 2 * kMaxNp + 4 * static_cast<size_t>(np - 1) * k + np);
     static bool configured = false;
     if (!configured) {
         TS_CUDA_CHECK(cudaFuncSetAttribute(jacobi_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -295,7 +494,7 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
     auto* rot = sc.alloc_n<double2>(static_cast<size_t>(kMaxSweeps) * (np - 1) * k);
     double* dpos = sc.alloc_n<double>(static_cast<size_t>(np));
     int* info = sc.alloc_n<int>(2);
-    jacobi_values_kernel<<<1, kThreads, smem, sc.stream()>>>(C, ldc, n, rot, dpos, info);
+    jacobi_values_kernel<<<1, kValThreads, smem, sc.stream()>>>(C, ldc, n, rot, dpos, info, eig_probe_buffer());
     TS_LAUNCH_CHECK();
     jacobi_vectors_kernel<<<(np + 3) / 4, 128, 0, sc.stream()>>>(n, rot, dpos, info, lambda, V);
     TS_LAUNCH_CHECK();
@@ -306,7 +505,11 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
 
 }  // namespace ts
 
-// Kept for the C ABI debug hook; the two-kernel solver has no phase probe.
+// C ABI debug hook: per-phase clock totals of the last values-kernel run when
+// TS_EIG_PROFILE is set (see jacobi_values_kernel), else zeros.
 extern "C" void tsi_read_eig_profile(long long* out) {
-    for (int i = 0; i < 4; ++i) out[i] = 0;
+    unsigned long long* p = ts::eig_probe_buffer();
+    unsigned long long h[5] = {0, 0, 0, 0, 0};
+    if (p) TS_CUDA_CHECK(cudaMemcpy(h, p, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 5; ++i) out[i] = static_cast<long long>(h[i]);
 }

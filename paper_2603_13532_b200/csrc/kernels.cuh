@@ -129,5 +129,7 @@ void launch_scale_columns(const double* F, int64_t n, int64_t R, const double* s
 void launch_atom_sumsq(const double* cores, const Atom* atoms, int natoms, int order, double* out, CallScratch& sc);
 
 int max_tsqr_cols();
+// Device buffer of the values-kernel phase probe (non-null iff TS_EIG_PROFILE is set).
+unsigned long long* eig_probe_buffer();
 
 }  // namespace ts
