@@ -1128,8 +1128,8 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
 
 void tsi_read_eig_profile(long long* out);
 // Debug: phase clock totals of the last n ≤ 64 values-kernel run (TS_EIG_PROFILE=1).
-int ts_debug_eig_profile(long long* out5) {
-    return guarded([&] { tsi_read_eig_profile(out5); });
+int ts_debug_eig_profile(long long* out17) {
+    return guarded([&] { tsi_read_eig_profile(out17); });
 }
 
 // Symmetric eigensolver of the ST-HOSVD fast path (reference sym_eig,

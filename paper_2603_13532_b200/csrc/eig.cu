@@ -111,6 +111,22 @@ __device__ __forceinline__ void rotate_block(double2 ri, double2 rj, double a11,
     d22 = rj.y * b21 + rj.x * b22;
 }
 
+// rotation_or_identity without branches (both outcomes computed, then
+// selected; the discarded one may be inf/NaN when apq = 0).
+__device__ __forceinline__ double2 rotation_select(double a, double b, double g, double abs_floor) {
+    const double theta = (b - a) * rcp_approx(2.0 * g);
+    const double at = fabs(theta);
+    const double u = fma(theta, theta, 1.0);
+    const double t_small = copysign(rcp_approx(at + u * rsqrt_approx(u)), theta);
+    const double t = at > 1e150 ? 0.5 * rcp_approx(theta) : t_small;
+    const double w = fma(t, t, 1.0);
+    double r = rsqrt_approx(w);
+    r = r * fma(-0.5 * w, r * r, 1.5);
+    r = r * fma(-0.5 * w, r * r, 1.5);
+    const bool rotate = fabs(g) > abs_floor && g * g > 1e-30 * fabs(a * b);
+    return rotate ? make_double2(r, t * r) : make_double2(1.0, 0.0);
+}
+
 __device__ __forceinline__ double2 rotation_or_identity(double app, double aqq, double apq, double abs_floor) {
     double c = 1.0, s = 0.0;
     if (fabs(apq) > abs_floor && apq * apq > 1e-30 * fabs(app * aqq)) rotation(app, aqq, apq, c, s);
@@ -119,7 +135,8 @@ __device__ __forceinline__ double2 rotation_or_identity(double app, double aqq, 
 
 // info[0] = rounds performed, info[1] = sweeps; diag_out[p] = A[p][p] at the end
 // (position order), rot[round * k + i] = rotation of pair i in that round;
-// prof (optional) = {round-loop clocks, 0, 0, 0, rounds}.
+// prof (optional, TS_EIG_PROFILE) = {round-loop clocks, 0, 0, 0, rounds}; prof[7]
+// on entry selects ablations.
 //
 // One barrier per round.  A round is issue-bound (every block costs the same
 // few instructions), so the upper triangle's blocks are packed densely: worker
@@ -143,9 +160,8 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     const int ring = 2 * (np - 1);
     __shared__ int srcpos[kMaxNp];
     __shared__ unsigned xmask[kMaxNp / 2];
-    __shared__ int stop;
     __shared__ double red[2 * kValWarps];
-    __shared__ double prev_off, amax_s;
+    __shared__ double amax_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int idx = tid; idx < np * np; idx += kValThreads) {
         const int i = idx / np, j = idx % np;
@@ -156,11 +172,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     }
     if (tid < np) srcpos[dest_of(tid, k)] = tid;
     if (tid < kMaxNp / 2) xmask[tid] = 0u;
-    if (tid == 0) {
-        amax_s = 0.0;
-        prev_off = 0.0;
-        stop = 0;
-    }
+    if (tid == 0) amax_s = 0.0;
     __syncthreads();
     {
         double mx = 0.0;
@@ -276,8 +288,12 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     unsigned cur = 0;  // byte offset of the current matrix buffer (0 or matb)
     int rounds = 0, sweeps_done = 0, wslot = 0;
     const long long tloop = clock64();
-    const bool probe = prof != nullptr && lane == 0 && warp == kWorkWarps;
-    unsigned long long chain = 0, sweep_tail = 0;
+    // Timing ablations (TS_EIG_PROFILE=mode, tools/probe_jacobi.py): 4 = workers
+    // skip their blocks, 8 = the pivot forms identity rotations.
+    const int mode = prof != nullptr ? static_cast<int>(prof[7]) : 0;
+    const bool skip_work = (mode & 4) != 0, skip_rot = (mode & 8) != 0;
+    unsigned long long tail_clk = 0;
+    double prev_off = 0.0;
     for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
         sweeps_done = sweep + 1;
         for (int r = 0; r < np - 1; ++r, ++rounds) {
@@ -288,7 +304,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
                 // Workers start their shared-memory traffic only once the pivot
                 // warp's loads are queued ahead of it.
                 asm volatile("bar.sync 1, %0;" ::"n"(kValThreads) : "memory");
-                if (work) {
+                if (work && !skip_work) {
                     const double2 ri = lds128(C + rio), rj = lds128(C + rjo);
                     double d11, d12, d21, d22;
                     rotate_block(ri, rj, lds64(A + la[0]), lds64(A + la[1]), lds64(A + la[2]), lds64(A + la[3]), d11,
@@ -299,26 +315,32 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
                     sts64(An + sa[3], d22);
                 }
             } else {
-                const double2 rm = lds128(C + rmo), ra = lds128(C + rao), rb = lds128(C + rbo);
-                const double2 rp = lds128(C + rpo), rq = lds128(C + rqo);
-                const double a11 = lds64(A + dla[0]), a12 = lds64(A + dla[1]), a22 = lds64(A + dla[2]);
-                const double e11 = lds64(A + ela[0]), e12 = lds64(A + ela[1]), e21 = lds64(A + ela[2]),
-                             e22 = lds64(A + ela[3]);
+                // Loads in order of need: rotations, the entries that form the
+                // next rotation, then this lane's two blocks.
+                const double2 rp = lds128(C + rpo), rq = lds128(C + rqo), ra = lds128(C + rao), rb = lds128(C + rbo);
+                const double2 rm = lds128(C + rmo);
                 const double p11 = lds64(A + pla[0]), p12 = lds64(A + pla[1]), p22 = lds64(A + pla[2]);
                 const double q11 = lds64(A + qla[0]), q12 = lds64(A + qla[1]), q22 = lds64(A + qla[2]);
+                const double e11 = lds64(A + ela[0]), e12 = lds64(A + ela[1]), e21 = lds64(A + ela[2]),
+                             e22 = lds64(A + ela[3]);
+                const double a11 = lds64(A + dla[0]), a12 = lds64(A + dla[1]), a22 = lds64(A + dla[2]);
                 asm volatile("bar.arrive 1, %0;" ::"n"(kValThreads) : "memory");
-                long long ta = 0;
-                if (probe) ta = clock64() + static_cast<long long>(rm.x == 12345.0);
+                // Critical path first, branch-free so the block updates below can
+                // fill the rotation's latency.  Rotated diagonal entry at sp / sq:
+                // d11 of R_pᵀ·B·R_p, and d22 as d11 with (c, s) → (s, -c); the
+                // pairing entry (ex, ey) of R_aᵀ·E·R_b.
+                const double cp = sx ? rp.y : rp.x, spp = sx ? -rp.x : rp.y;
+                const double cq = sy ? rq.y : rq.x, sqq = sy ? -rq.x : rq.y;
+                const double app = cp * (cp * p11 - spp * p12) - spp * (cp * p12 - spp * p22);
+                const double aqq = cq * (cq * q11 - sqq * q12) - sqq * (cq * q12 - sqq * q22);
+                const double al = ex ? ra.y : ra.x, be = ex ? ra.x : -ra.y;
+                const double ga = ey ? rb.y : rb.x, de = ey ? rb.x : -rb.y;
+                const double e = ga * (al * e11 + be * e21) + de * (al * e12 + be * e22);
+                const double2 v = skip_rot ? make_double2(1.0, 0.0) : rotation_select(app, aqq, e, abs_floor);
                 double d11, d12, d21, d22;
                 rotate_block(rm, rm, a11, a12, a12, a22, d11, d12, d21, d22);
                 double f11, f12, f21, f22;
                 rotate_block(ra, rb, e11, e12, e21, e22, f11, f12, f21, f22);
-                double x11, x12, x21, x22, y11, y12, y21, y22;
-                rotate_block(rp, rp, p11, p12, p12, p22, x11, x12, x21, x22);
-                rotate_block(rq, rq, q11, q12, q12, q22, y11, y12, y21, y22);
-                const double e = ex ? (ey ? f22 : f21) : (ey ? f12 : f11);
-                const double2 v = rotation_or_identity(sx ? x22 : x11, sy ? y22 : y11, e, abs_floor);
-                if (probe) chain += clock64() + static_cast<long long>(v.x == 12345.0) - ta;
                 if (plane) {
                     sts128(csb + (static_cast<unsigned>((rounds + 1) & 1) << 9) + rmo, v);
                     sts128(logb + 16u * static_cast<unsigned>(wslot * k) + rmo, v);
@@ -334,48 +356,57 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
             cur = matb - cur;
             __syncthreads();
         }
-        const long long ttail = clock64();
+        const long long t_tail = clock64();
         {
-            const int r0 = sweep * (np - 1);
-            const double2* logs = reinterpret_cast<const double2*>(sm + 2 * mat + 2 * kMaxNp);
-            for (int e = tid; e < (np - 1) * k; e += kValThreads)
-                rot[static_cast<int64_t>(r0) * k + e] = logs[((r0 + e / k) % ring) * k + e % k];
+            // This sweep's rounds sit in one contiguous half of the ring.
+            const double2* logs = reinterpret_cast<const double2*>(sm + 2 * mat + 2 * kMaxNp) +
+                                  static_cast<size_t>(sweep & 1) * (np - 1) * k;
+            double2* dst = rot + static_cast<int64_t>(sweep) * (np - 1) * k;
+            for (int e = tid; e < (np - 1) * k; e += kValThreads) dst[e] = logs[e];
         }
-        // Stop at off(A) ≤ 1e-14·‖A‖_F, or once stalled on rounding noise ≤ 1e-12·‖A‖_F.
-        const double* A = sm + cur / 8;
-        double off = 0.0, tot = 0.0;
-        for (int idx = tid; idx < np * np; idx += kValThreads) {
-            const int i = idx / np, j = idx % np;
-            if (j < i) continue;
-            const double a = A[addr_of(i, j, k)];
-            const double w2 = (i == j) ? 1.0 : 2.0;
-            tot = fma(w2 * a, a, tot);
-            if (i != j) off = fma(w2 * a, a, off);
-        }
-        off = warp_sum(off);
-        tot = warp_sum(tot);
-        if (lane == 0) {
-            red[2 * warp] = off;
-            red[2 * warp + 1] = tot;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double o = 0.0, t = 0.0;
-            for (int w = 0; w < kValWarps; ++w) {
-                o += red[2 * w];
-                t += red[2 * w + 1];
+        // off(A) and Σ diag² over the same block partition the rounds use (every
+        // stored entry once; off-diagonal entries stand for both triangles).
+        {
+            const unsigned A = sbase + cur;
+            double off = 0.0, dia = 0.0;
+            if (work) {
+                for (int u = 0; u < 4; ++u) {
+                    const double x = lds64(A + la[u]);
+                    off = fma(x, x, off);
+                }
+            } else if (plane) {
+                const double a11 = lds64(A + dla[0]), a12 = lds64(A + dla[1]), a22 = lds64(A + dla[2]);
+                dia = a11 * a11 + a22 * a22;
+                off = a12 * a12;
+                for (int u = 0; u < 4; ++u) {
+                    const double x = lds64(A + ela[u]);
+                    off = fma(x, x, off);
+                }
             }
-            stop = (o <= 1e-28 * t) || (o <= 1e-24 * t && o > 0.25 * prev_off);
-            prev_off = o;
+            off = warp_sum(off);
+            dia = warp_sum(dia);
+            if (lane == 0) {
+                red[2 * warp] = off;
+                red[2 * warp + 1] = dia;
+            }
         }
         __syncthreads();
-        if (probe) sweep_tail += clock64() - ttail;
-        if (stop) break;
+        // Stop at off(A) ≤ 1e-14·‖A‖_F, or once stalled on rounding noise ≤
+        // 1e-12·‖A‖_F.  Every thread sums the per-warp partials in the same order,
+        // so the decision is uniform; red[] is next written a whole sweep later.
+        double o = 0.0, t = 0.0;
+        for (int w = 0; w < kValWarps; ++w) {
+            o += red[2 * w];
+            t += red[2 * w + 1];
+        }
+        o *= 2.0;
+        t += o;
+        const bool done = (o <= 1e-28 * t) || (o <= 1e-24 * t && o > 0.25 * prev_off);
+        prev_off = o;
+        if (prof != nullptr && tid == 0) tail_clk += clock64() + static_cast<long long>(done) - t_tail;
+        if (done) break;
     }
-    if (probe) {
-        prof[1] = chain;
-        prof[3] = sweep_tail;
-    }
+    __syncthreads();  // the last flush and the final matrix are complete
     const double* A = sm + cur / 8;
     for (int p = tid; p < np; p += kValThreads) diag_out[p] = A[addr_of(p, p, k)];
     if (tid == 0) {
@@ -383,7 +414,8 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
         info[1] = sweeps_done;
         if (prof) {
             prof[0] = static_cast<unsigned long long>(clock64() - tloop);
-            prof[2] = 0;
+            prof[1] = prof[2] = 0;
+            prof[3] = tail_clk;
             prof[4] = static_cast<unsigned long long>(rounds);
         }
     }
@@ -471,9 +503,9 @@ unsigned long long* eig_probe_buffer() {
     if (!init) {
         init = true;
         if (std::getenv("TS_EIG_PROFILE")) {
-            TS_CUDA_CHECK(cudaMalloc(&buf, 8 * sizeof(unsigned long long)));
-            const unsigned long long mode[8] = {0, 0, 0, 0, 0, 0, 0,
-                                                static_cast<unsigned long long>(std::atoi(std::getenv("TS_EIG_PROFILE")))};
+            TS_CUDA_CHECK(cudaMalloc(&buf, 32 * sizeof(unsigned long long)));
+            unsigned long long mode[32] = {};
+            mode[7] = static_cast<unsigned long long>(std::atoi(std::getenv("TS_EIG_PROFILE")));
             TS_CUDA_CHECK(cudaMemcpy(buf, mode, sizeof(mode), cudaMemcpyHostToDevice));
         }
     }
@@ -509,7 +541,7 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
 // TS_EIG_PROFILE is set (see jacobi_values_kernel), else zeros.
 extern "C" void tsi_read_eig_profile(long long* out) {
     unsigned long long* p = ts::eig_probe_buffer();
-    unsigned long long h[5] = {0, 0, 0, 0, 0};
+    unsigned long long h[17] = {};
     if (p) TS_CUDA_CHECK(cudaMemcpy(h, p, sizeof(h), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 5; ++i) out[i] = static_cast<long long>(h[i]);
+    for (int i = 0; i < 17; ++i) out[i] = static_cast<long long>(h[i]);
 }

@@ -29,7 +29,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtucksum_cuda.so")
+# TUCKSUM_LIB points at an alternative build of the same library (A/B timing).
+LIB_PATH = os.environ.get("TUCKSUM_LIB") or os.path.join(_HERE, "libtucksum_cuda.so")
 
 i64 = C.c_int64
 u64 = C.c_uint64
