@@ -279,7 +279,7 @@ def main():
             traffic = json.load(f).get(wl.name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"bound": "tensor", "kernel": "gemm_kernel<TN> (stage A, grouped over modes)",
+    roofline = {"bound": "tensor", "kernel": "gemm_tma_kernel<TN> (stage A: Z_j = Ω_jᵀ·F_j, one launch over all modes)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src,

@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-ccbin", "/usr/bin/g++"]
+# Extra nvcc flags for instrumented A/B builds (e.g. TS_NVCC_EXTRA="-DTS_CHOL_PROBE").
+FLAGS += os.environ.get("TS_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -82,24 +82,6 @@ __device__ __forceinline__ int addr_sym(int r, int c, int k) { return r <= c ? a
 // Stored address of the element at positions (r, c) after the permutation.
 __device__ __forceinline__ int addr_next(int r, int c, int k) { return addr_sym(dest_of(r, k), dest_of(c, k), k); }
 
-// Shared-space accesses by precomputed 32-bit address (no per-round address math).
-__device__ __forceinline__ double lds64(unsigned a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ double2 lds128(unsigned a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts64(unsigned a, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
-__device__ __forceinline__ void sts128(unsigned a, double2 v) {
-    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
-}
-
 // Rᵢᵀ·B·Rⱼ of one 2×2 block (R = [[c, s], [-s, c]]).
 __device__ __forceinline__ void rotate_block(double2 ri, double2 rj, double a11, double a12, double a21, double a22,
                                              double& d11, double& d12, double& d21, double& d22) {

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <stdexcept>
 
 #include "kernels.cuh"
 
@@ -596,34 +597,57 @@ __global__ void __launch_bounds__(kJacThreads) sym_jacobi_kernel(const double* _
 // Cholesky R (upper, RᵀR = G) of small SPD matrices and their inverses R⁻¹, one
 // CTA per matrix (blockIdx.x indexes the batch).  flag[b] |= 1 when a pivot is
 // not safely positive, |= 2 when check_identity and max|G - I| > 1e-2 (second
-// CholQR pass on a badly conditioned input).  The inverse is formed by recursive
-// 2×2 block doubling (X12 = -X11·R12·X22), i.e. log2(n) parallel levels instead
-// of an n-step back substitution.
-__global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(CholBatch cb) {
+// CholQR pass on a badly conditioned input).
+//
+// Thread (g, j) of the 4 × NC grid keeps column j, rows g, g+4, g+8, … in
+// registers; each elimination step is one broadcast of a pivot row through
+// shared memory plus one FMA per owned row — one barrier per step.  Both
+// loops are fully unrolled over the row blocks so every register index is
+// static (a run-time index would send the array to local memory) and rows
+// already finished drop out at compile time.
+//  1. outer-product Cholesky on unscaled rows: G = Uᵀ·D⁻¹·U, R = D^{-1/2}·U,
+//     D = diag(U).  Published rows carry zeros left of the diagonal, so the
+//     update needs no row predicate.
+//  2. R⁻¹ from the last row up: X[q][c] = d_q·(δ_qc − d_q·Σ_{m>q} U[q][m]·X[m][c]),
+//     d_q = U[q][q]^{-1/2} = 1 / R[q][q].
+#ifdef TS_CHOL_PROBE
+__device__ long long g_chol_probe[8];
+#define CHOL_T(i) if (threadIdx.x == 0 && blockIdx.x == 0) g_chol_probe[i] = clock64();
+#else
+#define CHOL_T(i)
+#endif
+template <int NC>
+__global__ void __launch_bounds__(4 * NC) chol_inv_kernel(CholBatch cb) {
+    constexpr int RPT = NC / 4;  // rows per thread
+    constexpr int LD = NC + 1;   // odd stride: the column-major store below is conflict-free
     const int b = blockIdx.x;
     const int n = cb.n;
     const double* __restrict__ G = cb.G[b];
     extern __shared__ __align__(16) double sm[];
-    const int ld = n + 1;
-    double* A = sm;              // n × ld, A[i*ld + j]: R (upper)
-    double* X = A + n * ld;      // n × ld: R⁻¹ in the upper part, level scratch T (transposed) below
-    double* piv = X + n * ld;    // n
+    double* U = sm;           // n × LD: published rows of U
+    double* X = U + n * LD;   // n × LD: rows of R⁻¹
+    double* rd = X + n * LD;  // n: U[q][q]^{-1/2}
     __shared__ int bad;
     __shared__ double dmax;
     const int tid = threadIdx.x;
+    const int j = tid % NC, g = tid / NC;
     if (tid == 0) {
         bad = 0;
         dmax = 0.0;
     }
     __syncthreads();
+    double a[RPT];
     double dev = 0.0, dm = 0.0;
-    for (int idx = tid; idx < n * n; idx += kJacThreads) {
-        const int i = idx % n, j = idx / n;
-        const double g = G[i + static_cast<int64_t>(j) * cb.ldg];
-        dev = fmax(dev, fabs(g - (i == j ? 1.0 : 0.0)));
-        if (i == j) dm = fmax(dm, g);
-        A[i * ld + j] = g;
-        X[i * ld + j] = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int i = g + 4 * r;
+        double v = 0.0;
+        if (i < n && j < n) {
+            v = G[i + static_cast<int64_t>(j) * cb.ldg];
+            dev = fmax(dev, fabs(v - (i == j ? 1.0 : 0.0)));
+            if (i == j) dm = fmax(dm, v);
+        }
+        a[r] = v;
     }
     if (cb.check_identity && dev > 1e-2) atomicOr(&bad, 2);
     for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
@@ -631,68 +655,72 @@ __global__ void __launch_bounds__(kJacThreads) chol_inv_kernel(CholBatch cb) {
         atomicMax(reinterpret_cast<unsigned long long*>(&dmax), __double_as_longlong(dm));
     __syncthreads();
     const double floor_piv = 1e-28 * dmax;
-    // Right-looking Cholesky; the scaling of row k-1 is deferred into step k.
-    // Rows of the trailing update go to warps, columns to lanes: no index
-    // divisions; one thread forms 1/p and 1/sqrt(p) per step.
-    const int warp = tid >> 5, lane = tid & 31;
-    __shared__ double s_ip, s_ir;
-    for (int k = 0; k < n; ++k) {
-        if (tid == 0) {
-            double p = A[k * ld + k];
-            if (!(p > floor_piv)) {
-                bad |= 1;
-                p = fmax(dmax, 1.0);
+    const double repl = fmax(dmax, 1.0);
+    const unsigned Ub = smem_u32(U), Xb = smem_u32(X), rdb = smem_u32(rd);
+    constexpr unsigned ld8 = 8u * LD;
+    const unsigned urow = Ub + g * ld8;  // this thread's first row of U (rows g + 4r)
+    CHOL_T(0)
+
+    // 1. Cholesky.  Step k = 4·kk + g4: the owners of row k publish it, everyone eliminates.
+#pragma unroll
+    for (int kk = 0; kk < RPT; ++kk) {
+#pragma unroll
+        for (int g4 = 0; g4 < 4; ++g4) {
+            const int k = 4 * kk + g4;
+            if (k < n) {
+                const unsigned rowk = Ub + k * ld8;
+                if (g == g4) {
+                    double v = (j >= k && j < n) ? a[kk] : 0.0;
+                    if (j == k && !(v > floor_piv)) {
+                        bad |= 1;  // benign race: every writer stores the same bit
+                        v = repl;
+                    }
+                    sts64(rowk + 8u * j, v);
+                }
+                __syncthreads();
+                const double p = lds64(rowk + 8u * k);
+                const double f = (j > k && j < n) ? lds64(rowk + 8u * j) / p : 0.0;
+#pragma unroll
+                for (int r = kk; r < RPT; ++r) a[r] = fma(-lds64(rowk + 8u * (g + 4 * r)), f, a[r]);
             }
-            piv[k] = p;
-            s_ip = 1.0 / p;
-            s_ir = 1.0 / sqrt(p);
-        }
-        __syncthreads();
-        const double ip = s_ip;
-        for (int i = k + 1 + warp; i < n; i += kJacWarps) {
-            const double aki = A[k * ld + i] * ip;
-            for (int j = i + lane; j < n; j += 32) A[i * ld + j] -= aki * A[k * ld + j];
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const double ir = s_ir;
-            for (int j = k + lane; j < n; j += 32) A[k * ld + j] = (j == k) ? piv[k] * ir : A[k * ld + j] * ir;
         }
     }
     __syncthreads();
+    for (int q = tid; q < n; q += 4 * NC) rd[q] = 1.0 / sqrt(U[q * LD + q]);
     __syncthreads();
-    for (int i = tid; i < n; i += kJacThreads) X[i * ld + i] = 1.0 / A[i * ld + i];
-    __syncthreads();
-    // Block doubling: for diagonal pairs (o, o+bs), X12 = -X11 · (R12 · X22).
-    for (int bs = 1; bs < n; bs <<= 1) {
-        const int pairs = (n + 2 * bs - 1) / (2 * bs);
-        const int per = bs * bs;
-        for (int idx = tid; idx < pairs * per; idx += kJacThreads) {
-            const int pr = idx / per, e = idx % per;
-            const int o = pr * 2 * bs, i = e % bs, j = e / bs;
-            const int r = o + i, c = o + bs + j;
-            if (c >= n) continue;
-            double acc = 0.0;
-            for (int k = o + bs; k <= c; ++k) acc = fma(A[r * ld + k], X[k * ld + c], acc);
-            X[c * ld + r] = acc;  // T(r, c) kept transposed in the free lower triangle
+    CHOL_T(1)
+
+    // 2. R⁻¹, last row first; a[r] accumulates Σ_m U[i][m]·X[m][j] for own rows i.
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) a[r] = 0.0;
+#pragma unroll
+    for (int qq = RPT - 1; qq >= 0; --qq) {
+#pragma unroll
+        for (int g4 = 3; g4 >= 0; --g4) {
+            const int q = 4 * qq + g4;
+            if (q < n) {
+                const unsigned rowq = Xb + q * ld8;
+                if (g == g4) {
+                    const double dq = lds64(rdb + 8u * q);
+                    const double v = (j >= q && j < n) ? dq * ((j == q ? 1.0 : 0.0) - dq * a[qq]) : 0.0;
+                    sts64(rowq + 8u * j, v);
+                }
+                __syncthreads();
+                const double xq = lds64(rowq + 8u * j);
+#pragma unroll
+                for (int r = 0; r <= qq; ++r) a[r] = fma(lds64(urow + r * 4u * ld8 + 8u * q), xq, a[r]);
+            }
         }
-        __syncthreads();
-        for (int idx = tid; idx < pairs * per; idx += kJacThreads) {
-            const int pr = idx / per, e = idx % per;
-            const int o = pr * 2 * bs, i = e % bs, j = e / bs;
-            const int r = o + i, c = o + bs + j;
-            if (c >= n) continue;
-            double acc = 0.0;
-            for (int k = r; k < o + bs; ++k) acc = fma(X[r * ld + k], X[c * ld + k], acc);
-            X[r * ld + c] = -acc;
-        }
-        __syncthreads();
     }
+    __syncthreads();
+    CHOL_T(2)
+    CHOL_T(3)
     double* Rinv = cb.Rinv[b];
-    for (int idx = tid; idx < n * n; idx += kJacThreads) {
-        const int i = idx % n, j = idx / n;
-        Rinv[i + static_cast<int64_t>(j) * cb.ldri] = i <= j ? X[i * ld + j] : 0.0;
+    for (int idx = tid; idx < n * n; idx += 4 * NC) {
+        const int i = idx % n, c = idx / n;
+        Rinv[i + static_cast<int64_t>(c) * cb.ldri] = X[i * LD + c];
     }
+    CHOL_T(4)
     if (tid == 0 && bad) atomicOr(cb.flag[b], bad);
 }
 
@@ -770,6 +798,10 @@ int tsqr_block_rows(int64_t cols) {
 }
 
 }  // namespace
+
+#ifdef TS_CHOL_PROBE
+extern "C" void tsi_read_chol_probe(long long* out) { cudaMemcpyFromSymbol(out, g_chol_probe, 8 * sizeof(long long)); }
+#endif
 
 int max_tsqr_cols() { return 96; }
 
@@ -960,13 +992,17 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
 
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
     if (count <= 0) return;
-    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(cb.n) * (cb.n + 1) + cb.n);
+    if (cb.n > 96) throw std::invalid_argument("chol_inv: n > 96");
+    const size_t ldc = cb.n <= 64 ? 65 : 97;  // LD of the kernel instance
+    const size_t smem = sizeof(double) * (2 * static_cast<size_t>(cb.n) * ldc + cb.n);
     static bool configured = false;
     if (!configured) {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    chol_inv_kernel<<<count, kJacThreads, smem, sc.stream()>>>(cb);
+    if (cb.n <= 64) chol_inv_kernel<64><<<count, 4 * 64, smem, sc.stream()>>>(cb);
+    else chol_inv_kernel<96><<<count, 4 * 96, smem, sc.stream()>>>(cb);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
