@@ -714,7 +714,6 @@ __global__ void __launch_bounds__(4 * NC) chol_inv_kernel(CholBatch cb) {
     }
     __syncthreads();
     CHOL_T(2)
-    CHOL_T(3)
     double* Rinv = cb.Rinv[b];
     for (int idx = tid; idx < n * n; idx += 4 * NC) {
         const int i = idx % n, c = idx / n;

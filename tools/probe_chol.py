@@ -2,7 +2,7 @@
 
 Build an instrumented library with TS_NVCC_EXTRA=-DTS_CHOL_PROBE, point
 TUCKSUM_LIB at it, and run: prints the clocks of CTA 0 of the last launch
-(load → Cholesky → scaling → inverse → store)."""
+(Cholesky → inverse → store)."""
 import ctypes as C
 import json
 import os
@@ -19,5 +19,5 @@ for _ in range(3):
     res = eng.krp_sum(batch, wl.weights, wl.widths, wl.seed, wl.eps, wl.cap)
 t = (C.c_longlong * 8)()
 T.lib().tsi_read_chol_probe(t)
-print(json.dumps({"cholesky": t[1] - t[0], "scale": t[2] - t[1], "inverse": t[3] - t[2], "store": t[4] - t[3],
+print(json.dumps({"cholesky_clk": t[1] - t[0], "inverse_clk": t[2] - t[1], "store_clk": t[4] - t[2],
                   "n": wl.widths[0]}))
