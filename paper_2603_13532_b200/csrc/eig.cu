@@ -423,9 +423,12 @@ __global__ void __launch_bounds__(128) jacobi_vectors_kernel(int n, const double
     double g = (row == 2 * lane + 1) ? 1.0 : 0.0;  // position 2·lane + 1
     // The log streams through shared memory in chunks of kChunk rounds
     // (cp.async, double-buffered, shared by the CTA's four rows) so the
-    // loop-carried chain never waits on L2.
+    // loop-carried chain never waits on L2.  Slots of lanes ≥ k hold the
+    // identity, so the round loop has no branch.
     constexpr int kChunk = 32;
     __shared__ __align__(16) double2 logbuf[2][kChunk * 32];
+    for (int e = threadIdx.x; e < 2 * kChunk * 32; e += blockDim.x)
+        if ((e & 31) >= k) logbuf[e / (kChunk * 32)][e % (kChunk * 32)] = make_double2(1.0, 0.0);
     auto stage = [&](int chunk, int b) {
         const int r0 = chunk * kChunk;
         const int nr = min(kChunk, rounds - r0);
@@ -440,18 +443,21 @@ __global__ void __launch_bounds__(128) jacobi_vectors_kernel(int n, const double
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        const double2* cur = logbuf[ch & 1];
+        const double2* cur = logbuf[ch & 1] + lane;
         const int nr = min(kChunk, rounds - ch * kChunk);
+        // Lane l+1 ≥ 2 takes x of lane l, lane 1 takes y of lane 0 (the fixed
+        // player's partner moves up); lane l < k-1 takes y of lane l+1 and lane
+        // k-1 keeps its own x.  Two shuffles per round.
+        double2 rr = cur[0];
         for (int ri = 0; ri < nr; ++ri) {
-            const double2 rr = vlane ? cur[ri * 32 + lane] : make_double2(1.0, 0.0);
+            const double2 rn = cur[min(ri + 1, kChunk - 1) * 32];
             const double x = rr.x * f - rr.y * g;
             const double y = rr.y * f + rr.x * g;
-            const double x_up = __shfl_up_sync(0xffffffffu, x, 1);
-            const double y_dn = __shfl_down_sync(0xffffffffu, y, 1);
-            const double y0 = __shfl_sync(0xffffffffu, y, 0);
-            const double xk = __shfl_sync(0xffffffffu, x, k - 1);
-            f = lane == 0 ? x : (lane == 1 ? y0 : x_up);
-            g = lane == k - 1 ? xk : y_dn;
+            const double up = __shfl_up_sync(0xffffffffu, lane == 0 ? y : x, 1);
+            const double dn = __shfl_down_sync(0xffffffffu, y, 1);
+            f = lane == 0 ? x : up;
+            g = lane == k - 1 ? x : dn;
+            rr = rn;
         }
         __syncthreads();
     }
