@@ -128,6 +128,9 @@ struct ts_ctx {
     std::int64_t launches = 0;
     std::vector<cudaEvent_t> events;
     int last_qr_fallbacks = 0, last_svd_fallbacks = 0;  // accurate-path uses in the last call
+    // Speculative tail (see krp_sum_impl): on while the last call needed no
+    // accurate-path fallback.
+    bool spec_ok = true;
 };
 
 struct ts_batch {
@@ -287,7 +290,8 @@ std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double the
 }
 
 ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
-                        std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank) {
+                        std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank,
+                        bool allow_spec = true) {
     // Validation mirrors src/sketch.cpp:16-30,66-87.
     if (b == nullptr || b->count < 1) invalid("sum request needs matching, nonempty summands and weights");
     if (weights == nullptr) invalid("sum request needs matching, nonempty summands and weights");
@@ -405,6 +409,15 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             res->inter_cols[1][n] = s;
         }
     }
+    // Speculative tail: the fast paths of stages D and G (CholeskyQR2; Gram +
+    // Jacobi with the rank fixed by eps = 0 and the cap) are taken without
+    // waiting for their acceptance checks, which run on the device; one sync at
+    // the end reads them, and a rejected call is recomputed on the synchronous
+    // path (identical results whenever the checks pass).  A context falls back
+    // to the synchronous path while its last call needed an accurate path.
+    const bool spec = allow_spec && ctx->spec_ok && !ctx->debug;
+    int* dflags = nullptr;  // stage-D acceptance (CholQR2 pivots / second Gram)
+    int* gflags = nullptr;  // stage-G acceptance (gram_rank checks)
     // ---- Stage D: Û_n = thin Q of Y_n.  Fast path CholeskyQR2 (Gram GEMM, small
     // Cholesky + inverse, GEMM, twice); R = R₂R₁ has a positive diagonal, so Û is
     // the Householder Q with R_ii ≥ 0 of the reference.  Modes whose Y is too
@@ -481,11 +494,16 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             ts::launch_grouped_gemm(Layout::TN, g2, sc, ctx->num_sms);
             ts::launch_chol_inv(cb2, nb, sc);
             ts::launch_grouped_gemm(Layout::NN, q2, sc, ctx->num_sms);
-            std::vector<int> hf(static_cast<size_t>(d), 0);
-            TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
-            TS_CUDA_CHECK(cudaStreamSynchronize(st));
-            for (int n = 0; n < d; ++n)
-                if (hf[static_cast<size_t>(n)] != 0) chol[static_cast<size_t>(n)] = 0;
+            if (spec) {
+                dflags = flags;
+            } else {
+                std::vector<int> hf(static_cast<size_t>(d), 0);
+                TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * static_cast<size_t>(d),
+                                              cudaMemcpyDeviceToHost, st));
+                TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                for (int n = 0; n < d; ++n)
+                    if (hf[static_cast<size_t>(n)] != 0) chol[static_cast<size_t>(n)] = 0;
+            }
         }
         std::vector<ts::TsqrPlan> plans(static_cast<size_t>(d));
         std::vector<ts::TsqrPlan*> pp;
@@ -638,12 +656,19 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     double* Pk[TS_MAX_ORDER] = {};  // q_k × q_k left singular vectors (first rank_k columns used)
     std::int64_t rank[TS_MAX_ORDER];
     double* g = h;
+    const bool spec_g = spec && eps == 0.0;
+    if (spec_g) {
+        gflags = sc.alloc_n<int>(static_cast<size_t>(d));
+        TS_CUDA_CHECK(cudaMemsetAsync(gflags, 0, sizeof(int) * static_cast<size_t>(d), st));
+    }
     {
-        double* d_ss = sc.alloc_n<double>(1);
-        ts::launch_sumsq(h, hsize, d_ss, sc);
-        double hss = 0.0;
-        TS_CUDA_CHECK(cudaMemcpyAsync(&hss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
-        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        double hss = 0.0;  // θ = ε²‖h‖²/d vanishes at ε = 0
+        if (eps != 0.0) {
+            double* d_ss = sc.alloc_n<double>(1);
+            ts::launch_sumsq(h, hsize, d_ss, sc);
+            TS_CUDA_CHECK(cudaMemcpyAsync(&hss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
+            TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
         const double theta = eps * eps * hss / static_cast<double>(d);
         ctx->last_svd_fallbacks = 0;
         std::vector<int> mode_order(static_cast<size_t>(d));
@@ -675,25 +700,34 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             static const bool dbg_sweeps = std::getenv("TS_DEBUG_SWEEPS") != nullptr;
             int* dsw = dbg_sweeps ? sc.alloc_n<int>(1) : nullptr;
             ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
-            std::vector<double> lv(static_cast<size_t>(qk));
-            TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk), cudaMemcpyDeviceToHost, st));
-            int hsw = 0;
-            if (dsw) TS_CUDA_CHECK(cudaMemcpyAsync(&hsw, dsw, sizeof(int), cudaMemcpyDeviceToHost, st));
-            TS_CUDA_CHECK(cudaStreamSynchronize(st));
-            if (dsw) std::fprintf(stderr, "[ts] st-hosvd mode %d: n=%lld sweeps=%d lam1=%.3e lam_last=%.3e\n", k,
-                                  static_cast<long long>(qk), hsw, lv[0], lv.back());
             const std::int64_t capk = max_rank ? max_rank[k] : 0;
-            bool ok = false;
-            std::int64_t rk = gram_rank(lv, eps, theta, capk, &ok);
-            if (!ok) {
-                double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
-                unfolding_svd_accurate(X, rest, qk, sigma, Pk[k], sc);
-                std::vector<double> sig(static_cast<size_t>(qk));
-                TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
+            std::int64_t rk = 0;
+            if (spec_g && !dsw) {
+                // At ε = 0 the fast-path rank is fixed (cap, else q); its checks run on the device.
+                rk = (capk > 0 && capk < qk) ? capk : qk;
+                ts::launch_gram_check(lam, static_cast<int>(qk), static_cast<int>(capk), gflags + k, sc);
+            } else {
+                std::vector<double> lv(static_cast<size_t>(qk));
+                TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
                                               cudaMemcpyDeviceToHost, st));
+                int hsw = 0;
+                if (dsw) TS_CUDA_CHECK(cudaMemcpyAsync(&hsw, dsw, sizeof(int), cudaMemcpyDeviceToHost, st));
                 TS_CUDA_CHECK(cudaStreamSynchronize(st));
-                rk = hosvd_rank(sig, eps, theta, capk);
-                ++ctx->last_svd_fallbacks;
+                if (dsw)
+                    std::fprintf(stderr, "[ts] st-hosvd mode %d: n=%lld sweeps=%d lam1=%.3e lam_last=%.3e\n", k,
+                                 static_cast<long long>(qk), hsw, lv[0], lv.back());
+                bool ok = false;
+                rk = gram_rank(lv, eps, theta, capk, &ok);
+                if (!ok) {
+                    double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
+                    unfolding_svd_accurate(X, rest, qk, sigma, Pk[k], sc);
+                    std::vector<double> sig(static_cast<size_t>(qk));
+                    TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
+                                                  cudaMemcpyDeviceToHost, st));
+                    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                    rk = hosvd_rank(sig, eps, theta, capk);
+                    ++ctx->last_svd_fallbacks;
+                }
             }
             rank[k] = rk;
             // g ← g ×_k P_kᵀ
@@ -764,6 +798,23 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     }
     mark(ctx, 11);
     ctx->launches += sc.launches;
+    if (spec) {
+        std::vector<int> hf(2 * static_cast<size_t>(d), 0);
+        if (dflags)
+            TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
+        if (gflags)
+            TS_CUDA_CHECK(cudaMemcpyAsync(hf.data() + d, gflags, sizeof(int) * static_cast<size_t>(d),
+                                          cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int x : hf)
+            if (x != 0) {
+                ctx->spec_ok = false;
+                res.reset();
+                return krp_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, false);
+            }
+    } else {
+        ctx->spec_ok = ctx->last_qr_fallbacks == 0 && ctx->last_svd_fallbacks == 0;
+    }
     TS_CUDA_CHECK(cudaStreamSynchronize(st));
     if (ctx->timing) {
         ctx->stage_ms.assign(kNumStages, 0.0);

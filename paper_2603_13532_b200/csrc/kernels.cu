@@ -724,6 +724,29 @@ __global__ void __launch_bounds__(4 * NC) chol_inv_kernel(CholBatch cb) {
 }
 
 // ------------------------------------------------------------------ misc
+// Device twin of the ε = 0 branch of gram_rank (capi.cu): with the rank fixed to
+// the cap (else q), accept the Gram fast path only when λ_rank is resolvable and
+// the kept subspace is separated enough for the 1e-10 parity bar; *flag |= 1
+// otherwise.
+__global__ void gram_check_kernel(const double* __restrict__ lam, int q, int cap, int* __restrict__ flag) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double l1 = lam[0];
+    bool ok = l1 > 0.0;
+    if (ok) {
+        const double resolvable = 1e-8 * l1;
+        const int rank = (cap > 0 && cap < q) ? cap : q;
+        const double lr = fmax(lam[rank - 1], 0.0);
+        ok = lr >= resolvable;
+        if (ok && rank < q) {
+            const double lnext = fmax(lam[rank], 0.0);
+            const double gap = lr - lnext;
+            ok = gap > 0.0;
+            if (ok) ok = !(1e-14 * l1 / gap * sqrt(lnext / l1) > 1e-11);
+        }
+    }
+    if (!ok) atomicOr(flag, 1);
+}
+
 struct UnfoldArgs {
     int64_t shape[kMaxOrder];
     int order, mode;
@@ -985,6 +1008,12 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
         configured = true;
     }
     sym_jacobi_kernel<<<1, kJacThreads, smem, sc.stream()>>>(C, ldc, n, lambda, V, sweeps);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
+void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch& sc) {
+    gram_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, flag);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }

@@ -115,6 +115,8 @@ struct CholBatch {
     int check_identity;
 };
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc);
+// Device check of the ε = 0 Gram fast path (twin of capi.cu gram_rank): *flag |= 1 on rejection.
+void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch& sc);
 
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);

@@ -90,6 +90,27 @@ def test_numerical_paths_are_exercised(engine):
     assert engine.last_paths()[1] >= 1
 
 
+def test_speculative_tail_matches_synchronous_path():
+    """The speculative tail (stage D/G acceptance checks on the device, one sync
+    per call) gives bitwise the synchronous path's result when accepted, and a
+    rejected speculation is recomputed on the synchronous path."""
+    wl1, wl3 = make_workload(1), make_workload(3)
+    s1, s3 = (wl1.seed.seed, wl1.seed.stream), (wl3.seed.seed, wl3.seed.stream)
+    eng = T.Engine(0)
+    try:
+        spec1, _ = gpu_sum(eng, wl1.summands, wl1.weights, wl1.widths, s1, wl1.eps, wl1.cap)  # accepted
+        out3, _ = gpu_sum(eng, wl3.summands, wl3.weights, wl3.widths, s3, wl3.eps, wl3.cap)  # rejected → rerun
+        ref3, _ = O.krp_sum(wl3.summands, wl3.weights, wl3.widths, s3, wl3.eps, cap=wl3.cap, threads=8)
+        assert out3.ranks == ref3.ranks and rel_diff(out3, ref3) <= PARITY
+        sync1, _ = gpu_sum(eng, wl1.summands, wl1.weights, wl1.widths, s1, wl1.eps, wl1.cap)  # synchronous path
+        assert sync1.ranks == spec1.ranks
+        assert np.array_equal(sync1.dense_core(), spec1.dense_core())
+        for a, b in zip(sync1.factors, spec1.factors):
+            assert np.array_equal(a, b)
+    finally:
+        eng.close()
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_reference_semantics_eps(engine, cfg):
     """Pure reference semantics (eps > 0, no rank cap) on the same inputs."""
