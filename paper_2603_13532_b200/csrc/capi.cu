@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <map>
 #include <memory>
@@ -1222,14 +1223,46 @@ void ts_result_dims(const ts_result* r, int64_t* dims) {
 void ts_result_ranks(const ts_result* r, int64_t* ranks) {
     for (int n = 0; n < r->order; ++n) ranks[n] = r->ranks[n];
 }
+// Device → caller buffer.  Pageable destinations go through a pinned staging
+// buffer (one per thread, grown on demand): a direct pageable copy runs at a
+// fraction of the link rate.  Registered / pinned destinations are copied to
+// directly.
+static void download(double* out, const double* src, size_t n, cudaStream_t st) {
+    const size_t bytes = sizeof(double) * n;
+    if (bytes == 0) return;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, out) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // pageable pointers may set a sticky-free error on some drivers
+    if (pinned || bytes < (64u << 10)) {
+        TS_CUDA_CHECK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        return;
+    }
+    struct Staging {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Staging() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Staging stage;
+    if (stage.cap < bytes) {
+        if (stage.p) TS_CUDA_CHECK(cudaFreeHost(stage.p));
+        stage.p = nullptr;
+        stage.cap = 0;
+        TS_CUDA_CHECK(cudaMallocHost(&stage.p, bytes));
+        stage.cap = bytes;
+    }
+    TS_CUDA_CHECK(cudaMemcpyAsync(stage.p, src, bytes, cudaMemcpyDeviceToHost, st));
+    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::memcpy(out, stage.p, bytes);
+}
+
 int ts_result_factor(const ts_result* r, int64_t mode, double* out) {
     return guarded([&] {
         if (!r || mode < 0 || mode >= r->order) invalid("ts_result_factor: bad mode");
         TS_CUDA_CHECK(cudaSetDevice(r->device));
-        TS_CUDA_CHECK(cudaMemcpyAsync(out, r->factors[mode],
-                                      sizeof(double) * static_cast<size_t>(r->dims[mode] * r->ranks[mode]),
-                                      cudaMemcpyDeviceToHost, r->stream));
-        TS_CUDA_CHECK(cudaStreamSynchronize(r->stream));
+        download(out, r->factors[mode], static_cast<size_t>(r->dims[mode] * r->ranks[mode]), r->stream);
     });
 }
 int ts_result_core(const ts_result* r, double* out) {
@@ -1238,9 +1271,7 @@ int ts_result_core(const ts_result* r, double* out) {
         std::int64_t n = 1;
         for (int k = 0; k < r->order; ++k) n *= r->ranks[k];
         TS_CUDA_CHECK(cudaSetDevice(r->device));
-        TS_CUDA_CHECK(cudaMemcpyAsync(out, r->core, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost,
-                                      r->stream));
-        TS_CUDA_CHECK(cudaStreamSynchronize(r->stream));
+        download(out, r->core, static_cast<size_t>(n), r->stream);
     });
 }
 const double* ts_result_factor_device(const ts_result* r, int64_t mode) {

@@ -121,6 +121,8 @@ def _check(rc: int):
 
 
 def _f64(a) -> np.ndarray:
+    if isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.f_contiguous:
+        return a
     return np.asfortranarray(np.asarray(a, dtype=np.float64))
 
 
@@ -315,31 +317,46 @@ class SumStats:
 
 # ---------------------------------------------------------------------------- device engine
 class _Views:
-    """Marshals TuckerTensors into ts_tucker_view structs (keeps buffers alive)."""
+    """Marshals TuckerTensors into ts_tucker_view structs (keeps buffers alive).
+
+    Shape metadata is shared between summands of equal structure and pointer
+    arrays are built from raw addresses: marshalling K = 256 summands must not
+    cost more than their PCIe transfer."""
 
     def __init__(self, tensors: Sequence[TuckerTensor]):
         self.keep = []
+        self._meta = {}
         self.arr = (TsTuckerView * max(1, len(tensors)))()
         for i, t in enumerate(tensors):
             if t is None:
                 raise ValueError("sum request holds a null summand")
             self.arr[i] = self._view(t)
 
+    def _shape_meta(self, t: TuckerTensor):
+        key = (tuple(t.dims), tuple(t.ranks), tuple((tuple(b.offsets), b.data.shape) for b in t.blocks))
+        meta = self._meta.get(key)
+        if meta is None:
+            dims = np.asarray(t.dims, dtype=np.int64)
+            ranks = np.asarray(t.ranks, dtype=np.int64)
+            offs = np.asarray([b.offsets for b in t.blocks], dtype=np.int64).reshape(-1)
+            shps = np.asarray([list(b.data.shape) for b in t.blocks], dtype=np.int64).reshape(-1)
+            meta = (dims, ranks, offs, shps, dims.ctypes.data_as(i64p), ranks.ctypes.data_as(i64p),
+                    offs.ctypes.data_as(i64p), shps.ctypes.data_as(i64p))
+            self._meta[key] = meta
+        return meta
+
     def _view(self, t: TuckerTensor) -> TsTuckerView:
         order = len(t.dims)
         if order > MAX_ORDER:
             raise TucksumCudaError(TS_UNSUPPORTED, "order exceeds TS_MAX_ORDER")
-        dims = np.asarray(t.dims, dtype=np.int64)
-        ranks = np.asarray(t.ranks, dtype=np.int64)
+        _, _, _, _, pdims, pranks, poffs, pshps = self._shape_meta(t)
         facs = [_f64(f) for f in t.factors]
-        fptrs = (dptr * order)(*[_p(f) for f in facs])
-        offs = np.asarray([b.offsets for b in t.blocks], dtype=np.int64).reshape(-1)
-        shps = np.asarray([list(b.data.shape) for b in t.blocks], dtype=np.int64).reshape(-1)
         datas = [_f64(b.data) for b in t.blocks]
-        bptrs = (dptr * len(datas))(*[_p(x) for x in datas])
-        self.keep += [dims, ranks, facs, fptrs, offs, shps, datas, bptrs]
-        return TsTuckerView(order, dims.ctypes.data_as(i64p), ranks.ctypes.data_as(i64p), fptrs, len(datas),
-                            offs.ctypes.data_as(i64p), shps.ctypes.data_as(i64p), bptrs)
+        fptrs = (C.c_void_p * order)(*[f.ctypes.data for f in facs])
+        bptrs = (C.c_void_p * len(datas))(*[x.ctypes.data for x in datas])
+        self.keep += [facs, fptrs, datas, bptrs]
+        return TsTuckerView(order, pdims, pranks, C.cast(fptrs, C.POINTER(dptr)), len(datas), poffs, pshps,
+                            C.cast(bptrs, C.POINTER(dptr)))
 
 
 class DeviceBatch:
@@ -381,10 +398,10 @@ class DeviceResult:
         L = lib()
         factors = []
         for k in range(self.order):
-            f = np.zeros((self.dims[k], self.ranks[k]), order="F")
+            f = np.empty((self.dims[k], self.ranks[k]), order="F")
             _check(L.ts_result_factor(self.handle, i64(k), _p(f)))
             factors.append(f)
-        core = np.zeros(tuple(self.ranks), order="F")
+        core = np.empty(tuple(self.ranks), order="F")
         _check(L.ts_result_core(self.handle, _p(core)))
         return TuckerTensor(core, factors)
 
