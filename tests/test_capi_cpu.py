@@ -126,3 +126,16 @@ def test_workload_generator_small():
     wl3 = make_workload(3, K=2)
     q = wl3.summands[0].factors[1]
     assert q.shape == (64, 10) and np.linalg.norm(q.T @ q - np.eye(10)) <= 1e-13
+
+
+def test_cpp_host_caller_builds():
+    """The C ABI is consumable from C++ with no Python: tests/cpp/capi_host.cpp
+    compiles (-Wall -Wextra) and links against the in-tree library."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([os.path.join(root, "tests", "cpp", "build.sh")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "warning" not in r.stderr
+    assert os.path.exists(os.path.join(root, "tests", "cpp", "capi_host"))

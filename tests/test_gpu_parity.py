@@ -111,6 +111,21 @@ def test_speculative_tail_matches_synchronous_path():
         eng.close()
 
 
+def test_cpp_host_caller():
+    """A C++ program drives the C ABI end to end (upload, two krp_sum calls,
+    malformed requests, ranks, orthonormality, determinism, exact-sum norm)."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "capi_host")
+    if not os.path.exists(exe):
+        subprocess.run([os.path.join(root, "tests", "cpp", "build.sh")], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "capi_host ok" in r.stdout
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_reference_semantics_eps(engine, cfg):
     """Pure reference semantics (eps > 0, no rank cap) on the same inputs."""
