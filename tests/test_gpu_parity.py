@@ -111,6 +111,25 @@ def test_speculative_tail_matches_synchronous_path():
         eng.close()
 
 
+def test_nccl_path_single_rank_matches():
+    """The multi-GPU code path — NCCL resolved at run time, a communicator, the
+    two in-place all-reduces on the library stream — run with one rank gives
+    bitwise the single-GPU result (only one GPU is available to this build)."""
+    wl = make_workload(5, K=16)
+    seed = (wl.seed.seed, wl.seed.stream)
+    ref, _ = gpu_sum(T.Engine(0), wl.summands, wl.weights, wl.widths, seed, wl.eps, wl.cap)
+    eng = T.Engine(0)
+    try:
+        eng.init_nccl(T.Engine.nccl_unique_id(), 1, 0)
+        out, _ = gpu_sum(eng, wl.summands, wl.weights, wl.widths, seed, wl.eps, wl.cap)
+    finally:
+        eng.close()
+    assert out.ranks == ref.ranks
+    assert np.array_equal(out.dense_core(), ref.dense_core())
+    for a, b in zip(out.factors, ref.factors):
+        assert np.array_equal(a, b)
+
+
 def test_cpp_host_caller():
     """A C++ program drives the C ABI end to end (upload, two krp_sum calls,
     malformed requests, ranks, orthonormality, determinism, exact-sum norm)."""
