@@ -110,6 +110,16 @@ int ts_omega_prepare(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t wi
  * per-mode rank cap of SURVEY.md §8(d); NULL reproduces the reference exactly. */
 int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
+/* Independent sums in one call (SURVEY.md §8(f) row 2 — one round_sum per NDG
+ * node, many GMRES steps): sum i = krp_sum of batches[i] with weights[i] and the
+ * Ω stream (seeds[i], streams[i]); widths / eps / max_rank are shared.  Sums run
+ * concurrently on up to `lanes` internal streams (<= 16); each result equals
+ * the corresponding ts_krp_sum call bitwise.  out[count] receives owned results
+ * (all NULL on error).  Replaces a caller-side loop over tucksum::krp_sum
+ * (proj/src/ndg.cpp:401-462, proj/src/cookie.cpp:389-421). */
+int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, const double* const* weights,
+                    const int64_t* widths, const uint64_t* seeds, const uint64_t* streams, double eps,
+                    const int64_t* max_rank, int lanes, ts_result** out);
 /* Plan stage for Strategy::Krp (src/sketch.cpp:272-349): effective ranks,
  * targets and the uniform widths.  oversampling[order] >= 0. */
 int ts_effective_subrank(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps,

@@ -27,6 +27,7 @@
 #include <memory>
 #include <tuple>
 #include <mutex>
+#include <thread>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -132,6 +133,11 @@ struct ts_ctx {
     // Speculative tail (see krp_sum_impl): on while the last call needed no
     // accurate-path fallback.
     bool spec_ok = true;
+    // ts_krp_sum_many: child contexts (own stream, staging, history) that share
+    // this context's device and Ω cache; created on first use.
+    ts_ctx* parent = nullptr;
+    std::vector<ts_ctx*> lanes;
+    std::mutex omega_mu;
 };
 
 struct ts_batch {
@@ -177,6 +183,8 @@ using ts::Layout;
 
 double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, std::int64_t width, std::uint64_t seed,
                   std::uint64_t stream) {
+    if (ctx->parent) ctx = ctx->parent;  // lanes share the parent's cache
+    std::lock_guard<std::mutex> lock(ctx->omega_mu);
     OmegaKey key{seed, stream, width, std::vector<std::int64_t>(dims, dims + order)};
     auto it = ctx->omega.find(key);
     if (it != ctx->omega.end()) return it->second;
@@ -857,6 +865,7 @@ int ts_ctx_create(int device, ts_ctx** out) {
 int ts_ctx_destroy(ts_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
+        for (ts_ctx* lane : ctx->lanes) ts_ctx_destroy(lane);
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         for (auto& kv : ctx->omega) cudaFree(kv.second);
@@ -1072,6 +1081,60 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
     return guarded([&] {
         if (!ctx || !out) invalid("ts_krp_sum: null argument");
         *out = krp_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank);
+    });
+}
+
+// Independent sums (one round_sum per NDG node, many
+// GMRES steps).  Small sums are latency-bound — one CTA runs the eigensolver
+// while the rest of the GPU idles — so they run side by side: sum i goes to lane
+// i mod L, each lane a child context with its own stream driven by its own host
+// thread.  Every sum computes exactly what ts_krp_sum computes (bitwise).  With
+// a NCCL communicator the sums run in order on the context itself (collectives
+// must be issued in the same order on every rank).
+int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, const double* const* weights,
+                    const int64_t* widths, const uint64_t* seeds, const uint64_t* streams, double eps,
+                    const int64_t* max_rank, int lanes, ts_result** out) {
+    return guarded([&] {
+        if (!ctx || !out || count < 0 || (count > 0 && (!batches || !weights || !seeds || !streams)))
+            invalid("ts_krp_sum_many: null argument");
+        for (int64_t i = 0; i < count; ++i) out[i] = nullptr;
+        if (count == 0) return;
+        if (ctx->comm || count == 1 || lanes <= 1) {
+            for (int64_t i = 0; i < count; ++i)
+                out[i] = krp_sum_impl(ctx, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank);
+            return;
+        }
+        const int L = static_cast<int>(std::min<int64_t>(std::min(lanes, 16), count));
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // batches were uploaded on this stream
+        while (static_cast<int>(ctx->lanes.size()) < L) {
+            ts_ctx* lane = nullptr;
+            if (ts_ctx_create(ctx->device, &lane) != TS_OK) throw ts::Error(TS_RUNTIME, g_err);
+            lane->parent = ctx;
+            ctx->lanes.push_back(lane);
+        }
+        std::vector<std::string> errs(static_cast<size_t>(L));
+        std::vector<int> codes(static_cast<size_t>(L), TS_OK);
+        std::vector<std::thread> workers;
+        for (int t = 0; t < L; ++t)
+            workers.emplace_back([&, t] {
+                ts_ctx* lane = ctx->lanes[static_cast<size_t>(t)];
+                codes[static_cast<size_t>(t)] = guarded([&] {
+                    TS_CUDA_CHECK(cudaSetDevice(lane->device));
+                    for (int64_t i = t; i < count; i += L)
+                        out[i] = krp_sum_impl(lane, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank);
+                });
+                if (codes[static_cast<size_t>(t)] != TS_OK) errs[static_cast<size_t>(t)] = g_err;
+            });
+        for (auto& w : workers) w.join();
+        for (int t = 0; t < L; ++t)
+            if (codes[static_cast<size_t>(t)] != TS_OK) {
+                for (int64_t i = 0; i < count; ++i) {
+                    delete out[i];
+                    out[i] = nullptr;
+                }
+                throw ts::Error(codes[static_cast<size_t>(t)], errs[static_cast<size_t>(t)]);
+            }
     });
 }
 

@@ -486,17 +486,16 @@ __global__ void __launch_bounds__(128) jacobi_vectors_kernel(int n, const double
 }  // namespace
 
 unsigned long long* eig_probe_buffer() {
-    static unsigned long long* buf = nullptr;
-    static bool init = false;
-    if (!init) {
-        init = true;
+    static unsigned long long* const buf = [] {  // thread-safe one-time setup
+        unsigned long long* p = nullptr;
         if (std::getenv("TS_EIG_PROFILE")) {
-            TS_CUDA_CHECK(cudaMalloc(&buf, 32 * sizeof(unsigned long long)));
+            TS_CUDA_CHECK(cudaMalloc(&p, 32 * sizeof(unsigned long long)));
             unsigned long long mode[32] = {};
             mode[7] = static_cast<unsigned long long>(std::atoi(std::getenv("TS_EIG_PROFILE")));
-            TS_CUDA_CHECK(cudaMemcpy(buf, mode, sizeof(mode), cudaMemcpyHostToDevice));
+            TS_CUDA_CHECK(cudaMemcpy(p, mode, sizeof(mode), cudaMemcpyHostToDevice));
         }
-    }
+        return p;
+    }();
     return buf;
 }
 
@@ -506,11 +505,12 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
     if (np > kMaxNp || np < 4) return false;
     const int k = np / 2;
     const size_t smem = sizeof(double) * (2 * static_cast<size_t>(np) * np + 2 * kMaxNp + 4 * static_cast<size_t>(np - 1) * k + np);
-    static bool configured = false;
-    if (!configured) {
+    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+    static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(jacobi_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     auto* rot = sc.alloc_n<double2>(static_cast<size_t>(kMaxSweeps) * (np - 1) * k);
     double* dpos = sc.alloc_n<double>(static_cast<size_t>(np));
     int* info = sc.alloc_n<int>(2);

@@ -213,12 +213,13 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM,
 void launch_kernel(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStream_t stream) {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
     auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
-    static bool configured = false;
-    if (!configured) {
+    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+    static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(Cfg::kSmemBytes)));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     kern<<<static_cast<unsigned>(units), Cfg::kThreads, Cfg::kSmemBytes, stream>>>(d_descs, ngroups);
     TS_LAUNCH_CHECK();
 }
@@ -226,14 +227,14 @@ void launch_kernel(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStre
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
 int occupancy_of() {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
-    static int occ = 0;
-    if (occ == 0) {
+    static const int occ = [] {  // thread-safe one-time query
+        int o = 0;
         auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
         TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(Cfg::kSmemBytes)));
-        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::kThreads, Cfg::kSmemBytes));
-        occ = std::max(occ, 1);
-    }
+        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads, Cfg::kSmemBytes));
+        return std::max(o, 1);
+    }();
     return occ;
 }
 

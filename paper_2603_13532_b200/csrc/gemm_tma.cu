@@ -297,11 +297,10 @@ bool ok16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 }  // namespace
 
 bool tma_gemm_enabled() {
-    static int en = -1;
-    if (en < 0) {
+    static const int en = [] {  // thread-safe one-time read
         const char* e = std::getenv("TS_GEMM_TMA");
-        en = (e && e[0] == '0') ? 0 : 1;
-    }
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
     return en == 1 && encode_fn() != nullptr;
 }
 
@@ -320,14 +319,14 @@ bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallS
         total_tiles += static_cast<int64_t>((p.M + kBM - 1) / kBM) * ((p.N + kBN - 1) / kBN);
     }
     if (total_tiles == 0) return true;
-    static int occ = 0;
-    if (occ == 0) {
+    static const int occ = [] {  // thread-safe one-time setup
+        int o = 0;
         auto k1 = gemm_tma_kernel<false>, k2 = gemm_tma_kernel<true>;
         TS_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
         TS_CUDA_CHECK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1, kThreads, kSmemBytes));
-        occ = std::max(occ, 1);
-    }
+        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k1, kThreads, kSmemBytes));
+        return std::max(o, 1);
+    }();
     const int64_t slots = static_cast<int64_t>(num_sms) * occ;
     size_t ws_elems = 0;
     std::vector<int> red;

@@ -956,12 +956,13 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
         nlev = std::max(nlev, p->levels.size());
         napp = std::max(napp, p->applies.size());
     }
-    static bool configured = false;
-    if (!configured) {
+    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+    static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     for (size_t L = 0; L < nlev; ++L) {
         std::vector<QrTask> tasks;
         size_t smem = 0;
@@ -1002,11 +1003,12 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
     if (launch_sym_jacobi_pp(C, ldc, n, lambda, V, sc, sweeps)) return;  // eig.cu, n ≤ 64
     const size_t np = static_cast<size_t>(n + (n & 1));
     const size_t smem = sizeof(double) * (2 * np * (np + 1) + 2 * np + 3 * np + np) + 16;
-    static bool configured = false;
-    if (!configured) {
+    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+    static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(sym_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     sym_jacobi_kernel<<<1, kJacThreads, smem, sc.stream()>>>(C, ldc, n, lambda, V, sweeps);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
@@ -1023,12 +1025,13 @@ void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
     if (cb.n > 96) throw std::invalid_argument("chol_inv: n > 96");
     const size_t ldc = cb.n <= 64 ? 65 : 97;  // LD of the kernel instance
     const size_t smem = sizeof(double) * (2 * static_cast<size_t>(cb.n) * ldc + cb.n);
-    static bool configured = false;
-    if (!configured) {
+    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+    static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     if (cb.n <= 64) chol_inv_kernel<64><<<count, 4 * 64, smem, sc.stream()>>>(cb);
     else chol_inv_kernel<96><<<count, 4 * 96, smem, sc.stream()>>>(cb);
     TS_LAUNCH_CHECK();
@@ -1037,11 +1040,12 @@ void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
 
 void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigma, double* U, CallScratch& sc) {
     const size_t smem = sizeof(double) * (static_cast<size_t>(m) * nc + static_cast<size_t>(nc) * nc + nc);
-    static bool configured = false;
-    if (!configured) {
+    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+    static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
-    }
+        return true;
+    }();
+    (void)configured;
     jacobi_svd_kernel<<<1, kJacThreads, smem, sc.stream()>>>(R, ldr, m, nc, sigma, U);
     TS_LAUNCH_CHECK();
     sc.launches += 1;

@@ -325,11 +325,12 @@ void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc) {
     if (use3 && args.order == 3 && max_shape <= k3Rows) {
         const size_t smem =
             sizeof(double) * (2 * k3Rows * k3MLD + 2 * k3Rows * k3GLD + static_cast<size_t>(max_shape) * kCT);
-        static bool configured = false;
-        if (!configured) {
+        // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
+        static const bool configured = [&] {
             TS_CUDA_CHECK(cudaFuncSetAttribute(krp3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-            configured = true;
-        }
+            return true;
+        }();
+        (void)configured;
         dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>((args.s + kCT - 1) / kCT));
         krp3_dmma_kernel<<<grid, kThreads, smem, sc.stream()>>>(args);
         TS_LAUNCH_CHECK();

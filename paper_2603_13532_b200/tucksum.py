@@ -44,7 +44,7 @@ MAX_ORDER = 8
 EXPORTED_SYMBOLS = [
     "ts_last_error", "ts_version", "ts_ctx_create", "ts_ctx_destroy", "ts_nccl_unique_id", "ts_ctx_init_nccl",
     "ts_ctx_stream", "ts_ctx_launch_count", "ts_batch_upload", "ts_batch_free", "ts_batch_count", "ts_batch_bytes",
-    "ts_substream", "ts_gaussian_matrix", "ts_omega_prepare", "ts_krp_sum", "ts_effective_subrank",
+    "ts_substream", "ts_gaussian_matrix", "ts_omega_prepare", "ts_krp_sum", "ts_krp_sum_many", "ts_effective_subrank",
     "ts_result_order", "ts_result_dims", "ts_result_ranks", "ts_result_factor", "ts_result_core",
     "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
@@ -528,6 +528,34 @@ class Engine:
                                 u64(seed.stream), C.c_double(eps),
                                 cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
         return DeviceResult(h)
+
+    def krp_sum_many(self, batches: Sequence[DeviceBatch], weights: Sequence, widths, seeds: Sequence[RngSeed],
+                     eps: float, max_rank=None, lanes: int = 8) -> List[DeviceResult]:
+        """Independent sums side by side (ts_krp_sum_many):
+        result i equals krp_sum(batches[i], weights[i], widths, seeds[i], eps, max_rank)."""
+        n = len(batches)
+        if len(weights) != n or len(seeds) != n:
+            raise ValueError("krp_sum_many needs one weight vector and one seed per batch")
+        ws = []
+        for b, w in zip(batches, weights):
+            w = np.ascontiguousarray(np.asarray(w, dtype=np.float64))
+            if len(w) != b.count:
+                raise ValueError("sum request needs matching, nonempty summands and weights")
+            ws.append(w)
+        wd = np.ascontiguousarray(np.asarray(widths, dtype=np.int64))
+        if n and len(wd) != batches[0].order:
+            raise ValueError("plan order does not match summand order")
+        cap = None if max_rank is None else np.ascontiguousarray(np.asarray(max_rank, dtype=np.int64))
+        bh = (C.c_void_p * max(1, n))(*[b.handle for b in batches])
+        wp = (dptr * max(1, n))(*[_p(w) for w in ws])
+        sd = np.ascontiguousarray([s.seed for s in seeds], dtype=np.uint64)
+        st = np.ascontiguousarray([s.stream for s in seeds], dtype=np.uint64)
+        out = (C.c_void_p * max(1, n))()
+        _check(lib().ts_krp_sum_many(self.handle, i64(n), bh, wp, wd.ctypes.data_as(i64p),
+                                     sd.ctypes.data_as(C.POINTER(C.c_uint64)), st.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                     C.c_double(eps), cap.ctypes.data_as(i64p) if cap is not None else None,
+                                     C.c_int(lanes), out))
+        return [DeviceResult(C.c_void_p(out[i])) for i in range(n)]
 
     def effective_subrank(self, batch: DeviceBatch, weights, eps: float, oversampling):
         order = batch.order
