@@ -385,6 +385,23 @@ def test_cfg5_full_properties(engine):
     assert O.rel_error_to_sum(r3, [r1], [2.0]) <= 1e-12
 
 
+def test_cfg5_full_size_parity(engine):
+    """BASELINE config 5 at full size (K = 256, n = 8192, s = 64, cap 48): the
+    device result against the CPU oracle on identical inputs and Ω — 1e-10
+    relative Frobenius on factors × core, same ranks, and the same error to the
+    exact sum to 3 significant digits (Gram-based, both on the oracle)."""
+    wl = make_workload(5)
+    seed = (wl.seed.seed, wl.seed.stream)
+    threads = O.num_threads()
+    ref, _ = O.krp_sum(wl.summands, wl.weights, wl.widths, seed, wl.eps, cap=wl.cap, threads=threads)
+    out, _ = gpu_sum(engine, wl.summands, wl.weights, wl.widths, seed, wl.eps, wl.cap)
+    assert out.ranks == ref.ranks == [48, 48, 48]
+    assert rel_diff(out, ref) <= PARITY
+    e_gpu = O.rel_error_gram(out, wl.summands, wl.weights, threads)
+    e_ref = O.rel_error_gram(ref, wl.summands, wl.weights, threads)
+    assert abs(e_gpu - e_ref) <= 5e-4 * e_ref
+
+
 def test_sym_eig_matches_oracle(engine):
     """Device Jacobi eigensolver vs the oracle's sym_eig (test_tensor_kernels.cpp:237-248 style)."""
     for n, seed in [(6, 1), (26, 2), (50, 3), (64, 4), (96, 5)]:
