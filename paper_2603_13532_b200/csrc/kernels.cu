@@ -18,123 +18,140 @@ constexpr int kQrMaxCPW = 6;  // columns per warp: 96 / 16
 // Householder parameters with Eigen's makeHouseholder convention: beta =
 // -sign(c0)·‖x‖, tau = (beta - c0)/beta, v = [1; x_tail/(c0 - beta)]; tau = 0
 // when the tail is below the smallest normal (see oracle/tucksum_oracle.cpp).
+// sqrt / reciprocal from the MUFU approximations plus Newton steps (≤ 1 ulp):
+// no IEEE div/sqrt slow-path call sites, which would force the register-resident
+// TSQR block out to local memory around every call.
+__device__ __forceinline__ double nr_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = y * fma(-x, y, 2.0);
+    y = y * fma(-x, y, 2.0);
+    return fma(y, fma(-x, y, 1.0), y);
+}
+__device__ __forceinline__ double nr_sqrt(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    r = r * fma(-0.5 * x, r * r, 1.5);
+    const double s = x * r;
+    return fma(0.5 * r, fma(-s, s, x), s);  // one Newton step on s = √x
+}
+
 __device__ __forceinline__ void householder_params(double c0, double tail, double* beta, double* tau, double* inv) {
     if (tail <= DBL_MIN) {
         *tau = 0.0;
         *beta = c0;
         *inv = 0.0;
     } else {
-        double b = sqrt(c0 * c0 + tail);
+        double b = nr_sqrt(fma(c0, c0, tail));
         if (c0 >= 0.0) b = -b;
         *beta = b;
-        *inv = 1.0 / (c0 - b);
-        *tau = (b - c0) / b;
+        *inv = nr_rcp(c0 - b);
+        *tau = (b - c0) * nr_rcp(b);
     }
 }
 
-// Householder QR of one rows × cols block held column-major in shared memory.
-// One block barrier per reflector: the reflector k is applied with its vector
-// still unscaled (the 1/(c0 - beta) factor folded into the update), its
-// scaling is deferred to step k+1, and warp 0 — which owns column k+1 — derives
-// the next reflector right after updating that column.  Each warp reduces the
-// dot products of all its columns together so their shuffle latencies overlap.
-__global__ void __launch_bounds__(kQrThreads) tsqr_factor_kernel(const QrTask* __restrict__ tasks) {
+// Householder QR of one rows × cols block (rows ≤ 256, cols ≤ 96), register
+// resident: warp w owns columns w, w+16, …, w+80; lane l owns rows l, l+32, …, so
+// the trailing update needs no shared-memory traffic except the reflector
+// itself.  Step k: the owner warp of column k forms the reflector (Eigen's
+// makeHouseholder convention, see householder_params) and publishes the scaled
+// vector v = [1; x·inv] through a double-buffered shared array; after ONE
+// barrier every warp applies H_k = I − τ·v·vᵀ to its own columns j > k.
+constexpr int kQrRowsPerLane = 8;  // 256 rows
+constexpr int kQrFThreads = 512;  // factor kernel: 16 warps × 6 columns (96 cols)
+constexpr int kQrFWarps = kQrFThreads / 32;
+constexpr int kQrFCPW = 6;
+
+__global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* __restrict__ tasks) {
     const QrTask tk = tasks[blockIdx.x];
     const int rows = tk.rows, cols = tk.cols, kk = min(rows, cols);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    extern __shared__ __align__(16) double As[];
-    __shared__ double pb[2], pt[2], pv[2];
-    for (int idx = tid; idx < rows * cols; idx += kQrThreads) {
-        const int i = idx % rows, c = idx / rows;
-        As[idx] = tk.A[i + static_cast<int64_t>(c) * tk.lda];
+    __shared__ __align__(16) double vbuf[2][kQrRowsPerLane * 32];
+    __shared__ double s_tau[2];
+    double a[kQrFCPW][kQrRowsPerLane];
+#pragma unroll
+    for (int i = 0; i < kQrFCPW; ++i) {
+        const int c = warp + kQrFWarps * i;
+        const double* __restrict__ col = tk.A + static_cast<int64_t>(c < cols ? c : 0) * tk.lda + lane;
+#pragma unroll
+        for (int t = 0; t < kQrRowsPerLane; ++t)
+            a[i][t] = (c < cols && lane + 32 * t < rows) ? __ldg(col + 32 * t) : 0.0;
     }
-    __syncthreads();
-    if (warp == 0 && kk > 0) {
-        double tail = 0.0;
-        for (int i = 1 + lane; i < rows; i += 32) tail += As[i] * As[i];
-        tail = warp_sum(tail);
-        if (lane == 0) householder_params(As[0], tail, &pb[0], &pt[0], &pv[0]);
-    }
-    __syncthreads();
     for (int k = 0; k < kk; ++k) {
-        const int sl = k & 1;
-        const double tau = pt[sl], inv = pv[sl];
-        const double* x = As + k * rows;
-        if (k > 0) {  // deferred scaling of reflector k-1 (column k-1 is not read in this step)
-            const int ps = sl ^ 1;
-            const double ptau = pt[ps], pinv = pv[ps];
-            double* xp = As + (k - 1) * rows;
-            for (int i = k + tid; i < rows; i += kQrThreads) xp[i] = ptau == 0.0 ? 0.0 : xp[i] * pinv;
-            if (tid == 0) {
-                xp[k - 1] = pb[ps];
-                tk.tau[k - 1] = ptau;
+        const int buf = k & 1;
+        const int ow = k % kQrFWarps, oi = k / kQrFWarps;  // owner warp / slot of column k
+        if (warp == ow) {
+            // Column k = slot oi (run-time) of this warp, read and written through
+            // selects so every register index stays static (no local memory).
+            auto col = [&](int t) {
+                double v = a[0][t];
+#pragma unroll
+                for (int i = 1; i < kQrFCPW; ++i) v = i == oi ? a[i][t] : v;
+                return v;
+            };
+            double tail = 0.0, c0 = 0.0;
+#pragma unroll
+            for (int t = 0; t < kQrRowsPerLane; ++t) {
+                const int r = lane + 32 * t;
+                const double v = col(t);
+                if (r > k && r < rows) tail = fma(v, v, tail);
+                if (r == k) c0 = v;
             }
-        }
-        int js[kQrMaxCPW];
-        int nj = 0;
-#pragma unroll
-        for (int i = 0; i < kQrMaxCPW; ++i) {
-            const int j = k + 1 + warp + kQrWarps * i;
-            js[i] = j;
-            if (j < cols) nj = i + 1;
-        }
-        if (tau != 0.0 && nj > 0) {
-            double dot[kQrMaxCPW];
-#pragma unroll
-            for (int i = 0; i < kQrMaxCPW; ++i) dot[i] = 0.0;
-            for (int r = k + 1 + lane; r < rows; r += 32) {
-                const double xr = x[r];
-#pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i)
-                    if (i < nj) dot[i] = fma(xr, As[r + js[i] * rows], dot[i]);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
-            double w[kQrMaxCPW];
-#pragma unroll
-            for (int i = 0; i < kQrMaxCPW; ++i) w[i] = i < nj ? tau * (As[k + js[i] * rows] + inv * dot[i]) : 0.0;
-            for (int r = k + 1 + lane; r < rows; r += 32) {
-                const double xr = x[r] * inv;
-#pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i)
-                    if (i < nj) As[r + js[i] * rows] -= w[i] * xr;
-            }
-            __syncwarp();
-            if (lane == 0)
-#pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i)
-                    if (i < nj) As[k + js[i] * rows] -= w[i];
-            __syncwarp();
-        }
-        if (warp == 0 && k + 1 < kk) {  // next reflector from the freshly updated column k+1
-            const double* y = As + (k + 1) * rows;
-            double tail = 0.0;
-            for (int i = k + 2 + lane; i < rows; i += 32) tail += y[i] * y[i];
             tail = warp_sum(tail);
-            if (lane == 0) householder_params(y[k + 1], tail, &pb[sl ^ 1], &pt[sl ^ 1], &pv[sl ^ 1]);
+            c0 = __shfl_sync(0xffffffffu, c0, k & 31);
+            double beta, tau, inv;
+            householder_params(c0, tail, &beta, &tau, &inv);
+#pragma unroll
+            for (int t = 0; t < kQrRowsPerLane; ++t) {
+                const int r = lane + 32 * t;
+                const double xv = col(t);
+                double v = 0.0, nv = xv;
+                if (r == k) {
+                    v = 1.0;
+                    nv = beta;  // R_kk
+                } else if (r > k && r < rows) {
+                    v = tau == 0.0 ? 0.0 : xv * inv;
+                    nv = v;  // Householder vector below the diagonal
+                }
+                vbuf[buf][r] = v;
+#pragma unroll
+                for (int i = 0; i < kQrFCPW; ++i) a[i][t] = i == oi ? nv : a[i][t];
+            }
+            if (lane == 0) {
+                s_tau[buf] = tau;
+                tk.tau[k] = tau;
+            }
         }
         __syncthreads();
-    }
-    if (kk > 0) {
-        const int ps = (kk - 1) & 1;
-        const double ptau = pt[ps], pinv = pv[ps];
-        double* xp = As + (kk - 1) * rows;
-        for (int i = kk + tid; i < rows; i += kQrThreads) xp[i] = ptau == 0.0 ? 0.0 : xp[i] * pinv;
-        if (tid == 0) {
-            xp[kk - 1] = pb[ps];
-            tk.tau[kk - 1] = ptau;
+        const double tau = s_tau[buf];
+        if (tau != 0.0) {
+            const double* vb = vbuf[buf] + lane;  // v is 0 above row k
+#pragma unroll
+            for (int i = 0; i < kQrFCPW; ++i) {
+                const int c = warp + kQrFWarps * i;
+                if (c <= k || c >= cols) continue;  // warp-uniform
+                double dot = 0.0;
+#pragma unroll
+                for (int t = 0; t < kQrRowsPerLane; ++t) dot = fma(vb[32 * t], a[i][t], dot);
+                const double w = tau * warp_sum(dot);
+#pragma unroll
+                for (int t = 0; t < kQrRowsPerLane; ++t) a[i][t] = fma(-w, vb[32 * t], a[i][t]);
+            }
         }
     }
-    __syncthreads();
-    for (int idx = tid; idx < rows * cols; idx += kQrThreads) {
-        const int i = idx % rows, c = idx / rows;
-        tk.A[i + static_cast<int64_t>(c) * tk.lda] = As[idx];
-    }
-    for (int idx = tid; idx < kk * cols; idx += kQrThreads) {
-        const int i = idx % kk, c = idx / kk;
-        tk.R[i + static_cast<int64_t>(c) * tk.ldr] = i <= c ? As[i + c * rows] : 0.0;
+#pragma unroll
+    for (int i = 0; i < kQrFCPW; ++i) {
+        const int c = warp + kQrFWarps * i;
+        if (c >= cols) continue;
+        double* __restrict__ colA = tk.A + static_cast<int64_t>(c) * tk.lda + lane;
+        double* __restrict__ colR = tk.R + static_cast<int64_t>(c) * tk.ldr + lane;
+#pragma unroll
+        for (int t = 0; t < kQrRowsPerLane; ++t) {
+            const int r = lane + 32 * t;
+            if (r < rows) colA[32 * t] = a[i][t];
+            if (r < kk) colR[32 * t] = r <= c ? a[i][t] : 0.0;
+        }
     }
 }
 
@@ -147,6 +164,7 @@ __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTas
     extern __shared__ __align__(16) double Qs[];
     double* vbuf = Qs + rows * q;      // 2 × rows
     double* taus = vbuf + 2 * rows;    // kk
+    const unsigned Qb = smem_u32(Qs);
     for (int idx = tid; idx < rows * q; idx += kQrThreads) {
         const int i = idx % rows, c = idx / rows;
         double val = 0.0;
@@ -166,23 +184,25 @@ __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTas
                 cp_async8(vbuf + ((k - 1) & 1) * rows + i, tk.V + i + static_cast<int64_t>(k - 1) * tk.ldv, 8);
         cp_async_commit();
         const double tau = taus[k];
-        const double* v = vbuf + (k & 1) * rows;
         if (tau != 0.0) {
-            int cs[kQrMaxCPW];
+            // Explicit shared addresses (see tsqr_factor_kernel).
+            const unsigned vb = Qb + 8u * static_cast<unsigned>(rows * q + (k & 1) * rows);
             int nc = 0;
+            unsigned cb[kQrMaxCPW];
 #pragma unroll
             for (int i = 0; i < kQrMaxCPW; ++i) {
-                cs[i] = warp + kQrWarps * i;
-                if (cs[i] < q) nc = i + 1;
+                const int c = warp + kQrWarps * i;
+                if (c < q) nc = i + 1;
+                cb[i] = Qb + 8u * static_cast<unsigned>((c < q ? c : 0) * rows);
             }
             double dot[kQrMaxCPW];
 #pragma unroll
             for (int i = 0; i < kQrMaxCPW; ++i) dot[i] = 0.0;
             for (int r = k + 1 + lane; r < rows; r += 32) {
-                const double vr = v[r];
+                const double vr = lds64(vb + 8u * r);
 #pragma unroll
                 for (int i = 0; i < kQrMaxCPW; ++i)
-                    if (i < nc) dot[i] = fma(vr, Qs[r + cs[i] * rows], dot[i]);
+                    if (i < nc) dot[i] = fma(vr, lds64(cb[i] + 8u * r), dot[i]);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
@@ -190,18 +210,18 @@ __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTas
                 for (int i = 0; i < kQrMaxCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
             double w[kQrMaxCPW];
 #pragma unroll
-            for (int i = 0; i < kQrMaxCPW; ++i) w[i] = i < nc ? tau * (Qs[k + cs[i] * rows] + dot[i]) : 0.0;
+            for (int i = 0; i < kQrMaxCPW; ++i) w[i] = i < nc ? tau * (lds64(cb[i] + 8u * k) + dot[i]) : 0.0;
             for (int r = k + 1 + lane; r < rows; r += 32) {
-                const double vr = v[r];
+                const double vr = lds64(vb + 8u * r);
 #pragma unroll
                 for (int i = 0; i < kQrMaxCPW; ++i)
-                    if (i < nc) Qs[r + cs[i] * rows] -= w[i] * vr;
+                    if (i < nc) sts64(cb[i] + 8u * r, lds64(cb[i] + 8u * r) - w[i] * vr);
             }
             __syncwarp();
             if (lane == 0)
 #pragma unroll
                 for (int i = 0; i < kQrMaxCPW; ++i)
-                    if (i < nc) Qs[k + cs[i] * rows] -= w[i];
+                    if (i < nc) sts64(cb[i] + 8u * k, lds64(cb[i] + 8u * k) - w[i]);
         }
         cp_async_wait<0>();
         __syncthreads();
@@ -289,6 +309,8 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
     double* J = W + m * nc;     // nc × nc (ld nc)
     double* nrm = J + nc * nc;  // nc (squared norms, then norms)
     __shared__ int rotated;
+    __shared__ double maxn;
+    const unsigned Wb = smem_u32(W), Jb = smem_u32(J);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int idx = tid; idx < m * nc; idx += kJacThreads) {
         const int i = idx % m, c = idx / m;
@@ -305,33 +327,43 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
             a = warp_sum(a);
             if (lane == 0) nrm[c] = a;
         }
-        if (tid == 0) rotated = 0;
+        if (tid == 0) {
+            rotated = 0;
+            double mx = 0.0;
+            for (int c = 0; c < nc; ++c) mx = fmax(mx, nrm[c]);
+            maxn = mx;
+        }
         __syncthreads();
+        // Pairs whose coupling is below (1e-15·max‖w_c‖)² are left alone: they
+        // move singular values by less than 1e-15·σ₁ (under the reference's own
+        // accuracy and the 1e-14·σ₁ rank floor), and rotating them only churns
+        // the rounding-noise subspace of rank-deficient inputs sweep after sweep.
+        const double abs_floor = 1e-30 * maxn;
         for (int r = 0; r < np - 1; ++r) {
             for (int pi = warp; pi < np / 2; pi += kJacWarps) {
                 int p, q;
                 pair_of(r, pi, np, &p, &q);
                 if (q >= nc) continue;
-                double* wp = W + p * m;
-                double* wq = W + q * m;
+                // Explicit shared addresses (run-time column offsets into the
+                // extern array otherwise re-derive its window base per access).
+                const unsigned wp = Wb + 8u * static_cast<unsigned>(p * m), wq = Wb + 8u * static_cast<unsigned>(q * m);
                 double ga = 0.0;
-                for (int i = lane; i < m; i += 32) ga = fma(wp[i], wq[i], ga);
+                for (int i = lane; i < m; i += 32) ga = fma(lds64(wp + 8u * i), lds64(wq + 8u * i), ga);
                 ga = warp_sum(ga);
                 const double al = nrm[p], be = nrm[q];
-                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be)) continue;
+                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be) || fabs(ga) <= abs_floor) continue;
                 double c, s, t;
                 jacobi_rotation(al, be, ga, c, s, t);
                 for (int i = lane; i < m; i += 32) {
-                    const double x = wp[i], y = wq[i];
-                    wp[i] = c * x - s * y;
-                    wq[i] = s * x + c * y;
+                    const double x = lds64(wp + 8u * i), y = lds64(wq + 8u * i);
+                    sts64(wp + 8u * i, c * x - s * y);
+                    sts64(wq + 8u * i, s * x + c * y);
                 }
-                double* jp = J + p * nc;
-                double* jq = J + q * nc;
+                const unsigned jp = Jb + 8u * static_cast<unsigned>(p * nc), jq = Jb + 8u * static_cast<unsigned>(q * nc);
                 for (int i = lane; i < nc; i += 32) {
-                    const double x = jp[i], y = jq[i];
-                    jp[i] = c * x - s * y;
-                    jq[i] = s * x + c * y;
+                    const double x = lds64(jp + 8u * i), y = lds64(jq + 8u * i);
+                    sts64(jp + 8u * i, c * x - s * y);
+                    sts64(jq + 8u * i, s * x + c * y);
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -974,7 +1006,7 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
                 }
         if (tasks.empty()) continue;
         auto* d = static_cast<const QrTask*>(sc.upload(tasks.data(), tasks.size() * sizeof(QrTask)));
-        tsqr_factor_kernel<<<static_cast<unsigned>(tasks.size()), kQrThreads, smem, sc.stream()>>>(d);
+        tsqr_factor_kernel<<<static_cast<unsigned>(tasks.size()), kQrFThreads, 0, sc.stream()>>>(d);
         TS_LAUNCH_CHECK();
         sc.launches += 1;
     }
