@@ -127,14 +127,23 @@ __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* 
         const double tau = s_tau[buf];
         if (tau != 0.0) {
             const double* vb = vbuf[buf] + lane;  // v is 0 above row k
+            // All owned columns' dot products first, then one interleaved
+            // reduction (their shuffle latencies overlap), then the updates.
+            double dot[kQrFCPW];
+#pragma unroll
+            for (int i = 0; i < kQrFCPW; ++i) {
+                dot[i] = 0.0;
+#pragma unroll
+                for (int t = 0; t < kQrRowsPerLane; ++t) dot[i] = fma(vb[32 * t], a[i][t], dot[i]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < kQrFCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
 #pragma unroll
             for (int i = 0; i < kQrFCPW; ++i) {
                 const int c = warp + kQrFWarps * i;
-                if (c <= k || c >= cols) continue;  // warp-uniform
-                double dot = 0.0;
-#pragma unroll
-                for (int t = 0; t < kQrRowsPerLane; ++t) dot = fma(vb[32 * t], a[i][t], dot);
-                const double w = tau * warp_sum(dot);
+                const double w = (c > k && c < cols) ? tau * dot[i] : 0.0;  // columns ≤ k are final
 #pragma unroll
                 for (int t = 0; t < kQrRowsPerLane; ++t) a[i][t] = fma(-w, vb[32 * t], a[i][t]);
             }
