@@ -17,6 +17,10 @@
  *   ts_krp_sum            ← krp_sum(req, plan, stats) → sketched_sum(krp=true)
  *                           (include/tucksum/sketch.hpp:85-86, src/sketch.cpp:66-181,360-362)
  *   ts_effective_subrank  ← effective_subrank(..., Strategy::Krp, ...) (src/sketch.cpp:272-349)
+ *   ts_kron_sum           ← kron_sum(req, plan, stats) → sketched_sum(krp=false)
+ *                           (include/tucksum/sketch.hpp:89-90, src/sketch.cpp:66-181,364-366)
+ *   ts_effective_subrank_kron ← effective_subrank(..., Strategy::Kron, ...) (src/sketch.cpp:272-349)
+ *   ts_kron_sketch_dims   ← kron_sketch_dims (src/sketch.cpp:222-270)
  *   ts_substream          ← RngSeed::substream (include/tucksum/types.hpp:17-24, src/kernels.cpp:23-25)
  *   ts_gaussian_matrix    ← gaussian_matrix (src/kernels.cpp:88-101)
  *   status codes          ← std::invalid_argument / std::runtime_error thrown by
@@ -110,6 +114,14 @@ int ts_omega_prepare(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t wi
  * per-mode rank cap of SURVEY.md §8(d); NULL reproduces the reference exactly. */
 int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
+/* kron_sum with the plan given: Ω_n is
+ * dims[n] × widths[n] and the mode-n sketch has C_n = prod_{j != n} widths[j]
+ * columns (src/sketch.cpp:91-101,132-140); every C_n must be <= 96.  Other
+ * arguments as ts_krp_sum. */
+int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
+                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
+/* Kron widths for per-mode targets (host arithmetic, bit-identical rule). */
+int ts_kron_sketch_dims(int64_t order, const int64_t* targets, const int64_t* dims, int64_t* out_widths);
 /* Independent sums in one call (SURVEY.md §8(f) row 2 — one round_sum per NDG
  * node, many GMRES steps): sum i = krp_sum of batches[i] with weights[i] and the
  * Ω stream (seeds[i], streams[i]); widths / eps / max_rank are shared.  Sums run
@@ -124,6 +136,10 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
  * targets and the uniform widths.  oversampling[order] >= 0. */
 int ts_effective_subrank(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps,
                          const int64_t* oversampling, int64_t* effective_ranks, int64_t* targets, int64_t* widths);
+/* Plan stage for Strategy::Kron: same ranks/targets, widths = kron_sketch_dims(targets, dims). */
+int ts_effective_subrank_kron(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps,
+                              const int64_t* oversampling, int64_t* effective_ranks, int64_t* targets,
+                              int64_t* widths);
 
 /* Small symmetric eigensolver used by ST-HOSVD's fast path (reference sym_eig,
  * src/kernels.cpp:70-86): a (n × n, column-major, host), n <= 96 → values

@@ -65,6 +65,8 @@ def lib():
         L.or_num_threads.restype = C.c_int
         L.or_krp_sum.argtypes = [C.POINTER(OrTuckerView), i64, dptr, i64p, i64, u64, u64, C.c_double, i64p,
                                  C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.or_sketched_sum.argtypes = [C.POINTER(OrTuckerView), i64, dptr, i64p, i64, u64, u64, C.c_double, i64p,
+                                      C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         for name in ("or_result_order", "or_result_dims", "or_result_ranks", "or_result_widths", "or_result_factor",
                      "or_result_core", "or_result_inter", "or_result_free"):
             getattr(L, name).argtypes = None
@@ -231,9 +233,11 @@ class OracleTucker:
 
 
 def krp_sum(summands, weights, widths=None, seed=(0, 0), eps=1e-8, cap=None, oversampling=5, threads=1,
-            intermediates=False):
-    """Oracle krp_sum. Returns (OracleTucker, info dict)."""
+            intermediates=False, strategy="krp"):
+    """Oracle krp_sum (strategy "krp") or kron_sum ("kron"). Returns (OracleTucker, info dict)."""
     L = lib()
+    if strategy not in ("krp", "kron"):
+        raise ValueError("unknown strategy")
     if len(summands) == 0 or len(summands) != len(weights):
         raise ValueError("sum request needs matching, nonempty summands and weights")  # src/sketch.cpp:18-20
     views = _Views(summands)
@@ -241,10 +245,11 @@ def krp_sum(summands, weights, widths=None, seed=(0, 0), eps=1e-8, cap=None, ove
     wid = None if widths is None else np.ascontiguousarray(np.asarray(widths, dtype=np.int64))
     capa = None if cap is None else np.ascontiguousarray(np.asarray(cap, dtype=np.int64))
     h = C.c_void_p()
-    rc = L.or_krp_sum(views.arr, i64(len(summands)), _p(w) if len(w) else dptr(),
-                      wid.ctypes.data_as(i64p) if wid is not None else None, i64(oversampling), u64(seed[0]),
-                      u64(seed[1]), C.c_double(eps), capa.ctypes.data_as(i64p) if capa is not None else None,
-                      C.c_int(threads), C.c_int(1 if intermediates else 0), C.byref(h))
+    rc = L.or_sketched_sum(views.arr, i64(len(summands)), _p(w) if len(w) else dptr(),
+                           wid.ctypes.data_as(i64p) if wid is not None else None, i64(oversampling), u64(seed[0]),
+                           u64(seed[1]), C.c_double(eps), capa.ctypes.data_as(i64p) if capa is not None else None,
+                           C.c_int(threads), C.c_int(1 if intermediates else 0), C.c_int(strategy == "krp"),
+                           C.byref(h))
     _check(rc)
     try:
         order = L.or_result_order(h)
@@ -281,7 +286,24 @@ def krp_sum(summands, weights, widths=None, seed=(0, 0), eps=1e-8, cap=None, ove
         L.or_result_free(h)
 
 
-def effective_subrank_krp(summands, weights, eps, oversampling):
+def kron_sum(summands, weights, widths=None, **kw):
+    """Oracle kron_sum (reference src/sketch.cpp:364-366)."""
+    return krp_sum(summands, weights, widths, strategy="kron", **kw)
+
+
+def kron_sketch_dims(targets, dims):
+    """Reference kron_sketch_dims (src/sketch.cpp:222-270)."""
+    t = np.ascontiguousarray(np.asarray(targets, dtype=np.int64))
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+    if len(t) != len(d):
+        raise ValueError("kron_sketch_dims: need order >= 2 and matching dims")
+    out = np.zeros(max(1, len(t)), dtype=np.int64)
+    _check(lib().or_kron_sketch_dims(i64(len(t)), t.ctypes.data_as(i64p), d.ctypes.data_as(i64p),
+                                     out.ctypes.data_as(i64p)))
+    return [int(x) for x in out[:len(t)]]
+
+
+def effective_subrank_krp(summands, weights, eps, oversampling, strategy="krp"):
     order = len(summands[0].dims)
     ov = np.asarray(oversampling if np.ndim(oversampling) else [oversampling] * order, dtype=np.int64)
     if len(ov) != order:
@@ -291,10 +313,14 @@ def effective_subrank_krp(summands, weights, eps, oversampling):
     wd = np.zeros(order, dtype=np.int64)
     views = _Views(summands)
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
-    _check(lib().or_effective_subrank_krp(views.arr, i64(len(summands)), _p(w), C.c_double(eps),
-                                          ov.ctypes.data_as(i64p), eff.ctypes.data_as(i64p), tg.ctypes.data_as(i64p),
-                                          wd.ctypes.data_as(i64p)))
+    _check(lib().or_effective_subrank(views.arr, i64(len(summands)), _p(w), C.c_double(eps),
+                                      ov.ctypes.data_as(i64p), C.c_int(strategy == "krp"), eff.ctypes.data_as(i64p),
+                                      tg.ctypes.data_as(i64p), wd.ctypes.data_as(i64p)))
     return [int(x) for x in eff], [int(x) for x in tg], [int(x) for x in wd]
+
+
+def effective_subrank(summands, weights, eps, oversampling, strategy="krp"):
+    return effective_subrank_krp(summands, weights, eps, oversampling, strategy)
 
 
 def partial_sketch(summands, weights, s, seed):

@@ -770,31 +770,46 @@ struct SumIntermediates {
     Tensor h;
 };
 
-// Partial range-finder accumulation over summands [i0, i1): src/sketch.cpp:103-143 (krp branch).
+// Partial range-finder accumulation over summands [i0, i1): src/sketch.cpp:103-143.
+// krp: one Khatri-Rao contraction per (block, mode); otherwise (Kron) the block
+// is multiplied by m[j] = Ω_jᵀU_j in every mode j ≠ n (:132-140) and its mode-n
+// unfolding has Π_{j≠n} s_j columns.
 void accumulate_sketch(const std::vector<const Tucker*>& xs, const std::vector<double>& ws, size_t i0, size_t i1,
-                       const std::vector<Mat>& omega, std::vector<Mat>& y) {
+                       const std::vector<Mat>& omega, std::vector<Mat>& y, bool krp = true) {
     for (size_t i = i0; i < i1; ++i) {
         const Tucker& x = *xs[i];
         const double w = ws[i];
         const Index order = x.order();
         const size_t ou = static_cast<size_t>(order);
         std::vector<Mat> m(ou);
-        for (size_t j = 0; j < ou; ++j) m[j] = matmul(x.factors[j], true, omega[j], false);  // :108-112
+        for (size_t j = 0; j < ou; ++j)  // :108-112
+            m[j] = krp ? matmul(x.factors[j], true, omega[j], false) : matmul(omega[j], true, x.factors[j], false);
         for (Index n = 0; n < order; ++n) {
             const size_t nu = static_cast<size_t>(n);
             for (const Block& b : x.blocks) {
-                Mat k;
-                bool first = true;
-                for (Index j = order - 1; j >= 0; --j) {  // :117-129, highest mode outermost
-                    if (j == n) continue;
-                    const size_t ju = static_cast<size_t>(j);
-                    Mat slice = middle_rows(m[ju], b.off[ju], b.data.dim(j));
-                    k = first ? std::move(slice) : khatri_rao(k, slice);
-                    first = false;
+                Mat v;
+                if (krp) {
+                    Mat k;
+                    bool first = true;
+                    for (Index j = order - 1; j >= 0; --j) {  // :117-129, highest mode outermost
+                        if (j == n) continue;
+                        const size_t ju = static_cast<size_t>(j);
+                        Mat slice = middle_rows(m[ju], b.off[ju], b.data.dim(j));
+                        k = first ? std::move(slice) : khatri_rao(k, slice);
+                        first = false;
+                    }
+                    v = matmul(unfold(b.data, n), false, k, false);  // :130
+                } else {
+                    Tensor t = b.data;  // :133-139
+                    for (Index j = 0; j < order; ++j) {
+                        if (j == n) continue;
+                        const size_t ju = static_cast<size_t>(j);
+                        t = ttm(t, middle_cols(m[ju], b.off[ju], b.data.dim(j)), j);
+                    }
+                    v = unfold(t, n);
                 }
-                Mat v = matmul(unfold(b.data, n), false, k, false);  // :130
                 Mat fs = middle_cols(x.factors[nu], b.off[nu], b.data.dim(n));
-                // :131 y[n] += w * (factor_slice * v)
+                // :131 / :140 y[n] += w * (factor_slice * v)
                 gemm(false, false, fs.r, v.c, fs.c, w, fs.a.data(), fs.r, v.a.data(), v.r, 1.0, y[nu].a.data(), y[nu].r);
             }
         }
@@ -830,10 +845,25 @@ void for_ranges(size_t count, int parts, F fn) {
     }
 }
 
-// src/sketch.cpp:66-181 with krp = true and the plan passed in (mode_sketch_dims
-// = widths).  `cap` is the optional rank cap (nullptr ≡ reference semantics).
-Tucker krp_sum(const std::vector<const Tucker*>& xs, const std::vector<double>& ws, const std::vector<Index>& widths,
-               Seed seed, double eps, const Index* cap, int threads, SumIntermediates* inter) {
+// Π_{j≠skip} v_j, saturating (src/sketch.cpp complement_product).
+Index complement_product(const std::vector<Index>& v, size_t skip) {
+    const Index cap = Index(1) << 50;
+    Index prod = 1;
+    for (size_t j = 0; j < v.size(); ++j) {
+        if (j == skip) continue;
+        const Index f = std::max<Index>(v[j], 1);
+        if (prod > cap / f) return cap;
+        prod *= f;
+    }
+    return prod;
+}
+
+// src/sketch.cpp:66-181 with the plan passed in (mode_sketch_dims = widths);
+// krp = true: uniform width s = max widths; krp = false (Kron): Ω_n is
+// n_n × widths[n] and Y_n has Π_{j≠n} widths[j] columns.  `cap` is the optional
+// rank cap (nullptr ≡ reference semantics).
+Tucker sketched_sum(const std::vector<const Tucker*>& xs, const std::vector<double>& ws, const std::vector<Index>& widths,
+                    Seed seed, double eps, const Index* cap, int threads, SumIntermediates* inter, bool krp) {
     validate_request(xs, ws);
     if (eps < 0.0) throw std::invalid_argument("tolerance must be nonnegative");
     const Index order = xs.front()->order();
@@ -845,15 +875,18 @@ Tucker krp_sum(const std::vector<const Tucker*>& xs, const std::vector<double>& 
         if (s < 1) throw std::invalid_argument("plan sketch widths must be positive");
     const Index s = *std::max_element(widths.begin(), widths.end());
     std::vector<Mat> omega(ou);
-    for (size_t n = 0; n < ou; ++n) omega[n] = gaussian_matrix(dims[n], s, seed.substream(n));  // :91-95
+    for (size_t n = 0; n < ou; ++n)  // :91-95
+        omega[n] = gaussian_matrix(dims[n], krp ? s : widths[n], seed.substream(n));
 
     const int parts = std::max(1, std::min<int>(threads, static_cast<int>(xs.size())));
     std::vector<std::vector<Mat>> ys(static_cast<size_t>(parts));
     for (auto& yp : ys) {
         yp.resize(ou);
-        for (size_t n = 0; n < ou; ++n) yp[n] = Mat(dims[n], s);
+        for (size_t n = 0; n < ou; ++n) yp[n] = Mat(dims[n], krp ? s : complement_product(widths, n));  // :97-101
     }
-    for_ranges(xs.size(), parts, [&](size_t i0, size_t i1, int p) { accumulate_sketch(xs, ws, i0, i1, omega, ys[static_cast<size_t>(p)]); });
+    for_ranges(xs.size(), parts, [&](size_t i0, size_t i1, int p) {
+        accumulate_sketch(xs, ws, i0, i1, omega, ys[static_cast<size_t>(p)], krp);
+    });
     std::vector<Mat> y = std::move(ys[0]);
     for (int p = 1; p < parts; ++p)
         for (size_t n = 0; n < ou; ++n)
@@ -883,10 +916,56 @@ Tucker krp_sum(const std::vector<const Tucker*>& xs, const std::vector<double>& 
     return make_dense_tucker(std::move(fin.core), std::move(out_factors));
 }
 
-// src/sketch.cpp:272-349 (krp widths: uniform max target).
-std::vector<Index> effective_subrank_krp(const std::vector<const Tucker*>& xs, const std::vector<double>& ws, double eps,
-                                         const std::vector<Index>& oversampling, std::vector<Index>* eff_out,
-                                         std::vector<Index>* targets_out) {
+Tucker krp_sum(const std::vector<const Tucker*>& xs, const std::vector<double>& ws, const std::vector<Index>& widths,
+               Seed seed, double eps, const Index* cap, int threads, SumIntermediates* inter) {
+    return sketched_sum(xs, ws, widths, seed, eps, cap, threads, inter, true);
+}
+
+// src/sketch.cpp:222-270: balanced Kron widths, then the deterministic repair.
+std::vector<Index> kron_sketch_dims(const std::vector<Index>& targets, const std::vector<Index>& dims) {
+    const size_t n = targets.size();
+    if (n < 2 || n != dims.size())
+        throw std::invalid_argument("kron_sketch_dims: need order >= 2 and matching dims");
+    for (size_t i = 0; i < n; ++i) {
+        if (targets[i] < 1 || dims[i] < 1)
+            throw std::invalid_argument("kron_sketch_dims: targets and dims must be positive");
+        if (targets[i] > complement_product(dims, i))
+            throw std::invalid_argument("kron_sketch_dims: target exceeds attainable mode rank");
+    }
+    long double logp = 0.0L;
+    for (Index t : targets) logp += std::log(static_cast<long double>(t));
+    const long double root = std::exp(logp / static_cast<long double>(n - 1));
+    std::vector<Index> s(n);
+    for (size_t i = 0; i < n; ++i) {
+        long double q = root / static_cast<long double>(targets[i]);
+        const long double snapped = std::round(q);
+        if (snapped >= 1.0L && std::fabs(q - snapped) < 1e-9L) q = snapped;
+        const auto si = static_cast<Index>(std::ceil(static_cast<double>(q)));
+        s[i] = std::clamp<Index>(si, 1, dims[i]);
+    }
+    bool changed = true;
+    while (changed) {
+        changed = false;
+        for (size_t m = 0; m < n; ++m) {
+            while (complement_product(s, m) < targets[m]) {
+                size_t pick = n;
+                for (size_t j = 0; j < n; ++j) {
+                    if (j == m || s[j] >= dims[j]) continue;
+                    if (pick == n || s[j] < s[pick]) pick = j;
+                }
+                if (pick == n) throw std::logic_error("kron_sketch_dims: infeasible despite capped targets");
+                ++s[pick];
+                changed = true;
+            }
+        }
+    }
+    return s;
+}
+
+// src/sketch.cpp:272-349 (krp widths: uniform max target; kron: kron_sketch_dims).
+std::vector<Index> effective_subrank(const std::vector<const Tucker*>& xs, const std::vector<double>& ws, double eps,
+                                     const std::vector<Index>& oversampling, std::vector<Index>* eff_out,
+                                     std::vector<Index>* targets_out, bool krp = true) {
     validate_request(xs, ws);
     if (eps < 0.0) throw std::invalid_argument("tolerance must be nonnegative");
     const Index order = xs.front()->order();
@@ -902,17 +981,6 @@ std::vector<Index> effective_subrank_krp(const std::vector<const Tucker*>& xs, c
             for (double v : b.data.a) sq += v * v;
         energy[i] = std::fabs(ws[i]) * std::sqrt(sq);
     }
-    auto complement_product = [&](size_t skip) {
-        const Index cap = Index(1) << 50;
-        Index prod = 1;
-        for (size_t j = 0; j < dims.size(); ++j) {
-            if (j == skip) continue;
-            const Index f = std::max<Index>(dims[j], 1);
-            if (prod > cap / f) return cap;
-            prod *= f;
-        }
-        return prod;
-    };
     std::vector<Index> eff(ou), targets(ou);
     for (size_t n = 0; n < ou; ++n) {
         Index total = 0;
@@ -943,11 +1011,12 @@ std::vector<Index> effective_subrank_krp(const std::vector<const Tucker*>& xs, c
             }
         eff[n] = keep;
         Index target = keep + oversampling[n];
-        target = std::min({target, dims[n], complement_product(n)});
+        target = std::min({target, dims[n], complement_product(dims, n)});
         targets[n] = std::max<Index>(target, 1);
     }
     if (eff_out) *eff_out = eff;
     if (targets_out) *targets_out = targets;
+    if (!krp) return kron_sketch_dims(targets, dims);  // :340-341
     const Index smax = *std::max_element(targets.begin(), targets.end());
     return std::vector<Index>(ou, smax);
 }
@@ -1130,9 +1199,10 @@ int or_sym_eig(std::int64_t n, const double* a, double* values, double* vectors)
 
 // Runs krp_sum on K summand views. widths == nullptr → the plan is built by
 // effective_subrank (src/sketch.cpp:75-79) with the given oversampling.
-int or_krp_sum(const OrTuckerView* views, std::int64_t count, const double* weights, const std::int64_t* widths,
-               std::int64_t oversampling, std::uint64_t seed, std::uint64_t stream, double eps,
-               const std::int64_t* cap, int threads, int keep_intermediates, void** out) {
+// krp != 0: krp_sum (src/sketch.cpp:360-362); krp == 0: kron_sum (:364-366).
+int or_sketched_sum(const OrTuckerView* views, std::int64_t count, const double* weights, const std::int64_t* widths,
+                    std::int64_t oversampling, std::uint64_t seed, std::uint64_t stream, double eps,
+                    const std::int64_t* cap, int threads, int keep_intermediates, int krp, void** out) {
     return guarded([&] {
         std::vector<oracle::Tucker> xs = views_to_tuckers(views, count);
         std::vector<const oracle::Tucker*> ptrs;
@@ -1145,18 +1215,34 @@ int or_krp_sum(const OrTuckerView* views, std::int64_t count, const double* weig
             res->widths.assign(widths, widths + order);
         } else {
             if (order < 2) throw std::invalid_argument("sketched summation needs order >= 2");
-            res->widths = oracle::effective_subrank_krp(ptrs, ws, eps, std::vector<std::int64_t>(order, oversampling),
-                                                        &res->eff, &res->targets);
+            res->widths = oracle::effective_subrank(ptrs, ws, eps, std::vector<std::int64_t>(order, oversampling),
+                                                    &res->eff, &res->targets, krp != 0);
         }
-        res->t = oracle::krp_sum(ptrs, ws, res->widths, oracle::Seed{seed, stream}, eps, cap, threads,
-                                 keep_intermediates ? &res->inter : nullptr);
+        res->t = oracle::sketched_sum(ptrs, ws, res->widths, oracle::Seed{seed, stream}, eps, cap, threads,
+                                      keep_intermediates ? &res->inter : nullptr, krp != 0);
         *out = res.release();
     });
 }
 
-int or_effective_subrank_krp(const OrTuckerView* views, std::int64_t count, const double* weights, double eps,
-                             const std::int64_t* oversampling, std::int64_t* eff, std::int64_t* targets,
-                             std::int64_t* widths) {
+int or_krp_sum(const OrTuckerView* views, std::int64_t count, const double* weights, const std::int64_t* widths,
+               std::int64_t oversampling, std::uint64_t seed, std::uint64_t stream, double eps,
+               const std::int64_t* cap, int threads, int keep_intermediates, void** out) {
+    return or_sketched_sum(views, count, weights, widths, oversampling, seed, stream, eps, cap, threads,
+                           keep_intermediates, 1, out);
+}
+
+int or_kron_sketch_dims(std::int64_t order, const std::int64_t* targets, const std::int64_t* dims, std::int64_t* out) {
+    return guarded([&] {
+        const size_t o = static_cast<size_t>(std::max<std::int64_t>(order, 0));
+        std::vector<std::int64_t> s =
+            oracle::kron_sketch_dims(std::vector<std::int64_t>(targets, targets + o), std::vector<std::int64_t>(dims, dims + o));
+        std::copy(s.begin(), s.end(), out);
+    });
+}
+
+int or_effective_subrank(const OrTuckerView* views, std::int64_t count, const double* weights, double eps,
+                         const std::int64_t* oversampling, int krp, std::int64_t* eff, std::int64_t* targets,
+                         std::int64_t* widths) {
     return guarded([&] {
         std::vector<oracle::Tucker> xs = views_to_tuckers(views, count);
         std::vector<const oracle::Tucker*> ptrs;
@@ -1166,7 +1252,8 @@ int or_effective_subrank_krp(const OrTuckerView* views, std::int64_t count, cons
         const size_t order = ptrs.front()->ranks.size();
         std::vector<std::int64_t> e, t;
         std::vector<std::int64_t> w =
-            oracle::effective_subrank_krp(ptrs, ws, eps, std::vector<std::int64_t>(oversampling, oversampling + order), &e, &t);
+            oracle::effective_subrank(ptrs, ws, eps, std::vector<std::int64_t>(oversampling, oversampling + order), &e, &t,
+                                      krp != 0);
         std::copy(e.begin(), e.end(), eff);
         std::copy(t.begin(), t.end(), targets);
         std::copy(w.begin(), w.end(), widths);

@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -106,10 +107,10 @@ int guarded(F fn) {
 
 struct OmegaKey {
     std::uint64_t seed, stream;
-    std::int64_t width;
+    std::vector<std::int64_t> widths;  // per mode (uniform for the KRP sketch)
     std::vector<std::int64_t> dims;
     bool operator<(const OmegaKey& o) const {
-        return std::tie(seed, stream, width, dims) < std::tie(o.seed, o.stream, o.width, o.dims);
+        return std::tie(seed, stream, widths, dims) < std::tie(o.seed, o.stream, o.widths, o.dims);
     }
 };
 
@@ -181,22 +182,25 @@ using ts::CallScratch;
 using ts::GemmProblem;
 using ts::Layout;
 
-double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, std::int64_t width, std::uint64_t seed,
+// Ω_n = gaussian_matrix(dims[n], widths[n], {seed, stream}.substream(n)), all
+// modes concatenated (column-major each), cached on the device.
+double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, const std::int64_t* widths, std::uint64_t seed,
                   std::uint64_t stream) {
     if (ctx->parent) ctx = ctx->parent;  // lanes share the parent's cache
     std::lock_guard<std::mutex> lock(ctx->omega_mu);
-    OmegaKey key{seed, stream, width, std::vector<std::int64_t>(dims, dims + order)};
+    OmegaKey key{seed, stream, std::vector<std::int64_t>(widths, widths + order),
+                 std::vector<std::int64_t>(dims, dims + order)};
     auto it = ctx->omega.find(key);
     if (it != ctx->omega.end()) return it->second;
     std::int64_t total = 0;
-    for (int n = 0; n < order; ++n) total += dims[n] * width;
+    for (int n = 0; n < order; ++n) total += dims[n] * widths[n];
     std::vector<double> host(static_cast<size_t>(total));
     std::int64_t off = 0;
     for (int n = 0; n < order; ++n) {
         std::uint64_t s2, t2;
         ts::substream(seed, stream, static_cast<std::uint64_t>(n), &s2, &t2);
-        ts::gaussian_fill(dims[n], width, s2, t2, host.data() + off);
-        off += dims[n] * width;
+        ts::gaussian_fill(dims[n], widths[n], s2, t2, host.data() + off);
+        off += dims[n] * widths[n];
     }
     double* d = nullptr;
     TS_CUDA_CHECK(cudaMalloc(&d, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(total, 1))));
@@ -298,9 +302,106 @@ std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double the
     return rank;
 }
 
-ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
-                        std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank,
-                        bool allow_spec = true) {
+// Π_{j≠skip} v_j, saturating at 2^50 (reference complement_product, src/sketch.cpp).
+std::int64_t complement_product(const std::int64_t* v, int order, int skip) {
+    const std::int64_t cap = std::int64_t(1) << 50;
+    std::int64_t prod = 1;
+    for (int j = 0; j < order; ++j) {
+        if (j == skip) continue;
+        const std::int64_t f = std::max<std::int64_t>(v[j], 1);
+        if (prod > cap / f) return cap;
+        prod *= f;
+    }
+    return prod;
+}
+
+// Stage B of the Kron sketch (src/sketch.cpp:132-140): every atom's core block
+// is multiplied by M_j = Ω_jᵀU_j (its column slice of Z_j, ow_j × r_j) in every
+// mode j ≠ n, ascending — one grouped batched DMMA GEMM launch over all atoms per
+// step — and the gather writes w_b·unfold(V, n)ᵀ into Wt_n (C_n × R_n).
+void kron_stage_b(const ts_batch* b, double* const* Z, const std::int64_t* ow, double* const* Wt,
+                  const std::int64_t* yc, const double* d_w, CallScratch& sc, int num_sms) {
+    const int d = b->order;
+    const size_t na = b->atoms.size();
+    for (int n = 0; n < d; ++n) {
+        std::vector<const double*> cur(na);
+        std::vector<std::array<std::int64_t, TS_MAX_ORDER>> shp(na);
+        for (size_t a = 0; a < na; ++a) {
+            cur[a] = b->cores + b->atoms[a].core_off;
+            for (int j = 0; j < d; ++j) shp[a][static_cast<size_t>(j)] = b->atoms[a].shape[j];
+        }
+        for (int m = 0; m < d; ++m) {
+            if (m == n) continue;
+            std::vector<std::int64_t> outoff(na);
+            std::int64_t tot = 0;
+            for (size_t a = 0; a < na; ++a) {
+                std::int64_t e = ow[m];
+                for (int j = 0; j < d; ++j)
+                    if (j != m) e *= shp[a][static_cast<size_t>(j)];
+                outoff[a] = tot;
+                tot += e;
+            }
+            double* outbuf = sc.alloc_n<double>(static_cast<size_t>(std::max<std::int64_t>(tot, 1)));
+            std::vector<GemmProblem> ps;
+            ps.reserve(na);
+            for (size_t a = 0; a < na; ++a) {
+                const ts::Atom& at = b->atoms[a];
+                std::int64_t left = 1, right = 1;
+                for (int j = 0; j < m; ++j) left *= shp[a][static_cast<size_t>(j)];
+                for (int j = m + 1; j < d; ++j) right *= shp[a][static_cast<size_t>(j)];
+                const std::int64_t rm = shp[a][static_cast<size_t>(m)];
+                double* out = outbuf + outoff[a];
+                GemmProblem p{};
+                if (m == 0) {
+                    // out (ow_0 × right) = M_0 (ow_0 × r_0) · T (r_0 × right)
+                    p.A = Z[0] + static_cast<std::int64_t>(at.col[0]) * ow[0];
+                    p.lda = ow[0];
+                    p.B = cur[a];
+                    p.ldb = rm;
+                    p.C = out;
+                    p.ldc = ow[0];
+                    p.M = static_cast<int>(ow[0]);
+                    p.N = static_cast<int>(right);
+                    p.K = static_cast<int>(rm);
+                } else {
+                    // per right slice: out (left × ow_m) = T (left × r_m) · M_mᵀ
+                    p.A = cur[a];
+                    p.lda = left;
+                    p.sA = left * rm;
+                    p.B = Z[m] + static_cast<std::int64_t>(at.col[m]) * ow[m];
+                    p.ldb = ow[m];
+                    p.sB = 0;
+                    p.C = out;
+                    p.ldc = left;
+                    p.sC = left * ow[m];
+                    p.M = static_cast<int>(left);
+                    p.N = static_cast<int>(ow[m]);
+                    p.K = static_cast<int>(rm);
+                    p.batch = static_cast<int>(right);
+                }
+                ps.push_back(p);
+                cur[a] = out;
+                shp[a][static_cast<size_t>(m)] = ow[m];
+            }
+            ts::launch_grouped_gemm(m == 0 ? Layout::NN : Layout::NT, ps, sc, num_sms);
+        }
+        std::vector<ts::KronGather> g(na);
+        for (size_t a = 0; a < na; ++a) {
+            std::int64_t L = 1;
+            for (int j = 0; j < n; ++j) L *= shp[a][static_cast<size_t>(j)];
+            g[a] = ts::KronGather{cur[a], L, b->atoms[a].shape[n], b->atoms[a].col[n], b->atoms[a].summand, 0};
+        }
+        ts::launch_kron_gather(g, yc[n], Wt[n], d_w, sc);
+    }
+}
+
+// krp = true: krp_sum → sketched_sum(krp=true); krp = false: kron_sum →
+// sketched_sum(krp=false) (src/sketch.cpp:66-181,360-366).  The two differ in the
+// Ω widths (uniform s vs plan widths), stage B and the sketch width of Y_n
+// (s vs C_n = Π_{j≠n} s_j); everything from stage D on is shared.
+ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
+                             std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank,
+                             bool krp, bool allow_spec = true) {
     // Validation mirrors src/sketch.cpp:16-30,66-87.
     if (b == nullptr || b->count < 1) invalid("sum request needs matching, nonempty summands and weights");
     if (weights == nullptr) invalid("sum request needs matching, nonempty summands and weights");
@@ -311,9 +412,14 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     for (int n = 0; n < d; ++n)
         if (widths[n] < 1) invalid("plan sketch widths must be positive");
     const std::int64_t s = *std::max_element(widths, widths + d);
-    if (s > ts::max_tsqr_cols())
-        throw ts::Error(TS_UNSUPPORTED, "sketch width " + std::to_string(s) + " exceeds the supported maximum of " +
-                                            std::to_string(ts::max_tsqr_cols()));
+    std::int64_t ow[TS_MAX_ORDER], yc[TS_MAX_ORDER];  // Ω_n widths, Y_n widths
+    for (int n = 0; n < d; ++n) {
+        ow[n] = krp ? s : widths[n];
+        yc[n] = krp ? s : complement_product(widths, d, n);
+        if (yc[n] > ts::max_tsqr_cols())
+            throw ts::Error(TS_UNSUPPORTED, "sketch width " + std::to_string(yc[n]) +
+                                                " exceeds the supported maximum of " + std::to_string(ts::max_tsqr_cols()));
+    }
     for (std::int64_t i = 0; i < b->count; ++i)
         if (!std::isfinite(weights[i])) invalid("weights must be finite");
 
@@ -328,16 +434,16 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     }
     mark(ctx, 0);
 
-    double* omega = omega_get(ctx, d, dims, s, seed, stream);
+    double* omega = omega_get(ctx, d, dims, ow, seed, stream);
     std::int64_t q[TS_MAX_ORDER];
     std::int64_t ooff[TS_MAX_ORDER], yoff[TS_MAX_ORDER];
     std::int64_t ytot = 0, acc = 0;
     for (int n = 0; n < d; ++n) {
-        q[n] = std::min(dims[n], s);
+        q[n] = std::min(dims[n], yc[n]);
         ooff[n] = acc;
-        acc += dims[n] * s;
+        acc += dims[n] * ow[n];
         yoff[n] = ytot;
-        ytot += dims[n] * s;
+        ytot += dims[n] * yc[n];
     }
     auto* d_w = static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
 
@@ -346,15 +452,15 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     {
         std::vector<GemmProblem> ps;
         for (int j = 0; j < d; ++j) {
-            Z[j] = sc.alloc_n<double>(static_cast<size_t>(s * b->R[j]));
+            Z[j] = sc.alloc_n<double>(static_cast<size_t>(ow[j] * b->R[j]));
             GemmProblem p{};
             p.A = omega + ooff[j];
             p.lda = dims[j];
             p.B = b->F[j];
             p.ldb = dims[j];
             p.C = Z[j];
-            p.ldc = s;
-            p.M = static_cast<int>(s);
+            p.ldc = ow[j];
+            p.M = static_cast<int>(ow[j]);
             p.N = static_cast<int>(b->R[j]);
             p.K = static_cast<int>(dims[j]);
             ps.push_back(p);
@@ -362,9 +468,12 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
         ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
     }
     mark(ctx, 1);
-    // ---- Stage B: W_n (R_n × s)
+    // ---- Stage B: W_n (R_n × s), stored transposed
     double* W[TS_MAX_ORDER];
-    {
+    if (!krp) {
+        for (int n = 0; n < d; ++n) W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * yc[n]));
+        kron_stage_b(b, Z, ow, W, yc, d_w, sc, ctx->num_sms);
+    } else {
         ts::KrpArgs ka{};
         for (int n = 0; n < d; ++n) {
             W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * s));
@@ -389,12 +498,12 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             GemmProblem p{};
             p.A = b->F[n];
             p.lda = dims[n];
-            p.B = W[n];  // stored transposed: Wt_n (s × R_n)
-            p.ldb = s;
+            p.B = W[n];  // stored transposed: Wt_n (yc_n × R_n)
+            p.ldb = yc[n];
             p.C = Y + yoff[n];
             p.ldc = dims[n];
             p.M = static_cast<int>(dims[n]);
-            p.N = static_cast<int>(s);
+            p.N = static_cast<int>(yc[n]);
             p.K = static_cast<int>(b->R[n]);
             ps.push_back(p);
         }
@@ -410,12 +519,12 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
     res->order = d;
     if (ctx->debug) {
         for (int n = 0; n < d; ++n) {
-            copy_to_host(res->inter[0][n], omega + ooff[n], dims[n] * s, st);
+            copy_to_host(res->inter[0][n], omega + ooff[n], dims[n] * ow[n], st);
             res->inter_rows[0][n] = dims[n];
-            res->inter_cols[0][n] = s;
-            copy_to_host(res->inter[1][n], Y + yoff[n], dims[n] * s, st);
+            res->inter_cols[0][n] = ow[n];
+            copy_to_host(res->inter[1][n], Y + yoff[n], dims[n] * yc[n], st);
             res->inter_rows[1][n] = dims[n];
-            res->inter_cols[1][n] = s;
+            res->inter_cols[1][n] = yc[n];
         }
     }
     // Speculative tail: the fast paths of stages D and G (CholeskyQR2; Gram +
@@ -441,24 +550,25 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
         double *G1[TS_MAX_ORDER], *G2[TS_MAX_ORDER], *Ri1[TS_MAX_ORDER], *Ri2[TS_MAX_ORDER], *Q1[TS_MAX_ORDER];
         bool any = false;
         for (int n = 0; n < d; ++n) {
+            const std::int64_t c = yc[n];
             Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
-            chol[static_cast<size_t>(n)] = dims[n] >= 2 * s;
+            chol[static_cast<size_t>(n)] = dims[n] >= 2 * c;
             if (!chol[static_cast<size_t>(n)]) continue;
             any = true;
-            G1[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
-            G2[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
-            Ri1[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
-            Ri2[n] = sc.alloc_n<double>(static_cast<size_t>(s * s));
-            Q1[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * s));
+            G1[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
+            G2[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
+            Ri1[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
+            Ri2[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
+            Q1[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * c));
             GemmProblem p{};
-            p.M = p.N = static_cast<int>(s);
+            p.M = p.N = static_cast<int>(c);
             p.K = static_cast<int>(dims[n]);
             p.A = Y + yoff[n];
             p.lda = dims[n];
             p.B = Y + yoff[n];
             p.ldb = dims[n];
             p.C = G1[n];
-            p.ldc = s;
+            p.ldc = c;
             g1.push_back(p);
             p.A = Q1[n];
             p.B = Q1[n];
@@ -466,12 +576,12 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             g2.push_back(p);
             GemmProblem m{};
             m.M = static_cast<int>(dims[n]);
-            m.N = static_cast<int>(s);
-            m.K = static_cast<int>(s);
+            m.N = static_cast<int>(c);
+            m.K = static_cast<int>(c);
             m.A = Y + yoff[n];
             m.lda = dims[n];
             m.B = Ri1[n];
-            m.ldb = s;
+            m.ldb = c;
             m.C = Q1[n];
             m.ldc = dims[n];
             q1.push_back(m);
@@ -481,27 +591,33 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             q2.push_back(m);
         }
         if (any) {
-            ts::CholBatch cb1{}, cb2{};
-            int nb = 0;
-            for (int n = 0; n < d; ++n) {
-                if (!chol[static_cast<size_t>(n)]) continue;
-                cb1.G[nb] = G1[n];
-                cb1.Rinv[nb] = Ri1[n];
-                cb1.flag[nb] = flags + n;
-                cb2.G[nb] = G2[n];
-                cb2.Rinv[nb] = Ri2[n];
-                cb2.flag[nb] = flags + n;
-                ++nb;
-            }
-            cb1.ldg = cb1.ldri = cb2.ldg = cb2.ldri = s;
-            cb1.n = cb2.n = static_cast<int>(s);
-            cb1.check_identity = 0;
-            cb2.check_identity = 1;
+            // One Cholesky batch per distinct sketch width (all modes share it
+            // for the KRP sketch).
+            std::vector<std::int64_t> cw;
+            for (int n = 0; n < d; ++n)
+                if (chol[static_cast<size_t>(n)] && std::find(cw.begin(), cw.end(), yc[n]) == cw.end()) cw.push_back(yc[n]);
+            auto chol_batches = [&](bool second) {
+                for (std::int64_t c : cw) {
+                    ts::CholBatch cb{};
+                    int nb = 0;
+                    for (int n = 0; n < d; ++n) {
+                        if (!chol[static_cast<size_t>(n)] || yc[n] != c) continue;
+                        cb.G[nb] = second ? G2[n] : G1[n];
+                        cb.Rinv[nb] = second ? Ri2[n] : Ri1[n];
+                        cb.flag[nb] = flags + n;
+                        ++nb;
+                    }
+                    cb.ldg = cb.ldri = c;
+                    cb.n = static_cast<int>(c);
+                    cb.check_identity = second ? 1 : 0;
+                    ts::launch_chol_inv(cb, nb, sc);
+                }
+            };
             ts::launch_grouped_gemm(Layout::TN, g1, sc, ctx->num_sms);
-            ts::launch_chol_inv(cb1, nb, sc);
+            chol_batches(false);
             ts::launch_grouped_gemm(Layout::NN, q1, sc, ctx->num_sms);
             ts::launch_grouped_gemm(Layout::TN, g2, sc, ctx->num_sms);
-            ts::launch_chol_inv(cb2, nb, sc);
+            chol_batches(true);
             ts::launch_grouped_gemm(Layout::NN, q2, sc, ctx->num_sms);
             if (spec) {
                 dflags = flags;
@@ -518,7 +634,7 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
         std::vector<ts::TsqrPlan*> pp;
         for (int n = 0; n < d; ++n) {
             if (chol[static_cast<size_t>(n)]) continue;
-            plans[static_cast<size_t>(n)] = ts::plan_tsqr(Y + yoff[n], dims[n], dims[n], s, Uh[n], dims[n], sc);
+            plans[static_cast<size_t>(n)] = ts::plan_tsqr(Y + yoff[n], dims[n], dims[n], yc[n], Uh[n], dims[n], sc);
             pp.push_back(&plans[static_cast<size_t>(n)]);
         }
         if (!pp.empty()) ts::run_tsqr(pp, sc, true);
@@ -819,7 +935,7 @@ ts_result* krp_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, c
             if (x != 0) {
                 ctx->spec_ok = false;
                 res.reset();
-                return krp_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, false);
+                return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, krp, false);
             }
     } else {
         ctx->spec_ok = ctx->last_qr_fallbacks == 0 && ctx->last_svd_fallbacks == 0;
@@ -1072,7 +1188,8 @@ int ts_omega_prepare(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t wi
     return guarded([&] {
         if (!ctx || order < 1 || order > TS_MAX_ORDER || width < 1) invalid("ts_omega_prepare: bad arguments");
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
-        omega_get(ctx, static_cast<int>(order), dims, width, seed, stream);
+        const std::vector<std::int64_t> wv(static_cast<size_t>(order), width);
+        omega_get(ctx, static_cast<int>(order), dims, wv.data(), seed, stream);
     });
 }
 
@@ -1080,7 +1197,15 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_krp_sum: null argument");
-        *out = krp_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank);
+        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, true);
+    });
+}
+
+int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
+                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
+    return guarded([&] {
+        if (!ctx || !out) invalid("ts_kron_sum: null argument");
+        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, false);
     });
 }
 
@@ -1101,7 +1226,7 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
         if (count == 0) return;
         if (ctx->comm || count == 1 || lanes <= 1) {
             for (int64_t i = 0; i < count; ++i)
-                out[i] = krp_sum_impl(ctx, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank);
+                out[i] = sketched_sum_impl(ctx, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, true);
             return;
         }
         const int L = static_cast<int>(std::min<int64_t>(std::min(lanes, 16), count));
@@ -1122,7 +1247,7 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
                 codes[static_cast<size_t>(t)] = guarded([&] {
                     TS_CUDA_CHECK(cudaSetDevice(lane->device));
                     for (int64_t i = t; i < count; i += L)
-                        out[i] = krp_sum_impl(lane, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank);
+                        out[i] = sketched_sum_impl(lane, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, true);
                 });
                 if (codes[static_cast<size_t>(t)] != TS_OK) errs[static_cast<size_t>(t)] = g_err;
             });
@@ -1142,9 +1267,9 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
 // of the energy-weighted stacked factors V_n = F_n·diag(e) is obtained as the
 // squared singular values of V_n (TSQR + Jacobi on device), with the reference's
 // floor / tail rule applied on the returned values.
-int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, double eps, const int64_t* oversampling,
-                         int64_t* effective_ranks, int64_t* targets, int64_t* widths) {
-    return guarded([&] {
+static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, double eps, const int64_t* oversampling,
+                         int64_t* effective_ranks, int64_t* targets) {
+    {
         if (!ctx || !b || !weights || !oversampling) invalid("sum request needs matching, nonempty summands and weights");
         if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
         const int d = b->order;
@@ -1167,17 +1292,6 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
         std::vector<double> energy(static_cast<size_t>(b->count));
         for (std::int64_t i = 0; i < b->count; ++i)
             energy[static_cast<size_t>(i)] = std::fabs(weights[i]) * b->core_norm[static_cast<size_t>(i)];
-        auto complement_product = [&](int skip) {
-            const std::int64_t cap = std::int64_t(1) << 50;
-            std::int64_t prod = 1;
-            for (int j = 0; j < d; ++j) {
-                if (j == skip) continue;
-                const std::int64_t f = std::max<std::int64_t>(b->dims[j], 1);
-                if (prod > cap / f) return cap;
-                prod *= f;
-            }
-            return prod;
-        };
         for (int n = 0; n < d; ++n) {
             const std::int64_t rows = b->dims[n], R = b->R[n];
             const std::int64_t small = std::min(rows, R);
@@ -1231,13 +1345,82 @@ int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, 
                 }
             effective_ranks[n] = keep;
             std::int64_t target = keep + oversampling[n];
-            target = std::min({target, b->dims[n], complement_product(n)});
+            target = std::min({target, b->dims[n], complement_product(b->dims, d, n)});
             targets[n] = std::max<std::int64_t>(target, 1);
         }
-        const std::int64_t smax = *std::max_element(targets, targets + d);
-        for (int n = 0; n < d; ++n) widths[n] = smax;
         ctx->launches += sc.launches;
         TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+}
+
+// Reference kron_sketch_dims (src/sketch.cpp:222-270): balanced widths whose
+// complementary products cover the targets, then a deterministic repair.
+static std::vector<std::int64_t> kron_sketch_dims(const std::vector<std::int64_t>& targets,
+                                                  const std::vector<std::int64_t>& dims) {
+    const size_t n = targets.size();
+    if (n < 2 || n != dims.size()) invalid("kron_sketch_dims: need order >= 2 and matching dims");
+    for (size_t i = 0; i < n; ++i) {
+        if (targets[i] < 1 || dims[i] < 1) invalid("kron_sketch_dims: targets and dims must be positive");
+        if (targets[i] > complement_product(dims.data(), static_cast<int>(n), static_cast<int>(i)))
+            invalid("kron_sketch_dims: target exceeds attainable mode rank");
+    }
+    long double logp = 0.0L;
+    for (std::int64_t t : targets) logp += std::log(static_cast<long double>(t));
+    const long double root = std::exp(logp / static_cast<long double>(n - 1));
+    std::vector<std::int64_t> s(n);
+    for (size_t i = 0; i < n; ++i) {
+        long double q = root / static_cast<long double>(targets[i]);
+        const long double snapped = std::round(q);
+        if (snapped >= 1.0L && std::fabs(q - snapped) < 1e-9L) q = snapped;
+        const auto si = static_cast<std::int64_t>(std::ceil(static_cast<double>(q)));
+        s[i] = std::clamp<std::int64_t>(si, 1, dims[i]);
+    }
+    bool changed = true;
+    while (changed) {
+        changed = false;
+        for (size_t m = 0; m < n; ++m) {
+            while (complement_product(s.data(), static_cast<int>(n), static_cast<int>(m)) < targets[m]) {
+                size_t pick = n;
+                for (size_t j = 0; j < n; ++j) {
+                    if (j == m || s[j] >= dims[j]) continue;
+                    if (pick == n || s[j] < s[pick]) pick = j;
+                }
+                if (pick == n) throw ts::Error(TS_RUNTIME, "kron_sketch_dims: infeasible despite capped targets");
+                ++s[pick];
+                changed = true;
+            }
+        }
+    }
+    return s;
+}
+
+int ts_effective_subrank(ts_ctx* ctx, const ts_batch* b, const double* weights, double eps, const int64_t* oversampling,
+                         int64_t* effective_ranks, int64_t* targets, int64_t* widths) {
+    return guarded([&] {
+        plan_targets(ctx, b, weights, eps, oversampling, effective_ranks, targets);
+        const std::int64_t smax = *std::max_element(targets, targets + b->order);  // src/sketch.cpp:342-344
+        for (int n = 0; n < b->order; ++n) widths[n] = smax;
+    });
+}
+
+int ts_effective_subrank_kron(ts_ctx* ctx, const ts_batch* b, const double* weights, double eps,
+                              const int64_t* oversampling, int64_t* effective_ranks, int64_t* targets, int64_t* widths) {
+    return guarded([&] {
+        plan_targets(ctx, b, weights, eps, oversampling, effective_ranks, targets);
+        const int d = b->order;
+        const std::vector<std::int64_t> w = kron_sketch_dims(std::vector<std::int64_t>(targets, targets + d),
+                                                             std::vector<std::int64_t>(b->dims, b->dims + d));
+        std::copy(w.begin(), w.end(), widths);  // src/sketch.cpp:340-341
+    });
+}
+
+int ts_kron_sketch_dims(int64_t order, const int64_t* targets, const int64_t* dims, int64_t* out) {
+    return guarded([&] {
+        if (order < 0 || (order > 0 && (!targets || !dims || !out))) invalid("kron_sketch_dims: null argument");
+        const size_t o = static_cast<size_t>(order);
+        const std::vector<std::int64_t> w =
+            kron_sketch_dims(std::vector<std::int64_t>(targets, targets + o), std::vector<std::int64_t>(dims, dims + o));
+        std::copy(w.begin(), w.end(), out);
     });
 }
 

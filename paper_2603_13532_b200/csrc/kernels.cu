@@ -1127,4 +1127,37 @@ void launch_sumsq(const double* x, int64_t n, double* out, CallScratch& sc) {
     sc.launches += 2;
 }
 
+namespace {
+// Kron stage B epilogue: Wt[c + C·(col + i)] = w · V[l + L·(i + r·t)], c = l + L·t
+// (the mode-n unfolding of the atom's sketched block, transposed and scaled).
+__global__ void kron_gather_kernel(const KronGather* __restrict__ g, int count, int64_t C, double* __restrict__ Wt,
+                                   const double* __restrict__ weights) {
+    for (int a = blockIdx.y; a < count; a += gridDim.y) {
+        const KronGather d = g[a];
+        const double w = weights[d.summand];
+        const int64_t total = C * d.r;
+        for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+             e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t c = e % C, i = e / C;
+            const int64_t l = c % d.L, t = c / d.L;
+            Wt[c + C * (d.col + i)] = w * d.V[l + d.L * (i + static_cast<int64_t>(d.r) * t)];
+        }
+    }
+}
+}  // namespace
+
+void launch_kron_gather(const std::vector<KronGather>& g, int64_t C, double* Wt, const double* weights,
+                        CallScratch& sc) {
+    if (g.empty()) return;
+    int64_t most = 1;
+    for (const auto& x : g) most = std::max<int64_t>(most, C * x.r);
+    auto* dg = static_cast<KronGather*>(sc.upload(g.data(), sizeof(KronGather) * g.size()));
+    const int threads = 256;
+    const unsigned bx = static_cast<unsigned>(std::min<int64_t>((most + threads - 1) / threads, 64));
+    const unsigned by = static_cast<unsigned>(std::min<size_t>(g.size(), 65535));
+    kron_gather_kernel<<<dim3(bx, by), threads, 0, sc.stream()>>>(dg, static_cast<int>(g.size()), C, Wt, weights);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
 }  // namespace ts

@@ -130,6 +130,21 @@ void launch_scale_columns(const double* F, int64_t n, int64_t R, const double* s
 // out[a] = Σ core(atom a)² (one CTA per atom, deterministic).
 void launch_atom_sumsq(const double* cores, const Atom* atoms, int natoms, int order, double* out, CallScratch& sc);
 
+// Kron stage B epilogue (reference src/sketch.cpp:132-140): per atom, the
+// sketched block V (column-major; L = Π_{j<n} extents, r = its mode-n extent)
+// is unfolded along n, transposed, scaled by its summand's weight and written to
+// columns [col, col + r) of Wt_n (C × R_n, C = Π_{j≠n} s_j).
+struct KronGather {
+    const double* V;
+    int64_t L;
+    int r;
+    int col;
+    int summand;
+    int pad;
+};
+void launch_kron_gather(const std::vector<KronGather>& g, int64_t C, double* Wt, const double* weights,
+                        CallScratch& sc);
+
 int max_tsqr_cols();
 // Device buffer of the values-kernel phase probe (non-null iff TS_EIG_PROFILE is set).
 unsigned long long* eig_probe_buffer();

@@ -48,6 +48,7 @@ EXPORTED_SYMBOLS = [
     "ts_result_order", "ts_result_dims", "ts_result_ranks", "ts_result_factor", "ts_result_core",
     "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
+    "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron",
 ]
 
 
@@ -98,7 +99,10 @@ def lib():
         L.ts_result_core_device.restype = C.c_void_p
         L.ts_krp_sum.argtypes = [C.c_void_p, C.c_void_p, dptr, i64p, u64, u64, C.c_double, i64p,
                                  C.POINTER(C.c_void_p)]
+        L.ts_kron_sum.argtypes = L.ts_krp_sum.argtypes
         L.ts_effective_subrank.argtypes = [C.c_void_p, C.c_void_p, dptr, C.c_double, i64p, i64p, i64p, i64p]
+        L.ts_effective_subrank_kron.argtypes = L.ts_effective_subrank.argtypes
+        L.ts_kron_sketch_dims.argtypes = [i64, i64p, i64p, i64p]
         L.ts_batch_upload.argtypes = [C.c_void_p, C.POINTER(TsTuckerView), i64, C.POINTER(C.c_void_p)]
         L.ts_omega_prepare.argtypes = [C.c_void_p, i64, i64p, i64, u64, u64]
         for name in ("ts_result_factor", "ts_result_core", "ts_result_free", "ts_result_dims", "ts_result_ranks",
@@ -280,15 +284,44 @@ class SketchPlan:
     eps: float = 0.0
     seed: RngSeed = RngSeed()
 
-    def report(self) -> str:  # reference src/sketch.cpp:203-220 (Krp fields)
+    def report(self) -> str:  # reference src/sketch.cpp:203-220
         def fld(v, i):
             return str(v[i]) if i < len(v) else "-"
 
         lines = [f"summation plan ({strategy_name(self.strategy)}): eps={self.eps:g}, seed=({self.seed.seed},{self.seed.stream})"]
         for n in range(len(self.mode_sketch_dims)):
-            lines.append(f"  mode {n + 1}: effective_rank={fld(self.effective_ranks, n)} oversample="
-                         f"{fld(self.oversampling, n)} target={fld(self.targets, n)} sketch_dim={self.mode_sketch_dims[n]}")
+            line = (f"  mode {n + 1}: effective_rank={fld(self.effective_ranks, n)} oversample="
+                    f"{fld(self.oversampling, n)} target={fld(self.targets, n)} sketch_dim={self.mode_sketch_dims[n]}")
+            if self.strategy == Strategy.Kron:
+                line += f" complement_width={complement_product(self.mode_sketch_dims, n)}"
+            lines.append(line)
         return "\n".join(lines) + "\n"
+
+
+def complement_product(v, skip: int) -> int:
+    """Π_{j≠skip} v_j, saturating at 2^50 (reference src/sketch.cpp complement_product)."""
+    cap = 1 << 50
+    prod = 1
+    for j, x in enumerate(v):
+        if j == skip:
+            continue
+        f = max(int(x), 1)
+        if prod > cap // f:
+            return cap
+        prod *= f
+    return prod
+
+
+def kron_sketch_dims(targets, dims) -> List[int]:
+    """Kron widths for per-mode targets (reference src/sketch.cpp:222-270), via the C ABI."""
+    t = np.ascontiguousarray(np.asarray(targets, dtype=np.int64))
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.int64))
+    if len(t) != len(d):
+        raise ValueError("kron_sketch_dims: need order >= 2 and matching dims")
+    out = np.zeros(max(1, len(t)), dtype=np.int64)
+    _check(lib().ts_kron_sketch_dims(i64(len(t)), t.ctypes.data_as(i64p), d.ctypes.data_as(i64p),
+                                     out.ctypes.data_as(i64p)))
+    return [int(x) for x in out[:len(t)]]
 
 
 @dataclass
@@ -515,7 +548,9 @@ class Engine:
                                       u64(seed.stream)))
 
     def krp_sum(self, batch: DeviceBatch, weights, widths, seed: RngSeed, eps: float,
-                max_rank=None) -> DeviceResult:
+                max_rank=None, strategy: "Strategy" = None) -> DeviceResult:
+        """ts_krp_sum (or ts_kron_sum when strategy is Strategy.Kron)."""
+        kron = strategy == Strategy.Kron
         w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
         if len(w) != batch.count:
             raise ValueError("sum request needs matching, nonempty summands and weights")
@@ -524,10 +559,13 @@ class Engine:
             raise ValueError("plan order does not match summand order")
         cap = None if max_rank is None else np.ascontiguousarray(np.asarray(max_rank, dtype=np.int64))
         h = C.c_void_p()
-        _check(lib().ts_krp_sum(self.handle, batch.handle, _p(w), wd.ctypes.data_as(i64p), u64(seed.seed),
-                                u64(seed.stream), C.c_double(eps),
-                                cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
+        fn = lib().ts_kron_sum if kron else lib().ts_krp_sum
+        _check(fn(self.handle, batch.handle, _p(w), wd.ctypes.data_as(i64p), u64(seed.seed), u64(seed.stream),
+                  C.c_double(eps), cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
         return DeviceResult(h)
+
+    def kron_sum(self, batch: DeviceBatch, weights, widths, seed: RngSeed, eps: float, max_rank=None) -> DeviceResult:
+        return self.krp_sum(batch, weights, widths, seed, eps, max_rank, Strategy.Kron)
 
     def krp_sum_many(self, batches: Sequence[DeviceBatch], weights: Sequence, widths, seeds: Sequence[RngSeed],
                      eps: float, max_rank=None, lanes: int = 8) -> List[DeviceResult]:
@@ -557,15 +595,16 @@ class Engine:
                                      C.c_int(lanes), out))
         return [DeviceResult(C.c_void_p(out[i])) for i in range(n)]
 
-    def effective_subrank(self, batch: DeviceBatch, weights, eps: float, oversampling):
+    def effective_subrank(self, batch: DeviceBatch, weights, eps: float, oversampling, strategy: "Strategy" = None):
         order = batch.order
         ov = np.asarray(oversampling if np.ndim(oversampling) else [oversampling] * order, dtype=np.int64)
         if len(ov) != order:
             raise ValueError("oversampling vector must have one entry per mode")
         w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
         eff, tg, wd = (np.zeros(order, dtype=np.int64) for _ in range(3))
-        _check(lib().ts_effective_subrank(self.handle, batch.handle, _p(w), C.c_double(eps), ov.ctypes.data_as(i64p),
-                                          eff.ctypes.data_as(i64p), tg.ctypes.data_as(i64p), wd.ctypes.data_as(i64p)))
+        fn = lib().ts_effective_subrank_kron if strategy == Strategy.Kron else lib().ts_effective_subrank
+        _check(fn(self.handle, batch.handle, _p(w), C.c_double(eps), ov.ctypes.data_as(i64p),
+                  eff.ctypes.data_as(i64p), tg.ctypes.data_as(i64p), wd.ctypes.data_as(i64p)))
         return [int(x) for x in eff], [int(x) for x in tg], [int(x) for x in wd]
 
     def close(self):
@@ -597,7 +636,7 @@ def _validate_request(summands, weights):  # reference src/sketch.cpp:16-30
 
 def effective_subrank(summands, weights, eps, oversampling, strategy=Strategy.Krp, seed=RngSeed(),
                       engine: Optional[Engine] = None) -> SketchPlan:
-    """Plan stage for Strategy.Krp (reference src/sketch.cpp:272-358), on the GPU."""
+    """Plan stage for Strategy.Krp / Strategy.Kron (reference src/sketch.cpp:272-358), on the GPU."""
     _validate_request(summands, weights)
     if eps < 0:
         raise ValueError("tolerance must be nonnegative")
@@ -607,20 +646,30 @@ def effective_subrank(summands, weights, eps, oversampling, strategy=Strategy.Kr
         raise ValueError("oversampling vector must have one entry per mode")
     if any(p < 0 for p in ov):
         raise ValueError("oversampling must be nonnegative")
-    if strategy != Strategy.Krp:
-        raise NotImplementedError("only Strategy.Krp plans are on the B200 hot path")
+    if strategy not in (Strategy.Krp, Strategy.Kron):
+        raise NotImplementedError("only Strategy.Krp / Strategy.Kron plans are on the B200 path")
     eng = engine or default_engine()
     batch = eng.upload(summands)
     try:
-        eff, tg, wd = eng.effective_subrank(batch, weights, eps, ov)
+        eff, tg, wd = eng.effective_subrank(batch, weights, eps, ov, strategy)
     finally:
         batch.free()
-    return SketchPlan(Strategy.Krp, eff, ov, tg, wd, eps, seed)
+    return SketchPlan(strategy, eff, ov, tg, wd, eps, seed)
 
 
 def krp_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[SumStats] = None,
             engine: Optional[Engine] = None) -> TuckerTensor:
     """KRP sketched summation (reference src/sketch.cpp:66-181 via krp_sum, :360-362)."""
+    return _sketched_sum(req, plan, stats, engine, Strategy.Krp)
+
+
+def kron_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[SumStats] = None,
+             engine: Optional[Engine] = None) -> TuckerTensor:
+    """Kronecker sketched summation (reference src/sketch.cpp:66-181 via kron_sum, :364-366)."""
+    return _sketched_sum(req, plan, stats, engine, Strategy.Kron)
+
+
+def _sketched_sum(req, plan, stats, engine, strategy):
     _validate_request(req.summands, req.weights)
     if req.eps < 0:
         raise ValueError("tolerance must be nonnegative")
@@ -634,13 +683,13 @@ def krp_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[
             ov = [int(req.oversampling)] * order
             if any(p < 0 for p in ov):
                 raise ValueError("oversampling must be nonnegative")
-            eff, tg, wd = eng.effective_subrank(batch, req.weights, req.eps, ov)
-            plan = SketchPlan(Strategy.Krp, eff, ov, tg, wd, req.eps, req.seed)
+            eff, tg, wd = eng.effective_subrank(batch, req.weights, req.eps, ov, strategy)
+            plan = SketchPlan(strategy, eff, ov, tg, wd, req.eps, req.seed)
         if len(plan.mode_sketch_dims) != order:
             raise ValueError("plan order does not match summand order")
         if any(s < 1 for s in plan.mode_sketch_dims):
             raise ValueError("plan sketch widths must be positive")
-        res = eng.krp_sum(batch, req.weights, plan.mode_sketch_dims, req.seed, req.eps, req.max_rank)
+        res = eng.krp_sum(batch, req.weights, plan.mode_sketch_dims, req.seed, req.eps, req.max_rank, strategy)
         out = res.to_tucker()
         res.free()
     finally:
@@ -653,8 +702,10 @@ def krp_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[
 
 def round_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[SumStats] = None,
               engine: Optional[Engine] = None) -> TuckerTensor:
-    """Strategy dispatcher (reference src/sketch.cpp:368-376); only Krp is on the B200 path."""
+    """Strategy dispatcher (reference src/sketch.cpp:368-376); Krp and Kron are on the B200 path."""
     if req.strategy == Strategy.Krp:
         return krp_sum(req, plan, stats, engine)
+    if req.strategy == Strategy.Kron:
+        return kron_sum(req, plan, stats, engine)
     _validate_request(req.summands, req.weights)
     raise NotImplementedError(f"strategy {strategy_name(req.strategy)} is outside the B200 hot path (SURVEY.md §8)")

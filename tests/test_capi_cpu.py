@@ -139,3 +139,32 @@ def test_cpp_host_caller_builds():
     assert r.returncode == 0, r.stderr
     assert "warning" not in r.stderr
     assert os.path.exists(os.path.join(root, "tests", "cpp", "capi_host"))
+
+
+def test_kron_sketch_dims_host_rule_matches_oracle():
+    """ts_kron_sketch_dims (host arithmetic behind the C ABI, no GPU needed) equals
+    the oracle's restatement of src/sketch.cpp:222-270 on the reference's frozen
+    cases (test_sketch_sum.cpp:159-184) and on 300 random instances."""
+    import oracle as O
+
+    assert T.kron_sketch_dims([4, 4, 4], [20, 20, 20]) == [2, 2, 2]
+    assert T.kron_sketch_dims([10, 2, 2], [30, 30, 30]) == [1, 4, 4]
+    assert T.kron_sketch_dims([3, 3, 3], [9, 9, 9]) == [2, 2, 2]
+    assert T.kron_sketch_dims([2, 8, 8], [2, 10, 10]) == [2, 4, 4]
+    for bad in (([5, 2, 2], [6, 2, 2]), ([2], [4]), ([0, 2], [4, 4])):
+        with pytest.raises(ValueError):
+            T.kron_sketch_dims(*bad)
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        order = int(rng.integers(2, 6))
+        dims = [int(x) for x in rng.integers(1, 40, size=order)]
+        targets = [int(rng.integers(1, min(d, T.complement_product(dims, n)) + 1)) for n, d in enumerate(dims)]
+        assert T.kron_sketch_dims(targets, dims) == O.kron_sketch_dims(targets, dims)
+
+
+def test_kron_plan_report_lists_complement_widths():
+    """test_sketch_sum.cpp:549-557."""
+    plan = T.SketchPlan(T.Strategy.Kron, [2, 3, 2], [2, 2, 2], [4, 5, 4], [2, 2, 3], 1e-6, T.RngSeed(95, 0))
+    text = plan.report()
+    for key in ("kron", "mode 1:", "mode 3:", "sketch_dim=", "complement_width=6"):
+        assert key in text
