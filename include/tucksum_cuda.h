@@ -21,6 +21,11 @@
  *                           (include/tucksum/sketch.hpp:89-90, src/sketch.cpp:66-181,364-366)
  *   ts_effective_subrank_kron ← effective_subrank(..., Strategy::Kron, ...) (src/sketch.cpp:272-349)
  *   ts_kron_sketch_dims   ← kron_sketch_dims (src/sketch.cpp:222-270)
+ *   ts_lazy_sum           ← round_sum with Strategy::Lazy = tucker_rounding(formal_sum(...), eps)
+ *                           (src/sketch.cpp:48-50, src/tucker.cpp:132-159,285-296)
+ *   ts_tucker_norm        ← tucker_norm(formal_sum(...)) (src/tucker.cpp:132-159)
+ *   ts_tucker_inner       ← tucker_inner (src/tucker.cpp:161-181), weighted over two batches
+ *   ts_rel_error_to_sum   ← tucker_rel_error(x, formal_sum(summands, weights)) (src/tucker.cpp:298-303)
  *   ts_substream          ← RngSeed::substream (include/tucksum/types.hpp:17-24, src/kernels.cpp:23-25)
  *   ts_gaussian_matrix    ← gaussian_matrix (src/kernels.cpp:88-101)
  *   status codes          ← std::invalid_argument / std::runtime_error thrown by
@@ -120,6 +125,26 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
  * arguments as ts_krp_sum. */
 int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
                 uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
+/* Lazy rounding of the formal sum (the paper's deterministic baseline):
+ * orthogonalize the stacked factors (thin QR of F_n), absorb R_n into the block
+ * cores, st_hosvd(eps [, max_rank]) and Q·P — on the device, through the same
+ * stage D-H kernels as ts_krp_sum.  Needs sum_k ranks_n^(k) <= 96 per mode and
+ * order >= 2; not available with a NCCL communicator. */
+int ts_lazy_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps, const int64_t* max_rank,
+                ts_result** out);
+/* ‖Σ_k w_k X_k‖_F by the reference's orthogonalized-core norm (thin QR of every
+ * stacked factor, R absorbed into the block cores): accurate for cancelling
+ * sums; same size limits as ts_lazy_sum. */
+int ts_tucker_norm(ts_ctx* ctx, const ts_batch* batch, const double* weights, double* out);
+/* Σ_{a,b} wx_a wy_b <X_a, Y_b> by per-block Gram contractions (the reference's
+ * tucker_inner, no densification, any size): one cross-Gram DMMA GEMM per mode
+ * plus one stage-F projection per block of x. */
+int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_batch* y, const double* wy,
+                    double* out);
+/* ‖r − Σ_k w_k X_k‖ / ‖Σ_k w_k X_k‖ through ts_tucker_inner expansions
+ * (‖r‖² − 2<r, S> + ‖S‖²): meant for large sums (config 5); resolves relative
+ * errors down to ~1e-6 (fp64 cancellation below that). */
+int ts_rel_error_to_sum(ts_ctx* ctx, const ts_result* r, const ts_batch* batch, const double* weights, double* out);
 /* Kron widths for per-mode targets (host arithmetic, bit-identical rule). */
 int ts_kron_sketch_dims(int64_t order, const int64_t* targets, const int64_t* dims, int64_t* out_widths);
 /* Independent sums in one call (SURVEY.md §8(f) row 2 — one round_sum per NDG

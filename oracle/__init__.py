@@ -286,6 +286,38 @@ def krp_sum(summands, weights, widths=None, seed=(0, 0), eps=1e-8, cap=None, ove
         L.or_result_free(h)
 
 
+def _result(h, order_hint=None):
+    L = lib()
+    try:
+        order = L.or_result_order(h)
+        dims = np.zeros(order, dtype=np.int64)
+        ranks = np.zeros(order, dtype=np.int64)
+        L.or_result_dims(h, dims.ctypes.data_as(i64p))
+        L.or_result_ranks(h, ranks.ctypes.data_as(i64p))
+        factors = []
+        for k in range(order):
+            f = np.zeros((dims[k], ranks[k]), order="F")
+            L.or_result_factor(h, i64(k), _p(f))
+            factors.append(f)
+        core = np.zeros(tuple(ranks), order="F")
+        L.or_result_core(h, _p(core))
+        return OracleTucker(core, factors)
+    finally:
+        L.or_result_free(h)
+
+
+def lazy_sum(summands, weights, eps, cap=None):
+    """Oracle lazy_sum: tucker_rounding(formal_sum(summands, weights), eps) (reference
+    src/sketch.cpp:48-50, src/tucker.cpp:285-296)."""
+    views = _Views(summands)
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    capa = None if cap is None else np.ascontiguousarray(np.asarray(cap, dtype=np.int64))
+    h = C.c_void_p()
+    _check(lib().or_lazy_sum(views.arr, i64(len(summands)), _p(w) if len(w) else dptr(), C.c_double(eps),
+                             capa.ctypes.data_as(i64p) if capa is not None else None, C.byref(h)))
+    return _result(h)
+
+
 def kron_sum(summands, weights, widths=None, **kw):
     """Oracle kron_sum (reference src/sketch.cpp:364-366)."""
     return krp_sum(summands, weights, widths, strategy="kron", **kw)

@@ -754,6 +754,16 @@ StHosvd st_hosvd(Tensor g, double tau, const Index* cap) {
     return out;
 }
 
+// src/tucker.cpp:285-296 (Lazy rounding), plus the optional rank cap.
+Tucker tucker_rounding(const Tucker& x, double tau, const Index* cap) {
+    if (tau < 0.0) throw std::invalid_argument("tucker_rounding: tolerance must be nonnegative");
+    Orthogonalized o = orthogonalize(x);
+    StHosvd st = st_hosvd(std::move(o.core), tau, cap);
+    std::vector<Mat> factors(static_cast<size_t>(x.order()));
+    for (size_t k = 0; k < factors.size(); ++k) factors[k] = matmul(o.q[k], false, st.factors[k], false);
+    return make_dense_tucker(std::move(st.core), std::move(factors));
+}
+
 void validate_request(const std::vector<const Tucker*>& xs, const std::vector<double>& ws) {
     // src/sketch.cpp:16-30.
     if (xs.empty() || xs.size() != ws.size())
@@ -1229,6 +1239,21 @@ int or_krp_sum(const OrTuckerView* views, std::int64_t count, const double* weig
                const std::int64_t* cap, int threads, int keep_intermediates, void** out) {
     return or_sketched_sum(views, count, weights, widths, oversampling, seed, stream, eps, cap, threads,
                            keep_intermediates, 1, out);
+}
+
+// lazy_sum (src/sketch.cpp:48-50): tucker_rounding(formal_sum(summands, weights), eps).
+int or_lazy_sum(const OrTuckerView* views, std::int64_t count, const double* weights, double eps,
+                const std::int64_t* cap, void** out) {
+    return guarded([&] {
+        std::vector<oracle::Tucker> xs = views_to_tuckers(views, count);
+        std::vector<const oracle::Tucker*> ptrs;
+        for (auto& x : xs) ptrs.push_back(&x);
+        std::vector<double> ws(weights, weights + std::max<std::int64_t>(count, 0));
+        auto res = std::make_unique<OrResult>();
+        res->t = oracle::tucker_rounding(oracle::formal_sum(ptrs, ws), eps, cap);
+        res->widths.assign(res->t.ranks.size(), 0);
+        *out = res.release();
+    });
 }
 
 int or_kron_sketch_dims(std::int64_t order, const std::int64_t* targets, const std::int64_t* dims, std::int64_t* out) {

@@ -395,30 +395,246 @@ void kron_stage_b(const ts_batch* b, double* const* Z, const std::int64_t* ow, d
     }
 }
 
-// krp = true: krp_sum → sketched_sum(krp=true); krp = false: kron_sum →
-// sketched_sum(krp=false) (src/sketch.cpp:66-181,360-366).  The two differ in the
-// Ω widths (uniform s vs plan widths), stage B and the sketch width of Y_n
-// (s vs C_n = Π_{j≠n} s_j); everything from stage D on is shared.
+// Stages F1 + F2 (src/sketch.cpp:152-169): h = Σ_atoms w_b · G_b ×_n P_n[:, cols_b]
+// for given projections P_n (q_n × R_n, ld q_n).  Order 3 fuses the chain per
+// core slice (ttm3.cu); other orders run a per-atom grouped GEMM chain.  The sum
+// over atoms is the K dimension of the final GEMM (deterministic split-K).
+double* project_core(ts_ctx* ctx, const ts_batch* b, double* const* P, const std::int64_t* q, const double* d_w,
+                     const double* weights, CallScratch& sc, std::int64_t* hsize) {
+    const int d = b->order;
+    // ---- Stage F1: per-atom multi-TTM over modes 0..d-2 into T_stack (Q' × R_{d-1})
+    std::int64_t Qp = 1;
+    for (int j = 0; j < d - 1; ++j) Qp *= q[j];
+    double* Tstack = sc.alloc_n<double>(static_cast<size_t>(Qp * b->R[d - 1]));
+    bool f1_done = false;
+    if (d == 3) {  // fused per-slice chain (ttm3.cu)
+        ts::Ttm3Args ta{};
+        for (int n = 0; n < d; ++n) {
+            ta.P[n] = P[n];
+            ta.q[n] = q[n];
+        }
+        ta.atoms = b->d_atoms;
+        ta.cores = b->cores;
+        ta.weights = d_w;
+        ta.Tstack = Tstack;
+        ta.Qp = Qp;
+        ta.natoms = static_cast<int>(b->atoms.size());
+        int max_r2 = 0;
+        for (const auto& at : b->atoms) max_r2 = std::max(max_r2, at.shape[2]);
+        f1_done = ts::launch_ttm3(ta, b->max_shape, max_r2, sc);
+    }
+    if (!f1_done) {
+        const size_t na = b->atoms.size();
+        std::vector<double*> cur(na), nxt(na);
+        for (int m = 0; m <= d - 2; ++m) {
+            const bool last = (m == d - 2);
+            double* outbuf = nullptr;
+            std::vector<std::int64_t> outoff(na);
+            if (!last) {
+                std::int64_t tot = 0;
+                for (size_t a = 0; a < na; ++a) {
+                    std::int64_t e = 1;
+                    for (int j = 0; j <= m; ++j) e *= q[j];
+                    for (int j = m + 1; j < d; ++j) e *= b->atoms[a].shape[j];
+                    outoff[a] = tot;
+                    tot += e;
+                }
+                outbuf = sc.alloc_n<double>(static_cast<size_t>(tot));
+            }
+            std::vector<GemmProblem> ps;
+            ps.reserve(na);
+            for (size_t a = 0; a < na; ++a) {
+                const ts::Atom& at = b->atoms[a];
+                double* out = last ? Tstack + static_cast<std::int64_t>(at.col[d - 1]) * Qp : outbuf + outoff[a];
+                const double alpha = last ? weights[at.summand] : 1.0;
+                std::int64_t left = 1, right = 1;
+                for (int j = 0; j < m; ++j) left *= q[j];
+                for (int j = m + 1; j < d; ++j) right *= at.shape[j];
+                GemmProblem p{};
+                p.alpha = alpha;
+                if (m == 0) {
+                    // out (q0 × right) = P_0[:, cols] (q0 × r0) · G_(0) (r0 × right)
+                    p.A = P[0] + static_cast<std::int64_t>(at.col[0]) * q[0];
+                    p.lda = q[0];
+                    p.B = b->cores + at.core_off;
+                    p.ldb = at.shape[0];
+                    p.C = out;
+                    p.ldc = q[0];
+                    p.M = static_cast<int>(q[0]);
+                    p.N = static_cast<int>(right);
+                    p.K = at.shape[0];
+                } else {
+                    // per right slice: out (left × q_m) = T (left × r_m) · P_m[:, cols]ᵀ
+                    p.A = cur[a];
+                    p.lda = left;
+                    p.sA = left * at.shape[m];
+                    p.B = P[m] + static_cast<std::int64_t>(at.col[m]) * q[m];
+                    p.ldb = q[m];
+                    p.sB = 0;
+                    p.C = out;
+                    p.ldc = left;
+                    p.sC = left * q[m];
+                    p.M = static_cast<int>(left);
+                    p.N = static_cast<int>(q[m]);
+                    p.K = at.shape[m];
+                    p.batch = static_cast<int>(right);
+                }
+                ps.push_back(p);
+                nxt[a] = out;
+            }
+            ts::launch_grouped_gemm(m == 0 ? Layout::NN : Layout::NT, ps, sc, ctx->num_sms);
+            std::swap(cur, nxt);
+        }
+    }
+    mark(ctx, 7);
+    // ---- Stage F2: h (Q' × q_{d-1}) = T_stack · P_{d-1}ᵀ
+    *hsize = Qp * q[d - 1];
+    double* h = sc.alloc_n<double>(static_cast<size_t>(*hsize));
+    {
+        GemmProblem p{};
+        p.A = Tstack;
+        p.lda = Qp;
+        p.B = P[d - 1];
+        p.ldb = q[d - 1];
+        p.C = h;
+        p.ldc = Qp;
+        p.M = static_cast<int>(Qp);
+        p.N = static_cast<int>(q[d - 1]);
+        p.K = static_cast<int>(b->R[d - 1]);
+        ts::launch_grouped_gemm(Layout::NT, {p}, sc, ctx->num_sms);
+    }
+    return h;
+}
+
+enum class Method { Krp, Kron, Lazy };
+
+// Σ_{a∈X, b∈Y} wX_a wY_b ⟨X_a, Y_b⟩ over the atoms of two device batches — the
+// reference's tucker_inner (src/tucker.cpp:161-181) with weights, restated for the
+// stacked layout: one cross-Gram per mode, M_n = F^Xᵀ_n F^Y_n (one grouped DMMA
+// GEMM), then per atom a of X the rows of M_n that belong to it act as stage-E
+// projections: h_a = Σ_b wY_b G_b ×_n M_n[a, b] (stage F kernels), and
+// ⟨G_a, h_a⟩ is accumulated in atom order (deterministic).
+double inner_impl(ts_ctx* ctx, const ts_batch* X, const double* wX, const ts_batch* Y, const double* wY) {
+    if (!X || !Y || !wX || !wY) invalid("tucker_inner: null operand");
+    if (X->order != Y->order) invalid("tucker_inner: operands must share dims");
+    const int d = X->order;
+    for (int n = 0; n < d; ++n)
+        if (X->dims[n] != Y->dims[n]) invalid("tucker_inner: operands must share dims");
+    TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+    ctx->stage.reset();
+    cudaStream_t st = ctx->stream;
+    CallScratch sc(st, ctx->stage);
+    auto* d_wY = static_cast<double*>(sc.upload(wY, sizeof(double) * static_cast<size_t>(Y->count)));
+    double* M[TS_MAX_ORDER];
+    {
+        std::vector<GemmProblem> ps;
+        for (int n = 0; n < d; ++n) {
+            M[n] = sc.alloc_n<double>(static_cast<size_t>(X->R[n] * Y->R[n]));
+            GemmProblem p{};
+            p.A = X->F[n];
+            p.lda = X->dims[n];
+            p.B = Y->F[n];
+            p.ldb = Y->dims[n];
+            p.C = M[n];
+            p.ldc = X->R[n];
+            p.M = static_cast<int>(X->R[n]);
+            p.N = static_cast<int>(Y->R[n]);
+            p.K = static_cast<int>(X->dims[n]);
+            ps.push_back(p);
+        }
+        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+    }
+    double* acc = sc.alloc_n<double>(1);
+    TS_CUDA_CHECK(cudaMemsetAsync(acc, 0, sizeof(double), st));
+    for (const ts::Atom& a : X->atoms) {
+        CallScratch it(st, ctx->stage);  // per-atom buffers go back to the pool each iteration
+        double* P[TS_MAX_ORDER];
+        std::int64_t q[TS_MAX_ORDER];
+        for (int n = 0; n < d; ++n) {
+            q[n] = a.shape[n];
+            P[n] = it.alloc_n<double>(static_cast<size_t>(q[n] * Y->R[n]));
+            TS_CUDA_CHECK(cudaMemcpy2DAsync(P[n], sizeof(double) * static_cast<size_t>(q[n]), M[n] + a.col[n],
+                                            sizeof(double) * static_cast<size_t>(X->R[n]),
+                                            sizeof(double) * static_cast<size_t>(q[n]), static_cast<size_t>(Y->R[n]),
+                                            cudaMemcpyDeviceToDevice, st));
+        }
+        std::int64_t hs = 0;
+        double* h = project_core(ctx, Y, P, q, d_wY, wY, it, &hs);
+        ts::launch_dot_accumulate(X->cores + a.core_off, h, hs, wX[a.summand], acc, it);
+        sc.launches += it.launches;
+    }
+    double out = 0.0;
+    TS_CUDA_CHECK(cudaMemcpyAsync(&out, acc, sizeof(double), cudaMemcpyDeviceToHost, st));
+    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    ctx->launches += sc.launches;
+    return out;
+}
+
+// A result as a one-summand batch (non-owning view of its device factors and core).
+struct ResultView {
+    ts_batch b;
+    explicit ResultView(ts_ctx* ctx, const ts_result* r) {
+        b.ctx = ctx;
+        b.order = r->order;
+        b.count = 1;
+        ts::Atom at{};
+        std::int64_t core = 1;
+        for (int n = 0; n < r->order; ++n) {
+            b.dims[n] = r->dims[n];
+            b.R[n] = r->ranks[n];
+            b.F[n] = r->factors[n];
+            at.col[n] = 0;
+            at.shape[n] = static_cast<int>(r->ranks[n]);
+            b.max_shape = std::max(b.max_shape, at.shape[n]);
+            core *= r->ranks[n];
+        }
+        b.cores = r->core;
+        b.core_elems = core;
+        b.atoms.push_back(at);
+        TS_CUDA_CHECK(cudaMallocAsync(&b.d_atoms, sizeof(ts::Atom), ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(b.d_atoms, &b.atoms[0], sizeof(ts::Atom), cudaMemcpyHostToDevice, ctx->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+    ~ResultView() { cudaFreeAsync(b.d_atoms, b.ctx->stream); }
+};
+
+// Krp: krp_sum → sketched_sum(krp=true); Kron: kron_sum → sketched_sum(krp=false)
+// (src/sketch.cpp:66-181,360-366).  The two differ in the Ω widths (uniform s vs
+// plan widths), stage B and the sketch width of Y_n (s vs C_n = Π_{j≠n} s_j);
+// everything from stage D on is shared.  Lazy: tucker_rounding(formal_sum(...))
+// (src/sketch.cpp:48-50, src/tucker.cpp:132-159,285-296): the "sketch" Y_n is the
+// stacked factor F_n itself (Y_n = F_n, no Ω, stages A-C skipped), so stage D is
+// orthogonalize's QR of F_n, stage E gives its R factor (P_n = Q_nᵀF_n), stage F
+// absorbs R into the block cores, and stages G/H are the rounding's st_hosvd and
+// Q·P.  Needs Σ_k r_n^(k) ≤ 96.
 ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
                              std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank,
-                             bool krp, bool allow_spec = true) {
+                             Method method, bool allow_spec = true, double* norm_out = nullptr) {
+    const bool krp = method == Method::Krp, lazy = method == Method::Lazy;
     // Validation mirrors src/sketch.cpp:16-30,66-87.
     if (b == nullptr || b->count < 1) invalid("sum request needs matching, nonempty summands and weights");
     if (weights == nullptr) invalid("sum request needs matching, nonempty summands and weights");
     if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
     const int d = b->order;
-    if (d < 2) invalid("sketched summation needs order >= 2");
-    if (widths == nullptr) invalid("plan order does not match summand order");
-    for (int n = 0; n < d; ++n)
-        if (widths[n] < 1) invalid("plan sketch widths must be positive");
-    const std::int64_t s = *std::max_element(widths, widths + d);
+    if (d < 2) {
+        if (lazy) throw ts::Error(TS_UNSUPPORTED, "lazy rounding of first-order tensors is not on the device path");
+        invalid("sketched summation needs order >= 2");
+    }
+    std::int64_t s = 0;
+    if (!lazy) {
+        if (widths == nullptr) invalid("plan order does not match summand order");
+        for (int n = 0; n < d; ++n)
+            if (widths[n] < 1) invalid("plan sketch widths must be positive");
+        s = *std::max_element(widths, widths + d);
+    }
     std::int64_t ow[TS_MAX_ORDER], yc[TS_MAX_ORDER];  // Ω_n widths, Y_n widths
     for (int n = 0; n < d; ++n) {
-        ow[n] = krp ? s : widths[n];
-        yc[n] = krp ? s : complement_product(widths, d, n);
+        ow[n] = lazy ? 0 : krp ? s : widths[n];
+        yc[n] = lazy ? b->R[n] : krp ? s : complement_product(widths, d, n);
         if (yc[n] > ts::max_tsqr_cols())
-            throw ts::Error(TS_UNSUPPORTED, "sketch width " + std::to_string(yc[n]) +
-                                                " exceeds the supported maximum of " + std::to_string(ts::max_tsqr_cols()));
+            throw ts::Error(TS_UNSUPPORTED, std::string(lazy ? "stacked rank " : "sketch width ") +
+                                                std::to_string(yc[n]) + " exceeds the supported maximum of " +
+                                                std::to_string(ts::max_tsqr_cols()));
     }
     for (std::int64_t i = 0; i < b->count; ++i)
         if (!std::isfinite(weights[i])) invalid("weights must be finite");
@@ -434,7 +650,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     }
     mark(ctx, 0);
 
-    double* omega = omega_get(ctx, d, dims, ow, seed, stream);
+    double* omega = lazy ? nullptr : omega_get(ctx, d, dims, ow, seed, stream);
     std::int64_t q[TS_MAX_ORDER];
     std::int64_t ooff[TS_MAX_ORDER], yoff[TS_MAX_ORDER];
     std::int64_t ytot = 0, acc = 0;
@@ -447,67 +663,76 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     }
     auto* d_w = static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
 
-    // ---- Stage A: Z_j = Ω_jᵀ F_j (s × R_j)
-    double* Z[TS_MAX_ORDER];
-    {
-        std::vector<GemmProblem> ps;
-        for (int j = 0; j < d; ++j) {
-            Z[j] = sc.alloc_n<double>(static_cast<size_t>(ow[j] * b->R[j]));
-            GemmProblem p{};
-            p.A = omega + ooff[j];
-            p.lda = dims[j];
-            p.B = b->F[j];
-            p.ldb = dims[j];
-            p.C = Z[j];
-            p.ldc = ow[j];
-            p.M = static_cast<int>(ow[j]);
-            p.N = static_cast<int>(b->R[j]);
-            p.K = static_cast<int>(dims[j]);
-            ps.push_back(p);
-        }
-        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
-    }
-    mark(ctx, 1);
-    // ---- Stage B: W_n (R_n × s), stored transposed
-    double* W[TS_MAX_ORDER];
-    if (!krp) {
-        for (int n = 0; n < d; ++n) W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * yc[n]));
-        kron_stage_b(b, Z, ow, W, yc, d_w, sc, ctx->num_sms);
-    } else {
-        ts::KrpArgs ka{};
-        for (int n = 0; n < d; ++n) {
-            W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * s));
-            ka.Z[n] = Z[n];
-            ka.W[n] = W[n];
-            ka.R[n] = b->R[n];
-        }
-        ka.order = d;
-        ka.s = static_cast<int>(s);
-        ka.natoms = static_cast<int>(b->atoms.size());
-        ka.atoms = b->d_atoms;
-        ka.cores = b->cores;
-        ka.weights = d_w;
-        ts::launch_krp_contract(ka, b->max_shape, sc);
-    }
-    mark(ctx, 2);
-    // ---- Stage C: Y_n = F_n W_n (n × s), all modes in one buffer
     double* Y = sc.alloc_n<double>(static_cast<size_t>(ytot));
-    {
-        std::vector<GemmProblem> ps;
-        for (int n = 0; n < d; ++n) {
-            GemmProblem p{};
-            p.A = b->F[n];
-            p.lda = dims[n];
-            p.B = W[n];  // stored transposed: Wt_n (yc_n × R_n)
-            p.ldb = yc[n];
-            p.C = Y + yoff[n];
-            p.ldc = dims[n];
-            p.M = static_cast<int>(dims[n]);
-            p.N = static_cast<int>(yc[n]);
-            p.K = static_cast<int>(b->R[n]);
-            ps.push_back(p);
+    if (lazy) {
+        // Y_n = F_n (copied: stage D factors its input in place).
+        for (int n = 0; n < d; ++n)
+            TS_CUDA_CHECK(cudaMemcpyAsync(Y + yoff[n], b->F[n], sizeof(double) * static_cast<size_t>(dims[n] * yc[n]),
+                                          cudaMemcpyDeviceToDevice, st));
+        mark(ctx, 1);
+        mark(ctx, 2);
+    } else {
+        // ---- Stage A: Z_j = Ω_jᵀ F_j (s × R_j)
+        double* Z[TS_MAX_ORDER];
+        {
+            std::vector<GemmProblem> ps;
+            for (int j = 0; j < d; ++j) {
+                Z[j] = sc.alloc_n<double>(static_cast<size_t>(ow[j] * b->R[j]));
+                GemmProblem p{};
+                p.A = omega + ooff[j];
+                p.lda = dims[j];
+                p.B = b->F[j];
+                p.ldb = dims[j];
+                p.C = Z[j];
+                p.ldc = ow[j];
+                p.M = static_cast<int>(ow[j]);
+                p.N = static_cast<int>(b->R[j]);
+                p.K = static_cast<int>(dims[j]);
+                ps.push_back(p);
+            }
+            ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
         }
-        ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+        mark(ctx, 1);
+        // ---- Stage B: W_n (R_n × s), stored transposed
+        double* W[TS_MAX_ORDER];
+        if (!krp) {
+            for (int n = 0; n < d; ++n) W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * yc[n]));
+            kron_stage_b(b, Z, ow, W, yc, d_w, sc, ctx->num_sms);
+        } else {
+            ts::KrpArgs ka{};
+            for (int n = 0; n < d; ++n) {
+                W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * s));
+                ka.Z[n] = Z[n];
+                ka.W[n] = W[n];
+                ka.R[n] = b->R[n];
+            }
+            ka.order = d;
+            ka.s = static_cast<int>(s);
+            ka.natoms = static_cast<int>(b->atoms.size());
+            ka.atoms = b->d_atoms;
+            ka.cores = b->cores;
+            ka.weights = d_w;
+            ts::launch_krp_contract(ka, b->max_shape, sc);
+        }
+        mark(ctx, 2);
+        // ---- Stage C: Y_n = F_n W_n (n × s), all modes in one buffer
+        {
+            std::vector<GemmProblem> ps;
+            for (int n = 0; n < d; ++n) {
+                GemmProblem p{};
+                p.A = b->F[n];
+                p.lda = dims[n];
+                p.B = W[n];  // stored transposed: Wt_n (yc_n × R_n)
+                p.ldb = yc[n];
+                p.C = Y + yoff[n];
+                p.ldc = dims[n];
+                p.M = static_cast<int>(dims[n]);
+                p.N = static_cast<int>(yc[n]);
+                p.K = static_cast<int>(b->R[n]);
+                ps.push_back(p);
+            }
+            ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+        }
     }
     mark(ctx, 3);
     if (ctx->comm) nccl_check(nccl_api().AllReduce(Y, Y, static_cast<size_t>(ytot), ncclFloat64, ncclSum, ctx->comm, st),
@@ -519,7 +744,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     res->order = d;
     if (ctx->debug) {
         for (int n = 0; n < d; ++n) {
-            copy_to_host(res->inter[0][n], omega + ooff[n], dims[n] * ow[n], st);
+            if (omega) copy_to_host(res->inter[0][n], omega + ooff[n], dims[n] * ow[n], st);
             res->inter_rows[0][n] = dims[n];
             res->inter_cols[0][n] = ow[n];
             copy_to_host(res->inter[1][n], Y + yoff[n], dims[n] * yc[n], st);
@@ -662,111 +887,22 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
     }
     mark(ctx, 6);
-    // ---- Stage F1: per-atom multi-TTM over modes 0..d-2 into T_stack (Q' × R_{d-1})
-    std::int64_t Qp = 1;
-    for (int j = 0; j < d - 1; ++j) Qp *= q[j];
-    double* Tstack = sc.alloc_n<double>(static_cast<size_t>(Qp * b->R[d - 1]));
-    bool f1_done = false;
-    if (d == 3) {  // fused per-slice chain (ttm3.cu)
-        ts::Ttm3Args ta{};
-        for (int n = 0; n < d; ++n) {
-            ta.P[n] = P[n];
-            ta.q[n] = q[n];
-        }
-        ta.atoms = b->d_atoms;
-        ta.cores = b->cores;
-        ta.weights = d_w;
-        ta.Tstack = Tstack;
-        ta.Qp = Qp;
-        ta.natoms = static_cast<int>(b->atoms.size());
-        int max_r2 = 0;
-        for (const auto& at : b->atoms) max_r2 = std::max(max_r2, at.shape[2]);
-        f1_done = ts::launch_ttm3(ta, b->max_shape, max_r2, sc);
-    }
-    if (!f1_done) {
-        const size_t na = b->atoms.size();
-        std::vector<double*> cur(na), nxt(na);
-        for (int m = 0; m <= d - 2; ++m) {
-            const bool last = (m == d - 2);
-            double* outbuf = nullptr;
-            std::vector<std::int64_t> outoff(na);
-            if (!last) {
-                std::int64_t tot = 0;
-                for (size_t a = 0; a < na; ++a) {
-                    std::int64_t e = 1;
-                    for (int j = 0; j <= m; ++j) e *= q[j];
-                    for (int j = m + 1; j < d; ++j) e *= b->atoms[a].shape[j];
-                    outoff[a] = tot;
-                    tot += e;
-                }
-                outbuf = sc.alloc_n<double>(static_cast<size_t>(tot));
-            }
-            std::vector<GemmProblem> ps;
-            ps.reserve(na);
-            for (size_t a = 0; a < na; ++a) {
-                const ts::Atom& at = b->atoms[a];
-                double* out = last ? Tstack + static_cast<std::int64_t>(at.col[d - 1]) * Qp : outbuf + outoff[a];
-                const double alpha = last ? weights[at.summand] : 1.0;
-                std::int64_t left = 1, right = 1;
-                for (int j = 0; j < m; ++j) left *= q[j];
-                for (int j = m + 1; j < d; ++j) right *= at.shape[j];
-                GemmProblem p{};
-                p.alpha = alpha;
-                if (m == 0) {
-                    // out (q0 × right) = P_0[:, cols] (q0 × r0) · G_(0) (r0 × right)
-                    p.A = P[0] + static_cast<std::int64_t>(at.col[0]) * q[0];
-                    p.lda = q[0];
-                    p.B = b->cores + at.core_off;
-                    p.ldb = at.shape[0];
-                    p.C = out;
-                    p.ldc = q[0];
-                    p.M = static_cast<int>(q[0]);
-                    p.N = static_cast<int>(right);
-                    p.K = at.shape[0];
-                } else {
-                    // per right slice: out (left × q_m) = T (left × r_m) · P_m[:, cols]ᵀ
-                    p.A = cur[a];
-                    p.lda = left;
-                    p.sA = left * at.shape[m];
-                    p.B = P[m] + static_cast<std::int64_t>(at.col[m]) * q[m];
-                    p.ldb = q[m];
-                    p.sB = 0;
-                    p.C = out;
-                    p.ldc = left;
-                    p.sC = left * q[m];
-                    p.M = static_cast<int>(left);
-                    p.N = static_cast<int>(q[m]);
-                    p.K = at.shape[m];
-                    p.batch = static_cast<int>(right);
-                }
-                ps.push_back(p);
-                nxt[a] = out;
-            }
-            ts::launch_grouped_gemm(m == 0 ? Layout::NN : Layout::NT, ps, sc, ctx->num_sms);
-            std::swap(cur, nxt);
-        }
-    }
-    mark(ctx, 7);
-    // ---- Stage F2: h (Q' × q_{d-1}) = T_stack · P_{d-1}ᵀ
-    const std::int64_t hsize = Qp * q[d - 1];
-    double* h = sc.alloc_n<double>(static_cast<size_t>(hsize));
-    {
-        GemmProblem p{};
-        p.A = Tstack;
-        p.lda = Qp;
-        p.B = P[d - 1];
-        p.ldb = q[d - 1];
-        p.C = h;
-        p.ldc = Qp;
-        p.M = static_cast<int>(Qp);
-        p.N = static_cast<int>(q[d - 1]);
-        p.K = static_cast<int>(b->R[d - 1]);
-        ts::launch_grouped_gemm(Layout::NT, {p}, sc, ctx->num_sms);
-    }
+    std::int64_t hsize = 0;
+    double* h = project_core(ctx, b, P, q, d_w, weights, sc, &hsize);
     mark(ctx, 8);
     if (ctx->comm) nccl_check(nccl_api().AllReduce(h, h, static_cast<size_t>(hsize), ncclFloat64, ncclSum, ctx->comm, st),
                               "ncclAllReduce(h)");
     mark(ctx, 9);
+    if (norm_out) {  // tucker_norm: ‖orthogonalized core‖ (src/tucker.cpp:159), no rounding
+        double* d_ss = sc.alloc_n<double>(1);
+        ts::launch_sumsq(h, hsize, d_ss, sc);
+        double ss = 0.0;
+        TS_CUDA_CHECK(cudaMemcpyAsync(&ss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        ctx->launches += sc.launches;
+        *norm_out = std::sqrt(ss);
+        return nullptr;
+    }
     if (ctx->debug) {
         for (int n = 0; n < d; ++n) {
             copy_to_host(res->inter[2][n], Uh[n], dims[n] * q[n], st);
@@ -935,7 +1071,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             if (x != 0) {
                 ctx->spec_ok = false;
                 res.reset();
-                return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, krp, false);
+                return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method, false);
             }
     } else {
         ctx->spec_ok = ctx->last_qr_fallbacks == 0 && ctx->last_svd_fallbacks == 0;
@@ -1197,7 +1333,7 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_krp_sum: null argument");
-        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, true);
+        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Krp);
     });
 }
 
@@ -1205,7 +1341,45 @@ int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const
                 uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_kron_sum: null argument");
-        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, false);
+        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Kron);
+    });
+}
+
+int ts_tucker_norm(ts_ctx* ctx, const ts_batch* batch, const double* weights, double* out) {
+    return guarded([&] {
+        if (!ctx || !out) invalid("ts_tucker_norm: null argument");
+        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "tucker_norm does not shard: use a context without NCCL");
+        sketched_sum_impl(ctx, batch, weights, nullptr, 0, 0, 0.0, nullptr, Method::Lazy, false, out);
+    });
+}
+
+int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_batch* y, const double* wy,
+                    double* out) {
+    return guarded([&] {
+        if (!ctx || !out) invalid("ts_tucker_inner: null argument");
+        *out = inner_impl(ctx, x, wx, y, wy);
+    });
+}
+
+int ts_rel_error_to_sum(ts_ctx* ctx, const ts_result* r, const ts_batch* batch, const double* weights, double* out) {
+    return guarded([&] {
+        if (!ctx || !r || !out) invalid("ts_rel_error_to_sum: null argument");
+        ResultView rv(ctx, r);
+        const double one = 1.0;
+        const double xx = inner_impl(ctx, &rv.b, &one, &rv.b, &one);
+        const double xs = inner_impl(ctx, &rv.b, &one, batch, weights);
+        const double ss = inner_impl(ctx, batch, weights, batch, weights);
+        const double diff = std::sqrt(std::max(xx - 2.0 * xs + ss, 0.0));
+        *out = ss > 0.0 ? diff / std::sqrt(ss) : diff;  // src/tucker.cpp:298-303
+    });
+}
+
+int ts_lazy_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps, const int64_t* max_rank,
+                ts_result** out) {
+    return guarded([&] {
+        if (!ctx || !out) invalid("ts_lazy_sum: null argument");
+        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "lazy rounding does not shard: use a context without NCCL");
+        *out = sketched_sum_impl(ctx, batch, weights, nullptr, 0, 0, eps, max_rank, Method::Lazy);
     });
 }
 
@@ -1226,7 +1400,7 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
         if (count == 0) return;
         if (ctx->comm || count == 1 || lanes <= 1) {
             for (int64_t i = 0; i < count; ++i)
-                out[i] = sketched_sum_impl(ctx, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, true);
+                out[i] = sketched_sum_impl(ctx, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, Method::Krp);
             return;
         }
         const int L = static_cast<int>(std::min<int64_t>(std::min(lanes, 16), count));
@@ -1247,7 +1421,7 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
                 codes[static_cast<size_t>(t)] = guarded([&] {
                     TS_CUDA_CHECK(cudaSetDevice(lane->device));
                     for (int64_t i = t; i < count; i += L)
-                        out[i] = sketched_sum_impl(lane, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, true);
+                        out[i] = sketched_sum_impl(lane, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, Method::Krp);
                 });
                 if (codes[static_cast<size_t>(t)] != TS_OK) errs[static_cast<size_t>(t)] = g_err;
             });

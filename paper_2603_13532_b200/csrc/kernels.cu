@@ -1160,4 +1160,28 @@ void launch_kron_gather(const std::vector<KronGather>& g, int64_t C, double* Wt,
     sc.launches += 1;
 }
 
+namespace {
+// acc[0] += alpha · Σ x_i y_i, one CTA, fixed reduction order (deterministic).
+__global__ void __launch_bounds__(256) dot_accumulate_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                            int64_t n, double alpha, double* __restrict__ acc) {
+    __shared__ double part[8];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s = fma(x[i], y[i], s);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += part[w];
+        acc[0] += alpha * t;
+    }
+}
+}  // namespace
+
+void launch_dot_accumulate(const double* x, const double* y, int64_t n, double alpha, double* acc, CallScratch& sc) {
+    dot_accumulate_kernel<<<1, 256, 0, sc.stream()>>>(x, y, n, alpha, acc);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
 }  // namespace ts

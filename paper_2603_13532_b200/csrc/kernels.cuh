@@ -145,6 +145,9 @@ struct KronGather {
 void launch_kron_gather(const std::vector<KronGather>& g, int64_t C, double* Wt, const double* weights,
                         CallScratch& sc);
 
+// acc[0] += alpha · <x, y> (single CTA, deterministic; n ≲ 10^6).
+void launch_dot_accumulate(const double* x, const double* y, int64_t n, double alpha, double* acc, CallScratch& sc);
+
 int max_tsqr_cols();
 // Device buffer of the values-kernel phase probe (non-null iff TS_EIG_PROFILE is set).
 unsigned long long* eig_probe_buffer();

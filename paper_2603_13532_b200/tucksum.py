@@ -48,7 +48,8 @@ EXPORTED_SYMBOLS = [
     "ts_result_order", "ts_result_dims", "ts_result_ranks", "ts_result_factor", "ts_result_core",
     "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
-    "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron",
+    "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
+    "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum",
 ]
 
 
@@ -100,6 +101,10 @@ def lib():
         L.ts_krp_sum.argtypes = [C.c_void_p, C.c_void_p, dptr, i64p, u64, u64, C.c_double, i64p,
                                  C.POINTER(C.c_void_p)]
         L.ts_kron_sum.argtypes = L.ts_krp_sum.argtypes
+        L.ts_lazy_sum.argtypes = [C.c_void_p, C.c_void_p, dptr, C.c_double, i64p, C.POINTER(C.c_void_p)]
+        L.ts_tucker_norm.argtypes = [C.c_void_p, C.c_void_p, dptr, dptr]
+        L.ts_tucker_inner.argtypes = [C.c_void_p, C.c_void_p, dptr, C.c_void_p, dptr, dptr]
+        L.ts_rel_error_to_sum.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, dptr, dptr]
         L.ts_effective_subrank.argtypes = [C.c_void_p, C.c_void_p, dptr, C.c_double, i64p, i64p, i64p, i64p]
         L.ts_effective_subrank_kron.argtypes = L.ts_effective_subrank.argtypes
         L.ts_kron_sketch_dims.argtypes = [i64, i64p, i64p, i64p]
@@ -247,6 +252,67 @@ def formal_sum(xs: Sequence[TuckerTensor], weights: Sequence[float]) -> TuckerTe
             blocks.append(CoreBlock([shift[k] + b.offsets[k] for k in range(order)], b.data * float(w)))
         shift = [shift[k] + x.ranks[k] for k in range(order)]
     return TuckerTensor(ranks=ranks, blocks=blocks, factors=factors)
+
+
+def save_tucker(dst, x: TuckerTensor) -> None:
+    """Reference binary format (src/tucker.cpp:329-352): little-endian u64 order,
+    dims, ranks; each factor's column-major doubles; u64 block count; per block
+    u64 offsets, u64 extents and the column-major block data.  ``dst`` is a path
+    or a binary file object."""
+    import struct
+
+    def body(f):
+        u64s = lambda vals: f.write(struct.pack("<%dQ" % len(vals), *[int(v) for v in vals]))
+        u64s([len(x.dims)])
+        u64s(x.dims)
+        u64s(x.ranks)
+        for fac in x.factors:
+            f.write(np.asarray(fac, dtype="<f8").tobytes(order="F"))
+        u64s([len(x.blocks)])
+        for b in x.blocks:
+            u64s(b.offsets)
+            u64s(np.shape(b.data))
+            f.write(np.asarray(b.data, dtype="<f8").tobytes(order="F"))
+
+    if hasattr(dst, "write"):
+        body(dst)
+    else:
+        with open(dst, "wb") as f:
+            body(f)
+
+
+def load_tucker(src) -> TuckerTensor:
+    """Reads the format of save_tucker (reference src/tucker.cpp:354-383); a
+    truncated stream raises RuntimeError("load_tucker: truncated stream")."""
+    import struct
+
+    def body(f):
+        def read(n):
+            data = f.read(n)
+            if len(data) != n:
+                raise RuntimeError("load_tucker: truncated stream")
+            return data
+
+        def u64s(k):
+            return list(struct.unpack("<%dQ" % k, read(8 * k)))
+
+        order = u64s(1)[0]
+        if order == 0 or order > 32:
+            raise RuntimeError("load_tucker: implausible order")
+        dims, ranks = u64s(order), u64s(order)
+        factors = [np.frombuffer(read(8 * n * r), dtype="<f8").reshape((n, r), order="F").copy()
+                   for n, r in zip(dims, ranks)]
+        blocks = []
+        for _ in range(u64s(1)[0]):
+            off, shape = u64s(order), u64s(order)
+            data = np.frombuffer(read(8 * int(np.prod(shape))), dtype="<f8").reshape(shape, order="F").copy()
+            blocks.append(CoreBlock(off, data))
+        return TuckerTensor(ranks=ranks, blocks=blocks, factors=factors)
+
+    if hasattr(src, "read"):
+        return body(src)
+    with open(src, "rb") as f:
+        return body(f)
 
 
 def tucker_axby(alpha: float, x: TuckerTensor, beta: float, y: TuckerTensor) -> TuckerTensor:
@@ -567,6 +633,45 @@ class Engine:
     def kron_sum(self, batch: DeviceBatch, weights, widths, seed: RngSeed, eps: float, max_rank=None) -> DeviceResult:
         return self.krp_sum(batch, weights, widths, seed, eps, max_rank, Strategy.Kron)
 
+    def tucker_norm(self, batch: DeviceBatch, weights) -> float:
+        """‖Σ w_k X_k‖ by the orthogonalized-core norm (ts_tucker_norm)."""
+        w = self._weights(batch, weights)
+        out = C.c_double()
+        _check(lib().ts_tucker_norm(self.handle, batch.handle, _p(w), C.byref(out)))
+        return out.value
+
+    def inner(self, bx: DeviceBatch, wx, by: DeviceBatch, wy) -> float:
+        """Σ wx_a wy_b <X_a, Y_b> by per-block Gram contractions (ts_tucker_inner)."""
+        a, b = self._weights(bx, wx), self._weights(by, wy)
+        out = C.c_double()
+        _check(lib().ts_tucker_inner(self.handle, bx.handle, _p(a), by.handle, _p(b), C.byref(out)))
+        return out.value
+
+    def rel_error_to_sum(self, result: "DeviceResult", batch: DeviceBatch, weights) -> float:
+        """‖result − Σ w_k X_k‖ / ‖Σ w_k X_k‖ on the device (ts_rel_error_to_sum)."""
+        w = self._weights(batch, weights)
+        out = C.c_double()
+        _check(lib().ts_rel_error_to_sum(self.handle, result.handle, batch.handle, _p(w), C.byref(out)))
+        return out.value
+
+    @staticmethod
+    def _weights(batch: DeviceBatch, weights) -> np.ndarray:
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        if len(w) != batch.count:
+            raise ValueError("sum request needs matching, nonempty summands and weights")
+        return w
+
+    def lazy_sum(self, batch: DeviceBatch, weights, eps: float, max_rank=None) -> DeviceResult:
+        """ts_lazy_sum: tucker_rounding(formal_sum(batch, weights), eps) on the device."""
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        if len(w) != batch.count:
+            raise ValueError("formal_sum: need matching, nonempty summands and weights")
+        cap = None if max_rank is None else np.ascontiguousarray(np.asarray(max_rank, dtype=np.int64))
+        h = C.c_void_p()
+        _check(lib().ts_lazy_sum(self.handle, batch.handle, _p(w), C.c_double(eps),
+                                 cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
+        return DeviceResult(h)
+
     def krp_sum_many(self, batches: Sequence[DeviceBatch], weights: Sequence, widths, seeds: Sequence[RngSeed],
                      eps: float, max_rank=None, lanes: int = 8) -> List[DeviceResult]:
         """Independent sums side by side (ts_krp_sum_many):
@@ -700,12 +805,102 @@ def _sketched_sum(req, plan, stats, engine, strategy):
     return out
 
 
+def tucker_rounding(x: TuckerTensor, tau: float, engine: Optional[Engine] = None, max_rank=None) -> TuckerTensor:
+    """Lazy rounding (reference src/tucker.cpp:285-296) on the device: thin QR of
+    every factor, R absorbed into the (block) core, st_hosvd, Q·P (ts_lazy_sum)."""
+    if tau < 0:
+        raise ValueError("tucker_rounding: tolerance must be nonnegative")
+    eng = engine or default_engine()
+    batch = eng.upload([x])
+    try:
+        res = eng.lazy_sum(batch, [1.0], tau, max_rank)
+        out = res.to_tucker()
+        res.free()
+    finally:
+        batch.free()
+    return out
+
+
+def tucker_norm(x: TuckerTensor, engine: Optional[Engine] = None) -> float:
+    """Reference tucker_norm (src/tucker.cpp:159): orthogonalized-core norm, on the device."""
+    eng = engine or default_engine()
+    batch = eng.upload([x])
+    try:
+        return eng.tucker_norm(batch, [1.0])
+    finally:
+        batch.free()
+
+
+def tucker_inner(x: TuckerTensor, y: TuckerTensor, engine: Optional[Engine] = None) -> float:
+    """Reference tucker_inner (src/tucker.cpp:161-181) on the device."""
+    if x.dims != y.dims:
+        raise ValueError("tucker_inner: operands must share dims")
+    eng = engine or default_engine()
+    bx, by = eng.upload([x]), eng.upload([y])
+    try:
+        return eng.inner(bx, [1.0], by, [1.0])
+    finally:
+        bx.free()
+        by.free()
+
+
+def tucker_rel_error(x: TuckerTensor, ref: TuckerTensor, engine: Optional[Engine] = None) -> float:
+    """Reference tucker_rel_error (src/tucker.cpp:298-303): ‖x − ref‖ / ‖ref‖ with
+    both norms orthogonalized on the device (exact cancellation survives)."""
+    eng = engine or default_engine()
+    bd, br = eng.upload([x, ref]), eng.upload([ref])
+    try:
+        denom = eng.tucker_norm(br, [1.0])
+        diff = eng.tucker_norm(bd, [1.0, -1.0])
+    finally:
+        bd.free()
+        br.free()
+    return diff if denom == 0.0 else diff / denom
+
+
+def lazy_sum(req: SumRequest, engine: Optional[Engine] = None) -> TuckerTensor:
+    """Strategy.Lazy (reference src/sketch.cpp:48-50): round the formal sum once."""
+    if len(req.summands) == 0 or len(req.summands) != len(req.weights) or any(x is None for x in req.summands):
+        raise ValueError("formal_sum: need matching, nonempty summands and weights")
+    if any(x.dims != req.summands[0].dims for x in req.summands):
+        raise ValueError("formal_sum: all summands must share dims")
+    if req.eps < 0:
+        raise ValueError("tucker_rounding: tolerance must be nonnegative")
+    eng = engine or default_engine()
+    batch = eng.upload(req.summands)
+    try:
+        res = eng.lazy_sum(batch, req.weights, req.eps, req.max_rank)
+        out = res.to_tucker()
+        res.free()
+    finally:
+        batch.free()
+    return out
+
+
+def eager_sum(req: SumRequest, stats: Optional[SumStats] = None, engine: Optional[Engine] = None) -> TuckerTensor:
+    """Strategy.Eager (reference src/sketch.cpp:52-64): left fold, one device
+    rounding per added summand; a single summand comes back scaled, unrounded."""
+    _validate_request(req.summands, req.weights)
+    if stats is not None:
+        stats.eager_rank_trace = []
+    acc = formal_sum([req.summands[0]], [req.weights[0]])
+    for x, w in zip(req.summands[1:], req.weights[1:]):
+        acc = tucker_rounding(tucker_axby(1.0, acc, w, x), req.eps, engine)
+        if stats is not None:
+            stats.eager_rank_trace.append(list(acc.ranks))
+    return acc
+
+
 def round_sum(req: SumRequest, plan: Optional[SketchPlan] = None, stats: Optional[SumStats] = None,
               engine: Optional[Engine] = None) -> TuckerTensor:
-    """Strategy dispatcher (reference src/sketch.cpp:368-376); Krp and Kron are on the B200 path."""
+    """Strategy dispatcher (reference src/sketch.cpp:368-376), every strategy on the device."""
     if req.strategy == Strategy.Krp:
         return krp_sum(req, plan, stats, engine)
     if req.strategy == Strategy.Kron:
         return kron_sum(req, plan, stats, engine)
+    if req.strategy == Strategy.Lazy:
+        return lazy_sum(req, engine)
+    if req.strategy == Strategy.Eager:
+        return eager_sum(req, stats, engine)
     _validate_request(req.summands, req.weights)
     raise NotImplementedError(f"strategy {strategy_name(req.strategy)} is outside the B200 hot path (SURVEY.md §8)")

@@ -88,8 +88,6 @@ def test_mirror_request_validation():
         T.krp_sum(T.SumRequest([a], [1.0], eps=-1.0, strategy=T.Strategy.Krp))
     with pytest.raises(ValueError):
         T.TuckerTensor(np.ones((2, 2)), [np.ones((4, 3)), np.ones((4, 2))])
-    with pytest.raises(NotImplementedError):
-        T.round_sum(T.SumRequest([a], [1.0], strategy=T.Strategy.Lazy))
     assert T.strategy_from_name("krp") == T.Strategy.Krp
     with pytest.raises(ValueError):
         T.strategy_from_name("nope")
@@ -168,3 +166,17 @@ def test_kron_plan_report_lists_complement_widths():
     text = plan.report()
     for key in ("kron", "mode 1:", "mode 3:", "sketch_dim=", "complement_width=6"):
         assert key in text
+
+
+def test_every_strategy_fails_loudly_without_gpu():
+    """No CPU fallback: each round_sum strategy goes to the device library."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    x = T.TuckerTensor(np.ones((2, 2, 2)), [np.ones((8, 2)), np.ones((7, 2)), np.ones((6, 2))])
+    for strat in T.Strategy:
+        with pytest.raises(T.TucksumCudaError):
+            T.round_sum(T.SumRequest([x, x], [1.0, 2.0], strategy=strat))
+    with pytest.raises(T.TucksumCudaError):
+        T.tucker_norm(x)

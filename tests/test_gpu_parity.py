@@ -400,6 +400,15 @@ def test_cfg5_full_size_parity(engine):
     e_gpu = O.rel_error_gram(out, wl.summands, wl.weights, threads)
     e_ref = O.rel_error_gram(ref, wl.summands, wl.weights, threads)
     assert abs(e_gpu - e_ref) <= 5e-4 * e_ref
+    # The device error kernel (ts_rel_error_to_sum) agrees.
+    batch = engine.upload(wl.summands)
+    try:
+        res = engine.krp_sum(batch, wl.weights, wl.widths, wl.seed, wl.eps, wl.cap)
+        e_dev = engine.rel_error_to_sum(res, batch, wl.weights)
+        res.free()
+    finally:
+        batch.free()
+    assert abs(e_dev - e_ref) <= 5e-4 * e_ref
 
 
 def test_sym_eig_matches_oracle(engine):
