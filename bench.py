@@ -49,6 +49,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--stages", action="store_true", help="print per-stage times to stderr")
+    p.add_argument("--strategy", default="krp", choices=["krp", "kron", "lazy"],
+                   help="krp (the hot path, default); kron: Kronecker sketch with the reference's balanced "
+                        "widths for the config's targets; lazy: deterministic rounding of the formal sum")
+    p.add_argument("--no-error", action="store_true", help="skip the device error-to-exact-sum check")
     return p.parse_args()
 
 
@@ -124,11 +128,14 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def config_desc(wl, world):
+def config_desc(wl, world, strategy="krp", widths=None):
     r = wl.ranks[0]
+    plan = {"krp": "given (uniform KRP width)", "kron": f"given (Kron widths {widths} = kron_sketch_dims(targets "
+            f"{wl.widths}, dims), src/sketch.cpp:222-270)", "lazy": "none (Lazy: tucker_rounding of the formal sum)"}
     return {"workload": f"{wl.name}: d={len(wl.dims)} n={wl.dims} K={wl.K} r={r} s={wl.widths[0]} "
                         f"cap={wl.cap} eps={wl.eps} (BASELINE.json configs[{wl.cfg - 1}])",
-            "summands_per_gpu": wl.K // world, "plan": "given (uniform KRP width)", "omega": "cached on device",
+            "strategy": strategy,
+            "summands_per_gpu": wl.K // world, "plan": plan[strategy], "omega": "cached on device",
             "l2": "inputs larger than L2 (no flush)" if sum(s.nbytes for s in wl.slabs) > 126e6 else
             "inputs fit in L2; L2 flushed between steps",
             "parallelism": f"summand-sharded dp{world} + NCCL all-reduce of Y and h" if world > 1 else "1 GPU"}
@@ -216,12 +223,19 @@ def main():
     xs, ws = wl.summands[b:e], np.ascontiguousarray(wl.weights[b:e])
     eng = init_nccl_engine(local if world > 1 else 0, rank, world)
     stream = torch.cuda.ExternalStream(eng.stream)
-    eng.prepare_omega(wl.dims, max(wl.widths), wl.seed)
+    strat = {"krp": T.Strategy.Krp, "kron": T.Strategy.Kron, "lazy": T.Strategy.Lazy}[args.strategy]
+    widths = T.kron_sketch_dims(wl.widths, wl.dims) if args.strategy == "kron" else wl.widths
+    if args.strategy == "krp":
+        eng.prepare_omega(wl.dims, max(wl.widths), wl.seed)
     batch = eng.upload(xs)
 
+    def call(bt):
+        if args.strategy == "lazy":
+            return eng.lazy_sum(bt, ws, wl.eps, wl.cap)
+        return eng.krp_sum(bt, ws, widths, wl.seed, wl.eps, wl.cap, strat)
+
     def step():
-        res = eng.krp_sum(batch, ws, wl.widths, wl.seed, wl.eps, wl.cap)
-        return res
+        return call(batch)
 
     flush = None
     if sum(s.nbytes for s in wl.slabs) <= 126e6:
@@ -263,15 +277,22 @@ def main():
     total_ms = float(t.item())
     ms = total_ms / args.steps
     value = wl.K / (ms / 1000.0)
-    falg = f_alg(wl.dims, wl.ranks, wl.widths[0])
-    gflops = falg / (ms / 1000.0) / 1e9
+    krp = args.strategy == "krp"
+    falg = f_alg(wl.dims, wl.ranks, wl.widths[0]) if krp else None  # SURVEY.md §8(d) F_alg is the KRP count
+    gflops = falg / (ms / 1000.0) / 1e9 if krp else None
     peak, peak_src = fp64_peak()
 
-    # Dominant kernel: the stage-A grouped DMMA GEMM (Z_j = Ω_jᵀ F_j over all modes, one launch).
+    # Dominant kernel: the stage-A grouped DMMA GEMM (Z_j = Ω_jᵀ F_j over all modes, one launch);
+    # for Lazy (no stage A) the stage-E GEMM P_n = Q_nᵀ F_n.
     d = len(wl.dims)
     Kloc = e - b
-    fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * wl.widths[0] * Kloc for j in range(d))
-    ta = stages[0] if stages else float("nan")
+    if args.strategy == "lazy":
+        q = [min(wl.dims[j], sum(r[j] for r in wl.ranks[b:e])) for j in range(d)]
+        fa = sum(2.0 * q[j] * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d))
+        ta = stages[5] if stages else float("nan")
+    else:
+        fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * (wl.widths[0] if krp else widths[j]) * Kloc for j in range(d))
+        ta = stages[0] if stages else float("nan")
     achieved = fa / (ta / 1000.0) / 1e12 if ta == ta and ta > 0 else None
     traffic = None
     try:
@@ -279,11 +300,14 @@ def main():
             traffic = json.load(f).get(wl.name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"bound": "tensor", "kernel": "gemm_tma_kernel<TN> (stage A: Z_j = Ω_jᵀ·F_j, one launch over all modes)",
+    kname = ("gemm_tma_kernel<TN> (stage E: P_n = Q_nᵀ·F_n, one launch over all modes)" if args.strategy == "lazy"
+             else "gemm_tma_kernel<TN> (stage A: Z_j = Ω_jᵀ·F_j, one launch over all modes)")
+    roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src,
-                "whole_step_fp64_tflops": gflops / 1000.0, "whole_step_frac": gflops / 1000.0 / (peak * world)}
+                "whole_step_fp64_tflops": gflops / 1000.0 if krp else None,
+                "whole_step_frac": gflops / 1000.0 / (peak * world) if krp else None}
     stage_names = ["A_project", "B_krp", "C_expand", "allreduce_Y", "D_tsqr", "E_project", "F1_ttm", "F2_core",
                    "allreduce_h", "G_sthosvd", "H_output"]
     if args.stages and rank == 0:
@@ -305,7 +329,7 @@ def main():
                 dist.barrier()
             t0 = time.perf_counter()
             bt = eng.upload(xs)
-            res = eng.krp_sum(bt, ws, wl.widths, wl.seed, wl.eps, wl.cap)
+            res = call(bt)
             out = res.to_tucker()
             res.free()
             bt.free()
@@ -323,8 +347,17 @@ def main():
                "timing": "host wall clock around synchronous API calls, max over ranks, mean of "
                          f"{args.e2e_steps} steps after 1 warm-up"}
 
+    # Error to the exact sum, on the device (ts_rel_error_to_sum), outside the timed region.
+    err = None
+    if world == 1 and not args.no_error:
+        res = step()
+        err = {"rel_error_to_exact_sum": eng.rel_error_to_sum(res, batch, ws),
+               "how": "ts_rel_error_to_sum: per-block Gram inner products on the device (reference "
+                      "tucker_inner structure), outside the timed region"}
+        res.free()
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and krp:
         cpu = cpu_baseline(wl)
 
     if rank == 0:
@@ -332,10 +365,12 @@ def main():
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded BASELINE.json config recipe; no public dataset)",
-                "config": config_desc(wl, world), "gflops": gflops, "fp64_frac_of_peak": gflops / 1000.0 / (peak * world),
+                "config": config_desc(wl, world, args.strategy, widths), "gflops": gflops,
+                "fp64_frac_of_peak": gflops / 1000.0 / (peak * world) if krp else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages)),
-                "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]}}
+                "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]},
+                "accuracy": err}
         print(json.dumps(line), flush=True)
     batch.free()
     eng.close()
