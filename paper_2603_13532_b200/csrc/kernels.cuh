@@ -36,6 +36,8 @@ struct KrpArgs {
     const Atom* atoms;
     const double* cores;
     const double* weights;  // per summand
+    double* Wpart[kMaxOrder];  // split-J partials (set by launch_krp_contract)
+    int splits;
 };
 void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc);
 

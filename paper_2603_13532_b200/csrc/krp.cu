@@ -39,7 +39,10 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
     constexpr int WM = Cfg::WM, WN = Cfg::WN;
     const Atom& at = args.atoms[blockIdx.x];
     const int n = blockIdx.y;
-    const int c0 = blockIdx.z * kCT;
+    // blockIdx.z = column chunk × splits + split: split `sp` takes its share of
+    // the complement chunks (split-J, partials summed in split order afterwards).
+    const int sp = static_cast<int>(blockIdx.z) % args.splits;
+    const int c0 = (static_cast<int>(blockIdx.z) / args.splits) * kCT;
     const int order = args.order, s = args.s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -58,7 +61,9 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
     int64_t jtot = 1;
     for (int j = 0; j < order; ++j)
         if (j != n) jtot *= shape[j];
-    const int64_t nchunks = (jtot + kJC - 1) / kJC;
+    const int64_t nall = (jtot + kJC - 1) / kJC;
+    const int64_t ch_begin = nall * sp / args.splits, ch_end = nall * (sp + 1) / args.splits;
+    const int64_t nchunks = ch_end - ch_begin;
 
     extern __shared__ __align__(16) double sm[];
     int moff[kMaxOrder];
@@ -84,7 +89,9 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
     }
     const double w = args.weights[at.summand];
     const double* __restrict__ core = args.cores + at.core_off;
-    double* Wn = args.W[n];
+    // Unsplit: the weighted result goes straight to Wt_n; split: partial sums
+    // (already weighted) go to this split's slab of the workspace.
+    double* Wn = args.splits == 1 ? args.W[n] : args.Wpart[n] + static_cast<int64_t>(sp) * args.R[n] * s;
 
     auto decode = [&](int64_t chunk, int buf) {
         if (tid < kJC) {
@@ -125,7 +132,7 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
             for (int j = 0; j < WN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         double gv[Cfg::GPT];
         __syncthreads();
-        decode(0, 0);
+        decode(ch_begin, 0);
         __syncthreads();
         gather(0, a0, gv);
         for (int64_t ch = 0; ch < nchunks; ++ch) {
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(kThreads) krp_dmma_kernel(KrpArgs args) {
                 }
                 Ks[jj * kKS + c] = v;
             }
-            if (ch + 1 < nchunks) decode(ch + 1, buf ^ 1);
+            if (ch + 1 < nchunks) decode(ch_begin + ch + 1, buf ^ 1);
             __syncthreads();
             if (ch + 1 < nchunks) gather(buf ^ 1, a0, gv);  // prefetch the next chunk during the MMAs
 #pragma unroll
@@ -316,7 +323,21 @@ __global__ void __launch_bounds__(kThreads) krp3_dmma_kernel(KrpArgs args) {
 
 }  // namespace
 
-void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc) {
+// Wt_n = Σ_split Wpart[split] in split order (deterministic).
+__global__ void krp_split_reduce(KrpArgs args) {
+    const int n = blockIdx.y;
+    const int64_t total = args.R[n] * args.s;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double v = 0.0;
+        for (int sp = 0; sp < args.splits; ++sp) v += args.Wpart[n][sp * total + e];
+        args.W[n][e] = v;
+    }
+}
+
+void launch_krp_contract(const KrpArgs& args_in, int max_shape, CallScratch& sc) {
+    KrpArgs args = args_in;
+    args.splits = 1;
     if (args.natoms == 0) return;
     static const bool use3 = [] {
         const char* e = std::getenv("TS_KRP_GENERIC");
@@ -340,8 +361,22 @@ void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc) {
     const int RT = max_shape <= 32 ? 32 : 64;
     const size_t smem = sizeof(double) * (static_cast<size_t>(max_shape) * args.order * kCT + kJC * kKS + RT * kGS) +
                         sizeof(int64_t) * 2 * kJC + sizeof(int) * 2 * kJC * kMaxOrder;
+    // Few (atom, mode, column-chunk) CTAs each walking a long complement (order
+    // ≥ 4: Π_{j≠n} r_j KRP rows) leave most of the 148 SMs idle; split the
+    // complement so the grid covers about two waves.
+    const int cchunks = (args.s + kCT - 1) / kCT;
+    const int64_t base = static_cast<int64_t>(args.natoms) * args.order * cchunks;
+    std::int64_t most = 1;
+    for (int j = 0; j < args.order; ++j) most *= max_shape;
+    most /= std::max(1, max_shape);
+    const int64_t nall = (most + kJC - 1) / kJC;
+    args.splits = static_cast<int>(std::clamp<int64_t>((2 * 148 + base - 1) / base, 1, std::max<int64_t>(1, nall / 8)));
+    if (args.splits > 1) {
+        for (int n = 0; n < args.order; ++n)
+            args.Wpart[n] = sc.alloc_n<double>(static_cast<size_t>(args.splits * args.R[n] * args.s));
+    }
     dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>(args.order),
-              static_cast<unsigned>((args.s + kCT - 1) / kCT));
+              static_cast<unsigned>(cchunks * args.splits));
     auto go = [&](auto kern) {
         TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<grid, kThreads, smem, sc.stream()>>>(args);
@@ -350,6 +385,11 @@ void launch_krp_contract(const KrpArgs& args, int max_shape, CallScratch& sc) {
     if (RT == 32) go(krp_dmma_kernel<32>);
     else go(krp_dmma_kernel<64>);
     sc.launches += 1;
+    if (args.splits > 1) {
+        krp_split_reduce<<<dim3(64, static_cast<unsigned>(args.order)), 256, 0, sc.stream()>>>(args);
+        TS_LAUNCH_CHECK();
+        sc.launches += 1;
+    }
 }
 
 }  // namespace ts
