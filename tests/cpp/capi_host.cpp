@@ -224,6 +224,44 @@ int main() {
     CHECK(std::fabs(out_norm2 - exact_norm2) <= 1e-10 * exact_norm2, "‖X̃‖² = %.15e vs exact %.15e", out_norm2,
           exact_norm2);
 
+    // The same sum through the other device strategies and the device norms:
+    // Lazy rounding (stacked rank 4·6 = 24) and the Kron sketch recover rank 12,
+    // the orthogonalized norm of the formal sum equals the exact norm, and the
+    // device error of the KRP result to the exact sum is ~0 (exact rank).
+    {
+        double snorm = 0.0;
+        CHECK(ts_tucker_norm(ctx, batch, w.data(), &snorm) == TS_OK, "tucker_norm: %s", ts_last_error());
+        CHECK(std::fabs(snorm * snorm - exact_norm2) <= 1e-10 * exact_norm2, "tucker_norm² %.15e vs %.15e",
+              snorm * snorm, exact_norm2);
+        double ss = 0.0;
+        CHECK(ts_tucker_inner(ctx, batch, w.data(), batch, w.data(), &ss) == TS_OK, "tucker_inner: %s", ts_last_error());
+        CHECK(std::fabs(ss - exact_norm2) <= 1e-10 * exact_norm2, "tucker_inner %.15e vs %.15e", ss, exact_norm2);
+        ts_result* lz = nullptr;
+        CHECK(ts_lazy_sum(ctx, batch, w.data(), 1e-12, nullptr, &lz) == TS_OK, "lazy_sum: %s", ts_last_error());
+        if (lz) {
+            std::vector<int64_t> rk(static_cast<size_t>(order));
+            ts_result_ranks(lz, rk.data());
+            for (int k = 0; k < order; ++k) CHECK(rk[static_cast<size_t>(k)] == 12, "lazy rank[%d] = %lld", k,
+                                                  static_cast<long long>(rk[static_cast<size_t>(k)]));
+            double err = 1.0;
+            CHECK(ts_rel_error_to_sum(ctx, lz, batch, w.data(), &err) == TS_OK, "rel_error: %s", ts_last_error());
+            CHECK(err < 1e-6, "lazy error to the exact sum %.3e", err);
+            ts_result_free(lz);
+        }
+        std::vector<int64_t> kw(static_cast<size_t>(order)), tg(static_cast<size_t>(order), 16);
+        CHECK(ts_kron_sketch_dims(order, tg.data(), dims.data(), kw.data()) == TS_OK, "kron dims: %s", ts_last_error());
+        ts_result* kr = nullptr;
+        CHECK(ts_kron_sum(ctx, batch, w.data(), kw.data(), 7, 2, 1e-12, nullptr, &kr) == TS_OK, "kron_sum: %s",
+              ts_last_error());
+        if (kr) {
+            std::vector<int64_t> rk(static_cast<size_t>(order));
+            ts_result_ranks(kr, rk.data());
+            for (int k = 0; k < order; ++k) CHECK(rk[static_cast<size_t>(k)] == 12, "kron rank[%d] = %lld", k,
+                                                  static_cast<long long>(rk[static_cast<size_t>(k)]));
+            ts_result_free(kr);
+        }
+    }
+
     CHECK(ts_batch_free(batch) == TS_OK, "batch free");
     CHECK(ts_ctx_destroy(ctx) == TS_OK, "ctx destroy");
     if (failures == 0) std::printf("capi_host ok: ranks 12/12/12, |X|^2 = %.12e (exact %.12e)\n", out_norm2, exact_norm2);

@@ -180,3 +180,17 @@ def test_every_strategy_fails_loudly_without_gpu():
             T.round_sum(T.SumRequest([x, x], [1.0, 2.0], strategy=strat))
     with pytest.raises(T.TucksumCudaError):
         T.tucker_norm(x)
+
+
+def test_reference_adapter_compiles_against_stub_types():
+    """include/tucksum_cuda_adapter.hpp (krp_sum, kron_sum, round_sum over every
+    strategy, tucker_rounding / norm / inner / rel_error) compiles with -Wall
+    -Wextra against tests/cpp/stub — the reference's public types without Eigen."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
+                        "-I", os.path.join(root, "include"), "-I", os.path.join(root, "tests", "cpp", "stub"),
+                        os.path.join(root, "tests", "cpp", "adapter_compile.cpp")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
