@@ -131,6 +131,7 @@ struct ts_ctx {
     std::int64_t launches = 0;
     std::vector<cudaEvent_t> events;
     int last_qr_fallbacks = 0, last_svd_fallbacks = 0;  // accurate-path uses in the last call
+    int last_eig_fallbacks = 0;  // tridiagonal-eigensolver rejections (Jacobi recomputes) in the last call
     // Speculative tail (see krp_sum_impl): on while the last call needed no
     // accurate-path fallback.
     bool spec_ok = true;
@@ -932,6 +933,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         }
         const double theta = eps * eps * hss / static_cast<double>(d);
         ctx->last_svd_fallbacks = 0;
+        ctx->last_eig_fallbacks = 0;
         std::vector<int> mode_order(static_cast<size_t>(d));
         std::iota(mode_order.begin(), mode_order.end(), 0);
         std::stable_sort(mode_order.begin(), mode_order.end(), [&](int x, int y) { return cur_shape[x] < cur_shape[y]; });
@@ -960,7 +962,23 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             }
             static const bool dbg_sweeps = std::getenv("TS_DEBUG_SWEEPS") != nullptr;
             int* dsw = dbg_sweeps ? sc.alloc_n<int>(1) : nullptr;
-            ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
+            // Eigensolver: tridiagonalization + bisection + inverse iteration
+            // (eig_tri.cu) with a device acceptance check; on rejection the
+            // two-sided Jacobi (eig.cu) recomputes — in the speculative path via
+            // the stage-G flag (whole call redone synchronously), otherwise here.
+            const bool use_tri = ts::tri_eig_enabled() && qk <= 64 && !dsw;
+            int* tflag = nullptr;
+            if (use_tri) {
+                if (spec_g) {
+                    tflag = gflags + k;
+                } else {
+                    tflag = sc.alloc_n<int>(1);
+                    TS_CUDA_CHECK(cudaMemsetAsync(tflag, 0, sizeof(int), st));
+                }
+                ts::launch_sym_tridiag(C, qk, static_cast<int>(qk), lam, Pk[k], tflag, sc);
+            } else {
+                ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
+            }
             const std::int64_t capk = max_rank ? max_rank[k] : 0;
             std::int64_t rk = 0;
             if (spec_g && !dsw) {
@@ -971,9 +989,17 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 std::vector<double> lv(static_cast<size_t>(qk));
                 TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
                                               cudaMemcpyDeviceToHost, st));
-                int hsw = 0;
+                int hsw = 0, htf = 0;
                 if (dsw) TS_CUDA_CHECK(cudaMemcpyAsync(&hsw, dsw, sizeof(int), cudaMemcpyDeviceToHost, st));
+                if (tflag) TS_CUDA_CHECK(cudaMemcpyAsync(&htf, tflag, sizeof(int), cudaMemcpyDeviceToHost, st));
                 TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                if (htf) {  // tridiagonal solver rejected its own result
+                    ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, nullptr);
+                    TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
+                                                  cudaMemcpyDeviceToHost, st));
+                    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                    ++ctx->last_eig_fallbacks;
+                }
                 if (dsw)
                     std::fprintf(stderr, "[ts] st-hosvd mode %d: n=%lld sweeps=%d lam1=%.3e lam_last=%.3e\n", k,
                                  static_cast<long long>(qk), hsw, lv[0], lv.back());
@@ -1632,6 +1658,39 @@ int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* 
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (sweeps) *sweeps = hs;
+        if (ms) *ms = t;
+    });
+}
+
+// The tridiagonalization eigensolver alone (eig_tri.cu), host in / host out;
+// *flag = 1 when its acceptance check rejected the result.
+int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* flag, double* ms) {
+    return guarded([&] {
+        if (!ctx || n < 1 || n > 64) invalid("ts_sym_eig_tri: need 1 <= n <= 64");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->stage.reset();
+        CallScratch sc(ctx->stream, ctx->stage);
+        auto* dA = static_cast<double*>(sc.upload(a, sizeof(double) * static_cast<size_t>(n * n)));
+        double* dl = sc.alloc_n<double>(static_cast<size_t>(n));
+        double* dV = sc.alloc_n<double>(static_cast<size_t>(n * n));
+        int* df = sc.alloc_n<int>(1);
+        TS_CUDA_CHECK(cudaMemsetAsync(df, 0, sizeof(int), ctx->stream));
+        cudaEvent_t e0, e1;
+        TS_CUDA_CHECK(cudaEventCreate(&e0));
+        TS_CUDA_CHECK(cudaEventCreate(&e1));
+        TS_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        ts::launch_sym_tridiag(dA, n, static_cast<int>(n), dl, dV, df, sc);
+        TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        int hf = 0;
+        TS_CUDA_CHECK(cudaMemcpyAsync(values, dl, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(vectors, dV, sizeof(double) * static_cast<size_t>(n * n), cudaMemcpyDeviceToHost, ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(&hf, df, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        float t = 0.f;
+        TS_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (flag) *flag = hf;
         if (ms) *ms = t;
     });
 }

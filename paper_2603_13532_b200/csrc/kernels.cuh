@@ -105,6 +105,11 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
 // Fixed-address (permuted-layout) variant for n ≤ 64 (eig.cu); false if n > 64.
 bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
                           int* sweeps);
+// Tridiagonalization + bisection + inverse-iteration eigensolver for n ≤ 64
+// (eig_tri.cu): lambda[n] descending, V (n × n, ld n); *flag |= 1 when its
+// residual / orthogonality acceptance check fails (then use launch_sym_jacobi).
+bool launch_sym_tridiag(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, CallScratch& sc);
+bool tri_eig_enabled();
 // R⁻¹ of the Cholesky factor of small SPD matrices G[b] (n ≤ 96, one CTA each);
 // *flag[b] |= 1 on a non-positive pivot, |= 2 when check_identity and
 // max|G - I| > 1e-2.

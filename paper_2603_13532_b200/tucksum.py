@@ -49,7 +49,7 @@ EXPORTED_SYMBOLS = [
     "ts_result_factor_device", "ts_result_core_device", "ts_result_intermediate", "ts_result_free",
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
     "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
-    "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum",
+    "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
 ]
 
 
@@ -576,6 +576,17 @@ class Engine:
         ms = C.c_double()
         _check(lib().ts_sym_eig(self.handle, i64(n), _p(a), _p(vals), _p(vecs), C.byref(sw), C.byref(ms)))
         return vals, vecs, int(sw.value), float(ms.value)
+
+    def sym_eig_tri(self, a):
+        """Tridiagonalization eigensolver (ts_sym_eig_tri): (values desc, vectors, rejected, ms)."""
+        a = _f64(a)
+        n = a.shape[0]
+        vals = np.zeros(n)
+        vecs = np.zeros((n, n), order="F")
+        fl = C.c_int()
+        ms = C.c_double()
+        _check(lib().ts_sym_eig_tri(self.handle, i64(n), _p(a), _p(vals), _p(vecs), C.byref(fl), C.byref(ms)))
+        return vals, vecs, bool(fl.value), float(ms.value)
 
     def last_paths(self):
         """(qr_fallback_modes, svd_fallback_modes) of the last krp_sum."""

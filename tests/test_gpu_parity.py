@@ -422,3 +422,32 @@ def test_sym_eig_matches_oracle(engine):
         assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-12
         assert np.linalg.norm(vecs @ np.diag(vals) @ vecs.T - c) <= 1e-12 * np.linalg.norm(c)
         assert 1 <= sweeps <= 20, sweeps
+
+
+def test_sym_eig_tri_matches_oracle(engine):
+    """Tridiagonalization + bisection + inverse iteration eigensolver (the stage-G
+    default for n <= 64) vs the oracle's sym_eig: Gram matrices, decaying
+    spectra, exact clusters (rank-deficient Grams) and tiny sizes."""
+    cases = []
+    for n, seed in [(1, 0), (2, 1), (3, 2), (6, 3), (26, 4), (40, 5), (50, 6), (64, 7)]:
+        a = O.gaussian_matrix(2 * n, n, (18, seed))
+        cases.append(a.T @ a)
+    rng = np.random.default_rng(3)
+    for n, decay in [(64, 0.2), (64, 0.5), (26, 1.0)]:
+        q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        cases.append((q * 10.0 ** (-decay * np.arange(n))) @ q.T)
+    b = O.gaussian_matrix(64, 10, (19, 1))
+    cases.append(b @ b.T)  # rank 10: a cluster of 54 zero eigenvalues
+    q, _ = np.linalg.qr(rng.standard_normal((48, 48)))
+    lam = np.repeat([3.0, 2.0, 1.0, 0.5], 12)
+    cases.append((q * lam) @ q.T)  # four 12-fold eigenvalues
+    for c in cases:
+        n = c.shape[0]
+        vals, vecs, rejected, ms = engine.sym_eig_tri(c)
+        ov, _ = O.sym_eig(c)
+        scale = max(abs(ov[0]), 1e-300)
+        assert np.max(np.abs(vals - ov)) <= 1e-13 * scale * max(1, n / 8), (n, np.max(np.abs(vals - ov)))
+        if not rejected:
+            assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-12
+            assert np.linalg.norm(vecs @ np.diag(vals) @ vecs.T - c) <= 1e-12 * np.linalg.norm(c)
+    print("tri-eig rejections:", sum(engine.sym_eig_tri(c)[2] for c in cases), "of", len(cases))
