@@ -205,6 +205,12 @@ int ts_ctx_set_debug(ts_ctx* ctx, int enabled);
 /* Per-stage CUDA-event times (ms) of the last ts_krp_sum: A, B, C, allreduce Y,
  * D, E, F1, F2, allreduce h, G, H; returns the number written (<= cap). */
 int ts_ctx_stage_times(ts_ctx* ctx, double* ms, int cap);
+/* CUDA-graph replay of repeated calls (default on): the second identical call
+ * (same batch upload, weights, widths, cap, seed; eps == 0) is captured into a
+ * graph and later identical calls replay it with one launch.  0 disables it and
+ * drops the cache.  ts_ctx_graph_replays counts replays. */
+int ts_ctx_set_graphs(ts_ctx* ctx, int enabled);
+int64_t ts_ctx_graph_replays(ts_ctx* ctx);
 /* Enables per-stage event timing (adds event records; off by default). */
 int ts_ctx_set_timing(ts_ctx* ctx, int enabled);
 

@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <set>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -116,6 +118,46 @@ struct OmegaKey {
 
 constexpr int kNumStages = 11;
 
+// One captured call (CUDA graph) of the speculative ε = 0 path: everything from
+// stage A to the acceptance flags' download is replayed by one cudaGraphLaunch.
+// The graph owns its descriptor staging (pinned, never reset after capture), a
+// device weight buffer refreshed before each replay, and its output buffers,
+// copied into fresh result buffers after each replay.
+struct GraphKey {
+    std::uint64_t batch;
+    int method;
+    std::vector<std::int64_t> widths, cap;
+    std::uint64_t seed, stream;
+    std::vector<double> weights;  // some launches take a weight as a host scalar (GEMM alpha)
+    bool operator<(const GraphKey& o) const {
+        return std::tie(batch, method, widths, cap, seed, stream, weights) <
+               std::tie(o.batch, o.method, o.widths, o.cap, o.seed, o.stream, o.weights);
+    }
+};
+struct GraphEntry {
+    ts::HostStage stage;
+    cudaGraphExec_t exec = nullptr;
+    double* d_w = nullptr;   // device weights (count)
+    double* h_w = nullptr;   // pinned staging of the weights
+    std::int64_t count = 0;
+    double* out_f[TS_MAX_ORDER] = {};
+    double* out_core = nullptr;
+    std::int64_t dims[TS_MAX_ORDER] = {}, ranks[TS_MAX_ORDER] = {};
+    int order = 0;
+    int* h_flags = nullptr;  // pinned: [0, 2d) stage-D / stage-G acceptance flags
+    std::int64_t launches = 0;
+    std::uint64_t last_use = 0;
+    ~GraphEntry() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (d_w) cudaFree(d_w);
+        if (h_w) cudaFreeHost(h_w);
+        for (auto* f : out_f)
+            if (f) cudaFree(f);
+        if (out_core) cudaFree(out_core);
+        if (h_flags) cudaFreeHost(h_flags);
+    }
+};
+
 }  // namespace
 
 struct ts_ctx {
@@ -140,6 +182,12 @@ struct ts_ctx {
     ts_ctx* parent = nullptr;
     std::vector<ts_ctx*> lanes;
     std::mutex omega_mu;
+    // CUDA-graph cache of repeated speculative calls (see GraphEntry).
+    bool graphs = true;
+    std::map<GraphKey, std::unique_ptr<GraphEntry>> graph_cache;
+    std::set<GraphKey> graph_seen;
+    std::uint64_t graph_clock = 0;
+    std::int64_t graph_replays = 0;
 };
 
 struct ts_batch {
@@ -156,6 +204,7 @@ struct ts_batch {
     std::vector<double> core_norm;  // per summand ‖core‖_F (plan energies)
     int max_shape = 0;
     std::int64_t bytes = 0;
+    std::uint64_t id = 0;  // unique per upload (graph-cache key; never reused)
 };
 
 struct ts_result {
@@ -610,7 +659,8 @@ struct ResultView {
 // Q·P.  Needs Σ_k r_n^(k) ≤ 96.
 ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
                              std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank,
-                             Method method, bool allow_spec = true, double* norm_out = nullptr) {
+                             Method method, bool allow_spec = true, double* norm_out = nullptr,
+                             GraphEntry* ge = nullptr) {
     const bool krp = method == Method::Krp, lazy = method == Method::Lazy;
     // Validation mirrors src/sketch.cpp:16-30,66-87.
     if (b == nullptr || b->count < 1) invalid("sum request needs matching, nonempty summands and weights");
@@ -641,9 +691,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         if (!std::isfinite(weights[i])) invalid("weights must be finite");
 
     TS_CUDA_CHECK(cudaSetDevice(ctx->device));
-    ctx->stage.reset();
+    ts::HostStage& hstage = ge ? ge->stage : ctx->stage;
+    hstage.reset();
     cudaStream_t st = ctx->stream;
-    CallScratch sc(st, ctx->stage);
+    CallScratch sc(st, hstage);
     const std::int64_t* dims = b->dims;
     if (ctx->timing && ctx->events.empty()) {
         ctx->events.resize(kNumStages + 1);
@@ -662,7 +713,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         yoff[n] = ytot;
         ytot += dims[n] * yc[n];
     }
-    auto* d_w = static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
+    auto* d_w = ge ? ge->d_w : static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
 
     double* Y = sc.alloc_n<double>(static_cast<size_t>(ytot));
     if (lazy) {
@@ -1063,7 +1114,12 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         for (int n = 0; n < d; ++n) {
             res->dims[n] = dims[n];
             res->ranks[n] = rank[n];
-            TS_CUDA_CHECK(cudaMallocAsync(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n]), st));
+            if (ge) {  // captured call: outputs go to the graph's own buffers
+                if (ge->ranks[n] != rank[n]) throw ts::Error(TS_RUNTIME, "graph capture: rank mismatch");
+                res->factors[n] = ge->out_f[n];
+            } else {
+                TS_CUDA_CHECK(cudaMallocAsync(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n]), st));
+            }
             GemmProblem p{};
             p.A = Uh[n];
             p.lda = dims[n];
@@ -1079,11 +1135,26 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         ts::launch_grouped_gemm(Layout::NN, ps, sc, ctx->num_sms);
         std::int64_t csize = 1;
         for (int n = 0; n < d; ++n) csize *= rank[n];
-        TS_CUDA_CHECK(cudaMallocAsync(&res->core, sizeof(double) * static_cast<size_t>(csize), st));
+        if (ge) {
+            res->core = ge->out_core;
+        } else {
+            TS_CUDA_CHECK(cudaMallocAsync(&res->core, sizeof(double) * static_cast<size_t>(csize), st));
+        }
         TS_CUDA_CHECK(cudaMemcpyAsync(res->core, g, sizeof(double) * static_cast<size_t>(csize),
                                       cudaMemcpyDeviceToDevice, st));
     }
     mark(ctx, 11);
+    if (ge) {  // end of the captured region: flags to pinned host memory, no sync
+        ge->launches = sc.launches;
+        if (dflags)
+            TS_CUDA_CHECK(cudaMemcpyAsync(ge->h_flags, dflags, sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
+        if (gflags)
+            TS_CUDA_CHECK(cudaMemcpyAsync(ge->h_flags + d, gflags, sizeof(int) * static_cast<size_t>(d),
+                                          cudaMemcpyDeviceToHost, st));
+        for (int n = 0; n < d; ++n) res->factors[n] = nullptr;  // graph-owned, not the result's
+        res->core = nullptr;
+        return nullptr;
+    }
     ctx->launches += sc.launches;
     if (spec) {
         std::vector<int> hf(2 * static_cast<size_t>(d), 0);
@@ -1111,6 +1182,122 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             ctx->stage_ms[static_cast<size_t>(i)] = ms;
         }
     }
+    return res.release();
+}
+
+// Entry of ts_krp_sum / ts_kron_sum / ts_lazy_sum.  A call that repeats an
+// earlier one exactly (same batch upload, method, widths, cap, seed; ε = 0 so
+// the speculative path has no host decision) is captured into a CUDA graph the
+// second time and replayed from then on: one cudaGraphLaunch instead of ~40
+// launches, memsets and descriptor copies, which is what the latency-bound small
+// configurations pay for.  The key includes the weights (some launches carry a
+// weight as a host scalar).  A replay whose device
+// acceptance checks fail is redone on the synchronous path, like any
+// speculative call.
+ts_result* run_sum(ts_ctx* ctx, const ts_batch* b, const double* weights, const std::int64_t* widths,
+                   std::uint64_t seed, std::uint64_t stream, double eps, const std::int64_t* max_rank, Method method) {
+    static const bool env_off = [] {
+        const char* e = std::getenv("TS_GRAPHS");
+        return (e && e[0] == '0') || std::getenv("TS_DEBUG_SWEEPS") != nullptr;
+    }();
+    const bool graphable = !env_off && ctx->graphs && b != nullptr && weights != nullptr && eps == 0.0 &&
+                           !ctx->comm && !ctx->debug && !ctx->timing && ctx->spec_ok && ctx->parent == nullptr &&
+                           !ts::tri_eig_enabled();
+    if (!graphable)
+        return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method);
+    const int d = b->order;
+    GraphKey key{b->id, static_cast<int>(method),
+                 widths && method != Method::Lazy ? std::vector<std::int64_t>(widths, widths + d) : std::vector<std::int64_t>{},
+                 max_rank ? std::vector<std::int64_t>(max_rank, max_rank + d) : std::vector<std::int64_t>{}, seed, stream,
+                 std::vector<double>(weights, weights + b->count)};
+    auto it = ctx->graph_cache.find(key);
+    if (it == ctx->graph_cache.end()) {
+        if (ctx->graph_seen.insert(key).second)  // first sighting: plain call (also does one-time setups)
+            return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method);
+        // Second sighting: run it plainly once more to learn the output ranks, then capture.
+        std::unique_ptr<ts_result> probe(sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method));
+        if (!ctx->spec_ok) return probe.release();  // the speculative path was rejected: no graph
+        auto ge = std::make_unique<GraphEntry>();
+        ge->order = d;
+        ge->count = b->count;
+        TS_CUDA_CHECK(cudaMalloc(&ge->d_w, sizeof(double) * static_cast<size_t>(b->count)));
+        TS_CUDA_CHECK(cudaMallocHost(&ge->h_w, sizeof(double) * static_cast<size_t>(b->count)));
+        TS_CUDA_CHECK(cudaMallocHost(&ge->h_flags, sizeof(int) * 2 * TS_MAX_ORDER));
+        std::int64_t csize = 1;
+        for (int n = 0; n < d; ++n) {
+            ge->dims[n] = probe->dims[n];
+            ge->ranks[n] = probe->ranks[n];
+            csize *= probe->ranks[n];
+            TS_CUDA_CHECK(cudaMalloc(&ge->out_f[n], sizeof(double) * static_cast<size_t>(probe->dims[n] * probe->ranks[n])));
+        }
+        TS_CUDA_CHECK(cudaMalloc(&ge->out_core, sizeof(double) * static_cast<size_t>(csize)));
+        ge->stage.reserve(2 * ctx->stage.footprint() + (size_t(1) << 20));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        cudaStream_t st = ctx->stream;
+        TS_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        cudaGraph_t graph = nullptr;
+        try {
+            sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method, true, nullptr, ge.get());
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            ctx->graphs = false;  // do not try again on this context
+            return probe.release();
+        }
+        const cudaError_t e1 = cudaStreamEndCapture(st, &graph);
+        const cudaError_t e2 = e1 == cudaSuccess ? cudaGraphInstantiate(&ge->exec, graph, 0) : e1;
+        if (graph) cudaGraphDestroy(graph);
+        if (e2 != cudaSuccess) {  // not capturable here: stay on plain launches
+            (void)cudaGetLastError();
+            ge->exec = nullptr;
+            ctx->graphs = false;
+            return probe.release();
+        }
+        if (ctx->graph_cache.size() >= 8) {  // bounded cache: evict the least recently used
+            auto lru = ctx->graph_cache.begin();
+            for (auto g = ctx->graph_cache.begin(); g != ctx->graph_cache.end(); ++g)
+                if (g->second->last_use < lru->second->last_use) lru = g;
+            ctx->graph_cache.erase(lru);
+        }
+        it = ctx->graph_cache.emplace(key, std::move(ge)).first;
+        return probe.release();
+    }
+    GraphEntry& ge = *it->second;
+    if (b->count != ge.count) invalid("sum request needs matching, nonempty summands and weights");
+    for (std::int64_t i = 0; i < b->count; ++i)
+        if (!std::isfinite(weights[i])) invalid("weights must be finite");
+    ge.last_use = ++ctx->graph_clock;
+    TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    std::memcpy(ge.h_w, weights, sizeof(double) * static_cast<size_t>(b->count));
+    TS_CUDA_CHECK(cudaMemcpyAsync(ge.d_w, ge.h_w, sizeof(double) * static_cast<size_t>(b->count), cudaMemcpyHostToDevice, st));
+    std::memset(ge.h_flags, 0, sizeof(int) * 2 * TS_MAX_ORDER);
+    TS_CUDA_CHECK(cudaGraphLaunch(ge.exec, st));
+    auto res = std::make_unique<ts_result>();
+    res->device = ctx->device;
+    res->stream = st;
+    res->order = d;
+    std::int64_t csize = 1;
+    for (int n = 0; n < d; ++n) {
+        res->dims[n] = ge.dims[n];
+        res->ranks[n] = ge.ranks[n];
+        csize *= ge.ranks[n];
+        const size_t bytes = sizeof(double) * static_cast<size_t>(ge.dims[n] * ge.ranks[n]);
+        TS_CUDA_CHECK(cudaMallocAsync(&res->factors[n], bytes, st));
+        TS_CUDA_CHECK(cudaMemcpyAsync(res->factors[n], ge.out_f[n], bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    TS_CUDA_CHECK(cudaMallocAsync(&res->core, sizeof(double) * static_cast<size_t>(csize), st));
+    TS_CUDA_CHECK(cudaMemcpyAsync(res->core, ge.out_core, sizeof(double) * static_cast<size_t>(csize),
+                                  cudaMemcpyDeviceToDevice, st));
+    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    ctx->launches += ge.launches;
+    ++ctx->graph_replays;
+    for (int i = 0; i < 2 * d; ++i)
+        if (ge.h_flags[i] != 0) {  // speculation rejected: redo synchronously
+            ctx->spec_ok = false;
+            res.reset();
+            return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method, false);
+        }
     return res.release();
 }
 
@@ -1191,6 +1378,17 @@ int ts_ctx_set_debug(ts_ctx* ctx, int enabled) {
         ctx->debug = enabled != 0;
     });
 }
+int ts_ctx_set_graphs(ts_ctx* ctx, int enabled) {
+    return guarded([&] {
+        if (!ctx) invalid("ts_ctx_set_graphs: null context");
+        ctx->graphs = enabled != 0;
+        if (!ctx->graphs) {
+            ctx->graph_cache.clear();
+            ctx->graph_seen.clear();
+        }
+    });
+}
+int64_t ts_ctx_graph_replays(ts_ctx* ctx) { return ctx ? ctx->graph_replays : 0; }
 int ts_ctx_set_timing(ts_ctx* ctx, int enabled) {
     return guarded([&] {
         if (!ctx) invalid("null context");
@@ -1213,6 +1411,8 @@ int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_bat
         if (d < 1) invalid("TuckerTensor: order must be >= 1");
         if (d > TS_MAX_ORDER) throw ts::Error(TS_UNSUPPORTED, "order exceeds TS_MAX_ORDER");
         auto b = std::make_unique<ts_batch>();
+        static std::atomic<std::uint64_t> next_id{1};
+        b->id = next_id++;
         b->ctx = ctx;
         b->order = d;
         b->count = count;
@@ -1359,7 +1559,7 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_krp_sum: null argument");
-        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Krp);
+        *out = run_sum(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Krp);
     });
 }
 
@@ -1367,7 +1567,7 @@ int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const
                 uint64_t stream, double eps, const int64_t* max_rank, ts_result** out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_kron_sum: null argument");
-        *out = sketched_sum_impl(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Kron);
+        *out = run_sum(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Kron);
     });
 }
 
@@ -1405,7 +1605,7 @@ int ts_lazy_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, doubl
     return guarded([&] {
         if (!ctx || !out) invalid("ts_lazy_sum: null argument");
         if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "lazy rounding does not shard: use a context without NCCL");
-        *out = sketched_sum_impl(ctx, batch, weights, nullptr, 0, 0, eps, max_rank, Method::Lazy);
+        *out = run_sum(ctx, batch, weights, nullptr, 0, 0, eps, max_rank, Method::Lazy);
     });
 }
 

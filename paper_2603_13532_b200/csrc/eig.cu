@@ -145,7 +145,10 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     __shared__ double red[2 * kValWarps];
     __shared__ double amax_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int idx = tid; idx < np * np; idx += kValThreads) {
+    // Worker warps = enough for the round's off-diagonal blocks (launcher's choice,
+    // ≤ kWorkWarps): fewer warps make every round's barriers cheaper at small n.
+    const int nthreads = blockDim.x, nwork = nthreads / 32 - 1;
+    for (int idx = tid; idx < np * np; idx += nthreads) {
         const int i = idx / np, j = idx % np;
         double v = 0.0;
         if (i < n && j < n && j >= i)
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     __syncthreads();
     {
         double mx = 0.0;
-        for (int i = tid; i < n; i += kValThreads) mx = fmax(mx, fabs(sm[addr_of(i, i, k)]));
+        for (int i = tid; i < n; i += nthreads) mx = fmax(mx, fabs(sm[addr_of(i, i, k)]));
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0 && mx > 0.0) atomicMax(reinterpret_cast<unsigned long long*>(&amax_s), __double_as_longlong(mx));
     }
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     __syncthreads();
     bool work = false;
     unsigned la[4] = {0, 0, 0, 0}, sa[4] = {0, 0, 0, 0}, rio = 0, rjo = 0;
-    if (warp < kWorkWarps) {
+    if (warp < nwork) {
         const unsigned kmask = k == 32 ? 0xffffffffu : ((1u << k) - 1u);
         int t = tid, bi = -1, bj = -1;
         for (int i = 0; i < k - 1; ++i) {
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     // the diagonal blocks of sp and sq, whose rotated diagonal it recomputes
     // itself (same arithmetic as their owners) instead of exchanging it.  Lanes
     // ≥ k mirror lane k-1 and store nothing, so the warp stays converged.
-    const bool pwarp = warp == kWorkWarps;
+    const bool pwarp = warp == nwork;
     const bool plane = pwarp && lane < k;
     unsigned dla[3] = {0, 0, 0}, dsa[3] = {0, 0, 0}, ela[4] = {0, 0, 0, 0}, esa[4] = {0, 0, 0, 0};
     unsigned pla[3] = {0, 0, 0}, qla[3] = {0, 0, 0};
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
             if (!pwarp) {
                 // Workers start their shared-memory traffic only once the pivot
                 // warp's loads are queued ahead of it.
-                asm volatile("bar.sync 1, %0;" ::"n"(kValThreads) : "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
                 if (work && !skip_work) {
                     const double2 ri = lds128(C + rio), rj = lds128(C + rjo);
                     double d11, d12, d21, d22;
@@ -306,7 +309,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
                 const double e11 = lds64(A + ela[0]), e12 = lds64(A + ela[1]), e21 = lds64(A + ela[2]),
                              e22 = lds64(A + ela[3]);
                 const double a11 = lds64(A + dla[0]), a12 = lds64(A + dla[1]), a22 = lds64(A + dla[2]);
-                asm volatile("bar.arrive 1, %0;" ::"n"(kValThreads) : "memory");
+                asm volatile("bar.arrive 1, %0;" ::"r"(nthreads) : "memory");
                 // Critical path first, branch-free so the block updates below can
                 // fill the rotation's latency.  Rotated diagonal entry at sp / sq:
                 // d11 of R_pᵀ·B·R_p, and d22 as d11 with (c, s) → (s, -c); the
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
             const double2* logs = reinterpret_cast<const double2*>(sm + 2 * mat + 2 * kMaxNp) +
                                   static_cast<size_t>(sweep & 1) * (np - 1) * k;
             double2* dst = rot + static_cast<int64_t>(sweep) * (np - 1) * k;
-            for (int e = tid; e < (np - 1) * k; e += kValThreads) dst[e] = logs[e];
+            for (int e = tid; e < (np - 1) * k; e += nthreads) dst[e] = logs[e];
         }
         // off(A) and Σ diag² over the same block partition the rounds use (every
         // stored entry once; off-diagonal entries stand for both triangles).
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
         // 1e-12·‖A‖_F.  Every thread sums the per-warp partials in the same order,
         // so the decision is uniform; red[] is next written a whole sweep later.
         double o = 0.0, t = 0.0;
-        for (int w = 0; w < kValWarps; ++w) {
+        for (int w = 0; w <= nwork; ++w) {
             o += red[2 * w];
             t += red[2 * w + 1];
         }
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     }
     __syncthreads();  // the last flush and the final matrix are complete
     const double* A = sm + cur / 8;
-    for (int p = tid; p < np; p += kValThreads) diag_out[p] = A[addr_of(p, p, k)];
+    for (int p = tid; p < np; p += nthreads) diag_out[p] = A[addr_of(p, p, k)];
     if (tid == 0) {
         info[0] = rounds;
         info[1] = sweeps_done;
@@ -514,7 +517,16 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
     auto* rot = sc.alloc_n<double2>(static_cast<size_t>(kMaxSweeps) * (np - 1) * k);
     double* dpos = sc.alloc_n<double>(static_cast<size_t>(np));
     int* info = sc.alloc_n<int>(2);
-    jacobi_values_kernel<<<1, kValThreads, smem, sc.stream()>>>(C, ldc, n, rot, dpos, info, eig_probe_buffer());
+    // Upper bound on the off-diagonal blocks the workers own (all k(k-1)/2; the
+    // pivot warp takes a few of them).  At n = 64 the 15-warp cap is exact.
+    const int blocks = k * (k - 1) / 2;
+    static const int force_warps = [] {
+        const char* e = std::getenv("TS_EIG_WORK_WARPS");
+        return e ? std::atoi(e) : 0;
+    }();
+    int work = std::min(kWorkWarps, std::max(1, (blocks + 31) / 32));
+    if (force_warps > 0) work = std::max(work, std::min(force_warps, kWorkWarps));
+    jacobi_values_kernel<<<1, 32 * (work + 1), smem, sc.stream()>>>(C, ldc, n, rot, dpos, info, eig_probe_buffer());
     TS_LAUNCH_CHECK();
     jacobi_vectors_kernel<<<(np + 3) / 4, 128, 0, sc.stream()>>>(n, rot, dpos, info, lambda, V);
     TS_LAUNCH_CHECK();

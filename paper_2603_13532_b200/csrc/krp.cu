@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "../../include/tucksum_cuda.h"
 #include "kernels.cuh"
 
 namespace ts {
@@ -377,13 +378,18 @@ void launch_krp_contract(const KrpArgs& args_in, int max_shape, CallScratch& sc)
     }
     dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>(args.order),
               static_cast<unsigned>(cchunks * args.splits));
-    auto go = [&](auto kern) {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid, kThreads, smem, sc.stream()>>>(args);
-        TS_LAUNCH_CHECK();
-    };
-    if (RT == 32) go(krp_dmma_kernel<32>);
-    else go(krp_dmma_kernel<64>);
+    // Thread-safe one-time setup (the attribute call must not run inside a CUDA
+    // graph capture of a later call).
+    static const bool configured = [] {
+        TS_CUDA_CHECK(cudaFuncSetAttribute(krp_dmma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TS_CUDA_CHECK(cudaFuncSetAttribute(krp_dmma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        return true;
+    }();
+    (void)configured;
+    if (smem > 200 * 1024) throw Error(TS_UNSUPPORTED, "stage B: block ranks too large for shared memory");
+    if (RT == 32) krp_dmma_kernel<32><<<grid, kThreads, smem, sc.stream()>>>(args);
+    else krp_dmma_kernel<64><<<grid, kThreads, smem, sc.stream()>>>(args);
+    TS_LAUNCH_CHECK();
     sc.launches += 1;
     if (args.splits > 1) {
         krp_split_reduce<<<dim3(64, static_cast<unsigned>(args.order)), 256, 0, sc.stream()>>>(args);

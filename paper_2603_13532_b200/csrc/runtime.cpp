@@ -40,6 +40,20 @@ void* HostStage::put(const void* src, size_t bytes) {
     return p;
 }
 
+size_t HostStage::footprint() const {
+    size_t f = used_;
+    for (const auto& c : retired_) f += c.cap;
+    return f;
+}
+
+void HostStage::reserve(size_t bytes) {
+    if (cap_ - used_ >= bytes) return;
+    if (buf_) retired_.push_back({buf_, cap_});
+    cap_ = std::max<size_t>(bytes, size_t(1) << 20);
+    TS_CUDA_CHECK(cudaMallocHost(reinterpret_cast<void**>(&buf_), cap_));
+    used_ = 0;
+}
+
 CallScratch::~CallScratch() {
     for (void* p : ptrs_) cudaFreeAsync(p, stream_);
 }

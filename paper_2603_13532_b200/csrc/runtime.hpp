@@ -36,6 +36,11 @@ public:
     void reset();
     // Returns a pinned pointer holding a copy of src (bytes), 256-aligned.
     void* put(const void* src, size_t bytes);
+    // Upper bound of the bytes the calls since the last reset() staged.
+    size_t footprint() const;
+    // One pinned buffer of at least `bytes` (so a CUDA-graph capture never has
+    // to allocate pinned memory mid-capture).
+    void reserve(size_t bytes);
 
 private:
     struct Chunk {

@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = [
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
     "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
+    "ts_ctx_set_graphs", "ts_ctx_graph_replays",
 ]
 
 
@@ -89,6 +90,9 @@ def lib():
         L.ts_ctx_stream.restype = C.c_void_p
         L.ts_ctx_stream.argtypes = [C.c_void_p]
         L.ts_ctx_launch_count.restype = i64
+        L.ts_ctx_graph_replays.restype = i64
+        L.ts_ctx_graph_replays.argtypes = [C.c_void_p]
+        L.ts_ctx_set_graphs.argtypes = [C.c_void_p, C.c_int]
         L.ts_ctx_launch_count.argtypes = [C.c_void_p]
         L.ts_batch_count.restype = i64
         L.ts_batch_bytes.restype = i64
@@ -470,7 +474,8 @@ class DeviceBatch:
 
     def free(self):
         if self.handle:
-            lib().ts_batch_free(self.handle)
+            if self.engine is None or self.engine.handle:  # the context (and its stream) still exists
+                lib().ts_batch_free(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -483,8 +488,9 @@ class DeviceBatch:
 class DeviceResult:
     """A dense-core Tucker tensor in device memory (ts_result)."""
 
-    def __init__(self, handle: C.c_void_p):
+    def __init__(self, handle: C.c_void_p, engine: "Engine" = None):
         self.handle = handle
+        self.engine = engine  # results must not outlive their context's stream
         L = lib()
         order = int(L.ts_result_order(handle))
         dims = np.zeros(order, dtype=np.int64)
@@ -528,7 +534,8 @@ class DeviceResult:
 
     def free(self):
         if self.handle:
-            lib().ts_result_free(self.handle)
+            if self.engine is None or self.engine.handle:  # the context (and its stream) still exists
+                lib().ts_result_free(self.handle)
             self.handle = None
 
     def __del__(self):
@@ -588,6 +595,14 @@ class Engine:
         _check(lib().ts_sym_eig_tri(self.handle, i64(n), _p(a), _p(vals), _p(vecs), C.byref(fl), C.byref(ms)))
         return vals, vecs, bool(fl.value), float(ms.value)
 
+    def set_graphs(self, on: bool):
+        """CUDA-graph replay of repeated identical calls (ts_ctx_set_graphs)."""
+        _check(lib().ts_ctx_set_graphs(self.handle, 1 if on else 0))
+
+    @property
+    def graph_replays(self) -> int:
+        return int(lib().ts_ctx_graph_replays(self.handle))
+
     def last_paths(self):
         """(qr_fallback_modes, svd_fallback_modes) of the last krp_sum."""
         a, b = C.c_int(), C.c_int()
@@ -639,7 +654,7 @@ class Engine:
         fn = lib().ts_kron_sum if kron else lib().ts_krp_sum
         _check(fn(self.handle, batch.handle, _p(w), wd.ctypes.data_as(i64p), u64(seed.seed), u64(seed.stream),
                   C.c_double(eps), cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
-        return DeviceResult(h)
+        return DeviceResult(h, self)
 
     def kron_sum(self, batch: DeviceBatch, weights, widths, seed: RngSeed, eps: float, max_rank=None) -> DeviceResult:
         return self.krp_sum(batch, weights, widths, seed, eps, max_rank, Strategy.Kron)
@@ -681,7 +696,7 @@ class Engine:
         h = C.c_void_p()
         _check(lib().ts_lazy_sum(self.handle, batch.handle, _p(w), C.c_double(eps),
                                  cap.ctypes.data_as(i64p) if cap is not None else None, C.byref(h)))
-        return DeviceResult(h)
+        return DeviceResult(h, self)
 
     def krp_sum_many(self, batches: Sequence[DeviceBatch], weights: Sequence, widths, seeds: Sequence[RngSeed],
                      eps: float, max_rank=None, lanes: int = 8) -> List[DeviceResult]:
@@ -709,7 +724,7 @@ class Engine:
                                      sd.ctypes.data_as(C.POINTER(C.c_uint64)), st.ctypes.data_as(C.POINTER(C.c_uint64)),
                                      C.c_double(eps), cap.ctypes.data_as(i64p) if cap is not None else None,
                                      C.c_int(lanes), out))
-        return [DeviceResult(C.c_void_p(out[i])) for i in range(n)]
+        return [DeviceResult(C.c_void_p(out[i]), self) for i in range(n)]
 
     def effective_subrank(self, batch: DeviceBatch, weights, eps: float, oversampling, strategy: "Strategy" = None):
         order = batch.order
