@@ -360,7 +360,14 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
                 for (int i = lane; i < m; i += 32) ga = fma(lds64(wp + 8u * i), lds64(wq + 8u * i), ga);
                 ga = warp_sum(ga);
                 const double al = nrm[p], be = nrm[q];
-                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be) || fabs(ga) <= abs_floor) continue;
+                // Also skip when either column is itself below 1e-15·σ₁: such a
+                // column is rounding noise of a rank-deficient input (its σ falls
+                // under the 1e-14·σ₁ rank floor whatever its direction), and
+                // rotating it against a signal column only re-randomises it —
+                // every sweep would find O(1) relative coupling again.
+                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be) || fabs(ga) <= abs_floor ||
+                    fmin(al, be) <= abs_floor)
+                    continue;
                 double c, s, t;
                 jacobi_rotation(al, be, ga, c, s, t);
                 for (int i = lane; i < m; i += 32) {
