@@ -1583,6 +1583,7 @@ int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_b
                     double* out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_tucker_inner: null argument");
+        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "tucker_inner of sharded batches: use a context without NCCL");
         *out = inner_impl(ctx, x, wx, y, wy);
     });
 }
@@ -1590,6 +1591,7 @@ int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_b
 int ts_rel_error_to_sum(ts_ctx* ctx, const ts_result* r, const ts_batch* batch, const double* weights, double* out) {
     return guarded([&] {
         if (!ctx || !r || !out) invalid("ts_rel_error_to_sum: null argument");
+        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "rel_error_to_sum of a sharded batch: use a context without NCCL");
         ResultView rv(ctx, r);
         const double one = 1.0;
         const double xx = inner_impl(ctx, &rv.b, &one, &rv.b, &one);
