@@ -158,3 +158,31 @@ def test_kron_rejects_oversized_sketch(engine):
             engine.kron_sum(batch, [1.0], [3, 0, 3], T.RngSeed(1, 1), 1e-8)
     finally:
         batch.free()
+
+
+def test_kron_cfg5_full_size_parity(engine):
+    """BASELINE config 5 at full size through the Kron sketch (K = 256, n = 8192,
+    widths = kron_sketch_dims(64-targets) = (8, 8, 8), cap 48): device vs CPU
+    oracle on identical inputs and Ω — 1e-10 on factors × core, same ranks, and
+    the same error to the exact sum to 3 significant digits (device error kernel
+    vs the oracle's Gram-based error)."""
+    from paper_2603_13532_b200.workloads import make_workload
+
+    wl = make_workload(5)
+    widths = T.kron_sketch_dims(wl.widths, wl.dims)
+    assert widths == [8, 8, 8]
+    seed = (wl.seed.seed, wl.seed.stream)
+    threads = O.num_threads()
+    ref, _ = O.kron_sum(wl.summands, wl.weights, widths, seed=seed, eps=wl.eps, cap=wl.cap, threads=threads)
+    batch = engine.upload(wl.summands)
+    try:
+        res = engine.kron_sum(batch, wl.weights, widths, wl.seed, wl.eps, wl.cap)
+        e_dev = engine.rel_error_to_sum(res, batch, wl.weights)
+        out = res.to_tucker()
+        res.free()
+    finally:
+        batch.free()
+    assert out.ranks == ref.ranks == [48, 48, 48]
+    assert O.rel_error_to_sum(out, [ref], [1.0]) <= PARITY
+    e_ref = O.rel_error_gram(ref, wl.summands, wl.weights, threads)
+    assert abs(e_dev - e_ref) <= 5e-4 * e_ref
