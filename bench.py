@@ -356,6 +356,19 @@ def main():
                       "tucker_inner structure), outside the timed region"}
         res.free()
 
+    # Host generation of Ω (the reference's libstdc++ stream) for a fresh seed,
+    # outside the timed region: the reference times it inside its call
+    # (src/sketch.cpp:91-95); here it is generated once and cached on the device.
+    omega = None
+    if args.strategy == "krp" and rank == 0:
+        t0 = time.perf_counter()
+        eng.prepare_omega(wl.dims, max(wl.widths), T.RngSeed(wl.seed.seed + 1, wl.seed.stream))
+        om = 1000.0 * (time.perf_counter() - t0)
+        omega = {"host_generation_and_upload_ms": om,
+                 "ms_per_step_if_regenerated": ms + om,
+                 "e2e_ms_per_step_if_regenerated": (e2e["ms_per_step"] + om) if e2e else None,
+                 "note": "the reference regenerates Ω inside every call; here it is cached per (seed, stream, dims, s)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and krp:
         cpu = cpu_baseline(wl)
@@ -370,7 +383,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages)),
                 "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]},
-                "accuracy": err}
+                "accuracy": err, "omega": omega}
         print(json.dumps(line), flush=True)
     batch.free()
     eng.close()
