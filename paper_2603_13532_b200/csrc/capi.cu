@@ -1212,8 +1212,11 @@ ts_result* run_sum(ts_ctx* ctx, const ts_batch* b, const double* weights, const 
                  std::vector<double>(weights, weights + b->count)};
     auto it = ctx->graph_cache.find(key);
     if (it == ctx->graph_cache.end()) {
-        if (ctx->graph_seen.insert(key).second)  // first sighting: plain call (also does one-time setups)
+        if (!ctx->graph_seen.count(key)) {  // first sighting: plain call (also does one-time setups)
+            if (ctx->graph_seen.size() >= 256) ctx->graph_seen.clear();  // bounded: calls that never repeat
+            ctx->graph_seen.insert(key);
             return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method);
+        }
         // Second sighting: run it plainly once more to learn the output ranks, then capture.
         std::unique_ptr<ts_result> probe(sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method));
         if (!ctx->spec_ok) return probe.release();  // the speculative path was rejected: no graph
