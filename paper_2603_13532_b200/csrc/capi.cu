@@ -1526,6 +1526,10 @@ int ts_batch_free(ts_batch* b) {
     return guarded([&] {
         if (!b) return;
         cudaSetDevice(b->ctx->device);
+        // Graphs captured on this batch can never replay again: release them
+        // (and the memory their allocation nodes reserve).
+        for (auto it = b->ctx->graph_cache.begin(); it != b->ctx->graph_cache.end();)
+            it = it->first.batch == b->id ? b->ctx->graph_cache.erase(it) : std::next(it);
         cudaStream_t st = b->ctx->stream;  // stream-ordered: safe while kernels are still queued
         for (auto* f : b->F)
             if (f) cudaFreeAsync(f, st);
