@@ -1,6 +1,6 @@
 #!/bin/bash
 # Full GPU suite + smoke + bench lines for configs 1-5 with CUDA-graph replay.
-O=gpurun_out/r23
+O=gpurun_out/r35
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo "pytest rc=$?" >> $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
