@@ -174,6 +174,13 @@ struct ts_ctx {
     std::vector<cudaEvent_t> events;
     int last_qr_fallbacks = 0, last_svd_fallbacks = 0;  // accurate-path uses in the last call
     int last_eig_fallbacks = 0;  // tridiagonal-eigensolver rejections (Jacobi recomputes) in the last call
+    // ST-HOSVD modes that needed the accurate path in the last synchronous call
+    // with these sketch dims: the next such call goes there directly (a pure
+    // performance hint — the accurate path is valid for every input; every 16th
+    // call re-tries the fast path).
+    std::vector<std::int64_t> hint_q;
+    unsigned hint_accurate = 0;
+    std::uint64_t hint_calls = 0;
     // Speculative tail (see krp_sum_impl): on while the last call needed no
     // accurate-path fallback.
     bool spec_ok = true;
@@ -985,6 +992,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         const double theta = eps * eps * hss / static_cast<double>(d);
         ctx->last_svd_fallbacks = 0;
         ctx->last_eig_fallbacks = 0;
+        const std::vector<std::int64_t> qv(q, q + d);
+        const bool hints = !spec_g && ctx->hint_q == qv && (++ctx->hint_calls % 16) != 0;
+        unsigned accurate_modes = 0;
         std::vector<int> mode_order(static_cast<size_t>(d));
         std::iota(mode_order.begin(), mode_order.end(), 0);
         std::stable_sort(mode_order.begin(), mode_order.end(), [&](int x, int y) { return cur_shape[x] < cur_shape[y]; });
@@ -1013,6 +1023,20 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             }
             static const bool dbg_sweeps = std::getenv("TS_DEBUG_SWEEPS") != nullptr;
             int* dsw = dbg_sweeps ? sc.alloc_n<int>(1) : nullptr;
+            const std::int64_t capk = max_rank ? max_rank[k] : 0;
+            if (hints && (ctx->hint_accurate >> k & 1u)) {
+                // Last time this mode's Gram decision was not provably exact: go
+                // straight to the accurate TSQR + one-sided Jacobi SVD.
+                double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
+                unfolding_svd_accurate(X, rest, qk, sigma, Pk[k], sc);
+                std::vector<double> sig(static_cast<size_t>(qk));
+                TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
+                                              cudaMemcpyDeviceToHost, st));
+                TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                rank[k] = hosvd_rank(sig, eps, theta, capk);
+                ++ctx->last_svd_fallbacks;
+                accurate_modes |= 1u << k;
+            } else {
             // Eigensolver: tridiagonalization + bisection + inverse iteration
             // (eig_tri.cu) with a device acceptance check; on rejection the
             // two-sided Jacobi (eig.cu) recomputes — in the speculative path via
@@ -1030,7 +1054,6 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             } else {
                 ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
             }
-            const std::int64_t capk = max_rank ? max_rank[k] : 0;
             std::int64_t rk = 0;
             if (spec_g && !dsw) {
                 // At ε = 0 the fast-path rank is fixed (cap, else q); its checks run on the device.
@@ -1065,9 +1088,12 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                     TS_CUDA_CHECK(cudaStreamSynchronize(st));
                     rk = hosvd_rank(sig, eps, theta, capk);
                     ++ctx->last_svd_fallbacks;
+                    accurate_modes |= 1u << k;
                 }
             }
             rank[k] = rk;
+            }
+            const std::int64_t rk = rank[k];
             // g ← g ×_k P_kᵀ
             std::int64_t left = 1, right = 1, total_out = rk;
             for (int j = 0; j < d; ++j) {
@@ -1105,6 +1131,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             }
             g = gn;
             cur_shape[k] = rk;
+        }
+        if (!spec_g) {
+            ctx->hint_q = qv;
+            ctx->hint_accurate = accurate_modes;
         }
     }
     mark(ctx, 10);

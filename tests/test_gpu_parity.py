@@ -451,3 +451,28 @@ def test_sym_eig_tri_matches_oracle(engine):
             assert np.linalg.norm(vecs.T @ vecs - np.eye(n)) <= 1e-12
             assert np.linalg.norm(vecs @ np.diag(vals) @ vecs.T - c) <= 1e-12 * np.linalg.norm(c)
     print("tri-eig rejections:", sum(engine.sym_eig_tri(c)[2] for c in cases), "of", len(cases))
+
+
+def test_accurate_path_hint_is_bitwise_neutral():
+    """Config 3 needs the accurate ST-HOSVD path for its parameter modes; after
+    the first call a context goes there directly (a performance hint).  Repeated
+    calls and a fresh context give bitwise the same result."""
+    wl = make_workload(3)
+    outs = []
+    for fresh in (True, False):
+        eng = T.Engine(0)
+        try:
+            batch = eng.upload(wl.summands)
+            runs = 1 if fresh else 3
+            for _ in range(runs):
+                res = eng.krp_sum(batch, wl.weights, wl.widths, wl.seed, wl.eps, wl.cap)
+                outs.append(res.to_tucker())
+                res.free()
+            assert eng.last_paths()[1] >= 1  # accurate path used
+            batch.free()
+        finally:
+            eng.close()
+    for o in outs[1:]:
+        assert o.ranks == outs[0].ranks
+        assert all(np.array_equal(a, b) for a, b in zip(o.factors, outs[0].factors))
+        assert np.array_equal(o.dense_core(), outs[0].dense_core())
