@@ -58,24 +58,26 @@ __device__ __forceinline__ void householder_params(double c0, double tail, doubl
 // makeHouseholder convention, see householder_params) and publishes the scaled
 // vector v = [1; x·inv] through a double-buffered shared array; after ONE
 // barrier every warp applies H_k = I − τ·v·vᵀ to its own columns j > k.
-constexpr int kQrRowsPerLane = 8;  // 256 rows
-constexpr int kQrFThreads = 512;  // factor kernel: 16 warps × 6 columns (96 cols)
+constexpr int kQrFThreads = 512;  // factor kernel: 16 warps; ≤ 8 rows per lane (256-row blocks), ≤ 6 column slots (96 cols)
 constexpr int kQrFWarps = kQrFThreads / 32;
-constexpr int kQrFCPW = 6;
 
+// RPL rows per lane (32·RPL rows per block), CPW column slots per warp (16·CPW
+// columns): instantiated for the launch's largest block so small blocks (the
+// 64-row sketches of short modes, the last TSQR levels) carry no dead rows.
+template <int RPL, int CPW>
 __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* __restrict__ tasks) {
     const QrTask tk = tasks[blockIdx.x];
     const int rows = tk.rows, cols = tk.cols, kk = min(rows, cols);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __shared__ __align__(16) double vbuf[2][kQrRowsPerLane * 32];
+    __shared__ __align__(16) double vbuf[2][RPL * 32];
     __shared__ double s_tau[2];
-    double a[kQrFCPW][kQrRowsPerLane];
+    double a[CPW][RPL];
 #pragma unroll
-    for (int i = 0; i < kQrFCPW; ++i) {
+    for (int i = 0; i < CPW; ++i) {
         const int c = warp + kQrFWarps * i;
         const double* __restrict__ col = tk.A + static_cast<int64_t>(c < cols ? c : 0) * tk.lda + lane;
 #pragma unroll
-        for (int t = 0; t < kQrRowsPerLane; ++t)
+        for (int t = 0; t < RPL; ++t)
             a[i][t] = (c < cols && lane + 32 * t < rows) ? __ldg(col + 32 * t) : 0.0;
     }
     for (int k = 0; k < kk; ++k) {
@@ -87,12 +89,12 @@ __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* 
             auto col = [&](int t) {
                 double v = a[0][t];
 #pragma unroll
-                for (int i = 1; i < kQrFCPW; ++i) v = i == oi ? a[i][t] : v;
+                for (int i = 1; i < CPW; ++i) v = i == oi ? a[i][t] : v;
                 return v;
             };
             double tail = 0.0, c0 = 0.0;
 #pragma unroll
-            for (int t = 0; t < kQrRowsPerLane; ++t) {
+            for (int t = 0; t < RPL; ++t) {
                 const int r = lane + 32 * t;
                 const double v = col(t);
                 if (r > k && r < rows) tail = fma(v, v, tail);
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* 
             double beta, tau, inv;
             householder_params(c0, tail, &beta, &tau, &inv);
 #pragma unroll
-            for (int t = 0; t < kQrRowsPerLane; ++t) {
+            for (int t = 0; t < RPL; ++t) {
                 const int r = lane + 32 * t;
                 const double xv = col(t);
                 double v = 0.0, nv = xv;
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* 
                 }
                 vbuf[buf][r] = v;
 #pragma unroll
-                for (int i = 0; i < kQrFCPW; ++i) a[i][t] = i == oi ? nv : a[i][t];
+                for (int i = 0; i < CPW; ++i) a[i][t] = i == oi ? nv : a[i][t];
             }
             if (lane == 0) {
                 s_tau[buf] = tau;
@@ -129,34 +131,34 @@ __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* 
             const double* vb = vbuf[buf] + lane;  // v is 0 above row k
             // All owned columns' dot products first, then one interleaved
             // reduction (their shuffle latencies overlap), then the updates.
-            double dot[kQrFCPW];
+            double dot[CPW];
 #pragma unroll
-            for (int i = 0; i < kQrFCPW; ++i) {
+            for (int i = 0; i < CPW; ++i) {
                 dot[i] = 0.0;
 #pragma unroll
-                for (int t = 0; t < kQrRowsPerLane; ++t) dot[i] = fma(vb[32 * t], a[i][t], dot[i]);
+                for (int t = 0; t < RPL; ++t) dot[i] = fma(vb[32 * t], a[i][t], dot[i]);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-                for (int i = 0; i < kQrFCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
+                for (int i = 0; i < CPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
 #pragma unroll
-            for (int i = 0; i < kQrFCPW; ++i) {
+            for (int i = 0; i < CPW; ++i) {
                 const int c = warp + kQrFWarps * i;
                 const double w = (c > k && c < cols) ? tau * dot[i] : 0.0;  // columns ≤ k are final
 #pragma unroll
-                for (int t = 0; t < kQrRowsPerLane; ++t) a[i][t] = fma(-w, vb[32 * t], a[i][t]);
+                for (int t = 0; t < RPL; ++t) a[i][t] = fma(-w, vb[32 * t], a[i][t]);
             }
         }
     }
 #pragma unroll
-    for (int i = 0; i < kQrFCPW; ++i) {
+    for (int i = 0; i < CPW; ++i) {
         const int c = warp + kQrFWarps * i;
         if (c >= cols) continue;
         double* __restrict__ colA = tk.A + static_cast<int64_t>(c) * tk.lda + lane;
         double* __restrict__ colR = tk.R + static_cast<int64_t>(c) * tk.ldr + lane;
 #pragma unroll
-        for (int t = 0; t < kQrRowsPerLane; ++t) {
+        for (int t = 0; t < RPL; ++t) {
             const int r = lane + 32 * t;
             if (r < rows) colA[32 * t] = a[i][t];
             if (r < kk) colR[32 * t] = r <= c ? a[i][t] : 0.0;
@@ -1006,7 +1008,6 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
     }
     // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
     static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         return true;
     }();
@@ -1022,7 +1023,22 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
                 }
         if (tasks.empty()) continue;
         auto* d = static_cast<const QrTask*>(sc.upload(tasks.data(), tasks.size() * sizeof(QrTask)));
-        tsqr_factor_kernel<<<static_cast<unsigned>(tasks.size()), kQrFThreads, 0, sc.stream()>>>(d);
+        int mrows = 0, mcols = 0;
+        for (const QrTask& t : tasks) {
+            mrows = std::max(mrows, t.rows);
+            mcols = std::max(mcols, t.cols);
+        }
+        const unsigned nb = static_cast<unsigned>(tasks.size());
+        cudaStream_t st = sc.stream();
+        if (mcols <= 64) {
+            if (mrows <= 64) tsqr_factor_kernel<2, 4><<<nb, kQrFThreads, 0, st>>>(d);
+            else if (mrows <= 128) tsqr_factor_kernel<4, 4><<<nb, kQrFThreads, 0, st>>>(d);
+            else tsqr_factor_kernel<8, 4><<<nb, kQrFThreads, 0, st>>>(d);
+        } else {
+            if (mrows <= 64) tsqr_factor_kernel<2, 6><<<nb, kQrFThreads, 0, st>>>(d);
+            else if (mrows <= 128) tsqr_factor_kernel<4, 6><<<nb, kQrFThreads, 0, st>>>(d);
+            else tsqr_factor_kernel<8, 6><<<nb, kQrFThreads, 0, st>>>(d);
+        }
         TS_LAUNCH_CHECK();
         sc.launches += 1;
     }
