@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kQrFThreads) tsqr_factor_kernel(const QrTask* 
 
 // Q formation for one block: Q = H_0 ⋯ H_{kk-1} · [Qin; 0], optional column
 // signs.  Reflector k-1 is prefetched (cp.async) while reflector k is applied.
+template <int CPW>  // column slots per warp (16·CPW columns of Q)
 __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTask* __restrict__ tasks) {
     const QrApplyTask tk = tasks[blockIdx.x];
     const int rows = tk.rows, kk = tk.kk, q = tk.q;
@@ -199,39 +200,39 @@ __global__ void __launch_bounds__(kQrThreads) tsqr_apply_kernel(const QrApplyTas
             // Explicit shared addresses (see tsqr_factor_kernel).
             const unsigned vb = Qb + 8u * static_cast<unsigned>(rows * q + (k & 1) * rows);
             int nc = 0;
-            unsigned cb[kQrMaxCPW];
+            unsigned cb[CPW];
 #pragma unroll
-            for (int i = 0; i < kQrMaxCPW; ++i) {
+            for (int i = 0; i < CPW; ++i) {
                 const int c = warp + kQrWarps * i;
                 if (c < q) nc = i + 1;
                 cb[i] = Qb + 8u * static_cast<unsigned>((c < q ? c : 0) * rows);
             }
-            double dot[kQrMaxCPW];
+            double dot[CPW];
 #pragma unroll
-            for (int i = 0; i < kQrMaxCPW; ++i) dot[i] = 0.0;
+            for (int i = 0; i < CPW; ++i) dot[i] = 0.0;
             for (int r = k + 1 + lane; r < rows; r += 32) {
                 const double vr = lds64(vb + 8u * r);
 #pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i)
+                for (int i = 0; i < CPW; ++i)
                     if (i < nc) dot[i] = fma(vr, lds64(cb[i] + 8u * r), dot[i]);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
-            double w[kQrMaxCPW];
+                for (int i = 0; i < CPW; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
+            double w[CPW];
 #pragma unroll
-            for (int i = 0; i < kQrMaxCPW; ++i) w[i] = i < nc ? tau * (lds64(cb[i] + 8u * k) + dot[i]) : 0.0;
+            for (int i = 0; i < CPW; ++i) w[i] = i < nc ? tau * (lds64(cb[i] + 8u * k) + dot[i]) : 0.0;
             for (int r = k + 1 + lane; r < rows; r += 32) {
                 const double vr = lds64(vb + 8u * r);
 #pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i)
+                for (int i = 0; i < CPW; ++i)
                     if (i < nc) sts64(cb[i] + 8u * r, lds64(cb[i] + 8u * r) - w[i] * vr);
             }
             __syncwarp();
             if (lane == 0)
 #pragma unroll
-                for (int i = 0; i < kQrMaxCPW; ++i)
+                for (int i = 0; i < CPW; ++i)
                     if (i < nc) sts64(cb[i] + 8u * k, lds64(cb[i] + 8u * k) - w[i]);
         }
         cp_async_wait<0>();
@@ -286,13 +287,17 @@ __device__ __forceinline__ void jacobi_rotation(double a, double b, double g, do
 }
 
 __device__ __forceinline__ void pair_of(int r, int pi, int np, int* p, int* q) {
+    // r < np - 1 and pi < np / 2, so one conditional wrap replaces the modulo
+    // (an integer division on the round's critical path).
     int a, b;
     if (pi == 0) {
         a = np - 1;
         b = r;
     } else {
-        a = (r + pi) % (np - 1);
-        b = (r - pi + (np - 1)) % (np - 1);
+        a = r + pi;
+        if (a >= np - 1) a -= np - 1;
+        b = r - pi;
+        if (b < 0) b += np - 1;
     }
     *p = min(a, b);
     *q = max(a, b);
@@ -314,7 +319,8 @@ __device__ void sort_desc_store(const double* key, const double* J, int nc, doub
 // norms are carried through the rotations so each pair needs one reduction.
 __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* __restrict__ R, int64_t ldr, int m,
                                                                  int nc, double* __restrict__ sigma,
-                                                                 double* __restrict__ U) {
+                                                                 double* __restrict__ U,
+                                                                 unsigned long long* __restrict__ prof) {
     extern __shared__ __align__(16) double sm[];
     double* W = sm;             // m × nc (ld m)
     double* J = W + m * nc;     // nc × nc (ld nc)
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
                 // under the 1e-14·σ₁ rank floor whatever its direction), and
                 // rotating it against a signal column only re-randomises it —
                 // every sweep would find O(1) relative coupling again.
-                if (ga == 0.0 || fabs(ga) <= tol * sqrt(al * be) || fabs(ga) <= abs_floor ||
+                if (ga == 0.0 || ga * ga <= (tol * tol) * (al * be) || fabs(ga) <= abs_floor ||
                     fmin(al, be) <= abs_floor)
                     continue;
                 double c, s, t;
@@ -392,7 +398,10 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(const double* _
             }
             __syncthreads();
         }
-        if (!rotated) break;
+        if (!rotated) {
+            if (prof != nullptr && tid == 0) prof[16] = static_cast<unsigned long long>(sweep + 1);
+            break;
+        }
     }
     __syncthreads();
     for (int c = warp; c < nc; c += kJacWarps) {
@@ -1008,7 +1017,8 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
     }
     // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
     static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         return true;
     }();
     (void)configured;
@@ -1057,7 +1067,10 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
         }
         if (tasks.empty()) continue;
         auto* d = static_cast<const QrApplyTask*>(sc.upload(tasks.data(), tasks.size() * sizeof(QrApplyTask)));
-        tsqr_apply_kernel<<<static_cast<unsigned>(tasks.size()), kQrThreads, smem, sc.stream()>>>(d);
+        int mq = 0;
+        for (const QrApplyTask& t : tasks) mq = std::max(mq, t.q);
+        if (mq <= 64) tsqr_apply_kernel<4><<<static_cast<unsigned>(tasks.size()), kQrThreads, smem, sc.stream()>>>(d);
+        else tsqr_apply_kernel<6><<<static_cast<unsigned>(tasks.size()), kQrThreads, smem, sc.stream()>>>(d);
         TS_LAUNCH_CHECK();
         sc.launches += 1;
     }
@@ -1110,7 +1123,7 @@ void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigm
         return true;
     }();
     (void)configured;
-    jacobi_svd_kernel<<<1, kJacThreads, smem, sc.stream()>>>(R, ldr, m, nc, sigma, U);
+    jacobi_svd_kernel<<<1, kJacThreads, smem, sc.stream()>>>(R, ldr, m, nc, sigma, U, eig_probe_buffer());
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
