@@ -756,7 +756,21 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         double* W[TS_MAX_ORDER];
         if (!krp) {
             for (int n = 0; n < d; ++n) W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * yc[n]));
-            kron_stage_b(b, Z, ow, W, yc, d_w, sc, ctx->num_sms);
+            bool fused = false;
+            if (d == 3) {  // one fused launch (kron3.cu)
+                ts::Kron3Args ka{};
+                for (int n = 0; n < 3; ++n) {
+                    ka.Z[n] = Z[n];
+                    ka.W[n] = W[n];
+                    ka.s[n] = static_cast<int>(ow[n]);
+                }
+                ka.natoms = static_cast<int>(b->atoms.size());
+                ka.atoms = b->d_atoms;
+                ka.cores = b->cores;
+                ka.weights = d_w;
+                fused = ts::launch_kron3(ka, b->max_shape, sc);
+            }
+            if (!fused) kron_stage_b(b, Z, ow, W, yc, d_w, sc, ctx->num_sms);
         } else {
             ts::KrpArgs ka{};
             for (int n = 0; n < d; ++n) {

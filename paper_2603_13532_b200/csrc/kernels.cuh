@@ -155,6 +155,20 @@ void launch_kron_gather(const std::vector<KronGather>& g, int64_t C, double* Wt,
 // acc[0] += alpha · <x, y> (single CTA, deterministic; n ≲ 10^6).
 void launch_dot_accumulate(const double* x, const double* y, int64_t n, double alpha, double* acc, CallScratch& sc);
 
+// Kron stage B fused for order 3 (kron3.cu): Wt_n for all three modes in one
+// launch, one CTA per atom.  Returns false (nothing launched) when a block rank
+// exceeds 32 or a mode's sketch width Π_{j≠n} s_j exceeds 96.
+struct Kron3Args {
+    const double* Z[3];  // Z_j = Ω_jᵀF_j (s_j × R_j)
+    double* W[3];        // Wt_n (C_n × R_n)
+    int s[3];
+    int natoms;
+    const Atom* atoms;
+    const double* cores;
+    const double* weights;
+};
+bool launch_kron3(const Kron3Args& args, int max_shape, CallScratch& sc);
+
 int max_tsqr_cols();
 // Device buffer of the values-kernel phase probe (non-null iff TS_EIG_PROFILE is set).
 unsigned long long* eig_probe_buffer();
