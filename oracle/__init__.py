@@ -369,6 +369,23 @@ def partial_sketch(summands, weights, s, seed):
     return ys
 
 
+def partial_sketch_kron(summands, weights, widths, seed):
+    """Kron-sketch Y_n partial sums over `summands` (Y_n: dims[n] × Π_{j≠n} widths[j])."""
+    views = _Views(summands)
+    dims = summands[0].dims
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    wd = np.ascontiguousarray(np.asarray(widths, dtype=np.int64))
+    cols = [int(np.prod([wd[j] for j in range(len(dims)) if j != n])) for n in range(len(dims))]
+    out = np.zeros(sum(int(n) * c for n, c in zip(dims, cols)))
+    _check(lib().or_partial_sketch_ex(views.arr, i64(len(summands)), _p(w), wd.ctypes.data_as(i64p), C.c_int(0),
+                                      u64(seed[0]), u64(seed[1]), _p(out)))
+    ys, off = [], 0
+    for n, c in zip(dims, cols):
+        ys.append(out[off:off + n * c].reshape((n, c), order="F"))
+        off += n * c
+    return ys
+
+
 def partial_core(summands, weights, uhat):
     """h partial sum over `summands` projected on the given bases Û_n."""
     views = _Views(summands)

@@ -1309,6 +1309,33 @@ int or_partial_sketch(const OrTuckerView* views, std::int64_t count, const doubl
     });
 }
 
+// As or_partial_sketch with per-mode plan widths; krp = 0 is the Kron sketch
+// (Ω_n is dims[n] × widths[n], Y_n has Π_{j≠n} widths[j] columns).
+int or_partial_sketch_ex(const OrTuckerView* views, std::int64_t count, const double* weights,
+                         const std::int64_t* widths, int krp, std::uint64_t seed, std::uint64_t stream, double* y_out) {
+    return guarded([&] {
+        std::vector<oracle::Tucker> xs = views_to_tuckers(views, count);
+        std::vector<const oracle::Tucker*> ptrs;
+        for (auto& x : xs) ptrs.push_back(&x);
+        std::vector<double> ws(weights, weights + count);
+        const size_t ou = ptrs.front()->ranks.size();
+        std::vector<std::int64_t> wv(widths, widths + ou);
+        const std::int64_t smax = *std::max_element(wv.begin(), wv.end());
+        std::vector<oracle::Mat> omega(ou), y(ou);
+        for (size_t n = 0; n < ou; ++n) {
+            omega[n] = oracle::gaussian_matrix(ptrs.front()->dims[n], krp ? smax : wv[n],
+                                               oracle::Seed{seed, stream}.substream(n));
+            y[n] = oracle::Mat(ptrs.front()->dims[n], krp ? smax : oracle::complement_product(wv, n));
+        }
+        oracle::accumulate_sketch(ptrs, ws, 0, ptrs.size(), omega, y, krp != 0);
+        size_t off = 0;
+        for (size_t n = 0; n < ou; ++n) {
+            std::memcpy(y_out + off, y[n].a.data(), sizeof(double) * y[n].a.size());
+            off += y[n].a.size();
+        }
+    });
+}
+
 // h_out (prod qdims) = Σ_i w_i G_i ×_n (Û_nᵀ U_n^(i)) over the given summands.
 int or_partial_core(const OrTuckerView* views, std::int64_t count, const double* weights,
                     const double* const* uhat, const std::int64_t* qdims, double* h_out) {

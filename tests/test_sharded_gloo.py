@@ -23,7 +23,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, strategy="krp"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -38,15 +38,19 @@ def _worker(rank, world, port, out_dir):
     wl = make_workload(2, K=7, n_override=[60, 50, 40])
     b, e = shard_range(wl.K, world, rank)
     xs, ws = wl.summands[b:e], wl.weights[b:e]
-    s = wl.widths[0]
     seed = (wl.seed.seed, wl.seed.stream)
-    ys = O.partial_sketch(xs, ws, s, seed)
+    if strategy == "krp":
+        s = wl.widths[0]
+        ys = O.partial_sketch(xs, ws, s, seed)
+    else:  # Kron sketch with the reference's balanced widths
+        ys = O.partial_sketch_kron(xs, ws, O.kron_sketch_dims(wl.widths, wl.dims), seed)
     flat = torch.from_numpy(np.concatenate([y.ravel(order="F") for y in ys]))
     dist.all_reduce(flat)
     ys_full, off = [], 0
-    for n in wl.dims:
-        ys_full.append(flat[off:off + n * s].numpy().reshape((n, s), order="F"))
-        off += n * s
+    for n, y in zip(wl.dims, ys):
+        c = y.shape[1]
+        ys_full.append(flat[off:off + n * c].numpy().reshape((n, c), order="F"))
+        off += n * c
     uh = [O.qr_econ(y)[0] for y in ys_full]
     h = O.partial_core(xs, ws, uh)
     ht = torch.from_numpy(h.ravel(order="F").copy())
@@ -58,15 +62,17 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_two_rank_sharded_sum_matches_single_process(tmp_path):
+@pytest.mark.parametrize("strategy", ["krp", "kron"])
+def test_two_rank_sharded_sum_matches_single_process(tmp_path, strategy):
     import oracle as O
     from paper_2603_13532_b200.workloads import make_workload
 
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, port, str(tmp_path), strategy), nprocs=2, join=True)
     wl = make_workload(2, K=7, n_override=[60, 50, 40])
-    _, info = O.krp_sum(wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), 0.0, cap=wl.cap,
-                        intermediates=True)
+    widths = wl.widths if strategy == "krp" else O.kron_sketch_dims(wl.widths, wl.dims)
+    _, info = O.krp_sum(wl.summands, wl.weights, widths, (wl.seed.seed, wl.seed.stream), 0.0, cap=wl.cap,
+                        intermediates=True, strategy=strategy)
     y = np.load(tmp_path / "y.npy")
     yref = np.concatenate([m.ravel(order="F") for m in info["y"]])
     assert np.linalg.norm(y - yref) <= 1e-13 * np.linalg.norm(yref)
