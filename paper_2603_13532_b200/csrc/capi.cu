@@ -116,7 +116,7 @@ struct OmegaKey {
     }
 };
 
-constexpr int kNumStages = 11;
+constexpr int kNumStages = 11;  // + one extra event: end of stage A's GEMM kernel (before its reduce)
 
 // One captured call (CUDA graph) of the speculative ε = 0 path: everything from
 // stage A to the acceptance flags' download is replayed by one cudaGraphLaunch.
@@ -704,7 +704,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     CallScratch sc(st, hstage);
     const std::int64_t* dims = b->dims;
     if (ctx->timing && ctx->events.empty()) {
-        ctx->events.resize(kNumStages + 1);
+        ctx->events.resize(kNumStages + 3);
         for (auto& e : ctx->events) TS_CUDA_CHECK(cudaEventCreate(&e));
     }
     mark(ctx, 0);
@@ -729,9 +729,14 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             TS_CUDA_CHECK(cudaMemcpyAsync(Y + yoff[n], b->F[n], sizeof(double) * static_cast<size_t>(dims[n] * yc[n]),
                                           cudaMemcpyDeviceToDevice, st));
         mark(ctx, 1);
+        sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage A only
         mark(ctx, 2);
     } else {
-        // ---- Stage A: Z_j = Ω_jᵀ F_j (s × R_j)
+        if (ctx->timing) {
+        sc.before_next_gemm = ctx->events[kNumStages + 1];
+        sc.after_next_gemm = ctx->events[kNumStages + 2];
+    }
+    // ---- Stage A: Z_j = Ω_jᵀ F_j (s × R_j)
         double* Z[TS_MAX_ORDER];
         {
             std::vector<GemmProblem> ps;
@@ -752,6 +757,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
         }
         mark(ctx, 1);
+        sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage A only
         // ---- Stage B: W_n (R_n × s), stored transposed
         double* W[TS_MAX_ORDER];
         if (!krp) {
@@ -1219,11 +1225,19 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     }
     TS_CUDA_CHECK(cudaStreamSynchronize(st));
     if (ctx->timing) {
-        ctx->stage_ms.assign(kNumStages, 0.0);
+        ctx->stage_ms.assign(kNumStages + 1, 0.0);
         for (int i = 0; i < kNumStages; ++i) {
             float ms = 0.f;
             TS_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->events[static_cast<size_t>(i)], ctx->events[static_cast<size_t>(i + 1)]));
             ctx->stage_ms[static_cast<size_t>(i)] = ms;
+        }
+        {  // stage A's GEMM kernel alone (the two hook events around its launch)
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->events[kNumStages + 1], ctx->events[kNumStages + 2]) == cudaSuccess && ms > 0.f &&
+                ms <= ctx->stage_ms[0] + 1e-3)
+                ctx->stage_ms[kNumStages] = ms;
+            else
+                (void)cudaGetLastError();
         }
     }
     return res.release();

@@ -398,9 +398,17 @@ bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallS
     }
     auto* d_groups = static_cast<const TmaGroup*>(sc.upload(groups.data(), groups.size() * sizeof(TmaGroup)));
     const int ng = static_cast<int>(groups.size());
+    if (sc.before_next_gemm) {
+        TS_CUDA_CHECK(cudaEventRecord(sc.before_next_gemm, sc.stream()));
+        sc.before_next_gemm = nullptr;
+    }
     if (mn) gemm_tma_kernel<true><<<static_cast<unsigned>(units), kThreads, kSmemBytes, sc.stream()>>>(d_groups, ng);
     else gemm_tma_kernel<false><<<static_cast<unsigned>(units), kThreads, kSmemBytes, sc.stream()>>>(d_groups, ng);
     TS_LAUNCH_CHECK();
+    if (sc.after_next_gemm) {
+        TS_CUDA_CHECK(cudaEventRecord(sc.after_next_gemm, sc.stream()));
+        sc.after_next_gemm = nullptr;
+    }
     *launched = 1;
     if (!red.empty()) {
         const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));

@@ -67,6 +67,10 @@ public:
     void* upload(const void* src, size_t bytes);
     cudaStream_t stream() const { return stream_; }
     int64_t launches = 0;
+    // Timing hook: when set, the next TMA GEMM launch records these events right
+    // before and after its GEMM kernel (not its split-K reduction) and clears the
+    // hook — the dominant kernel's own duration for bench.py's roofline.
+    cudaEvent_t before_next_gemm = nullptr, after_next_gemm = nullptr;
 
 private:
     cudaStream_t stream_;
