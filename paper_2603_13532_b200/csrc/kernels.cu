@@ -1100,17 +1100,19 @@ void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
     if (count <= 0) return;
     if (cb.n > 96) throw std::invalid_argument("chol_inv: n > 96");
-    const size_t ldc = cb.n <= 32 ? 33 : cb.n <= 64 ? 65 : 97;  // LD of the kernel instance
+    const size_t ldc = cb.n <= 32 ? 33 : cb.n <= 48 ? 49 : cb.n <= 64 ? 65 : 97;  // LD of the kernel instance
     const size_t smem = sizeof(double) * (2 * static_cast<size_t>(cb.n) * ldc + cb.n);
     // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
     static const bool configured = [&] {
         TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         return true;
     }();
     (void)configured;
     if (cb.n <= 32) chol_inv_kernel<32><<<count, 4 * 32, smem, sc.stream()>>>(cb);  // small sketches: half the threads and rows
+    else if (cb.n <= 48) chol_inv_kernel<48><<<count, 4 * 48, smem, sc.stream()>>>(cb);
     else if (cb.n <= 64) chol_inv_kernel<64><<<count, 4 * 64, smem, sc.stream()>>>(cb);
     else chol_inv_kernel<96><<<count, 4 * 96, smem, sc.stream()>>>(cb);
     TS_LAUNCH_CHECK();
