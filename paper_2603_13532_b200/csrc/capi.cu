@@ -1024,31 +1024,48 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             std::int64_t rest = 1;
             for (int j = 0; j < d; ++j)
                 if (j != k) rest *= cur_shape[j];
-            double* X = sc.alloc_n<double>(static_cast<size_t>(rest * qk));
-            ts::launch_unfold_t(g, d, cur_shape, k, X, sc);
-            // Fast path: Gram C = XᵀX (DMMA GEMM) + two-sided Jacobi.
+            // X = g_(k)ᵀ (rest × q_k), formed only where needed: the Gram of the
+            // first and last modes reads g directly, the accurate path needs X.
+            double* X = nullptr;
+            auto need_X = [&]() {
+                if (!X) {
+                    X = sc.alloc_n<double>(static_cast<size_t>(rest * qk));
+                    ts::launch_unfold_t(g, d, cur_shape, k, X, sc);
+                }
+                return X;
+            };
+            const bool hinted = hints && (ctx->hint_accurate >> k & 1u);
+            // Fast path: Gram C = g_(k)·g_(k)ᵀ (DMMA GEMM) + two-sided Jacobi.
             double* C = sc.alloc_n<double>(static_cast<size_t>(qk * qk));
             double* lam = sc.alloc_n<double>(static_cast<size_t>(qk));
-            {
+            if (!hinted) {
                 GemmProblem p{};
                 p.M = p.N = static_cast<int>(qk);
                 p.K = static_cast<int>(rest);
-                p.A = X;
-                p.lda = rest;
-                p.B = X;
-                p.ldb = rest;
                 p.C = C;
                 p.ldc = qk;
-                ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
+                if (k == 0) {  // g as a q_0 × rest matrix: C = g·gᵀ
+                    p.A = p.B = g;
+                    p.lda = p.ldb = qk;
+                    ts::launch_grouped_gemm(Layout::NT, {p}, sc, ctx->num_sms);
+                } else if (k == d - 1) {  // g as a rest × q_last matrix M: C = MᵀM
+                    p.A = p.B = g;
+                    p.lda = p.ldb = rest;
+                    ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
+                } else {
+                    p.A = p.B = need_X();
+                    p.lda = p.ldb = rest;
+                    ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
+                }
             }
             static const bool dbg_sweeps = std::getenv("TS_DEBUG_SWEEPS") != nullptr;
             int* dsw = dbg_sweeps ? sc.alloc_n<int>(1) : nullptr;
             const std::int64_t capk = max_rank ? max_rank[k] : 0;
-            if (hints && (ctx->hint_accurate >> k & 1u)) {
+            if (hinted) {
                 // Last time this mode's Gram decision was not provably exact: go
                 // straight to the accurate TSQR + one-sided Jacobi SVD.
                 double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
-                unfolding_svd_accurate(X, rest, qk, sigma, Pk[k], sc);
+                unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc);
                 std::vector<double> sig(static_cast<size_t>(qk));
                 TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
                                               cudaMemcpyDeviceToHost, st));
@@ -1101,7 +1118,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 rk = gram_rank(lv, eps, theta, capk, &ok);
                 if (!ok) {
                     double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
-                    unfolding_svd_accurate(X, rest, qk, sigma, Pk[k], sc);
+                    unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc);
                     std::vector<double> sig(static_cast<size_t>(qk));
                     TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
                                                   cudaMemcpyDeviceToHost, st));
