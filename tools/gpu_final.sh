@@ -1,7 +1,7 @@
 #!/bin/bash
 # End-of-round evidence: full GPU suite, smoke, bench lines (configs 1-5, Kron,
 # Lazy), reference arm, config-5 launch list (kernel shares).
-O=gpurun_out/final2
+O=gpurun_out/final3
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo "pytest rc=$?" >> $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
