@@ -767,7 +767,8 @@ def _validate_request(summands, weights):  # reference src/sketch.cpp:16-30
 
 def effective_subrank(summands, weights, eps, oversampling, strategy=Strategy.Krp, seed=RngSeed(),
                       engine: Optional[Engine] = None) -> SketchPlan:
-    """Plan stage for Strategy.Krp / Strategy.Kron (reference src/sketch.cpp:272-358), on the GPU."""
+    """Plan stage (reference src/sketch.cpp:272-358), on the GPU: Krp → uniform max target,
+    Kron → kron_sketch_dims(targets), Lazy / Eager → the targets themselves (:340-346)."""
     _validate_request(summands, weights)
     if eps < 0:
         raise ValueError("tolerance must be nonnegative")
@@ -777,14 +778,15 @@ def effective_subrank(summands, weights, eps, oversampling, strategy=Strategy.Kr
         raise ValueError("oversampling vector must have one entry per mode")
     if any(p < 0 for p in ov):
         raise ValueError("oversampling must be nonnegative")
-    if strategy not in (Strategy.Krp, Strategy.Kron):
-        raise NotImplementedError("only Strategy.Krp / Strategy.Kron plans are on the B200 path")
     eng = engine or default_engine()
     batch = eng.upload(summands)
     try:
-        eff, tg, wd = eng.effective_subrank(batch, weights, eps, ov, strategy)
+        eff, tg, wd = eng.effective_subrank(batch, weights, eps, ov,
+                                            Strategy.Kron if strategy == Strategy.Kron else Strategy.Krp)
     finally:
         batch.free()
+    if strategy in (Strategy.Lazy, Strategy.Eager):
+        wd = list(tg)
     return SketchPlan(strategy, eff, ov, tg, wd, eps, seed)
 
 
