@@ -476,3 +476,18 @@ def test_accurate_path_hint_is_bitwise_neutral():
         assert o.ranks == outs[0].ranks
         assert all(np.array_equal(a, b) for a, b in zip(o.factors, outs[0].factors))
         assert np.array_equal(o.dense_core(), outs[0].dense_core())
+
+
+def test_plans_for_every_strategy_match_oracle(engine):
+    """effective_subrank on the device for Krp / Kron / Lazy / Eager (reference
+    src/sketch.cpp:340-346): ranks and targets equal the oracle's; widths follow
+    each strategy's rule."""
+    xs = [random_tucker([13, 9, 11], [2, 3, 2], (61, i)) for i in range(4)]
+    ws = [1.0 + 0.25 * i for i in range(4)]
+    eff, tg, wd_krp = O.effective_subrank(xs, ws, 1e-6, 2, strategy="krp")
+    _, _, wd_kron = O.effective_subrank(xs, ws, 1e-6, 2, strategy="kron")
+    for strat, want in ((T.Strategy.Krp, wd_krp), (T.Strategy.Kron, wd_kron), (T.Strategy.Lazy, tg),
+                        (T.Strategy.Eager, tg)):
+        plan = T.effective_subrank(xs, ws, 1e-6, 2, strat, engine=engine)
+        assert plan.strategy == strat
+        assert plan.effective_ranks == eff and plan.targets == tg and plan.mode_sketch_dims == want
