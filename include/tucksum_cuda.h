@@ -96,6 +96,13 @@ int64_t ts_ctx_launch_count(ts_ctx* ctx);
 /* ---- device-resident summand storage ---- */
 /* Copies K summands (host memory) to the device in the stacked formal-sum layout. */
 int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* summands, int64_t count, ts_batch** out);
+/* The same from data already in the stacked formal-sum layout (reference
+ * formal_sum, src/tucker.cpp:183-226, with dense cores): factors[j] is one
+ * column-major dims[j] × (Σ_k ranks[k*order + j]) host array per mode (the
+ * summands' factors side by side), cores the K dense cores concatenated, each
+ * column-major.  One H2D copy per mode + one for the cores. */
+int ts_batch_upload_stacked(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t count, const int64_t* ranks,
+                            const double* const* factors, const double* cores, ts_batch** out);
 int ts_batch_free(ts_batch* batch);
 int64_t ts_batch_count(const ts_batch* batch);
 /* Device bytes held by the batch (factors + cores + atom table). */

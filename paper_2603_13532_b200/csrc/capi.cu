@@ -1597,6 +1597,70 @@ int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_bat
     });
 }
 
+// Summands already in the stacked formal-sum layout on the host (per mode one
+// n_j × R_j column-major slab, dense cores concatenated in summand order): one
+// H2D copy per mode plus one for the cores, no per-summand views.
+int ts_batch_upload_stacked(ts_ctx* ctx, int64_t order, const int64_t* dims, int64_t count, const int64_t* ranks,
+                            const double* const* factors, const double* cores, ts_batch** out) {
+    return guarded([&] {
+        if (!ctx || !out || !dims || !ranks || !factors || !cores) invalid("ts_batch_upload_stacked: null argument");
+        if (count < 1) invalid("sum request needs matching, nonempty summands and weights");
+        if (order < 1) invalid("TuckerTensor: order must be >= 1");
+        if (order > TS_MAX_ORDER) throw ts::Error(TS_UNSUPPORTED, "order exceeds TS_MAX_ORDER");
+        const int d = static_cast<int>(order);
+        auto b = std::make_unique<ts_batch>();
+        static std::atomic<std::uint64_t> next_id{1u << 30};
+        b->id = next_id++;
+        b->ctx = ctx;
+        b->order = d;
+        b->count = count;
+        std::int64_t core_elems = 0;
+        b->atoms.resize(static_cast<size_t>(count));
+        for (int j = 0; j < d; ++j) {
+            if (dims[j] < 1) invalid("TuckerTensor: dims and ranks must be positive");
+            if (factors[j] == nullptr) invalid("TuckerTensor: one factor matrix per mode required");
+            b->dims[j] = dims[j];
+        }
+        for (std::int64_t i = 0; i < count; ++i) {
+            ts::Atom& at = b->atoms[static_cast<size_t>(i)];
+            at.summand = static_cast<int>(i);
+            at.core_off = core_elems;
+            std::int64_t e = 1;
+            for (int j = 0; j < d; ++j) {
+                const std::int64_t r = ranks[i * d + j];
+                if (r < 1) invalid("TuckerTensor: dims and ranks must be positive");
+                at.col[j] = static_cast<int>(b->R[j]);
+                at.shape[j] = static_cast<int>(r);
+                b->R[j] += r;
+                b->max_shape = std::max(b->max_shape, at.shape[j]);
+                e *= r;
+            }
+            core_elems += e;
+        }
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        std::int64_t bytes = 0;
+        for (int j = 0; j < d; ++j) {
+            const size_t n = sizeof(double) * static_cast<size_t>(b->dims[j] * b->R[j]);
+            TS_CUDA_CHECK(cudaMallocAsync(&b->F[j], n, st));
+            TS_CUDA_CHECK(cudaMemcpyAsync(b->F[j], factors[j], n, cudaMemcpyHostToDevice, st));
+            bytes += static_cast<std::int64_t>(n);
+        }
+        TS_CUDA_CHECK(cudaMallocAsync(&b->cores, sizeof(double) * static_cast<size_t>(core_elems), st));
+        TS_CUDA_CHECK(cudaMemcpyAsync(b->cores, cores, sizeof(double) * static_cast<size_t>(core_elems),
+                                      cudaMemcpyHostToDevice, st));
+        b->core_elems = core_elems;
+        bytes += sizeof(double) * core_elems;
+        TS_CUDA_CHECK(cudaMallocAsync(&b->d_atoms, sizeof(ts::Atom) * b->atoms.size(), st));
+        TS_CUDA_CHECK(cudaMemcpyAsync(b->d_atoms, b->atoms.data(), sizeof(ts::Atom) * b->atoms.size(),
+                                      cudaMemcpyHostToDevice, st));
+        bytes += sizeof(ts::Atom) * b->atoms.size();
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        b->bytes = bytes;
+        *out = b.release();
+    });
+}
+
 int ts_batch_free(ts_batch* b) {
     return guarded([&] {
         if (!b) return;

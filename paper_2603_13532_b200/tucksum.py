@@ -50,7 +50,7 @@ EXPORTED_SYMBOLS = [
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
     "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
-    "ts_ctx_set_graphs", "ts_ctx_graph_replays",
+    "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked",
 ]
 
 
@@ -628,6 +628,26 @@ class Engine:
         h = C.c_void_p()
         _check(lib().ts_batch_upload(self.handle, views.arr, i64(len(summands)), C.byref(h)))
         return DeviceBatch(self, h, len(summands), len(summands[0].dims), summands[0].dims)
+
+    def upload_stacked(self, factor_slabs, core_slab, ranks) -> DeviceBatch:
+        """Upload summands already stacked (ts_batch_upload_stacked): factor_slabs[j] is
+        dims[j] × Σ_k r_j^(k) (Fortran order), core_slab the dense cores concatenated,
+        ranks a K × order integer array."""
+        slabs = [np.asarray(f) for f in factor_slabs]
+        for f in slabs:
+            if f.dtype != np.float64 or not f.flags.f_contiguous:
+                raise ValueError("upload_stacked: factor slabs must be Fortran-ordered float64")
+        core = np.asarray(core_slab)
+        if core.dtype != np.float64 or not core.flags.c_contiguous:
+            raise ValueError("upload_stacked: the core slab must be contiguous float64")
+        rk = np.ascontiguousarray(np.asarray(ranks, dtype=np.int64))
+        order = len(slabs)
+        dims = np.ascontiguousarray([f.shape[0] for f in slabs], dtype=np.int64)
+        fptrs = (dptr * order)(*[_p(f) for f in slabs])
+        h = C.c_void_p()
+        _check(lib().ts_batch_upload_stacked(self.handle, i64(order), dims.ctypes.data_as(i64p), i64(rk.shape[0]),
+                                             rk.ctypes.data_as(i64p), fptrs, _p(core), C.byref(h)))
+        return DeviceBatch(self, h, int(rk.shape[0]), order, [int(x) for x in dims])
 
     def upload_views(self, views: "C.Array", count: int, order: int, dims) -> DeviceBatch:
         h = C.c_void_p()

@@ -491,3 +491,24 @@ def test_plans_for_every_strategy_match_oracle(engine):
         plan = T.effective_subrank(xs, ws, 1e-6, 2, strat, engine=engine)
         assert plan.strategy == strat
         assert plan.effective_ranks == eff and plan.targets == tg and plan.mode_sketch_dims == want
+
+
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_stacked_upload_equals_per_summand_upload(engine, cfg):
+    """ts_batch_upload_stacked (the workload's host slabs as they are) gives
+    bitwise the same sum as ts_batch_upload of the per-summand views."""
+    wl = make_workload(cfg)
+    d = len(wl.dims)
+    outs = []
+    for stacked in (False, True):
+        batch = engine.upload_stacked(wl.slabs[:d], wl.slabs[d], wl.ranks) if stacked else engine.upload(wl.summands)
+        try:
+            res = engine.krp_sum(batch, wl.weights, wl.widths, wl.seed, wl.eps, wl.cap)
+            outs.append(res.to_tucker())
+            res.free()
+        finally:
+            batch.free()
+    a, b = outs
+    assert a.ranks == b.ranks
+    assert all(np.array_equal(x, y) for x, y in zip(a.factors, b.factors))
+    assert np.array_equal(a.dense_core(), b.dense_core())
