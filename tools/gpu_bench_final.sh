@@ -1,6 +1,6 @@
 #!/bin/bash
 # Bench lines on the final code (after the stacked-upload e2e path).
-O=gpurun_out/final4
+O=gpurun_out/final5
 mkdir -p $O
 timeout 600 python bench.py > $O/bench_cfg5.json 2> $O/bench_cfg5.err
 for c in 1 2 3 4; do
