@@ -20,9 +20,15 @@ partial cores with NCCL.
 """
 from __future__ import annotations
 
+import os
+
+# Passive OpenMP waiting for the CPU legs: with torch's OpenMP runtime in the same
+# process, active waiting turned a 3 ms config-1 oracle call into ~48 ms on 8
+# threads.  Must be set before any OpenMP runtime loads.
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+
 import argparse
 import json
-import os
 import statistics
 import subprocess
 import sys
@@ -53,6 +59,10 @@ def parse():
                    help="krp (the hot path, default); kron: Kronecker sketch with the reference's balanced "
                         "widths for the config's targets; lazy: deterministic rounding of the formal sum")
     p.add_argument("--no-error", action="store_true", help="skip the device error-to-exact-sum check")
+    p.add_argument("--eps", type=float, default=None,
+                   help="truncation tolerance (default: the config's BASELINE mode eps = 0 + rank cap); "
+                        "with --no-cap this is the reference's own semantics (src/tucker.cpp:244-276)")
+    p.add_argument("--no-cap", action="store_true", help="no rank cap (max_rank = NULL, reference-exact mode)")
     return p.parse_args()
 
 
@@ -128,20 +138,57 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def config_desc(wl, world, strategy="krp", widths=None):
+def config_desc(wl, world, strategy="krp", widths=None, omega="cached on device"):
     r = wl.ranks[0]
     plan = {"krp": "given (uniform KRP width)", "kron": f"given (Kron widths {widths} = kron_sketch_dims(targets "
             f"{wl.widths}, dims), src/sketch.cpp:222-270)", "lazy": "none (Lazy: tucker_rounding of the formal sum)"}
-    return {"workload": f"{wl.name}: d={len(wl.dims)} n={wl.dims} K={wl.K} r={r} s={wl.widths[0]} "
+    return {"workload": f"{wl.name}: d={len(wl.dims)} n={wl.dims} K={wl.K_total} r={r} s={wl.widths[0]} "
                         f"cap={wl.cap} eps={wl.eps} (BASELINE.json configs[{wl.cfg - 1}])",
-            "strategy": strategy,
-            "summands_per_gpu": wl.K // world, "plan": plan[strategy], "omega": "cached on device",
+            "strategy": strategy, "mode": ("BASELINE mode (eps = 0 + rank cap)" if wl.cap else
+                                           "reference-exact mode (eps, no rank cap)"),
+            "summands_per_gpu": wl.K_total // world, "plan": plan[strategy], "omega": omega,
             "l2": "inputs larger than L2 (no flush)" if sum(s.nbytes for s in wl.slabs) > 126e6 else
             "inputs fit in L2; L2 flushed between steps",
             "parallelism": f"summand-sharded dp{world} + NCCL all-reduce of Y and h" if world > 1 else "1 GPU"}
 
 
+def apply_mode(wl, args):
+    """--eps / --no-cap: reference-exact truncation instead of BASELINE mode."""
+    if args.eps is not None:
+        wl.eps = float(args.eps)
+    if args.no_cap:
+        wl.cap = None
+
+
 # ----------------------------------------------------------------------------- CPU legs
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "nproc": usable, "logical_cpus": os.cpu_count()}
+
+
+def oracle_workload(cfg, k_end=None):
+    """The workload generated through the ORACLE's bit-identical RNG (never the
+    CUDA library's): the CPU legs must not map libtucksum_cuda.so."""
+    import oracle as O
+    from paper_2603_13532_b200.workloads import config_spec, make_workload
+
+    K = config_spec(cfg)["K"]
+    return make_workload(cfg, k_range=(0, min(K, k_end or K)), gaussian=O.gaussian_matrix,
+                         substream=lambda s, salt: O.substream(s[0], s[1], salt))
+
+
 def cpu_sample_run(wl, K_sample, threads):
     import oracle as O
 
@@ -152,31 +199,60 @@ def cpu_sample_run(wl, K_sample, threads):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(wl, budget_s=15.0):
-    """Oracle port on all host threads, bounded sample of the same workload."""
+def cpu_measure(wl, threads, target_s, trials=1):
+    """Oracle port (the reference's CPU path restated; one call incl. Ω generation,
+    as the reference times it, src/bench.cpp:353-358) on `threads` host threads,
+    over a prefix of the summands grown until one call takes ~target_s."""
+    k = min(wl.K, max(1, threads))
+    t = cpu_sample_run(wl, k, threads)
+    while t < target_s / 2 and k < wl.K:
+        k = min(wl.K, max(k + 1, int(k * min(8.0, target_s / max(t, 1e-3)))))
+        t = cpu_sample_run(wl, k, threads)
+    if t < target_s / 2:  # the whole workload is fast: repeat whole calls instead
+        trials = max(trials, min(200, int(target_s / 2 / max(t, 1e-4))))
+    ts = [t] + [cpu_sample_run(wl, k, threads) for _ in range(max(0, trials - 1))]
+    t = statistics.median(ts)
+    return {"value": k / t, "unit": "summands/s", "cores": threads, "kind": "port",
+            "sample": f"{k} of {wl.K_total} summands of {wl.name} (same shapes, Ω, plan, cap, eps), one krp_sum call "
+                      f"incl. Ω generation; median of {len(ts)} call(s), {t:.2f} s"}
+
+
+def cpu_baseline(wl_cfg, args, budget_s=24.0):
+    """The oracle port on 1 core (the reference's own configuration: no OpenMP,
+    Eigen pinned to one thread, src/bench.cpp:1271) and on all host cores
+    (OpenMP over summands, index-ordered reduction), bounded samples."""
     import oracle as O
 
-    threads = O.num_threads()
-    k = min(wl.K, max(2, threads))
-    t = cpu_sample_run(wl, k, threads)
-    # Scale the sample so the measured run takes ~budget_s / 2.
-    while t < budget_s / 4 and k < wl.K:
-        k = min(wl.K, k * 2)
-        t = cpu_sample_run(wl, k, threads)
-    return {"value": k / t, "unit": "summands/s", "cores": threads, "kind": "port",
-            "sample": f"{k} of {wl.K} summands of {wl.name} (same shapes, Ω, plan, cap), one call incl. Ω "
-                      f"generation, {t:.2f} s"}
+    info = cpu_info()
+    n = O.num_threads()
+    wl = oracle_workload(wl_cfg.cfg, k_end=max(64, 8 * n))
+    apply_mode(wl, args)
+    one = cpu_measure(wl, 1, budget_s / 3)
+    allc = cpu_measure(wl, n, budget_s / 3)
+    out = dict(allc)
+    out.update(info)
+    out["single_core"] = one
+    out["note"] = ("value/cores = the all-core OpenMP run of the oracle port; single_core = the reference's own "
+                   "configuration (1 thread); inputs generated by the oracle's RNG (bitwise equal to the GPU arm's)")
+    return out
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU path (the oracle port: the reference
+    itself needs Eigen >= 3.4, absent here) on all host threads, plus its
+    single-core configuration.  Never loads libtucksum_cuda.so."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_2603_13532_b200.workloads import make_workload
     import oracle as O
 
-    wl = make_workload(args.config)
+    from paper_2603_13532_b200.workloads import config_spec
+
     threads = O.num_threads()
+    info = cpu_info()
+    K = config_spec(args.config)["K"]
+    wl = oracle_workload(args.config, k_end=max(64, 8 * threads))
+    apply_mode(wl, args)
     # One step = a bounded sample sized so steps+warmup stay within a few minutes.
     k = min(wl.K, max(2, threads))
     t = cpu_sample_run(wl, k, threads)
@@ -188,14 +264,20 @@ def run_reference(args):
     times = [cpu_sample_run(wl, k, threads) for _ in range(args.steps)]
     ms = 1000.0 * statistics.mean(times)
     value = k / (ms / 1000.0)
+    one = cpu_measure(wl, 1, 8.0)
+    wl.K_total = K
+    cfgd = config_desc(wl, 1, omega="generated inside every call (as the reference does, src/sketch.cpp:91-95)")
+    cb = {"value": value, "unit": "summands/s", "cores": threads, "kind": "port",
+          "sample": f"{k} of {K} summands per step, one krp_sum call each incl. Ω generation (oracle port of the "
+                    f"reference CPU path; the reference needs Eigen>=3.4, absent from the image)",
+          "single_core": one}
+    cb.update(info)
     line = {"metric": "tucker_summands_per_sec", "value": value, "unit": "summands/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE.json recipe)",
-            "config": config_desc(wl, 1), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "summands/s", "cores": threads, "kind": "port",
-                             "sample": f"{k} of {wl.K} summands per step (oracle port of the reference CPU path; "
-                                       f"the reference needs Eigen>=3.4, absent from the image)"},
-            "e2e": {"value": value, "unit": "summands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": cfgd, "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "summands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_libs": sorted({ln.split()[-1] for ln in open("/proc/self/maps") if ".so" in ln and ROOT in ln})}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -210,7 +292,7 @@ def main():
 
     from paper_2603_13532_b200 import tucksum as T
     from paper_2603_13532_b200.sharding import init_nccl_engine, shard_range
-    from paper_2603_13532_b200.workloads import f_alg, make_workload
+    from paper_2603_13532_b200.workloads import config_spec, f_alg, make_workload
 
     rank, world, local = dist_env()
     if world > 1:
@@ -218,10 +300,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    wl = make_workload(args.config)
-    b, e = shard_range(wl.K, world, rank)
-    xs, ws = wl.summands[b:e], np.ascontiguousarray(wl.weights[b:e])
+    # Each rank generates (and later pins) only its own contiguous shard.
+    b, e = shard_range(config_spec(args.config)["K"], world, rank)
+    wl = make_workload(args.config, k_range=(b, e))
+    apply_mode(wl, args)
+    xs, ws = wl.summands, np.ascontiguousarray(wl.weights)
     eng = init_nccl_engine(local if world > 1 else 0, rank, world)
+    comm_count, comm_rank = eng.comm_info()
+    if world > 1:
+        print(f"[bench] rank {rank}: ncclCommCount = {comm_count}, ncclCommUserRank = {comm_rank}", file=sys.stderr,
+              flush=True)
     stream = torch.cuda.ExternalStream(eng.stream)
     strat = {"krp": T.Strategy.Krp, "kron": T.Strategy.Kron, "lazy": T.Strategy.Lazy}[args.strategy]
     widths = T.kron_sketch_dims(wl.widths, wl.dims) if args.strategy == "kron" else wl.widths
@@ -276,9 +364,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms = total_ms / args.steps
-    value = wl.K / (ms / 1000.0)
+    value = wl.K_total / (ms / 1000.0)
     krp = args.strategy == "krp"
-    falg = f_alg(wl.dims, wl.ranks, wl.widths[0]) if krp else None  # SURVEY.md §8(d) F_alg is the KRP count
+    falg = f_alg(wl.dims, [wl.ranks[0]] * wl.K_total, wl.widths[0]) if krp else None  # SURVEY.md §8(d) F_alg is the KRP count
     gflops = falg / (ms / 1000.0) / 1e9 if krp else None
     peak, peak_src = fp64_peak()
 
@@ -287,7 +375,7 @@ def main():
     d = len(wl.dims)
     Kloc = e - b
     if args.strategy == "lazy":
-        q = [min(wl.dims[j], sum(r[j] for r in wl.ranks[b:e])) for j in range(d)]
+        q = [min(wl.dims[j], sum(r[j] for r in wl.ranks)) for j in range(d)]
         fa = sum(2.0 * q[j] * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d))
         ta = stages[5] if stages else float("nan")
     else:
@@ -331,15 +419,12 @@ def main():
         # H2D copy per mode + one for the cores (ts_batch_upload_stacked); this
         # rank's shard is a column range of every slab.
         d_ = len(wl.dims)
-        rk = np.asarray([list(r) for r in wl.ranks], dtype=np.int64)
-        c0 = rk[:b].sum(axis=0)
-        c1 = rk[:e].sum(axis=0)
-        csz = np.prod(rk, axis=1)
-        shard_slabs = [wl.slabs[j][:, int(c0[j]):int(c1[j])] for j in range(d_)]
-        shard_cores = wl.slabs[d_][int(csz[:b].sum()):int(csz[:e].sum())]
+        rk = np.asarray([list(r) for r in wl.ranks], dtype=np.int64)  # this rank's shard only
+        shard_slabs = wl.slabs[:d_]
+        shard_cores = wl.slabs[d_]
 
         def upload_step():
-            return eng.upload_stacked(shard_slabs, shard_cores, rk[b:e])
+            return eng.upload_stacked(shard_slabs, shard_cores, rk)
 
         d2h = 0
         # (1) Sequential: upload, sum, download, one step after the other.
@@ -366,7 +451,7 @@ def main():
         pool = ThreadPoolExecutor(max_workers=1)
 
         def up_step():
-            return up.upload_stacked(shard_slabs, shard_cores, rk[b:e])
+            return up.upload_stacked(shard_slabs, shard_cores, rk)
 
         try:
             pool.submit(lambda: up_step().free()).result()  # warm-up
@@ -394,7 +479,7 @@ def main():
         te = torch.tensor([best, pipe, seq], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": wl.K / float(te[0].item()), "unit": "summands/s", "h2d_bytes_per_step": int(h2d) * world,
+        e2e = {"value": wl.K_total / float(te[0].item()), "unit": "summands/s", "h2d_bytes_per_step": int(h2d) * world,
                "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": 1000.0 * float(te[0].item()),
                "timing": "host wall clock, max over ranks; the faster of: pipelined (step i+1's upload on a second "
                          f"context/stream overlaps step i's sum + download; {args.e2e_steps} steps) and sequential "
@@ -427,7 +512,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and krp:
-        cpu = cpu_baseline(wl)
+        cpu = cpu_baseline(wl, args)
 
     if rank == 0:
         line = {"metric": "tucker_summands_per_sec", "value": value, "unit": "summands/s", "n_gpus": world,
@@ -439,7 +524,9 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages)),
                 "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]},
-                "accuracy": err, "omega": omega}
+                "accuracy": err, "omega": omega,
+                "comm": {"ncclCommCount": comm_count, "backend": "NCCL all-reduce inside ts_krp_sum" if world > 1
+                         else "none (1 GPU)"}}
         print(json.dumps(line), flush=True)
     batch.free()
     eng.close()

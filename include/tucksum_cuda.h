@@ -88,6 +88,16 @@ int ts_ctx_destroy(ts_ctx* ctx);
  * projected core h over the ranks; each rank passes its own shard of summands. */
 int ts_nccl_unique_id(void* unique_id_128);
 int ts_ctx_init_nccl(ts_ctx* ctx, const void* unique_id_128, int nranks, int rank);
+/* Alternative to NCCL: the two exchange points of a sharded sum (partial Y after
+ * stage C, partial h after stage F) call `fn(user, host_buf, count)`, which must
+ * replace host_buf[0..count) by its sum over the `nranks` ranks (e.g. a gloo
+ * all-reduce) and return 0.  The library copies the device buffer to the host,
+ * calls fn, and copies the sum back.  fn = NULL removes the hook. */
+typedef int (*ts_host_allreduce_fn)(void* user, double* host_buf, int64_t count);
+int ts_ctx_set_host_allreduce(ts_ctx* ctx, ts_host_allreduce_fn fn, void* user, int nranks, int rank);
+/* The communicator's size and this context's rank (ncclCommCount /
+ * ncclCommUserRank); 1 / 0 without a communicator. */
+int ts_ctx_comm_info(ts_ctx* ctx, int* nranks, int* rank);
 /* The CUDA stream (cudaStream_t) the context launches on. */
 void* ts_ctx_stream(ts_ctx* ctx);
 /* Number of kernels the context launched so far (for the bench's gpu_launches). */
@@ -178,10 +188,11 @@ int ts_effective_subrank_kron(ts_ctx* ctx, const ts_batch* batch, const double* 
  * (descending) and column eigenvectors (host).  sweeps / ms (nullable) report
  * the Jacobi sweeps and the kernel time. */
 int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms);
-/* The stage-G default for n <= 64: Householder tridiagonalization + multisection
- * bisection + inverse iteration in one CTA (same reference semantics); *flag = 1
- * when its residual / orthogonality acceptance check failed (the pipeline then
- * falls back to the Jacobi solver of ts_sym_eig). */
+/* Opt-in alternative (TS_EIG=tri; measured slower, not the default) for n <= 64:
+ * Householder tridiagonalization + multisection bisection + inverse iteration in
+ * one CTA (same reference semantics); *flag = 1 when its residual /
+ * orthogonality acceptance check failed (the pipeline then falls back to the
+ * Jacobi solver of ts_sym_eig). */
 int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* flag, double* ms);
 
 /* ---- result: a dense-core Tucker tensor owned by the library ---- */

@@ -58,6 +58,10 @@ def lib():
     if _lib is None:
         if not os.path.exists(_LIB_PATH):
             build()
+        # Passive OpenMP waiting: in a process that also loaded torch (whose own
+        # OpenMP runtime keeps spinning threads), active waiting made a 3 ms
+        # config-1 call take ~48 ms on 8 threads.  Read by libgomp when it loads.
+        os.environ.setdefault("OMP_WAIT_POLICY", "passive")
         L = C.CDLL(_LIB_PATH)
         L.or_last_error.restype = C.c_char_p
         L.or_result_order.restype = i64

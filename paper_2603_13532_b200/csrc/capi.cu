@@ -57,6 +57,8 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     std::string error;
 };
@@ -75,6 +77,8 @@ NcclApi& nccl_api() {
         api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        api.CommCount = reinterpret_cast<decltype(api.CommCount)>(dlsym(h, "ncclCommCount"));
+        api.CommUserRank = reinterpret_cast<decltype(api.CommUserRank)>(dlsym(h, "ncclCommUserRank"));
         if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce) api.error = "libnccl.so.2 lacks required symbols";
     });
     if (!api.error.empty()) throw ts::Error(TS_NCCL, "NCCL unavailable: " + api.error);
@@ -128,10 +132,11 @@ struct GraphKey {
     int method;
     std::vector<std::int64_t> widths, cap;
     std::uint64_t seed, stream;
+    double eps;
     std::vector<double> weights;  // some launches take a weight as a host scalar (GEMM alpha)
     bool operator<(const GraphKey& o) const {
-        return std::tie(batch, method, widths, cap, seed, stream, weights) <
-               std::tie(o.batch, o.method, o.widths, o.cap, o.seed, o.stream, o.weights);
+        return std::tie(batch, method, widths, cap, seed, stream, eps, weights) <
+               std::tie(o.batch, o.method, o.widths, o.cap, o.seed, o.stream, o.eps, o.weights);
     }
 };
 struct GraphEntry {
@@ -160,13 +165,29 @@ struct GraphEntry {
 
 }  // namespace
 
+struct OmegaEntry {
+    double* ptr = nullptr;
+    std::int64_t bytes = 0;
+    std::uint64_t last_use = 0;
+};
+
 struct ts_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     ts::HostStage stage;
-    std::map<OmegaKey, double*> omega;
+    // Device Ω cache (shared with the lanes), bounded: least recently used
+    // entries beyond kOmegaMaxEntries / kOmegaMaxBytes are freed (together with
+    // the captured graphs that read them).
+    std::map<OmegaKey, OmegaEntry> omega;
+    std::int64_t omega_bytes = 0;
+    std::uint64_t omega_clock = 0;
+    std::uint64_t omega_pin = ~std::uint64_t(0);  // entries used at clock >= pin are never evicted
     ncclComm_t comm = nullptr;
+    // Alternative exchange: a host all-reduce callback (e.g. gloo) — the same
+    // sharded orchestration without NCCL, for CPU-interconnect or testing setups.
+    ts_host_allreduce_fn host_ar = nullptr;
+    void* host_ar_user = nullptr;
     int nranks = 1, rank = 0;
     bool debug = false, timing = false;
     std::vector<double> stage_ms;
@@ -241,6 +262,9 @@ using ts::Layout;
 
 // Ω_n = gaussian_matrix(dims[n], widths[n], {seed, stream}.substream(n)), all
 // modes concatenated (column-major each), cached on the device.
+constexpr size_t kOmegaMaxEntries = 64;
+constexpr std::int64_t kOmegaMaxBytes = std::int64_t(1) << 30;
+
 double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, const std::int64_t* widths, std::uint64_t seed,
                   std::uint64_t stream) {
     if (ctx->parent) ctx = ctx->parent;  // lanes share the parent's cache
@@ -248,7 +272,10 @@ double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, const std::i
     OmegaKey key{seed, stream, std::vector<std::int64_t>(widths, widths + order),
                  std::vector<std::int64_t>(dims, dims + order)};
     auto it = ctx->omega.find(key);
-    if (it != ctx->omega.end()) return it->second;
+    if (it != ctx->omega.end()) {
+        it->second.last_use = ++ctx->omega_clock;
+        return it->second.ptr;
+    }
     std::int64_t total = 0;
     for (int n = 0; n < order; ++n) total += dims[n] * widths[n];
     std::vector<double> host(static_cast<size_t>(total));
@@ -259,15 +286,53 @@ double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, const std::i
         ts::gaussian_fill(dims[n], widths[n], s2, t2, host.data() + off);
         off += dims[n] * widths[n];
     }
+    const std::int64_t bytes = static_cast<std::int64_t>(sizeof(double)) * std::max<std::int64_t>(total, 1);
+    // Callers with a fresh seed per call (NDG steps, GMRES iterations) would
+    // otherwise grow the cache without bound: evict least recently used entries.
+    while (ctx->omega.size() + 1 > kOmegaMaxEntries || ctx->omega_bytes + bytes > kOmegaMaxBytes) {
+        auto lru = ctx->omega.end();
+        for (auto e = ctx->omega.begin(); e != ctx->omega.end(); ++e)
+            if (e->second.last_use < ctx->omega_pin && (lru == ctx->omega.end() || e->second.last_use < lru->second.last_use))
+                lru = e;
+        if (lru == ctx->omega.end()) break;  // everything is in use by a running ts_krp_sum_many
+        // Work queued on this context or its lanes may still read it.
+        TS_CUDA_CHECK(cudaDeviceSynchronize());
+        for (auto g = ctx->graph_cache.begin(); g != ctx->graph_cache.end();)
+            g = (g->first.seed == lru->first.seed && g->first.stream == lru->first.stream) ? ctx->graph_cache.erase(g)
+                                                                                         : std::next(g);
+        TS_CUDA_CHECK(cudaFree(lru->second.ptr));
+        ctx->omega_bytes -= lru->second.bytes;
+        ctx->omega.erase(lru);
+    }
     double* d = nullptr;
-    TS_CUDA_CHECK(cudaMalloc(&d, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(total, 1))));
+    TS_CUDA_CHECK(cudaMalloc(&d, static_cast<size_t>(bytes)));
     TS_CUDA_CHECK(cudaMemcpy(d, host.data(), sizeof(double) * static_cast<size_t>(total), cudaMemcpyHostToDevice));
-    ctx->omega.emplace(std::move(key), d);
+    ctx->omega.emplace(std::move(key), OmegaEntry{d, bytes, ++ctx->omega_clock});
+    ctx->omega_bytes += bytes;
     return d;
 }
 
+bool sharded(const ts_ctx* ctx) { return ctx->comm != nullptr || ctx->host_ar != nullptr; }
+
+// Sum `buf` (device, count doubles) over the ranks, in place, ordered on `st`:
+// ncclAllReduce on the library stream, or the host callback (D2H, callback, H2D).
+void allreduce_sum(ts_ctx* ctx, double* buf, std::int64_t count, cudaStream_t st, const char* what) {
+    if (ctx->comm) {
+        nccl_check(nccl_api().AllReduce(buf, buf, static_cast<size_t>(count), ncclFloat64, ncclSum, ctx->comm, st), what);
+    } else if (ctx->host_ar) {
+        std::vector<double> h(static_cast<size_t>(count));
+        TS_CUDA_CHECK(cudaMemcpyAsync(h.data(), buf, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (ctx->host_ar(ctx->host_ar_user, h.data(), count) != 0)
+            throw ts::Error(TS_NCCL, std::string(what) + ": host all-reduce callback failed");
+        TS_CUDA_CHECK(cudaMemcpyAsync(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+}
+
 void mark(ts_ctx* ctx, int idx) {
-    if (ctx->timing) TS_CUDA_CHECK(cudaEventRecord(ctx->events[static_cast<size_t>(idx)], ctx->stream));
+    if (ctx->timing && static_cast<size_t>(idx) < ctx->events.size())
+        TS_CUDA_CHECK(cudaEventRecord(ctx->events[static_cast<size_t>(idx)], ctx->stream));
 }
 
 void copy_to_host(std::vector<double>& dst, const double* src, std::int64_t n, cudaStream_t st) {
@@ -574,6 +639,8 @@ enum class Method { Krp, Kron, Lazy };
 double inner_impl(ts_ctx* ctx, const ts_batch* X, const double* wX, const ts_batch* Y, const double* wY) {
     if (!X || !Y || !wX || !wY) invalid("tucker_inner: null operand");
     if (X->order != Y->order) invalid("tucker_inner: operands must share dims");
+    if (X->ctx->device != ctx->device || Y->ctx->device != ctx->device)
+        invalid("tucker_inner: operands live on another device than this context's");
     const int d = X->order;
     for (int n = 0; n < d; ++n)
         if (X->dims[n] != Y->dims[n]) invalid("tucker_inner: operands must share dims");
@@ -672,6 +739,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     // Validation mirrors src/sketch.cpp:16-30,66-87.
     if (b == nullptr || b->count < 1) invalid("sum request needs matching, nonempty summands and weights");
     if (weights == nullptr) invalid("sum request needs matching, nonempty summands and weights");
+    if (b->ctx->device != ctx->device) invalid("batch was uploaded to another device than this context's");
     if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
     const int d = b->order;
     if (d < 2) {
@@ -814,8 +882,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         }
     }
     mark(ctx, 3);
-    if (ctx->comm) nccl_check(nccl_api().AllReduce(Y, Y, static_cast<size_t>(ytot), ncclFloat64, ncclSum, ctx->comm, st),
-                              "ncclAllReduce(Y)");
+    allreduce_sum(ctx, Y, ytot, st, "ncclAllReduce(Y)");
     mark(ctx, 4);
     auto res = std::make_unique<ts_result>();
     res->device = ctx->device;
@@ -969,8 +1036,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     std::int64_t hsize = 0;
     double* h = project_core(ctx, b, P, q, d_w, weights, sc, &hsize);
     mark(ctx, 8);
-    if (ctx->comm) nccl_check(nccl_api().AllReduce(h, h, static_cast<size_t>(hsize), ncclFloat64, ncclSum, ctx->comm, st),
-                              "ncclAllReduce(h)");
+    allreduce_sum(ctx, h, hsize, st, "ncclAllReduce(h)");
     mark(ctx, 9);
     if (norm_out) {  // tucker_norm: ‖orthogonalized core‖ (src/tucker.cpp:159), no rounding
         double* d_ss = sc.alloc_n<double>(1);
@@ -996,18 +1062,25 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     double* Pk[TS_MAX_ORDER] = {};  // q_k × q_k left singular vectors (first rank_k columns used)
     std::int64_t rank[TS_MAX_ORDER];
     double* g = h;
-    const bool spec_g = spec && eps == 0.0;
+    // At ε = 0 the fast-path rank is fixed by the cap (else q); at ε > 0 it is
+    // known in advance only for a captured call (the probe run's ranks): then the
+    // device re-derives the reference tail rule and flags any difference.
+    const std::int64_t* fixed_rank = ge ? ge->ranks : nullptr;
+    const bool spec_g = spec && (eps == 0.0 || fixed_rank != nullptr);
     if (spec_g) {
         gflags = sc.alloc_n<int>(static_cast<size_t>(d));
         TS_CUDA_CHECK(cudaMemsetAsync(gflags, 0, sizeof(int) * static_cast<size_t>(d), st));
     }
     {
         double hss = 0.0;  // θ = ε²‖h‖²/d vanishes at ε = 0
+        double* d_hss = nullptr;
         if (eps != 0.0) {
-            double* d_ss = sc.alloc_n<double>(1);
-            ts::launch_sumsq(h, hsize, d_ss, sc);
-            TS_CUDA_CHECK(cudaMemcpyAsync(&hss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
-            TS_CUDA_CHECK(cudaStreamSynchronize(st));
+            d_hss = sc.alloc_n<double>(1);
+            ts::launch_sumsq(h, hsize, d_hss, sc);
+            if (!spec_g) {
+                TS_CUDA_CHECK(cudaMemcpyAsync(&hss, d_hss, sizeof(double), cudaMemcpyDeviceToHost, st));
+                TS_CUDA_CHECK(cudaStreamSynchronize(st));
+            }
         }
         const double theta = eps * eps * hss / static_cast<double>(d);
         ctx->last_svd_fallbacks = 0;
@@ -1093,9 +1166,15 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             }
             std::int64_t rk = 0;
             if (spec_g && !dsw) {
-                // At ε = 0 the fast-path rank is fixed (cap, else q); its checks run on the device.
-                rk = (capk > 0 && capk < qk) ? capk : qk;
-                ts::launch_gram_check(lam, static_cast<int>(qk), static_cast<int>(capk), gflags + k, sc);
+                if (eps == 0.0) {
+                    // At ε = 0 the fast-path rank is fixed (cap, else q); its checks run on the device.
+                    rk = (capk > 0 && capk < qk) ? capk : qk;
+                    ts::launch_gram_check(lam, static_cast<int>(qk), static_cast<int>(capk), gflags + k, sc);
+                } else {
+                    rk = fixed_rank[k];
+                    ts::launch_gram_rank_check(lam, static_cast<int>(qk), static_cast<int>(capk), eps, d, d_hss,
+                                               static_cast<int>(rk), gflags + k, sc);
+                }
             } else {
                 std::vector<double> lv(static_cast<size_t>(qk));
                 TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
@@ -1261,9 +1340,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
 }
 
 // Entry of ts_krp_sum / ts_kron_sum / ts_lazy_sum.  A call that repeats an
-// earlier one exactly (same batch upload, method, widths, cap, seed; ε = 0 so
-// the speculative path has no host decision) is captured into a CUDA graph the
-// second time and replayed from then on: one cudaGraphLaunch instead of ~40
+// earlier one exactly (same batch upload, method, widths, cap, seed, ε) is
+// captured into a CUDA graph the second time and replayed from then on (at
+// ε > 0 the captured ranks are those of the probe run, and the replay's device
+// checks re-derive the reference rank rule and flag any difference): one cudaGraphLaunch instead of ~40
 // launches, memsets and descriptor copies, which is what the latency-bound small
 // configurations pay for.  The key includes the weights (some launches carry a
 // weight as a host scalar).  A replay whose device
@@ -1275,8 +1355,8 @@ ts_result* run_sum(ts_ctx* ctx, const ts_batch* b, const double* weights, const 
         const char* e = std::getenv("TS_GRAPHS");
         return (e && e[0] == '0') || std::getenv("TS_DEBUG_SWEEPS") != nullptr;
     }();
-    const bool graphable = !env_off && ctx->graphs && b != nullptr && weights != nullptr && eps == 0.0 &&
-                           !ctx->comm && !ctx->debug && !ctx->timing && ctx->spec_ok && ctx->parent == nullptr &&
+    const bool graphable = !env_off && ctx->graphs && b != nullptr && weights != nullptr && eps >= 0.0 &&
+                           !sharded(ctx) && !ctx->debug && !ctx->timing && ctx->spec_ok && ctx->parent == nullptr &&
                            !ts::tri_eig_enabled();
     if (!graphable)
         return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method);
@@ -1284,7 +1364,7 @@ ts_result* run_sum(ts_ctx* ctx, const ts_batch* b, const double* weights, const 
     GraphKey key{b->id, static_cast<int>(method),
                  widths && method != Method::Lazy ? std::vector<std::int64_t>(widths, widths + d) : std::vector<std::int64_t>{},
                  max_rank ? std::vector<std::int64_t>(max_rank, max_rank + d) : std::vector<std::int64_t>{}, seed, stream,
-                 std::vector<double>(weights, weights + b->count)};
+                 eps, std::vector<double>(weights, weights + b->count)};
     auto it = ctx->graph_cache.find(key);
     if (it == ctx->graph_cache.end()) {
         if (!ctx->graph_seen.count(key)) {  // first sighting: plain call (also does one-time setups)
@@ -1411,7 +1491,8 @@ int ts_ctx_destroy(ts_ctx* ctx) {
         for (ts_ctx* lane : ctx->lanes) ts_ctx_destroy(lane);
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
-        for (auto& kv : ctx->omega) cudaFree(kv.second);
+        ctx->graph_cache.clear();
+        for (auto& kv : ctx->omega) cudaFree(kv.second.ptr);
         for (auto& e : ctx->events) cudaEventDestroy(e);
         if (ctx->comm && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm);
         cudaStreamDestroy(ctx->stream);
@@ -1430,12 +1511,37 @@ int ts_nccl_unique_id(void* unique_id_128) {
 int ts_ctx_init_nccl(ts_ctx* ctx, const void* unique_id_128, int nranks, int rank) {
     return guarded([&] {
         if (!ctx || !unique_id_128 || nranks < 1 || rank < 0 || rank >= nranks) invalid("ts_ctx_init_nccl: bad arguments");
+        if (ctx->host_ar) invalid("ts_ctx_init_nccl: context already has a host all-reduce");
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
         ncclUniqueId id;
         std::memcpy(&id, unique_id_128, sizeof(id));
         nccl_check(nccl_api().CommInitRank(&ctx->comm, nranks, id, rank), "ncclCommInitRank");
         ctx->nranks = nranks;
         ctx->rank = rank;
+    });
+}
+
+int ts_ctx_set_host_allreduce(ts_ctx* ctx, ts_host_allreduce_fn fn, void* user, int nranks, int rank) {
+    return guarded([&] {
+        if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) invalid("ts_ctx_set_host_allreduce: bad arguments");
+        if (ctx->comm) invalid("ts_ctx_set_host_allreduce: context already has a NCCL communicator");
+        ctx->host_ar = fn;
+        ctx->host_ar_user = fn ? user : nullptr;
+        ctx->nranks = fn ? nranks : 1;
+        ctx->rank = fn ? rank : 0;
+    });
+}
+
+int ts_ctx_comm_info(ts_ctx* ctx, int* nranks, int* rank) {
+    return guarded([&] {
+        if (!ctx || !nranks || !rank) invalid("ts_ctx_comm_info: null argument");
+        *nranks = ctx->nranks;
+        *rank = ctx->rank;
+        if (!ctx->comm) return;
+        NcclApi& api = nccl_api();
+        if (!api.CommCount || !api.CommUserRank) throw ts::Error(TS_NCCL, "libnccl.so.2 lacks ncclCommCount");
+        nccl_check(api.CommCount(ctx->comm, nranks), "ncclCommCount");
+        nccl_check(api.CommUserRank(ctx->comm, rank), "ncclCommUserRank");
     });
 }
 
@@ -1720,7 +1826,7 @@ int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const
 int ts_tucker_norm(ts_ctx* ctx, const ts_batch* batch, const double* weights, double* out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_tucker_norm: null argument");
-        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "tucker_norm does not shard: use a context without NCCL");
+        if (sharded(ctx)) throw ts::Error(TS_UNSUPPORTED, "tucker_norm does not shard: use a context without NCCL");
         sketched_sum_impl(ctx, batch, weights, nullptr, 0, 0, 0.0, nullptr, Method::Lazy, false, out);
     });
 }
@@ -1729,7 +1835,7 @@ int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_b
                     double* out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_tucker_inner: null argument");
-        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "tucker_inner of sharded batches: use a context without NCCL");
+        if (sharded(ctx)) throw ts::Error(TS_UNSUPPORTED, "tucker_inner of sharded batches: use a context without NCCL");
         *out = inner_impl(ctx, x, wx, y, wy);
     });
 }
@@ -1737,7 +1843,8 @@ int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_b
 int ts_rel_error_to_sum(ts_ctx* ctx, const ts_result* r, const ts_batch* batch, const double* weights, double* out) {
     return guarded([&] {
         if (!ctx || !r || !out) invalid("ts_rel_error_to_sum: null argument");
-        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "rel_error_to_sum of a sharded batch: use a context without NCCL");
+        if (r->device != ctx->device) invalid("ts_rel_error_to_sum: result lives on another device than this context's");
+        if (sharded(ctx)) throw ts::Error(TS_UNSUPPORTED, "rel_error_to_sum of a sharded batch: use a context without NCCL");
         ResultView rv(ctx, r);
         const double one = 1.0;
         const double xx = inner_impl(ctx, &rv.b, &one, &rv.b, &one);
@@ -1752,7 +1859,7 @@ int ts_lazy_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, doubl
                 ts_result** out) {
     return guarded([&] {
         if (!ctx || !out) invalid("ts_lazy_sum: null argument");
-        if (ctx->comm) throw ts::Error(TS_UNSUPPORTED, "lazy rounding does not shard: use a context without NCCL");
+        if (sharded(ctx)) throw ts::Error(TS_UNSUPPORTED, "lazy rounding does not shard: use a context without NCCL");
         *out = run_sum(ctx, batch, weights, nullptr, 0, 0, eps, max_rank, Method::Lazy);
     });
 }
@@ -1772,12 +1879,23 @@ int ts_krp_sum_many(ts_ctx* ctx, int64_t count, const ts_batch* const* batches, 
             invalid("ts_krp_sum_many: null argument");
         for (int64_t i = 0; i < count; ++i) out[i] = nullptr;
         if (count == 0) return;
-        if (ctx->comm || count == 1 || lanes <= 1) {
+        if (sharded(ctx) || count == 1 || lanes <= 1) {
             for (int64_t i = 0; i < count; ++i)
                 out[i] = sketched_sum_impl(ctx, batches[i], weights[i], widths, seeds[i], streams[i], eps, max_rank, Method::Krp);
             return;
         }
         const int L = static_cast<int>(std::min<int64_t>(std::min(lanes, 16), count));
+        {  // Ω entries fetched by the lanes stay resident until every lane is done
+            std::lock_guard<std::mutex> lock(ctx->omega_mu);
+            ctx->omega_pin = ctx->omega_clock + 1;
+        }
+        struct Unpin {
+            ts_ctx* c;
+            ~Unpin() {
+                std::lock_guard<std::mutex> lock(c->omega_mu);
+                c->omega_pin = ~std::uint64_t(0);
+            }
+        } unpin{ctx};
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
         TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // batches were uploaded on this stream
         while (static_cast<int>(ctx->lanes.size()) < L) {
@@ -1819,6 +1937,7 @@ static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, 
                          int64_t* effective_ranks, int64_t* targets) {
     {
         if (!ctx || !b || !weights || !oversampling) invalid("sum request needs matching, nonempty summands and weights");
+        if (b->ctx->device != ctx->device) invalid("batch was uploaded to another device than this context's");
         if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
         const int d = b->order;
         for (int n = 0; n < d; ++n)
@@ -1847,19 +1966,13 @@ static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, 
                 throw ts::Error(TS_UNSUPPORTED, "effective_subrank: min(n, sum of ranks) exceeds the device eigen-solver size");
             // Per-column energy scale.
             std::vector<double> cscale(static_cast<size_t>(R));
-            std::int64_t c = 0;
-            std::vector<std::int64_t> rank_of(static_cast<size_t>(b->count), 0);
-            for (const auto& at : b->atoms) rank_of[static_cast<size_t>(at.summand)] += 0;
             // Column ranges per summand follow the stacking order.
             {
                 std::vector<std::int64_t> rk(static_cast<size_t>(b->count), 0);
-                std::int64_t cnt_cols = 0;
                 for (const auto& at : b->atoms) rk[static_cast<size_t>(at.summand)] += at.shape[n];
-                for (std::int64_t i = 0; i < b->count; ++i) {
+                std::int64_t c = 0;
+                for (std::int64_t i = 0; i < b->count; ++i)
                     for (std::int64_t t = 0; t < rk[static_cast<size_t>(i)]; ++t) cscale[static_cast<size_t>(c++)] = energy[static_cast<size_t>(i)];
-                    cnt_cols += rk[static_cast<size_t>(i)];
-                }
-                (void)cnt_cols;
             }
             auto* d_scale = static_cast<double*>(sc.upload(cscale.data(), sizeof(double) * static_cast<size_t>(R)));
             const bool tall = rows >= R;

@@ -508,12 +508,8 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
     if (np > kMaxNp || np < 4) return false;
     const int k = np / 2;
     const size_t smem = sizeof(double) * (2 * static_cast<size_t>(np) * np + 2 * kMaxNp + 4 * static_cast<size_t>(np - 1) * k + np);
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(jacobi_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+    set_max_smem(jacobi_values_kernel, 200 * 1024);
     auto* rot = sc.alloc_n<double2>(static_cast<size_t>(kMaxSweeps) * (np - 1) * k);
     double* dpos = sc.alloc_n<double>(static_cast<size_t>(np));
     int* info = sc.alloc_n<int>(2);

@@ -396,12 +396,7 @@ bool tri_eig_enabled() {
 
 bool launch_sym_tridiag(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, CallScratch& sc) {
     if (n < 1 || n > kTN) return false;
-    static const bool configured = [] {  // thread-safe one-time setup
-        TS_CUDA_CHECK(cudaFuncSetAttribute(tri_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(sizeof(TriSmem))));
-        return true;
-    }();
-    (void)configured;
+    set_max_smem(tri_eig_kernel, static_cast<int>(sizeof(TriSmem)));
     tri_eig_kernel<<<1, kTriThreads, sizeof(TriSmem), sc.stream()>>>(C, ldc, n, lambda, V, flag, eig_probe_buffer());
     TS_LAUNCH_CHECK();
     sc.launches += 1;

@@ -213,13 +213,7 @@ template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM,
 void launch_kernel(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStream_t stream) {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
     auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(Cfg::kSmemBytes)));
-        return true;
-    }();
-    (void)configured;
+    set_max_smem(kern, static_cast<int>(Cfg::kSmemBytes));
     kern<<<static_cast<unsigned>(units), Cfg::kThreads, Cfg::kSmemBytes, stream>>>(d_descs, ngroups);
     TS_LAUNCH_CHECK();
 }
@@ -227,12 +221,11 @@ void launch_kernel(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStre
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM>
 int occupancy_of() {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
-    static const int occ = [] {  // thread-safe one-time query
+    auto kern2 = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
+    set_max_smem(kern2, static_cast<int>(Cfg::kSmemBytes));  // per device
+    static const int occ = [&] {  // thread-safe one-time query (same on every B200)
         int o = 0;
-        auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, 2>;
-        TS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(Cfg::kSmemBytes)));
-        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, Cfg::kThreads, Cfg::kSmemBytes));
+        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern2, Cfg::kThreads, Cfg::kSmemBytes));
         return std::max(o, 1);
     }();
     return occ;

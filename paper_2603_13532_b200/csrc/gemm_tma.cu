@@ -319,12 +319,11 @@ bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallS
         total_tiles += static_cast<int64_t>((p.M + kBM - 1) / kBM) * ((p.N + kBN - 1) / kBN);
     }
     if (total_tiles == 0) return true;
-    static const int occ = [] {  // thread-safe one-time setup
+    set_max_smem(gemm_tma_kernel<false>, static_cast<int>(kSmemBytes));  // per device
+    set_max_smem(gemm_tma_kernel<true>, static_cast<int>(kSmemBytes));
+    static const int occ = [] {  // thread-safe one-time query (same on every B200)
         int o = 0;
-        auto k1 = gemm_tma_kernel<false>, k2 = gemm_tma_kernel<true>;
-        TS_CUDA_CHECK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-        TS_CUDA_CHECK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k1, kThreads, kSmemBytes));
+        TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gemm_tma_kernel<false>, kThreads, kSmemBytes));
         return std::max(o, 1);
     }();
     const int64_t slots = static_cast<int64_t>(num_sms) * occ;

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <stdexcept>
 
+#include "../../include/tucksum_cuda.h"
 #include "kernels.cuh"
 
 namespace ts {
@@ -806,6 +807,46 @@ __global__ void gram_check_kernel(const double* __restrict__ lam, int q, int cap
     if (!ok) atomicOr(flag, 1);
 }
 
+constexpr int kMaxRankRule = 128;
+
+// Device twin of the ε > 0 branch of gram_rank (capi.cu) for a call whose output
+// rank is already known (a CUDA-graph replay or a speculated call): recomputes
+// θ = ε²‖h‖²/d from the device ‖h‖², the reference tail rule on the Gram
+// eigenvalues (suffix sums in the same order, no FMA contraction, so the decision
+// is bitwise the host's), the provability margins and the subspace separation,
+// and sets *flag |= 1 unless the fast path is accepted with exactly `expect`.
+__global__ void gram_rank_check_kernel(const double* __restrict__ lam, int q, int cap, double eps, int order,
+                                       const double* __restrict__ hss, int expect, int* __restrict__ flag) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double l1 = fmax(lam[0], 0.0);
+    bool ok = lam[0] > 0.0;
+    int rank = 1;
+    if (ok) {
+        const double theta = __ddiv_rn(__dmul_rn(__dmul_rn(eps, eps), hss[0]), static_cast<double>(order));
+        const double noise = __dmul_rn(1e-12, l1);
+        double suffix[kMaxRankRule + 1];
+        suffix[q] = 0.0;
+        for (int j = q - 1; j >= 0; --j) suffix[j] = __dadd_rn(suffix[j + 1], fmax(lam[j], 0.0));
+        int r = q;
+        for (int i = 1; i <= q; ++i)
+            if (suffix[i] <= theta) {
+                r = i;
+                break;
+            }
+        const double margin = __dmul_rn(static_cast<double>(q), noise);
+        if (r < q && suffix[r] > __dsub_rn(theta, margin)) ok = false;
+        if (r > 1 && suffix[r - 1] <= __dadd_rn(theta, margin)) ok = false;
+        rank = (cap > 0 && cap < r) ? cap : r;
+        if (ok && rank < q) {
+            const double lr = fmax(lam[rank - 1], 0.0), lnext = fmax(lam[rank], 0.0);
+            const double gap = __dsub_rn(lr, lnext);
+            ok = gap > 0.0;
+            if (ok) ok = !(1e-14 * l1 / gap * sqrt(lnext / l1) > 1e-11);
+        }
+    }
+    if (!ok || rank != expect) atomicOr(flag, 1);
+}
+
 struct UnfoldArgs {
     int64_t shape[kMaxOrder];
     int order, mode;
@@ -1015,13 +1056,8 @@ void run_tsqr(const std::vector<TsqrPlan*>& plans, CallScratch& sc, bool form_q)
         nlev = std::max(nlev, p->levels.size());
         napp = std::max(napp, p->applies.size());
     }
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        TS_CUDA_CHECK(cudaFuncSetAttribute(tsqr_apply_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+    set_max_smem(tsqr_apply_kernel<4>, 200 * 1024); set_max_smem(tsqr_apply_kernel<6>, 200 * 1024);
     for (size_t L = 0; L < nlev; ++L) {
         std::vector<QrTask> tasks;
         size_t smem = 0;
@@ -1080,12 +1116,8 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
     if (launch_sym_jacobi_pp(C, ldc, n, lambda, V, sc, sweeps)) return;  // eig.cu, n ≤ 64
     const size_t np = static_cast<size_t>(n + (n & 1));
     const size_t smem = sizeof(double) * (2 * np * (np + 1) + 2 * np + 3 * np + np) + 16;
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(sym_jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+    set_max_smem(sym_jacobi_kernel, 200 * 1024);
     sym_jacobi_kernel<<<1, kJacThreads, smem, sc.stream()>>>(C, ldc, n, lambda, V, sweeps);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
@@ -1097,20 +1129,21 @@ void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch
     sc.launches += 1;
 }
 
+void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss, int expect,
+                            int* flag, CallScratch& sc) {
+    if (q > kMaxRankRule) throw Error(TS_UNSUPPORTED, "gram_rank_check: q exceeds the device maximum");
+    gram_rank_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, eps, order, hss, expect, flag);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
     if (count <= 0) return;
     if (cb.n > 96) throw std::invalid_argument("chol_inv: n > 96");
     const size_t ldc = cb.n <= 32 ? 33 : cb.n <= 48 ? 49 : cb.n <= 64 ? 65 : 97;  // LD of the kernel instance
     const size_t smem = sizeof(double) * (2 * static_cast<size_t>(cb.n) * ldc + cb.n);
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        TS_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+    set_max_smem(chol_inv_kernel<32>, 200 * 1024); set_max_smem(chol_inv_kernel<48>, 200 * 1024); set_max_smem(chol_inv_kernel<64>, 200 * 1024); set_max_smem(chol_inv_kernel<96>, 200 * 1024);
     if (cb.n <= 32) chol_inv_kernel<32><<<count, 4 * 32, smem, sc.stream()>>>(cb);  // small sketches: half the threads and rows
     else if (cb.n <= 48) chol_inv_kernel<48><<<count, 4 * 48, smem, sc.stream()>>>(cb);
     else if (cb.n <= 64) chol_inv_kernel<64><<<count, 4 * 64, smem, sc.stream()>>>(cb);
@@ -1121,12 +1154,8 @@ void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
 
 void launch_jacobi_svd(const double* R, int64_t ldr, int m, int nc, double* sigma, double* U, CallScratch& sc) {
     const size_t smem = sizeof(double) * (static_cast<size_t>(m) * nc + static_cast<size_t>(nc) * nc + nc);
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+    set_max_smem(jacobi_svd_kernel, 200 * 1024);
     jacobi_svd_kernel<<<1, kJacThreads, smem, sc.stream()>>>(R, ldr, m, nc, sigma, U, eig_probe_buffer());
     TS_LAUNCH_CHECK();
     sc.launches += 1;

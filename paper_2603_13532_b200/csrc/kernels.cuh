@@ -124,6 +124,10 @@ struct CholBatch {
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc);
 // Device check of the ε = 0 Gram fast path (twin of capi.cu gram_rank): *flag |= 1 on rejection.
 void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch& sc);
+// Device check of the ε > 0 Gram fast path with a known output rank `expect`
+// (twin of capi.cu gram_rank, θ from the device ‖h‖² *hss): *flag |= 1 on rejection.
+void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss, int expect,
+                            int* flag, CallScratch& sc);
 
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);

@@ -130,11 +130,7 @@ bool launch_kron3(const Kron3Args& args, int max_shape, CallScratch& sc) {
     if (max_shape > kMaxR || s1 * s2 > kMaxC || s0 * s2 > kMaxC || s0 * s1 > kMaxC) return false;
     const size_t smem = sizeof(double) * (static_cast<size_t>(s0 + s1 + s2) * kMaxR + 2 * kMaxR * kMaxR +
                                           static_cast<size_t>(kMaxR) * (s1 + s0));
-    static const bool configured = [] {  // thread-safe one-time setup (never inside a graph capture)
-        TS_CUDA_CHECK(cudaFuncSetAttribute(kron3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    set_max_smem(kron3_kernel, 200 * 1024);
     kron3_kernel<<<static_cast<unsigned>(args.natoms), kThreads, smem, sc.stream()>>>(args);
     TS_LAUNCH_CHECK();
     sc.launches += 1;

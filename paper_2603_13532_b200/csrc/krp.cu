@@ -347,12 +347,8 @@ void launch_krp_contract(const KrpArgs& args_in, int max_shape, CallScratch& sc)
     if (use3 && args.order == 3 && max_shape <= k3Rows) {
         const size_t smem =
             sizeof(double) * (2 * k3Rows * k3MLD + 2 * k3Rows * k3GLD + static_cast<size_t>(max_shape) * kCT);
-        // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-        static const bool configured = [&] {
-            TS_CUDA_CHECK(cudaFuncSetAttribute(krp3_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
-            return true;
-        }();
-        (void)configured;
+        // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+        set_max_smem(krp3_dmma_kernel, 120 * 1024);
         dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>((args.s + kCT - 1) / kCT));
         krp3_dmma_kernel<<<grid, kThreads, smem, sc.stream()>>>(args);
         TS_LAUNCH_CHECK();
@@ -380,12 +376,7 @@ void launch_krp_contract(const KrpArgs& args_in, int max_shape, CallScratch& sc)
               static_cast<unsigned>(cchunks * args.splits));
     // Thread-safe one-time setup (the attribute call must not run inside a CUDA
     // graph capture of a later call).
-    static const bool configured = [] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(krp_dmma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        TS_CUDA_CHECK(cudaFuncSetAttribute(krp_dmma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        return true;
-    }();
-    (void)configured;
+    set_max_smem(krp_dmma_kernel<32>, 200 * 1024); set_max_smem(krp_dmma_kernel<64>, 200 * 1024);
     if (smem > 200 * 1024) throw Error(TS_UNSUPPORTED, "stage B: block ranks too large for shared memory");
     if (RT == 32) krp_dmma_kernel<32><<<grid, kThreads, smem, sc.stream()>>>(args);
     else krp_dmma_kernel<64><<<grid, kThreads, smem, sc.stream()>>>(args);

@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/tucksum_cuda.h"
 
@@ -13,6 +16,20 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     std::snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e), file,
                   line, what);
     throw Error(e == cudaErrorMemoryAllocation ? TS_OOM : TS_CUDA, buf);
+}
+
+void set_max_smem(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    TS_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (!done.insert({dev, kernel}).second) return;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) {
+        done.erase({dev, kernel});
+        throw_cuda(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)", __FILE__, __LINE__);
+    }
 }
 
 HostStage::~HostStage() {

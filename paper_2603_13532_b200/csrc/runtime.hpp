@@ -26,6 +26,16 @@ struct Error : std::runtime_error {
 
 #define TS_LAUNCH_CHECK() TS_CUDA_CHECK(cudaGetLastError())
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: applied
+// once per (current device, kernel), thread-safe (concurrent lanes, one context
+// per GPU in one process).  Must not run inside a graph capture: every kernel
+// is first launched by a plain call before any call is captured.
+void set_max_smem(const void* kernel, int bytes);
+template <class K>
+inline void set_max_smem(K* kernel, int bytes) {
+    set_max_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // Pinned host staging ring for kernel descriptors: written by the host during a
 // call, copied to the device with cudaMemcpyAsync on the call's stream.  Every
 // call ends with a stream synchronisation, so the ring restarts at each call.

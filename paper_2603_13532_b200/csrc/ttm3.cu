@@ -134,12 +134,8 @@ bool launch_ttm3(const Ttm3Args& args, int max_shape, int max_r2, CallScratch& s
     if (args.natoms == 0) return true;
     if (max_shape > kR || args.q[0] > kQ || args.q[1] > kQ) return false;
     const size_t smem = sizeof(double) * (3 * kR * kLQ + 2 * kR * kLG);
-    // Thread-safe one-time setup (concurrent lanes of ts_krp_sum_many).
-    static const bool configured = [&] {
-        TS_CUDA_CHECK(cudaFuncSetAttribute(ttm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        return true;
-    }();
-    (void)configured;
+    // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
+    set_max_smem(ttm3_kernel, static_cast<int>(smem));
     dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>((max_r2 + kSPC - 1) / kSPC));
     ttm3_kernel<<<grid, kThreads, smem, sc.stream()>>>(args);
     TS_LAUNCH_CHECK();

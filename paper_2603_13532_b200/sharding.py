@@ -41,3 +41,23 @@ def init_nccl_engine(device: int, rank: int, world: int) -> Engine:
         dist.broadcast_object_list(obj, src=0)
         eng.init_nccl(obj[0], world, rank)
     return eng
+
+
+def gloo_allreduce(buf):
+    """Host all-reduce hook over torch.distributed (e.g. gloo): sums the numpy
+    buffer over the ranks in place."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(buf)
+    dist.all_reduce(t)
+
+
+def init_host_engine(device: int, rank: int, world: int) -> Engine:
+    """The rank's Engine with the host all-reduce hook (ts_ctx_set_host_allreduce)
+    over the default torch.distributed group instead of NCCL: the same sharded
+    ts_krp_sum orchestration, exchanges through host memory."""
+    eng = Engine(device)
+    if world > 1:
+        eng.set_host_allreduce(gloo_allreduce, world, rank)
+    return eng

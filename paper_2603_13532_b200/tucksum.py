@@ -50,8 +50,11 @@ EXPORTED_SYMBOLS = [
     "ts_ctx_set_debug", "ts_ctx_stage_times", "ts_ctx_set_timing", "ts_ctx_last_paths", "ts_sym_eig",
     "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
-    "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked",
+    "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked", "ts_ctx_comm_info",
+    "ts_ctx_set_host_allreduce",
 ]
+
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
 
 
 class TucksumCudaError(RuntimeError):
@@ -114,6 +117,7 @@ def lib():
         L.ts_kron_sketch_dims.argtypes = [i64, i64p, i64p, i64p]
         L.ts_batch_upload.argtypes = [C.c_void_p, C.POINTER(TsTuckerView), i64, C.POINTER(C.c_void_p)]
         L.ts_omega_prepare.argtypes = [C.c_void_p, i64, i64p, i64, u64, u64]
+        L.ts_ctx_set_host_allreduce.argtypes = [C.c_void_p, HOST_ALLREDUCE_FN, C.c_void_p, C.c_int, C.c_int]
         for name in ("ts_result_factor", "ts_result_core", "ts_result_free", "ts_result_dims", "ts_result_ranks",
                      "ts_batch_free", "ts_ctx_destroy", "ts_ctx_set_debug", "ts_ctx_set_timing",
                      "ts_ctx_stage_times", "ts_result_intermediate"):
@@ -564,6 +568,30 @@ class Engine:
     def init_nccl(self, unique_id: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(unique_id, 128)
         _check(lib().ts_ctx_init_nccl(self.handle, buf, C.c_int(nranks), C.c_int(rank)))
+
+    def set_host_allreduce(self, fn, nranks: int, rank: int):
+        """Sharded sums without NCCL: fn(buf: np.ndarray) must sum buf over the
+        ranks in place (e.g. a gloo all-reduce); None removes the hook."""
+        if fn is None:
+            self._host_ar = None
+            _check(lib().ts_ctx_set_host_allreduce(self.handle, None, None, C.c_int(1), C.c_int(0)))
+            return
+
+        def tramp(_user, buf, count):
+            try:
+                fn(np.ctypeslib.as_array(buf, shape=(int(count),)))
+                return 0
+            except Exception:  # noqa: BLE001 — reported to the library as a failed exchange
+                return 1
+
+        self._host_ar = HOST_ALLREDUCE_FN(tramp)  # kept alive with the engine
+        _check(lib().ts_ctx_set_host_allreduce(self.handle, self._host_ar, None, C.c_int(nranks), C.c_int(rank)))
+
+    def comm_info(self):
+        """(nranks, rank) of the context's NCCL communicator (ncclCommCount / ncclCommUserRank)."""
+        n, r = C.c_int(), C.c_int()
+        _check(lib().ts_ctx_comm_info(self.handle, C.byref(n), C.byref(r)))
+        return int(n.value), int(r.value)
 
     @property
     def stream(self) -> int:

@@ -10,16 +10,23 @@ G^(k) ← S.substream(900000 + k); weights ← S.substream(7); request seed ←
 S.substream(5000).
 
 All summands of one workload live in per-mode slabs (the stacked formal-sum
-layout), so a batch upload is one host→device copy per mode.
+layout), so a batch upload is one host→device copy per mode.  Summand k depends
+only on (cfg, k), so a rank of a sharded run generates (and pins) only its own
+contiguous block ``k_range`` of the K summands.
+
+The RNG backend is pluggable: by default the library's host generator
+(``ts_substream`` / ``ts_gaussian_matrix``); the reference arm of ``bench.py``
+passes the CPU oracle's bit-identical generator instead, so that arm never maps
+``libtucksum_cuda.so`` (tests/test_capi_cpu.py checks the two agree bitwise).
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Optional
+from typing import Callable, List, Optional, Tuple
 
 import numpy as np
 
-from .tucksum import RngSeed, TuckerTensor, gaussian_matrix
+from .tucksum import RngSeed, TuckerTensor
 
 
 @dataclass
@@ -34,11 +41,14 @@ class Workload:
     cap: Optional[List[int]]         # BASELINE target rank (SURVEY.md §8(d) rank cap)
     eps: float
     seed: RngSeed                    # request seed (Ω streams)
-    slabs: List[np.ndarray]          # per-mode stacked factors + core slab (host)
+    slabs: List[np.ndarray]          # per-mode stacked factors + core slab (host), this shard only
     reps: int = 1                    # repetitions per step (cfg4 time-stepping loop)
+    K_total: int = 0                 # summands of the whole job (all shards)
+    k_begin: int = 0                 # first summand index of this shard
 
     @property
     def K(self) -> int:
+        """Summands held by this Workload (= K_total unless built for a shard)."""
         return len(self.summands)
 
 
@@ -75,18 +85,45 @@ def config_spec(cfg: int) -> dict:
     return dict(_SPECS[cfg])
 
 
-def make_workload(cfg: int, K: Optional[int] = None, n_override: Optional[List[int]] = None) -> Workload:
-    """Builds BASELINE config `cfg` (1..5).  `K` / `n_override` shrink it for parity tests."""
+Gaussian = Callable[[int, int, Tuple[int, int]], np.ndarray]
+Substream = Callable[[Tuple[int, int], int], Tuple[int, int]]
+
+
+def _library_rng() -> Tuple[Gaussian, Substream]:
+    from . import tucksum as T
+
+    def gauss(rows, cols, seed):
+        return T.gaussian_matrix(rows, cols, T.RngSeed(*seed))
+
+    def sub(seed, salt):
+        x = T.RngSeed(*seed).substream(salt)
+        return x.seed, x.stream
+
+    return gauss, sub
+
+
+def make_workload(cfg: int, K: Optional[int] = None, n_override: Optional[List[int]] = None,
+                  k_range: Optional[Tuple[int, int]] = None, gaussian: Optional[Gaussian] = None,
+                  substream: Optional[Substream] = None) -> Workload:
+    """Builds BASELINE config `cfg` (1..5).  `K` / `n_override` shrink it for parity tests;
+    `k_range` = [begin, end) builds only that shard of the K summands; `gaussian` /
+    `substream` replace the library's host RNG by a bit-identical one (e.g. the oracle's)."""
     sp = _SPECS[cfg]
     dims = list(n_override or sp["dims"])
     K = int(K or sp["K"])
+    kb, ke = k_range if k_range is not None else (0, K)
+    if not 0 <= kb <= ke <= K:
+        raise ValueError("make_workload: bad k_range")
+    if gaussian is None or substream is None:
+        gaussian, substream = _library_rng()
     r = list(sp["r"])
     d = len(dims)
-    S = RngSeed(2603, cfg)
-    R = [K * r[j] for j in range(d)]
+    S = (2603, cfg)
+    Kl = ke - kb
+    R = [Kl * r[j] for j in range(d)]
     slabs = [np.zeros((dims[j], R[j]), order="F") for j in range(d)]
     core_size = int(np.prod(r))
-    core_slab = np.zeros(K * core_size)
+    core_slab = np.zeros(Kl * core_size)
     idx = np.indices(r).sum(axis=0).astype(np.float64)  # i1 + i2 + ... (0-based)
     decay = sp["decay"]
     if decay is None:
@@ -99,31 +136,32 @@ def make_workload(cfg: int, K: Optional[int] = None, n_override: Optional[List[i
         scale = decay[1] ** idx
     qleg = _legendre_q(dims[1], 10) if cfg == 3 else None
     summands = []
-    for k in range(K):
+    for k in range(kb, ke):
+        kl = k - kb
         factors = []
         for j in range(d):
-            g = gaussian_matrix(dims[j], r[j], S.substream(100000 + 16 * k + j))
+            g = gaussian(dims[j], r[j], substream(S, 100000 + 16 * k + j))
             if cfg == 3 and j > 0:
                 o = _thin_q(g[: r[j], : r[j]])  # random 10×10 orthogonal from the same stream
                 f = qleg @ o
             else:
                 f = _thin_q(g)
-            slabs[j][:, k * r[j]:(k + 1) * r[j]] = f
-            factors.append(slabs[j][:, k * r[j]:(k + 1) * r[j]])
-        core = gaussian_matrix(core_size, 1, S.substream(900000 + k)).reshape(r, order="F")
+            slabs[j][:, kl * r[j]:(kl + 1) * r[j]] = f
+            factors.append(slabs[j][:, kl * r[j]:(kl + 1) * r[j]])
+        core = gaussian(core_size, 1, substream(S, 900000 + k)).reshape(r, order="F")
         if scale is not None:
             core = core * scale
-        seg = core_slab[k * core_size:(k + 1) * core_size]
+        seg = core_slab[kl * core_size:(kl + 1) * core_size]
         seg[:] = core.reshape(-1, order="F")
         summands.append(TuckerTensor(seg.reshape(r, order="F"), factors))
     if cfg == 3:
-        weights = gaussian_matrix(K, 1, S.substream(7))[:, 0].copy()
+        weights = gaussian(K, 1, substream(S, 7))[kb:ke, 0].copy()
     else:
-        weights = np.ones(K)
+        weights = np.ones(Kl)
     widths = [min(sp["s"], max(dims))] * d
-    return Workload(name=sp["name"], cfg=cfg, dims=dims, ranks=[list(r) for _ in range(K)], summands=summands,
-                    weights=weights, widths=widths, cap=list(sp["cap"]), eps=0.0, seed=S.substream(5000),
-                    slabs=slabs + [core_slab], reps=int(sp.get("reps", 1)))
+    return Workload(name=sp["name"], cfg=cfg, dims=dims, ranks=[list(r) for _ in range(Kl)], summands=summands,
+                    weights=weights, widths=widths, cap=list(sp["cap"]), eps=0.0, seed=RngSeed(*substream(S, 5000)),
+                    slabs=slabs + [core_slab], reps=int(sp.get("reps", 1)), K_total=K, k_begin=kb)
 
 
 def f_alg(dims, ranks_per_summand, s, q=None) -> float:

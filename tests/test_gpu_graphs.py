@@ -16,15 +16,16 @@ def same(a, b):
         np.array_equal(a.dense_core(), b.dense_core())
 
 
-def run(eng, batch, wl, weights, strategy, n):
+def run(eng, batch, wl, weights, strategy, n, eps=0.0, cap="cfg"):
     outs = []
+    cap = wl.cap if cap == "cfg" else cap
     for _ in range(n):
         if strategy == "lazy":
-            res = eng.lazy_sum(batch, weights, 0.0, wl.cap)
+            res = eng.lazy_sum(batch, weights, eps, cap)
         else:
             widths = T.kron_sketch_dims(wl.widths, wl.dims) if strategy == "kron" else wl.widths
             st = T.Strategy.Kron if strategy == "kron" else T.Strategy.Krp
-            res = eng.krp_sum(batch, weights, widths, wl.seed, 0.0, wl.cap, st)
+            res = eng.krp_sum(batch, weights, widths, wl.seed, eps, cap, st)
         outs.append(res)
     return outs
 
@@ -63,6 +64,35 @@ def test_graph_replay_bitwise_equal_to_plain_launches(cfg, K, strategy):
         assert same(run(graphed, bg2, wl, wl.weights, strategy, 1)[0].to_tucker(), ref[0])
         assert graphed.graph_replays == before
         bp.free(), bg.free(), bg2.free()
+    finally:
+        plain.close()
+        graphed.close()
+
+
+@pytest.mark.parametrize("cfg,eps", [(1, 1e-6), (4, 1e-6), (2, 1e-10)])
+def test_graph_replay_reference_semantics_eps(cfg, eps):
+    """Reference-exact mode (eps > 0, no rank cap) also replays as a CUDA graph:
+    the captured ranks are the probe run's, and every replay re-derives the
+    reference tail rule on the device (gram_rank_check_kernel) — bitwise equal
+    to plain launches."""
+    wl = make_workload(cfg)
+    plain = T.Engine(0)
+    plain.set_graphs(False)
+    graphed = T.Engine(0)
+    try:
+        bp, bg = plain.upload(wl.summands), graphed.upload(wl.summands)
+        ref = run(plain, bp, wl, wl.weights, "krp", 1, eps, None)[0].to_tucker()
+        res = run(graphed, bg, wl, wl.weights, "krp", 5, eps, None)
+        if cfg in (1, 4):
+            assert graphed.graph_replays == 3
+        for r in res:
+            assert same(r.to_tucker(), ref)
+            r.free()
+        # A different tolerance is a different key (other ranks), never a stale replay.
+        ref2 = run(plain, bp, wl, wl.weights, "krp", 1, eps * 1e3, None)[0].to_tucker()
+        got2 = [r.to_tucker() for r in run(graphed, bg, wl, wl.weights, "krp", 3, eps * 1e3, None)]
+        assert all(same(g, ref2) for g in got2)
+        bp.free(), bg.free()
     finally:
         plain.close()
         graphed.close()

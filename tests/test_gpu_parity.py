@@ -120,7 +120,9 @@ def test_nccl_path_single_rank_matches():
     ref, _ = gpu_sum(T.Engine(0), wl.summands, wl.weights, wl.widths, seed, wl.eps, wl.cap)
     eng = T.Engine(0)
     try:
+        assert eng.comm_info() == (1, 0)
         eng.init_nccl(T.Engine.nccl_unique_id(), 1, 0)
+        assert eng.comm_info() == (1, 0)  # ncclCommCount / ncclCommUserRank
         out, _ = gpu_sum(eng, wl.summands, wl.weights, wl.widths, seed, wl.eps, wl.cap)
     finally:
         eng.close()
@@ -158,6 +160,29 @@ def test_krp_sum_many_matches_sequential_calls():
         eng.close()
 
 
+def test_krp_sum_many_matches_oracle_per_sum():
+    """Every sum of a ts_krp_sum_many call (mixed shapes, seeds, both truncation
+    modes) against the CPU oracle on its own inputs and Ω (1e-10, same ranks)."""
+    eng = T.Engine(0)
+    try:
+        cases = [make_workload(1), make_workload(2), make_workload(1, K=3), make_workload(2, K=5, n_override=[300, 200, 100])]
+        for eps, cap in [(0.0, [16, 16, 16]), (1e-6, None)]:
+            batches = [eng.upload(w.summands) for w in cases]
+            seeds = [T.RngSeed(w.seed.seed, w.seed.stream + 7 * i) for i, w in enumerate(cases)]
+            widths = [30, 30, 30]
+            many = eng.krp_sum_many(batches, [w.weights for w in cases], widths, seeds, eps, cap, lanes=3)
+            for w, sd, r in zip(cases, seeds, many):
+                out = r.to_tucker()
+                r.free()
+                ref, _ = O.krp_sum(w.summands, w.weights, widths, (sd.seed, sd.stream), eps, cap=cap, threads=8)
+                assert out.ranks == ref.ranks
+                assert rel_diff(out, ref) <= PARITY
+            for b in batches:
+                b.free()
+    finally:
+        eng.close()
+
+
 def test_cpp_host_caller():
     """A C++ program drives the C ABI end to end (upload, two krp_sum calls,
     malformed requests, ranks, orthonormality, determinism, exact-sum norm)."""
@@ -178,6 +203,24 @@ def test_reference_semantics_eps(engine, cfg):
     """Pure reference semantics (eps > 0, no rank cap) on the same inputs."""
     wl = make_workload(cfg)
     check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), 1e-6, None)
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-10])
+def test_reference_semantics_cfg4(engine, eps):
+    """The path the drop-in adapter runs (eps > 0, max_rank = NULL; reference
+    src/sketch.cpp:171, src/tucker.cpp:244-276) at BASELINE config 4 (d = 4)."""
+    wl = make_workload(4)
+    check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), eps, None, gram=True)
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-10])
+def test_reference_semantics_cfg5_full_size(engine, eps):
+    """Reference-exact mode at full config 5 (K = 256, n = 8192, s = 64, no cap):
+    1e-10 on factors × core, same ranks, error to the exact sum to 3 digits."""
+    wl = make_workload(5)
+    out, ref = check_pair(engine, wl.summands, wl.weights, wl.widths, (wl.seed.seed, wl.seed.stream), eps, None,
+                          gram=True)
+    assert out.ranks == ref.ranks and max(out.ranks) <= 64
 
 
 def test_stage_intermediates_cfg1(engine):
@@ -425,8 +468,8 @@ def test_sym_eig_matches_oracle(engine):
 
 
 def test_sym_eig_tri_matches_oracle(engine):
-    """Tridiagonalization + bisection + inverse iteration eigensolver (the stage-G
-    default for n <= 64) vs the oracle's sym_eig: Gram matrices, decaying
+    """Tridiagonalization + bisection + inverse iteration eigensolver (opt-in via
+    TS_EIG=tri for n <= 64; Jacobi is the default) vs the oracle's sym_eig: Gram matrices, decaying
     spectra, exact clusters (rank-deficient Grams) and tiny sizes."""
     cases = []
     for n, seed in [(1, 0), (2, 1), (3, 2), (6, 3), (26, 4), (40, 5), (50, 6), (64, 7)]:
