@@ -188,11 +188,11 @@ int ts_effective_subrank_kron(ts_ctx* ctx, const ts_batch* batch, const double* 
  * (descending) and column eigenvectors (host).  sweeps / ms (nullable) report
  * the Jacobi sweeps and the kernel time. */
 int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms);
-/* Opt-in alternative (TS_EIG=tri; measured slower, not the default) for n <= 64:
- * Householder tridiagonalization + multisection bisection + inverse iteration in
- * one CTA (same reference semantics); *flag = 1 when its residual /
- * orthogonality acceptance check failed (the pipeline then falls back to the
- * Jacobi solver of ts_sym_eig). */
+/* The stage-G default for n <= 64: register-resident Householder
+ * tridiagonalisation + multisection + inverse iteration + Löwdin
+ * re-orthonormalisation in one CTA (same reference semantics); *flag = 1 when
+ * its residual / orthogonality acceptance check failed (the pipeline then falls
+ * back to the Jacobi solver of ts_sym_eig). */
 int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* flag, double* ms);
 
 /* ---- result: a dense-core Tucker tensor owned by the library ---- */

@@ -6,7 +6,8 @@
 // libtucksum_cuda.so with the exact reference signatures
 // (include/tucksum/sketch.hpp:85-94, include/tucksum/tucker.hpp).  It needs the
 // reference headers and therefore Eigen >= 3.4 (include/tucksum/types.hpp:4); it is
-// not compiled in this image (no Eigen) — see INTEGRATION.md.
+// compiled (syntax only, -Werror) against the real reference headers with a minimal Eigen
+// shim by tests/test_capi_cpu.py — see INTEGRATION.md.
 #pragma once
 
 #include <cstdlib>
@@ -187,7 +188,7 @@ inline double tucker_rel_error(const TuckerTensor& x, const TuckerTensor& ref) {
     const double w[2] = {1.0, -1.0};
     double diff = 0.0;
     detail::check(ts_tucker_norm(detail::context(), bd.get(), w, &diff));
-    const double denom = tucker_norm(ref);
+    const double denom = cuda::tucker_norm(ref);  // qualified: ADL also finds tucksum::tucker_norm
     return denom == 0.0 ? diff : diff / denom;
 }
 
@@ -196,8 +197,8 @@ inline double tucker_rel_error(const TuckerTensor& x, const TuckerTensor& ref) {
 // fold with one device rounding per summand (src/sketch.cpp:52-64).
 inline TuckerTensor round_sum(const SumRequest& req, const SketchPlan* plan = nullptr, SumStats* stats = nullptr) {
     switch (req.strategy) {
-        case Strategy::Krp: return krp_sum(req, plan, stats);
-        case Strategy::Kron: return kron_sum(req, plan, stats);
+        case Strategy::Krp: return cuda::krp_sum(req, plan, stats);
+        case Strategy::Kron: return cuda::kron_sum(req, plan, stats);
         case Strategy::Lazy: {
             detail::BatchPtr b = detail::upload(req.summands);
             ts_result* res = nullptr;
@@ -210,7 +211,7 @@ inline TuckerTensor round_sum(const SumRequest& req, const SketchPlan* plan = nu
             if (stats != nullptr) stats->eager_rank_trace.clear();
             TuckerTensor acc = formal_sum(std::vector<const TuckerTensor*>{req.summands.front()}, {req.weights.front()});
             for (std::size_t i = 1; i < req.summands.size(); ++i) {
-                acc = tucker_rounding(tucker_axby(1.0, acc, req.weights[i], *req.summands[i]), req.eps);
+                acc = cuda::tucker_rounding(tucker_axby(1.0, acc, req.weights[i], *req.summands[i]), req.eps);
                 if (stats != nullptr) stats->eager_rank_trace.push_back(acc.ranks());
             }
             return acc;

@@ -182,15 +182,22 @@ def test_every_strategy_fails_loudly_without_gpu():
         T.tucker_norm(x)
 
 
-def test_reference_adapter_compiles_against_stub_types():
+REF_INCLUDE = "/root/reference/proj/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INCLUDE), reason="reference headers absent (GPU box)")
+def test_reference_adapter_compiles_against_reference_headers():
     """include/tucksum_cuda_adapter.hpp (krp_sum, kron_sum, round_sum over every
     strategy, tucker_rounding / norm / inner / rel_error) compiles with -Wall
-    -Wextra against tests/cpp/stub — the reference's public types without Eigen."""
-    import os
+    -Wextra -Werror against the REAL reference headers
+    (/root/reference/proj/include/tucksum/*.hpp) and a minimal Eigen shim
+    (tests/cpp/eigen_shim — Eigen is absent from the image), and each drop-in has
+    exactly the reference entry point's function type."""
     import subprocess
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
-                        "-I", os.path.join(root, "include"), "-I", os.path.join(root, "tests", "cpp", "stub"),
-                        os.path.join(root, "tests", "cpp", "adapter_compile.cpp")], capture_output=True, text=True)
+    r = subprocess.run(["g++", "-std=c++20", "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
+                        "-I", REF_INCLUDE, "-I", os.path.join(root, "tests", "cpp", "eigen_shim"),
+                        "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cpp", "adapter_compile_ref.cpp")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
