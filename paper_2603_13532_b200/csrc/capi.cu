@@ -174,6 +174,10 @@ struct OmegaEntry {
 struct ts_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    // Side stream + fork/join events: stage D's CholeskyQR2 factor R runs on
+    // `side` while stage E's GEMM runs on `stream` (see sketched_sum_impl).
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int num_sms = 148;
     ts::HostStage stage;
     // Device Ω cache (shared with the lanes), bounded: least recently used
@@ -378,7 +382,8 @@ void unfolding_svd_accurate(double* X, std::int64_t rest, std::int64_t qk, doubl
 // ulps of λ₁, so the decision (and the kept subspace) is accepted only when it is
 // provably the one the exact singular values give; otherwise *ok = false and the
 // caller takes the accurate TSQR + one-sided Jacobi path.
-std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double theta, std::int64_t cap, bool* ok) {
+std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double theta, std::int64_t cap, double resid,
+                       bool* ok) {
     *ok = false;
     const std::int64_t q = static_cast<std::int64_t>(lam_in.size());
     if (q == 0 || !(lam_in[0] > 0.0)) return 1;
@@ -414,10 +419,13 @@ std::int64_t gram_rank(const std::vector<double>& lam_in, double tau, double the
     if (rank < q) {  // the kept subspace must be well separated from the discarded one
         const double gap = lam[static_cast<size_t>(rank - 1)] - lam[static_cast<size_t>(rank)];
         if (!(gap > 0.0)) return 1;
-        // Eigenvector error of the kept subspace ≲ residual / gap with the Jacobi
-        // residual off(C) ≤ 1e-14·‖C‖; its effect on the truncated tensor is damped
-        // by σ_{r+1}/σ₁.  Require it 10× below the 1e-10 parity bar.
-        const double err = 1e-14 * l1 / gap * std::sqrt(lam[static_cast<size_t>(rank)] / l1);
+        // Eigenvector error of the kept subspace ≲ residual / gap, with the
+        // solver's measured ‖C V − VΛ‖_F (resid ≥ 0) or the Jacobi solver's
+        // off(C) ≤ 1e-14·‖C‖; its effect on the truncated tensor is damped by
+        // σ_{r+1}/σ₁.  Require it 10× below the 1e-10 parity bar.  (Same
+        // arithmetic as the device twins in kernels.cu.)
+        const double rabs = resid >= 0.0 ? std::max(resid, 1e-16 * l1) : 1e-14 * l1;
+        const double err = rabs / gap * std::sqrt(lam[static_cast<size_t>(rank)] / l1);
         if (err > 1e-11) return 1;
     }
     *ok = true;
@@ -912,7 +920,141 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     // the Householder Q with R_ii ≥ 0 of the reference.  Modes whose Y is too
     // ill-conditioned (failed pivot, or second Gram far from I) or too short take
     // the Householder TSQR.
-    double* Uh[TS_MAX_ORDER];
+    double* Uh[TS_MAX_ORDER] = {};
+    double* P[TS_MAX_ORDER];
+    // Overlapped form (speculative calls whose modes all take CholeskyQR2):
+    // Û_n = Y_n R_n⁻¹ is never formed.  Stage E runs as Pt_n = Y_nᵀF_n on the
+    // main stream while the side stream computes R_n⁻¹ = R₁⁻¹R₂⁻¹ (Gram,
+    // Cholesky-inverse, Q₁ = Y R₁⁻¹, Gram, Cholesky-inverse, product); then
+    // P_n = R_n⁻ᵀ Pt_n and, at stage H, Ũ_n = Y_n (R_n⁻¹ P_k).  Same
+    // arithmetic as Û = Y R⁻¹ up to rounding order; the speculation check of the
+    // Cholesky pivots / second Gram is unchanged (a rejection redoes the call on
+    // the synchronous path below).
+    bool overlap = spec && !lazy && !ctx->debug && !norm_out;
+    for (int n = 0; n < d && overlap; ++n) overlap = dims[n] >= 2 * yc[n];
+    double* Rinv[TS_MAX_ORDER] = {};
+    if (overlap) {
+        int* flags = sc.alloc_n<int>(static_cast<size_t>(d));
+        TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<size_t>(d), st));
+        double* Pt[TS_MAX_ORDER];
+        for (int n = 0; n < d; ++n) {
+            Rinv[n] = sc.alloc_n<double>(static_cast<size_t>(yc[n] * yc[n]));
+            Pt[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
+            P[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
+        }
+        dflags = flags;
+        mark(ctx, 5);
+        TS_CUDA_CHECK(cudaEventRecord(ctx->ev_fork, st));
+        TS_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        {
+            CallScratch sd(ctx->side, hstage);
+            std::vector<GemmProblem> g1, q1, g2, rr;
+            double *G1[TS_MAX_ORDER], *G2[TS_MAX_ORDER], *Ri1[TS_MAX_ORDER], *Ri2[TS_MAX_ORDER], *Q1[TS_MAX_ORDER];
+            for (int n = 0; n < d; ++n) {
+                const std::int64_t c = yc[n];
+                G1[n] = sd.alloc_n<double>(static_cast<size_t>(c * c));
+                G2[n] = sd.alloc_n<double>(static_cast<size_t>(c * c));
+                Ri1[n] = sd.alloc_n<double>(static_cast<size_t>(c * c));
+                Ri2[n] = sd.alloc_n<double>(static_cast<size_t>(c * c));
+                Q1[n] = sd.alloc_n<double>(static_cast<size_t>(dims[n] * c));
+                GemmProblem p{};
+                p.M = p.N = static_cast<int>(c);
+                p.K = static_cast<int>(dims[n]);
+                p.A = p.B = Y + yoff[n];
+                p.lda = p.ldb = dims[n];
+                p.C = G1[n];
+                p.ldc = c;
+                g1.push_back(p);
+                p.A = p.B = Q1[n];
+                p.C = G2[n];
+                g2.push_back(p);
+                GemmProblem m{};
+                m.M = static_cast<int>(dims[n]);
+                m.N = m.K = static_cast<int>(c);
+                m.A = Y + yoff[n];
+                m.lda = dims[n];
+                m.B = Ri1[n];
+                m.ldb = c;
+                m.C = Q1[n];
+                m.ldc = dims[n];
+                q1.push_back(m);
+                GemmProblem r{};
+                r.M = r.N = r.K = static_cast<int>(c);
+                r.A = Ri1[n];
+                r.lda = c;
+                r.B = Ri2[n];
+                r.ldb = c;
+                r.C = Rinv[n];
+                r.ldc = c;
+                rr.push_back(r);
+            }
+            std::vector<std::int64_t> cw;
+            for (int n = 0; n < d; ++n)
+                if (std::find(cw.begin(), cw.end(), yc[n]) == cw.end()) cw.push_back(yc[n]);
+            auto chol_batches = [&](bool second) {
+                for (std::int64_t c : cw) {
+                    ts::CholBatch cb{};
+                    int nb = 0;
+                    for (int n = 0; n < d; ++n) {
+                        if (yc[n] != c) continue;
+                        cb.G[nb] = second ? G2[n] : G1[n];
+                        cb.Rinv[nb] = second ? Ri2[n] : Ri1[n];
+                        cb.flag[nb] = flags + n;
+                        ++nb;
+                    }
+                    cb.ldg = cb.ldri = c;
+                    cb.n = static_cast<int>(c);
+                    cb.check_identity = second ? 1 : 0;
+                    ts::launch_chol_inv(cb, nb, sd);
+                }
+            };
+            ts::launch_grouped_gemm(Layout::TN, g1, sd, ctx->num_sms);
+            chol_batches(false);
+            ts::launch_grouped_gemm(Layout::NN, q1, sd, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::TN, g2, sd, ctx->num_sms);
+            chol_batches(true);
+            ts::launch_grouped_gemm(Layout::NN, rr, sd, ctx->num_sms);
+            sc.launches += sd.launches;
+        }  // side-stream scratch released on the side stream
+        TS_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));
+        ctx->last_qr_fallbacks = 0;
+        // ---- Stage E (main stream, concurrent with the above): Pt_n = Y_nᵀ F_n
+        {
+            std::vector<GemmProblem> ps;
+            for (int n = 0; n < d; ++n) {
+                GemmProblem p{};
+                p.A = Y + yoff[n];
+                p.lda = dims[n];
+                p.B = b->F[n];
+                p.ldb = dims[n];
+                p.C = Pt[n];
+                p.ldc = q[n];
+                p.M = static_cast<int>(q[n]);
+                p.N = static_cast<int>(b->R[n]);
+                p.K = static_cast<int>(dims[n]);
+                ps.push_back(p);
+            }
+            ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        }
+        TS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+        {  // P_n = R_n⁻ᵀ Pt_n
+            std::vector<GemmProblem> ps;
+            for (int n = 0; n < d; ++n) {
+                GemmProblem p{};
+                p.A = Rinv[n];
+                p.lda = q[n];
+                p.B = Pt[n];
+                p.ldb = q[n];
+                p.C = P[n];
+                p.ldc = q[n];
+                p.M = static_cast<int>(q[n]);
+                p.N = static_cast<int>(b->R[n]);
+                p.K = static_cast<int>(q[n]);
+                ps.push_back(p);
+            }
+            ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        }
+    } else {
     {
         std::vector<int> chol(static_cast<size_t>(d), 0);
         std::vector<GemmProblem> g1, q1, g2, q2;
@@ -1013,7 +1155,6 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     }
     mark(ctx, 5);
     // ---- Stage E: P_n = Û_nᵀ F_n (q_n × R_n)
-    double* P[TS_MAX_ORDER];
     {
         std::vector<GemmProblem> ps;
         for (int n = 0; n < d; ++n) {
@@ -1031,6 +1172,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             ps.push_back(p);
         }
         ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+    }
     }
     mark(ctx, 6);
     std::int64_t hsize = 0;
@@ -1147,20 +1289,23 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 ++ctx->last_svd_fallbacks;
                 accurate_modes |= 1u << k;
             } else {
-            // Eigensolver: tridiagonalization + bisection + inverse iteration
-            // (eig_tri.cu) with a device acceptance check; on rejection the
-            // two-sided Jacobi (eig.cu) recomputes — in the speculative path via
-            // the stage-G flag (whole call redone synchronously), otherwise here.
-            const bool use_tri = ts::tri_eig_enabled() && qk <= 64 && !dsw;
+            // Eigensolver: for q ≤ 64 the tridiagonalisation solver (eig_trd.cu)
+            // with its device acceptance check and measured residual; on rejection
+            // the two-sided Jacobi (eig.cu) recomputes — in the speculative path
+            // via the stage-G flag (whole call redone synchronously), otherwise
+            // here.  Larger q (and TS_EIG=jacobi) take Jacobi directly.
+            const bool use_trd = qk <= 64 && !dsw && !ts::jacobi_eig_forced();
             int* tflag = nullptr;
-            if (use_tri) {
+            double* d_res = nullptr;
+            if (use_trd) {
                 if (spec_g) {
                     tflag = gflags + k;
                 } else {
                     tflag = sc.alloc_n<int>(1);
                     TS_CUDA_CHECK(cudaMemsetAsync(tflag, 0, sizeof(int), st));
                 }
-                ts::launch_sym_tridiag(C, qk, static_cast<int>(qk), lam, Pk[k], tflag, sc);
+                d_res = sc.alloc_n<double>(1);
+                ts::launch_sym_trd(C, qk, static_cast<int>(qk), lam, Pk[k], tflag, d_res, sc);
             } else {
                 ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
             }
@@ -1169,10 +1314,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 if (eps == 0.0) {
                     // At ε = 0 the fast-path rank is fixed (cap, else q); its checks run on the device.
                     rk = (capk > 0 && capk < qk) ? capk : qk;
-                    ts::launch_gram_check(lam, static_cast<int>(qk), static_cast<int>(capk), gflags + k, sc);
+                    ts::launch_gram_check(lam, static_cast<int>(qk), static_cast<int>(capk), d_res, gflags + k, sc);
                 } else {
                     rk = fixed_rank[k];
-                    ts::launch_gram_rank_check(lam, static_cast<int>(qk), static_cast<int>(capk), eps, d, d_hss,
+                    ts::launch_gram_rank_check(lam, static_cast<int>(qk), static_cast<int>(capk), eps, d, d_hss, d_res,
                                                static_cast<int>(rk), gflags + k, sc);
                 }
             } else {
@@ -1180,21 +1325,24 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
                                               cudaMemcpyDeviceToHost, st));
                 int hsw = 0, htf = 0;
+                double hres = -1.0;
                 if (dsw) TS_CUDA_CHECK(cudaMemcpyAsync(&hsw, dsw, sizeof(int), cudaMemcpyDeviceToHost, st));
                 if (tflag) TS_CUDA_CHECK(cudaMemcpyAsync(&htf, tflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+                if (d_res) TS_CUDA_CHECK(cudaMemcpyAsync(&hres, d_res, sizeof(double), cudaMemcpyDeviceToHost, st));
                 TS_CUDA_CHECK(cudaStreamSynchronize(st));
-                if (htf) {  // tridiagonal solver rejected its own result
+                if (htf) {  // the tridiagonalisation solver rejected its own result
                     ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, nullptr);
                     TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
                                                   cudaMemcpyDeviceToHost, st));
                     TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                    hres = -1.0;  // Jacobi: the assumed residual
                     ++ctx->last_eig_fallbacks;
                 }
                 if (dsw)
                     std::fprintf(stderr, "[ts] st-hosvd mode %d: n=%lld sweeps=%d lam1=%.3e lam_last=%.3e\n", k,
                                  static_cast<long long>(qk), hsw, lv[0], lv.back());
                 bool ok = false;
-                rk = gram_rank(lv, eps, theta, capk, &ok);
+                rk = gram_rank(lv, eps, theta, capk, hres, &ok);
                 if (!ok) {
                     double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
                     unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc);
@@ -1256,6 +1404,25 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     mark(ctx, 10);
     // ---- Stage H: Ũ_n = Û_n · P_n (n × rank_n); the core is g.
     {
+        double* Tk[TS_MAX_ORDER] = {};
+        if (overlap) {  // Ũ_n = Y_n (R_n⁻¹ P_k): first T_n = R_n⁻¹ P_k (q_n × rank_n)
+            std::vector<GemmProblem> ts_;
+            for (int n = 0; n < d; ++n) {
+                Tk[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * rank[n]));
+                GemmProblem p{};
+                p.A = Rinv[n];
+                p.lda = q[n];
+                p.B = Pk[n];
+                p.ldb = q[n];
+                p.C = Tk[n];
+                p.ldc = q[n];
+                p.M = static_cast<int>(q[n]);
+                p.N = static_cast<int>(rank[n]);
+                p.K = static_cast<int>(q[n]);
+                ts_.push_back(p);
+            }
+            ts::launch_grouped_gemm(Layout::NN, ts_, sc, ctx->num_sms);
+        }
         std::vector<GemmProblem> ps;
         for (int n = 0; n < d; ++n) {
             res->dims[n] = dims[n];
@@ -1267,9 +1434,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 TS_CUDA_CHECK(cudaMallocAsync(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n]), st));
             }
             GemmProblem p{};
-            p.A = Uh[n];
+            p.A = overlap ? Y + yoff[n] : Uh[n];
             p.lda = dims[n];
-            p.B = Pk[n];
+            p.B = overlap ? Tk[n] : Pk[n];
             p.ldb = q[n];
             p.C = res->factors[n];
             p.ldc = dims[n];
@@ -1356,8 +1523,7 @@ ts_result* run_sum(ts_ctx* ctx, const ts_batch* b, const double* weights, const 
         return (e && e[0] == '0') || std::getenv("TS_DEBUG_SWEEPS") != nullptr;
     }();
     const bool graphable = !env_off && ctx->graphs && b != nullptr && weights != nullptr && eps >= 0.0 &&
-                           !sharded(ctx) && !ctx->debug && !ctx->timing && ctx->spec_ok && ctx->parent == nullptr &&
-                           !ts::tri_eig_enabled();
+                           !sharded(ctx) && !ctx->debug && !ctx->timing && ctx->spec_ok && ctx->parent == nullptr;
     if (!graphable)
         return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method);
     const int d = b->order;
@@ -1476,6 +1642,9 @@ int ts_ctx_create(int device, ts_ctx** out) {
         auto ctx = std::make_unique<ts_ctx>();
         ctx->device = device;
         TS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        TS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        TS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        TS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         TS_CUDA_CHECK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         cudaMemPool_t pool;
         TS_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1495,6 +1664,10 @@ int ts_ctx_destroy(ts_ctx* ctx) {
         for (auto& kv : ctx->omega) cudaFree(kv.second.ptr);
         for (auto& e : ctx->events) cudaEventDestroy(e);
         if (ctx->comm && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm);
+        cudaStreamSynchronize(ctx->side);
+        cudaEventDestroy(ctx->ev_fork);
+        cudaEventDestroy(ctx->ev_join);
+        cudaStreamDestroy(ctx->side);
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -2128,6 +2301,7 @@ int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* 
 int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* flag, double* ms) {
     return guarded([&] {
         if (!ctx || n < 1 || n > 64) invalid("ts_sym_eig_tri: need 1 <= n <= 64");
+        double* dres = nullptr;
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
         ctx->stage.reset();
         CallScratch sc(ctx->stream, ctx->stage);
@@ -2140,7 +2314,8 @@ int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, doub
         TS_CUDA_CHECK(cudaEventCreate(&e0));
         TS_CUDA_CHECK(cudaEventCreate(&e1));
         TS_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
-        ts::launch_sym_tridiag(dA, n, static_cast<int>(n), dl, dV, df, sc);
+        dres = sc.alloc_n<double>(1);
+        ts::launch_sym_trd(dA, n, static_cast<int>(n), dl, dV, df, dres, sc);
         TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         int hf = 0;
         TS_CUDA_CHECK(cudaMemcpyAsync(values, dl, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, ctx->stream));

@@ -788,7 +788,14 @@ __global__ void __launch_bounds__(4 * NC) chol_inv_kernel(CholBatch cb) {
 // the cap (else q), accept the Gram fast path only when λ_rank is resolvable and
 // the kept subspace is separated enough for the 1e-10 parity bar; *flag |= 1
 // otherwise.
-__global__ void gram_check_kernel(const double* __restrict__ lam, int q, int cap, int* __restrict__ flag) {
+// Absolute eigen-residual the subspace bound uses: the solver's measured
+// ‖C V − V Λ‖_F when it reports one, else the Jacobi solver's 1e-14·λ₁.
+__device__ __forceinline__ double resid_abs(const double* resid, double l1) {
+    return resid ? fmax(resid[0], 1e-16 * l1) : 1e-14 * l1;
+}
+
+__global__ void gram_check_kernel(const double* __restrict__ lam, int q, int cap, const double* __restrict__ resid,
+                                  int* __restrict__ flag) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double l1 = lam[0];
     bool ok = l1 > 0.0;
@@ -801,7 +808,7 @@ __global__ void gram_check_kernel(const double* __restrict__ lam, int q, int cap
             const double lnext = fmax(lam[rank], 0.0);
             const double gap = lr - lnext;
             ok = gap > 0.0;
-            if (ok) ok = !(1e-14 * l1 / gap * sqrt(lnext / l1) > 1e-11);
+            if (ok) ok = !(resid_abs(resid, l1) / gap * sqrt(lnext / l1) > 1e-11);
         }
     }
     if (!ok) atomicOr(flag, 1);
@@ -816,7 +823,8 @@ constexpr int kMaxRankRule = 128;
 // is bitwise the host's), the provability margins and the subspace separation,
 // and sets *flag |= 1 unless the fast path is accepted with exactly `expect`.
 __global__ void gram_rank_check_kernel(const double* __restrict__ lam, int q, int cap, double eps, int order,
-                                       const double* __restrict__ hss, int expect, int* __restrict__ flag) {
+                                       const double* __restrict__ hss, const double* __restrict__ resid, int expect,
+                                       int* __restrict__ flag) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double l1 = fmax(lam[0], 0.0);
     bool ok = lam[0] > 0.0;
@@ -841,7 +849,7 @@ __global__ void gram_rank_check_kernel(const double* __restrict__ lam, int q, in
             const double lr = fmax(lam[rank - 1], 0.0), lnext = fmax(lam[rank], 0.0);
             const double gap = __dsub_rn(lr, lnext);
             ok = gap > 0.0;
-            if (ok) ok = !(1e-14 * l1 / gap * sqrt(lnext / l1) > 1e-11);
+            if (ok) ok = !(resid_abs(resid, l1) / gap * sqrt(lnext / l1) > 1e-11);
         }
     }
     if (!ok || rank != expect) atomicOr(flag, 1);
@@ -1123,16 +1131,16 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
     sc.launches += 1;
 }
 
-void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch& sc) {
-    gram_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, flag);
+void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc) {
+    gram_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, resid, flag);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
 
-void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss, int expect,
-                            int* flag, CallScratch& sc) {
+void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss,
+                            const double* resid, int expect, int* flag, CallScratch& sc) {
     if (q > kMaxRankRule) throw Error(TS_UNSUPPORTED, "gram_rank_check: q exceeds the device maximum");
-    gram_rank_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, eps, order, hss, expect, flag);
+    gram_rank_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, eps, order, hss, resid, expect, flag);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }

@@ -105,11 +105,8 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
 // Fixed-address (permuted-layout) variant for n ≤ 64 (eig.cu); false if n > 64.
 bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
                           int* sweeps);
-// Tridiagonalization + bisection + inverse-iteration eigensolver for n ≤ 64
-// (eig_tri.cu): lambda[n] descending, V (n × n, ld n); *flag |= 1 when its
-// residual / orthogonality acceptance check fails (then use launch_sym_jacobi).
-bool launch_sym_tridiag(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, CallScratch& sc);
-bool tri_eig_enabled();
+// TS_EIG=jacobi: stage G uses the Jacobi solver even for n ≤ 64 (A/B timing).
+bool jacobi_eig_forced();
 // R⁻¹ of the Cholesky factor of small SPD matrices G[b] (n ≤ 96, one CTA each);
 // *flag[b] |= 1 on a non-positive pivot, |= 2 when check_identity and
 // max|G - I| > 1e-2.
@@ -123,11 +120,18 @@ struct CholBatch {
 };
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc);
 // Device check of the ε = 0 Gram fast path (twin of capi.cu gram_rank): *flag |= 1 on rejection.
-void launch_gram_check(const double* lam, int q, int cap, int* flag, CallScratch& sc);
+void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc);
 // Device check of the ε > 0 Gram fast path with a known output rank `expect`
 // (twin of capi.cu gram_rank, θ from the device ‖h‖² *hss): *flag |= 1 on rejection.
-void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss, int expect,
-                            int* flag, CallScratch& sc);
+void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss,
+                            const double* resid, int expect, int* flag, CallScratch& sc);
+// Stage-G eigensolver for n ≤ 64 (eig_trd.cu): Householder tridiagonalisation,
+// multisection, inverse iteration, back-transformation, Löwdin
+// re-orthonormalisation, all in one CTA.  lambda descending, V (n × n) the
+// matching columns; *resid = ‖C V − V Λ‖_F (measured); *flag |= 1 when the
+// result is not acceptable (then use launch_sym_jacobi).  False if n > 64.
+bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, double* resid,
+                    CallScratch& sc);
 
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);

@@ -468,9 +468,11 @@ def test_sym_eig_matches_oracle(engine):
 
 
 def test_sym_eig_tri_matches_oracle(engine):
-    """Tridiagonalization + bisection + inverse iteration eigensolver (opt-in via
-    TS_EIG=tri for n <= 64; Jacobi is the default) vs the oracle's sym_eig: Gram matrices, decaying
-    spectra, exact clusters (rank-deficient Grams) and tiny sizes."""
+    """The stage-G default eigensolver for n <= 64 (eig_trd.cu: register-resident
+    tridiagonalisation, multisection, inverse iteration, Löwdin) vs the oracle's
+    sym_eig: Gram matrices, decaying spectra, exact clusters (rank-deficient
+    Grams) and tiny sizes.  A rejected result (flag) is recomputed by Jacobi in
+    the pipeline; the well-separated Grams must be accepted."""
     cases = []
     for n, seed in [(1, 0), (2, 1), (3, 2), (6, 3), (26, 4), (40, 5), (50, 6), (64, 7)]:
         a = O.gaussian_matrix(2 * n, n, (18, seed))
@@ -484,9 +486,12 @@ def test_sym_eig_tri_matches_oracle(engine):
     q, _ = np.linalg.qr(rng.standard_normal((48, 48)))
     lam = np.repeat([3.0, 2.0, 1.0, 0.5], 12)
     cases.append((q * lam) @ q.T)  # four 12-fold eigenvalues
-    for c in cases:
+    accepted_required = list(range(8))  # the Gram matrices of Gaussian factors
+    for ci, c in enumerate(cases):
         n = c.shape[0]
         vals, vecs, rejected, ms = engine.sym_eig_tri(c)
+        if ci in accepted_required:
+            assert not rejected, (ci, n)
         ov, _ = O.sym_eig(c)
         scale = max(abs(ov[0]), 1e-300)
         assert np.max(np.abs(vals - ov)) <= 1e-13 * scale * max(1, n / 8), (n, np.max(np.abs(vals - ov)))
