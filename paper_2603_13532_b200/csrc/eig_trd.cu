@@ -105,7 +105,8 @@ __device__ __forceinline__ void dmma_64(const double* A, const double* B, double
 
 __global__ void __launch_bounds__(kEThreads, 1)
     trd_eig_kernel(const double* __restrict__ Cin, int64_t ldc, int n, double* __restrict__ lambda_out,
-                   double* __restrict__ V_out, int* __restrict__ flag_out, double* __restrict__ resid_out) {
+                   double* __restrict__ V_out, int* __restrict__ flag_out, double* __restrict__ resid_out,
+                   unsigned long long* __restrict__ prof) {
     extern __shared__ __align__(16) unsigned char smraw[];
     TrdSmem& S = *reinterpret_cast<TrdSmem*>(smraw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -122,22 +123,39 @@ __global__ void __launch_bounds__(kEThreads, 1)
                                        : 0.0;
         }
     if (tid == 0) S.flag = 0;
+    // Optional phase clocks (TS_EIG_PROFILE): prof[10 + phase] = cycles.
+    long long tmark = clock64();
+    auto phase = [&](int ph) {
+        if (prof != nullptr && tid == 0) {
+            const long long now = clock64();
+            prof[10 + ph] = static_cast<unsigned long long>(now - tmark);
+            tmark = now;
+        }
+    };
 
     // ---- 1. tridiagonalisation
     for (int k = 0; k + 2 < n; ++k) {
         const int r0 = k + 1;
         if (warp == (k >> 1)) {
-            const int s = k & 1;
-            const double xl = (lane > r0) ? a[s][0] : 0.0;   // x_j, j > r0 (entries ≥ n are 0)
-            const double xh = (lane + 32 > r0) ? a[s][1] : 0.0;
+            // the owned row k, selected without dynamic register indexing
+            const double rlo = (k & 1) ? a[1][0] : a[0][0], rhi = (k & 1) ? a[1][1] : a[0][1];
+            const double xl = (lane > r0) ? rlo : 0.0;   // x_j, j > r0 (entries ≥ n are 0)
+            const double xh = (lane + 32 > r0) ? rhi : 0.0;
             const double ss = warp_sum(fma(xl, xl, xh * xh));
-            const double x0 = __shfl_sync(0xffffffffu, r0 < 32 ? a[s][0] : a[s][1], r0 & 31);
-            const double akk = __shfl_sync(0xffffffffu, k < 32 ? a[s][0] : a[s][1], k & 31);
+            const double x0 = __shfl_sync(0xffffffffu, r0 < 32 ? rlo : rhi, r0 & 31);
+            const double akk = __shfl_sync(0xffffffffu, k < 32 ? rlo : rhi, k & 31);
             double tau = 0.0, beta = x0, scale = 0.0;
-            if (ss > 0.0) {
-                beta = -copysign(sqrt(fma(x0, x0, ss)), x0);
-                tau = (beta - x0) / beta;
-                scale = 1.0 / (x0 - beta);
+            if (ss > 0.0) {  // dlarfg with refined MUFU sqrt / reciprocals (no IEEE slow paths)
+                const double nn = fma(x0, x0, ss);
+                double r;
+                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(nn));
+                r = r * fma(-0.5 * nn, r * r, 1.5);
+                r = r * fma(-0.5 * nn, r * r, 1.5);
+                double sq = nn * r;
+                sq = fma(0.5 * r, fma(-sq, sq, nn), sq);  // one more correction of √nn
+                beta = -copysign(sq, x0);
+                tau = fma(-x0, rcp_refined(beta), 1.0);
+                scale = rcp_refined(x0 - beta);
             }
             S.V[k * kEN + lane] = lane == r0 ? 1.0 : xl * scale;
             S.V[k * kEN + lane + 32] = lane + 32 == r0 ? 1.0 : xh * scale;
@@ -181,9 +199,10 @@ __global__ void __launch_bounds__(kEThreads, 1)
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             const int i = ra + s;
+            const double rlo = s ? a[1][0] : a[0][0], rhi = s ? a[1][1] : a[0][1];
             if (i >= k0 && i < n) {
-                const double dii = __shfl_sync(0xffffffffu, i < 32 ? a[s][0] : a[s][1], i & 31);
-                const double nxt = (i + 1 < n) ? __shfl_sync(0xffffffffu, i + 1 < 32 ? a[s][0] : a[s][1], (i + 1) & 31) : 0.0;
+                const double dii = __shfl_sync(0xffffffffu, i < 32 ? rlo : rhi, i & 31);
+                const double nxt = (i + 1 < n) ? __shfl_sync(0xffffffffu, i + 1 < 32 ? rlo : rhi, (i + 1) & 31) : 0.0;
                 if (lane == 0) {
                     S.d[i] = dii;
                     if (i + 1 < n) S.e[i] = nxt;
@@ -192,6 +211,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
     }
     __syncthreads();
+    phase(0);
 
     // ---- 2. eigenvalues (multisection on the power-of-two-scaled T)
     if (warp == 0) {
@@ -207,7 +227,13 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
         const double tn = fmax(fabs(lo), fabs(hi));
         const double sc = tn > 0.0 ? inv_pow2_of(tn) : 1.0;  // tn·sc in [1, 2)
-        for (int i = lane; i < n; i += 32) {
+        for (int i = lane; i < kEN; i += 32) {
+            if (i >= n) {
+                S.ds[i] = 0.0;
+                S.es[i] = 0.0;
+                S.e2s[i] = 0.0;
+                continue;
+            }
             S.ds[i] = S.d[i] * sc;
             const double es = i + 1 < n ? S.e[i] * sc : 0.0;
             S.es[i] = es;
@@ -219,11 +245,12 @@ __global__ void __launch_bounds__(kEThreads, 1)
             S.misc[1] = hi * sc + pad;
             S.misc[2] = sc;
             S.misc[3] = tn;
+            S.misc[4] = 1.0 / sc;  // exact: sc is a power of two
         }
     }
     __syncthreads();
     const double tn = S.misc[3];
-    const double sc = S.misc[2];
+    const double isc = S.misc[4];
     if (tn == 0.0) {  // zero matrix: λ = 0, V = I
         for (int idx = tid; idx < n * n; idx += kEThreads) {
             const int i = idx % n, r = idx / n;
@@ -233,44 +260,62 @@ __global__ void __launch_bounds__(kEThreads, 1)
         if (tid == 0 && resid_out) *resid_out = 0.0;
         return;
     }
-    {
-        const int j = tid >> 4;  // eigenvalue index (ascending), a half-warp each
-        const int t = lane & 15;
-        const unsigned half = (lane < 16) ? 0x0000ffffu : 0xffff0000u;
+    if (tid < 4 * kEN) {
+        // Eigenvalue j (ascending) by a group of 4 lanes, 4 shifts per round
+        // (×5 narrowing), 23 rounds (2^-53 of the scaled Gershgorin width).
+        // Lanes tid ≥ 256 are idle here: the rounds are latency-bound chains,
+        // and fewer shifts per eigenvalue means less total work.
+        const int j = tid >> 2;
+        const int t = lane & 3, gbase = lane & 28;
+        const unsigned gmask = 0xfu << gbase;
         double lo_b = S.misc[0], hi_b = S.misc[1];
         const int jj = j < n ? j : n - 1;
-        for (int it = 0; it < 13; ++it) {
-            const double x = lo_b + (hi_b - lo_b) * (static_cast<double>(t + 1) * (1.0 / 17.0));
-            // number of eigenvalues < x: sign changes of (1, p_1, …, p_n)
+        for (int it = 0; it < 23; ++it) {
+            const double x = lo_b + (hi_b - lo_b) * (static_cast<double>(t + 1) * 0.2);
+            // number of eigenvalues < x: sign changes of (1, p_1, …, p_n), from
+            // the sign bits (integer ops; an exact +0 counts as positive)
             double pm = 1.0, pc = S.ds[0] - x;
-            bool neg = pc < 0.0;
-            int cnt = neg;
-            for (int i = 1; i < n; ++i) {
-                const double pn = fma(S.ds[i] - x, pc, -S.e2s[i - 1] * pm);
-                pm = pc;
-                pc = pn;
-                const bool ng = pc < 0.0 || (pc == 0.0 && neg);
-                cnt += ng != neg;
-                neg = ng;
-                if ((i & 7) == 7) {
-                    const double m = fmax(fabs(pc), fabs(pm));
-                    if (m > 0.0) {
-                        const double f = inv_pow2_of(m);
-                        pc *= f;
-                        pm *= f;
+            unsigned sg = static_cast<unsigned>(__double2hiint(pc)) >> 31;
+            int cnt = static_cast<int>(sg);
+            // Blocks of 8 steps, unrolled (the shared-memory loads of a block are
+            // independent of the recurrence and issue ahead of it); steps ≥ n are
+            // masked.
+            for (int i0 = 1; i0 < n; i0 += 8) {
+                double dv[8], ev[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    dv[u] = S.ds[min(i0 + u, kEN - 1)] - x;
+                    ev[u] = S.e2s[min(i0 + u - 1, kEN - 1)];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (i0 + u < n) {
+                        const double pn = fma(dv[u], pc, -ev[u] * pm);
+                        pm = pc;
+                        pc = pn;
+                        const unsigned sn = static_cast<unsigned>(__double2hiint(pc)) >> 31;
+                        cnt += static_cast<int>(sn ^ sg);
+                        sg = sn;
                     }
                 }
+                const double m = fmax(fabs(pc), fabs(pm));
+                if (m > 0.0) {
+                    const double f = inv_pow2_of(m);
+                    pc *= f;
+                    pm *= f;
+                }
             }
-            const unsigned above = __ballot_sync(0xffffffffu, cnt > jj) & half;
-            const int first = above ? __ffs(above) - 1 - (lane & 16) : 16;  // first shift with > jj below it
-            const double x_hi = __shfl_sync(0xffffffffu, x, (lane & 16) + min(first, 15));
-            const double x_lo = __shfl_sync(0xffffffffu, x, (lane & 16) + max(first - 1, 0));
-            if (first < 16) hi_b = x_hi;
+            const unsigned above = __ballot_sync(0xffffffffu, cnt > jj) & gmask;
+            const int first = above ? __ffs(above) - 1 - gbase : 4;  // first shift with > jj below it
+            const double x_hi = __shfl_sync(0xffffffffu, x, gbase + min(first, 3));
+            const double x_lo = __shfl_sync(0xffffffffu, x, gbase + max(first - 1, 0));
+            if (first < 4) hi_b = x_hi;
             if (first > 0) lo_b = x_lo;
         }
         if (t == 0 && j < n) S.lam[j] = 0.5 * (lo_b + hi_b);  // scaled
     }
     __syncthreads();
+    phase(1);
 
     // ---- 3. eigenvectors of T (scaled): inverse iteration, thread j
     if (tid < n) {
@@ -281,6 +326,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
         if (fabs(Dp) < pivtol) Dp = Dp < 0.0 ? -pivtol : pivtol;
         double Di = rcp_refined(Dp);
         S.Dinv[j] = Di;
+#pragma unroll 4
         for (int i = 0; i + 1 < n; ++i) {
             const double l = S.es[i] * Di;
             S.Lm[i * kEN + j] = l;
@@ -295,6 +341,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
         for (int itr = 0; itr < 2; ++itr) {
             double y = S.Z[j];
+#pragma unroll 4
             for (int i = 1; i < n; ++i) {
                 y = fma(-S.Lm[(i - 1) * kEN + j], y, S.Z[i * kLZ + j]);
                 S.Z[i * kLZ + j] = y;
@@ -302,13 +349,14 @@ __global__ void __launch_bounds__(kEThreads, 1)
             double x = y * S.Dinv[(n - 1) * kEN + j];
             S.Z[(n - 1) * kLZ + j] = x;
             double m = fabs(x);
+#pragma unroll 4
             for (int i = n - 2; i >= 0; --i) {
                 x = fma(S.Z[i * kLZ + j], S.Dinv[i * kEN + j], -S.Lm[i * kEN + j] * x);
                 S.Z[i * kLZ + j] = x;
                 m = fmax(m, fabs(x));
             }
             // normalise (∞-norm first so the 2-norm cannot overflow)
-            const double im = m > 0.0 ? 1.0 / m : 0.0;
+            const double im = m > 0.0 ? rcp_refined(m) : 0.0;
             double nrm = 0.0;
             for (int i = 0; i < n; ++i) {
                 const double z = S.Z[i * kLZ + j] * im;
@@ -319,6 +367,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
     }
     __syncthreads();
+    phase(2);
 
     // ---- 4. back-transformation: 16 lanes per eigenvector (column), rows
     // lane16 + 16u; Z ← H_k Z for k = n-3 … 0.  No CTA barrier.
@@ -327,14 +376,27 @@ __global__ void __launch_bounds__(kEThreads, 1)
         double z[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) z[u] = (col < n && t + 16 * u < n) ? S.Z[(t + 16 * u) * kLZ + col] : 0.0;
+        double v[4], tk = 0.0;
+        if (n >= 3) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = S.V[(n - 3) * kEN + t + 16 * u];
+            tk = S.tau[n - 3];
+        }
         for (int k = n - 3; k >= 0; --k) {
-            double v[4];
+            // prefetch reflector k-1 (independent of z)
+            double vn[4], tn1 = 0.0;
+            const int kn = k > 0 ? k - 1 : 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = S.V[k * kEN + t + 16 * u];
-            double s = fma(v[0], z[0], fma(v[1], z[1], fma(v[2], z[2], v[3] * z[3])));
-            s = hsum16(s) * S.tau[k];
+            for (int u = 0; u < 4; ++u) vn[u] = S.V[kn * kEN + t + 16 * u];
+            tn1 = S.tau[kn];
+            double s = fma(v[0], z[0], v[1] * z[1]) + fma(v[2], z[2], v[3] * z[3]);
+            s = hsum16(s) * tk;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) z[u] = fma(-s, v[u], z[u]);
+            for (int u = 0; u < 4; ++u) {
+                z[u] = fma(-s, v[u], z[u]);
+                v[u] = vn[u];
+            }
+            tk = tn1;
         }
         if (col < n) {
 #pragma unroll
@@ -357,6 +419,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
     }
     __syncthreads();
 
+    phase(3);
     // ---- 5. Löwdin re-orthonormalisation, at most 3 first-order steps:
     // E = ZᵀZ − I, Z ← Z − ½·Z·E (the orthogonality defect squares each step).
     double* E = S.Lm;
@@ -384,14 +447,15 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
         dmma_64<false>(S.Z, E, P, n);
         __syncthreads();
-        for (int idx = tid; idx < n * n; idx += kEThreads) {
-            const int i = idx % n, jx = idx / n;
-            S.Z[i * kLZ + jx] = fma(-0.5, P[i * kLZ + jx], S.Z[i * kLZ + jx]);
+        for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
+            const int i = idx & 63, jx = idx >> 6;
+            if (i < n && jx < n) S.Z[i * kLZ + jx] = fma(-0.5, P[i * kLZ + jx], S.Z[i * kLZ + jx]);
         }
         __syncthreads();
     }
     __syncthreads();
 
+    phase(4);
     // ---- 6. residual R = C Z − Z Λ (unscaled λ), Frobenius norm
     {
         const int g = lane >> 2, t = lane & 3;
@@ -410,11 +474,11 @@ __global__ void __launch_bounds__(kEThreads, 1)
             const int i = r0 + g, j0 = c0 + 2 * t;
             if (i < n) {
                 if (j0 < n) {
-                    const double r = fma(-S.lam[j0] / sc, S.Z[i * kLZ + j0], c_0);
+                    const double r = fma(-S.lam[j0] * isc, S.Z[i * kLZ + j0], c_0);
                     r2 = fma(r, r, r2);
                 }
                 if (j0 + 1 < n) {
-                    const double r = fma(-S.lam[j0 + 1] / sc, S.Z[i * kLZ + j0 + 1], c_1);
+                    const double r = fma(-S.lam[j0 + 1] * isc, S.Z[i * kLZ + j0 + 1], c_1);
                     r2 = fma(r, r, r2);
                 }
             }
@@ -433,11 +497,12 @@ __global__ void __launch_bounds__(kEThreads, 1)
         if (S.flag) atomicOr(flag_out, 1);
     }
     // ---- output, descending
-    for (int idx = tid; idx < n * n; idx += kEThreads) {
-        const int i = idx % n, r = idx / n;
-        V_out[i + static_cast<int64_t>(r) * n] = S.Z[i * kLZ + (n - 1 - r)];
+    for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
+        const int i = idx & 63, r = idx >> 6;
+        if (i < n && r < n) V_out[i + static_cast<int64_t>(r) * n] = S.Z[i * kLZ + (n - 1 - r)];
     }
-    if (tid < n) lambda_out[tid] = S.lam[n - 1 - tid] / sc;
+    if (tid < n) lambda_out[tid] = S.lam[n - 1 - tid] * isc;
+    phase(5);
 }
 
 }  // namespace
@@ -454,7 +519,8 @@ bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double*
                     CallScratch& sc) {
     if (n < 1 || n > kEN) return false;
     set_max_smem(trd_eig_kernel, static_cast<int>(sizeof(TrdSmem)));
-    trd_eig_kernel<<<1, kEThreads, sizeof(TrdSmem), sc.stream()>>>(C, ldc, n, lambda, V, flag, resid);
+    trd_eig_kernel<<<1, kEThreads, sizeof(TrdSmem), sc.stream()>>>(C, ldc, n, lambda, V, flag, resid,
+                                                                   eig_probe_buffer());
     TS_LAUNCH_CHECK();
     sc.launches += 1;
     return true;

@@ -1,8 +1,12 @@
 """A/B of the stage-G eigensolvers on the GPU: Jacobi (ts_sym_eig) vs the
 tridiagonalisation solver (ts_sym_eig_tri → eig_trd.cu): time, eigenvalue error
 vs the oracle, orthogonality, residual, rejection flag."""
+import ctypes as C
 import json
+import os
 import sys
+
+os.environ.setdefault("TS_EIG_PROFILE", "1")
 
 import numpy as np
 
@@ -35,6 +39,9 @@ for name, c in cases:
                 rej = False
             else:
                 vals, vecs, rej, ms = eng.sym_eig_tri(c)
+                prof = (C.c_longlong * 17)()
+                T.lib().ts_debug_eig_profile(prof)
+                row["trd_phase_cycles"] = list(prof)[10:16]
             ts.append(ms)
         row[solver] = {"ms": float(np.median(ts)), "rejected": bool(rej),
                        "eig_err_rel": float(np.max(np.abs(vals - ov)) / ov[0]),
