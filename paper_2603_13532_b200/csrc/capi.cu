@@ -920,37 +920,46 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     // the Householder Q with R_ii ≥ 0 of the reference.  Modes whose Y is too
     // ill-conditioned (failed pivot, or second Gram far from I) or too short take
     // the Householder TSQR.
+    // ---- Stages D + E.  Û_n = thin Q of Y_n (R_ii ≥ 0).  Fast path CholeskyQR2:
+    // Gram, small Cholesky + inverse, Q₁ = Y R₁⁻¹, Gram, Cholesky + inverse, so
+    // R = R₂R₁ has a positive diagonal and Û = Y R⁻¹ is the Householder Q with
+    // R_ii ≥ 0 of the reference.  Û is never formed for such modes ("R form"):
+    // stage E computes Pt_n = Y_nᵀF_n and P_n = R_n⁻ᵀPt_n (R_n⁻¹ = R₁⁻¹R₂⁻¹),
+    // stage H Ũ_n = Y_n (R_n⁻¹P_k).  Because stage E's big GEMM needs only Y,
+    // a speculative call whose modes all take CholeskyQR2 runs the R chain on
+    // the side stream concurrently with it ("overlap"); the kernels and their
+    // inputs are the same either way, so overlapped and synchronous results are
+    // bitwise equal.  Modes whose Y is too ill-conditioned (failed pivot, second
+    // Gram far from I) or too short take the Householder TSQR, which forms Û.
     double* Uh[TS_MAX_ORDER] = {};
     double* P[TS_MAX_ORDER];
-    // Overlapped form (speculative calls whose modes all take CholeskyQR2):
-    // Û_n = Y_n R_n⁻¹ is never formed.  Stage E runs as Pt_n = Y_nᵀF_n on the
-    // main stream while the side stream computes R_n⁻¹ = R₁⁻¹R₂⁻¹ (Gram,
-    // Cholesky-inverse, Q₁ = Y R₁⁻¹, Gram, Cholesky-inverse, product); then
-    // P_n = R_n⁻ᵀ Pt_n and, at stage H, Ũ_n = Y_n (R_n⁻¹ P_k).  Same
-    // arithmetic as Û = Y R⁻¹ up to rounding order; the speculation check of the
-    // Cholesky pivots / second Gram is unchanged (a rejection redoes the call on
-    // the synchronous path below).
+    double* Rinv[TS_MAX_ORDER] = {};
+    std::vector<int> rform(static_cast<size_t>(d), 0);
     bool overlap = spec && !lazy && !ctx->debug && !norm_out;
     for (int n = 0; n < d && overlap; ++n) overlap = dims[n] >= 2 * yc[n];
-    double* Rinv[TS_MAX_ORDER] = {};
-    if (overlap) {
+    {
+        std::vector<int>& chol = rform;
         int* flags = sc.alloc_n<int>(static_cast<size_t>(d));
         TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<size_t>(d), st));
-        double* Pt[TS_MAX_ORDER];
+        bool any = false;
         for (int n = 0; n < d; ++n) {
+            chol[static_cast<size_t>(n)] = dims[n] >= 2 * yc[n];
+            if (!chol[static_cast<size_t>(n)]) continue;
+            any = true;
             Rinv[n] = sc.alloc_n<double>(static_cast<size_t>(yc[n] * yc[n]));
-            Pt[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
-            P[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
         }
-        dflags = flags;
-        mark(ctx, 5);
-        TS_CUDA_CHECK(cudaEventRecord(ctx->ev_fork, st));
-        TS_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-        {
-            CallScratch sd(ctx->side, hstage);
+        for (int n = 0; n < d; ++n) P[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
+        if (overlap) {
+            mark(ctx, 5);
+            TS_CUDA_CHECK(cudaEventRecord(ctx->ev_fork, st));
+            TS_CUDA_CHECK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        }
+        if (any) {
+            CallScratch sd(overlap ? ctx->side : st, hstage);
             std::vector<GemmProblem> g1, q1, g2, rr;
             double *G1[TS_MAX_ORDER], *G2[TS_MAX_ORDER], *Ri1[TS_MAX_ORDER], *Ri2[TS_MAX_ORDER], *Q1[TS_MAX_ORDER];
             for (int n = 0; n < d; ++n) {
+                if (!chol[static_cast<size_t>(n)]) continue;
                 const std::int64_t c = yc[n];
                 G1[n] = sd.alloc_n<double>(static_cast<size_t>(c * c));
                 G2[n] = sd.alloc_n<double>(static_cast<size_t>(c * c));
@@ -988,124 +997,8 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 r.ldc = c;
                 rr.push_back(r);
             }
-            std::vector<std::int64_t> cw;
-            for (int n = 0; n < d; ++n)
-                if (std::find(cw.begin(), cw.end(), yc[n]) == cw.end()) cw.push_back(yc[n]);
-            auto chol_batches = [&](bool second) {
-                for (std::int64_t c : cw) {
-                    ts::CholBatch cb{};
-                    int nb = 0;
-                    for (int n = 0; n < d; ++n) {
-                        if (yc[n] != c) continue;
-                        cb.G[nb] = second ? G2[n] : G1[n];
-                        cb.Rinv[nb] = second ? Ri2[n] : Ri1[n];
-                        cb.flag[nb] = flags + n;
-                        ++nb;
-                    }
-                    cb.ldg = cb.ldri = c;
-                    cb.n = static_cast<int>(c);
-                    cb.check_identity = second ? 1 : 0;
-                    ts::launch_chol_inv(cb, nb, sd);
-                }
-            };
-            ts::launch_grouped_gemm(Layout::TN, g1, sd, ctx->num_sms);
-            chol_batches(false);
-            ts::launch_grouped_gemm(Layout::NN, q1, sd, ctx->num_sms);
-            ts::launch_grouped_gemm(Layout::TN, g2, sd, ctx->num_sms);
-            chol_batches(true);
-            ts::launch_grouped_gemm(Layout::NN, rr, sd, ctx->num_sms);
-            sc.launches += sd.launches;
-        }  // side-stream scratch released on the side stream
-        TS_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));
-        ctx->last_qr_fallbacks = 0;
-        // ---- Stage E (main stream, concurrent with the above): Pt_n = Y_nᵀ F_n
-        {
-            std::vector<GemmProblem> ps;
-            for (int n = 0; n < d; ++n) {
-                GemmProblem p{};
-                p.A = Y + yoff[n];
-                p.lda = dims[n];
-                p.B = b->F[n];
-                p.ldb = dims[n];
-                p.C = Pt[n];
-                p.ldc = q[n];
-                p.M = static_cast<int>(q[n]);
-                p.N = static_cast<int>(b->R[n]);
-                p.K = static_cast<int>(dims[n]);
-                ps.push_back(p);
-            }
-            ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
-        }
-        TS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-        {  // P_n = R_n⁻ᵀ Pt_n
-            std::vector<GemmProblem> ps;
-            for (int n = 0; n < d; ++n) {
-                GemmProblem p{};
-                p.A = Rinv[n];
-                p.lda = q[n];
-                p.B = Pt[n];
-                p.ldb = q[n];
-                p.C = P[n];
-                p.ldc = q[n];
-                p.M = static_cast<int>(q[n]);
-                p.N = static_cast<int>(b->R[n]);
-                p.K = static_cast<int>(q[n]);
-                ps.push_back(p);
-            }
-            ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
-        }
-    } else {
-    {
-        std::vector<int> chol(static_cast<size_t>(d), 0);
-        std::vector<GemmProblem> g1, q1, g2, q2;
-        int* flags = sc.alloc_n<int>(static_cast<size_t>(d));
-        TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<size_t>(d), st));
-        double *G1[TS_MAX_ORDER], *G2[TS_MAX_ORDER], *Ri1[TS_MAX_ORDER], *Ri2[TS_MAX_ORDER], *Q1[TS_MAX_ORDER];
-        bool any = false;
-        for (int n = 0; n < d; ++n) {
-            const std::int64_t c = yc[n];
-            Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
-            chol[static_cast<size_t>(n)] = dims[n] >= 2 * c;
-            if (!chol[static_cast<size_t>(n)]) continue;
-            any = true;
-            G1[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
-            G2[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
-            Ri1[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
-            Ri2[n] = sc.alloc_n<double>(static_cast<size_t>(c * c));
-            Q1[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * c));
-            GemmProblem p{};
-            p.M = p.N = static_cast<int>(c);
-            p.K = static_cast<int>(dims[n]);
-            p.A = Y + yoff[n];
-            p.lda = dims[n];
-            p.B = Y + yoff[n];
-            p.ldb = dims[n];
-            p.C = G1[n];
-            p.ldc = c;
-            g1.push_back(p);
-            p.A = Q1[n];
-            p.B = Q1[n];
-            p.C = G2[n];
-            g2.push_back(p);
-            GemmProblem m{};
-            m.M = static_cast<int>(dims[n]);
-            m.N = static_cast<int>(c);
-            m.K = static_cast<int>(c);
-            m.A = Y + yoff[n];
-            m.lda = dims[n];
-            m.B = Ri1[n];
-            m.ldb = c;
-            m.C = Q1[n];
-            m.ldc = dims[n];
-            q1.push_back(m);
-            m.A = Q1[n];
-            m.B = Ri2[n];
-            m.C = Uh[n];
-            q2.push_back(m);
-        }
-        if (any) {
-            // One Cholesky batch per distinct sketch width (all modes share it
-            // for the KRP sketch).
+            // One Cholesky batch per distinct sketch width (all modes share it for
+            // the KRP sketch).
             std::vector<std::int64_t> cw;
             for (int n = 0; n < d; ++n)
                 if (chol[static_cast<size_t>(n)] && std::find(cw.begin(), cw.end(), yc[n]) == cw.end()) cw.push_back(yc[n]);
@@ -1123,15 +1016,33 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                     cb.ldg = cb.ldri = c;
                     cb.n = static_cast<int>(c);
                     cb.check_identity = second ? 1 : 0;
-                    ts::launch_chol_inv(cb, nb, sc);
+                    ts::launch_chol_inv(cb, nb, sd);
                 }
             };
-            ts::launch_grouped_gemm(Layout::TN, g1, sc, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::TN, g1, sd, ctx->num_sms);
             chol_batches(false);
-            ts::launch_grouped_gemm(Layout::NN, q1, sc, ctx->num_sms);
-            ts::launch_grouped_gemm(Layout::TN, g2, sc, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::NN, q1, sd, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::TN, g2, sd, ctx->num_sms);
             chol_batches(true);
-            ts::launch_grouped_gemm(Layout::NN, q2, sc, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::NN, rr, sd, ctx->num_sms);
+            for (std::int64_t c : cw) {  // κ(Y) small enough for the R form?
+                ts::CholBatch cb{};
+                int nb = 0;
+                for (int n = 0; n < d; ++n) {
+                    if (!chol[static_cast<size_t>(n)] || yc[n] != c) continue;
+                    cb.G[nb] = G1[n];
+                    cb.Rinv[nb] = Rinv[n];
+                    cb.flag[nb] = flags + n;
+                    ++nb;
+                }
+                cb.ldg = cb.ldri = c;
+                cb.n = static_cast<int>(c);
+                ts::launch_rform_check(cb, nb, sd);
+            }
+            sc.launches += sd.launches;
+        }  // a side-stream scratch is released on the side stream
+        if (overlap) TS_CUDA_CHECK(cudaEventRecord(ctx->ev_join, ctx->side));
+        if (any) {
             if (spec) {
                 dflags = flags;
             } else {
@@ -1147,32 +1058,67 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         std::vector<ts::TsqrPlan*> pp;
         for (int n = 0; n < d; ++n) {
             if (chol[static_cast<size_t>(n)]) continue;
+            Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
             plans[static_cast<size_t>(n)] = ts::plan_tsqr(Y + yoff[n], dims[n], dims[n], yc[n], Uh[n], dims[n], sc);
             pp.push_back(&plans[static_cast<size_t>(n)]);
         }
         if (!pp.empty()) ts::run_tsqr(pp, sc, true);
         ctx->last_qr_fallbacks = static_cast<int>(pp.size());
     }
-    mark(ctx, 5);
-    // ---- Stage E: P_n = Û_nᵀ F_n (q_n × R_n)
+    if (!overlap) mark(ctx, 5);
+    // ---- Stage E: P_n = Û_nᵀ F_n (q_n × R_n); R-form modes: Pt_n = Y_nᵀF_n, P_n = R_n⁻ᵀPt_n
     {
-        std::vector<GemmProblem> ps;
+        double* Pt[TS_MAX_ORDER] = {};
+        std::vector<GemmProblem> ps, pr;
         for (int n = 0; n < d; ++n) {
-            P[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
+            const bool rf = rform[static_cast<size_t>(n)] != 0;
+            if (rf) Pt[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
             GemmProblem p{};
-            p.A = Uh[n];
+            p.A = rf ? Y + yoff[n] : Uh[n];
             p.lda = dims[n];
             p.B = b->F[n];
             p.ldb = dims[n];
-            p.C = P[n];
+            p.C = rf ? Pt[n] : P[n];
             p.ldc = q[n];
             p.M = static_cast<int>(q[n]);
             p.N = static_cast<int>(b->R[n]);
             p.K = static_cast<int>(dims[n]);
             ps.push_back(p);
+            if (rf) {
+                GemmProblem r{};
+                r.A = Rinv[n];
+                r.lda = q[n];
+                r.B = Pt[n];
+                r.ldb = q[n];
+                r.C = P[n];
+                r.ldc = q[n];
+                r.M = static_cast<int>(q[n]);
+                r.N = static_cast<int>(b->R[n]);
+                r.K = static_cast<int>(q[n]);
+                pr.push_back(r);
+            }
         }
         ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        if (overlap) TS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+        if (!pr.empty()) ts::launch_grouped_gemm(Layout::TN, pr, sc, ctx->num_sms);
     }
+    if (ctx->debug) {  // Û of the R-form modes, for the intermediates only
+        std::vector<GemmProblem> ps;
+        for (int n = 0; n < d; ++n) {
+            if (!rform[static_cast<size_t>(n)]) continue;
+            Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+            GemmProblem p{};
+            p.A = Y + yoff[n];
+            p.lda = dims[n];
+            p.B = Rinv[n];
+            p.ldb = q[n];
+            p.C = Uh[n];
+            p.ldc = dims[n];
+            p.M = static_cast<int>(dims[n]);
+            p.N = p.K = static_cast<int>(q[n]);
+            ps.push_back(p);
+        }
+        if (!ps.empty()) ts::launch_grouped_gemm(Layout::NN, ps, sc, ctx->num_sms);
     }
     mark(ctx, 6);
     std::int64_t hsize = 0;
@@ -1405,9 +1351,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     // ---- Stage H: Ũ_n = Û_n · P_n (n × rank_n); the core is g.
     {
         double* Tk[TS_MAX_ORDER] = {};
-        if (overlap) {  // Ũ_n = Y_n (R_n⁻¹ P_k): first T_n = R_n⁻¹ P_k (q_n × rank_n)
+        {  // R-form modes: Ũ_n = Y_n (R_n⁻¹ P_k), first T_n = R_n⁻¹ P_k (q_n × rank_n)
             std::vector<GemmProblem> ts_;
             for (int n = 0; n < d; ++n) {
+                if (!rform[static_cast<size_t>(n)]) continue;
                 Tk[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * rank[n]));
                 GemmProblem p{};
                 p.A = Rinv[n];
@@ -1421,7 +1368,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 p.K = static_cast<int>(q[n]);
                 ts_.push_back(p);
             }
-            ts::launch_grouped_gemm(Layout::NN, ts_, sc, ctx->num_sms);
+            if (!ts_.empty()) ts::launch_grouped_gemm(Layout::NN, ts_, sc, ctx->num_sms);
         }
         std::vector<GemmProblem> ps;
         for (int n = 0; n < d; ++n) {
@@ -1434,9 +1381,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 TS_CUDA_CHECK(cudaMallocAsync(&res->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rank[n]), st));
             }
             GemmProblem p{};
-            p.A = overlap ? Y + yoff[n] : Uh[n];
+            p.A = rform[static_cast<size_t>(n)] ? Y + yoff[n] : Uh[n];
             p.lda = dims[n];
-            p.B = overlap ? Tk[n] : Pk[n];
+            p.B = rform[static_cast<size_t>(n)] ? Tk[n] : Pk[n];
             p.ldb = q[n];
             p.C = res->factors[n];
             p.ldc = dims[n];

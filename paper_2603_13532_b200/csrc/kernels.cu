@@ -1145,6 +1145,31 @@ void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int o
     sc.launches += 1;
 }
 
+// R-form condition check (capi.cu stages D/E): κ_F(R)² = trace(YᵀY)·‖R⁻¹‖_F² ≥
+// κ₂(Y)²; the R form P = R⁻ᵀ(YᵀF) loses a factor κ(Y) of accuracy, so modes
+// with κ_F > 1e4 (error > ~1e-12) get *flag |= 4 (→ Householder TSQR).
+__global__ void rform_check_kernel(CholBatch cb) {
+    __shared__ double part[32];
+    const int b = blockIdx.x, n = cb.n;
+    double tr = 0.0, fr = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tr += cb.G[b][i + static_cast<int64_t>(i) * cb.ldg];
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const double v = cb.Rinv[b][e % n + static_cast<int64_t>(e / n) * cb.ldri];
+        fr = fma(v, v, fr);
+    }
+    tr = block_sum(tr, part);
+    __syncthreads();
+    fr = block_sum(fr, part);
+    if (threadIdx.x == 0 && !(tr * fr <= 1e8)) atomicOr(cb.flag[b], 4);
+}
+
+void launch_rform_check(const CholBatch& cb, int count, CallScratch& sc) {
+    if (count <= 0) return;
+    rform_check_kernel<<<count, 256, 0, sc.stream()>>>(cb);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc) {
     if (count <= 0) return;
     if (cb.n > 96) throw std::invalid_argument("chol_inv: n > 96");

@@ -119,6 +119,9 @@ struct CholBatch {
     int check_identity;
 };
 void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc);
+// R-form accuracy check: G = YᵀY, Rinv = R⁻¹; *flag[b] |= 4 when
+// trace(G)·‖R⁻¹‖_F² > 1e8 (κ_F(Y) > 1e4).
+void launch_rform_check(const CholBatch& cb, int count, CallScratch& sc);
 // Device check of the ε = 0 Gram fast path (twin of capi.cu gram_rank): *flag |= 1 on rejection.
 void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc);
 // Device check of the ε > 0 Gram fast path with a known output rank `expect`
