@@ -164,6 +164,19 @@ int ts_tucker_inner(ts_ctx* ctx, const ts_batch* x, const double* wx, const ts_b
 int ts_rel_error_to_sum(ts_ctx* ctx, const ts_result* r, const ts_batch* batch, const double* weights, double* out);
 /* Kron widths for per-mode targets (host arithmetic, bit-identical rule). */
 int ts_kron_sketch_dims(int64_t order, const int64_t* targets, const int64_t* dims, int64_t* out_widths);
+/* Segmented independent sums (one round_sum per NDG
+ * node with a shared plan, reference src/ndg.cpp:401-462; the GMRES sums of
+ * src/cookie.cpp:389-421): ONE batch holds the summands of `nsums` sums, sum s
+ * owning summands [segments[s], segments[s+1]) (segments[0] = 0,
+ * segments[nsums] = count, every segment nonempty); weights are per summand;
+ * all sums share `widths` (the plan) and `max_rank`; sum s uses the seed
+ * {seeds[s], streams[s]}.  out[s] = exactly ts_krp_sum of that segment.  Every
+ * stage runs as one launch over all sums (grouped GEMMs over (sum, mode),
+ * stage-B / F1 kernels over all atoms, one Cholesky / eigensolver CTA per
+ * (sum, mode)), so many small sums cost about what one does. */
+int ts_krp_sum_segmented(ts_ctx* ctx, const ts_batch* batch, int64_t nsums, const int64_t* segments,
+                         const double* weights, const int64_t* widths, const uint64_t* seeds, const uint64_t* streams,
+                         double eps, const int64_t* max_rank, ts_result** out);
 /* Independent sums in one call (SURVEY.md §8(f) row 2 — one round_sum per NDG
  * node, many GMRES steps): sum i = krp_sum of batches[i] with weights[i] and the
  * Ω stream (seeds[i], streams[i]); widths / eps / max_rank are shared.  Sums run

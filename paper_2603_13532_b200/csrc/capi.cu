@@ -234,6 +234,10 @@ struct ts_batch {
     std::vector<ts::Atom> atoms;
     ts::Atom* d_atoms = nullptr;
     std::vector<double> core_norm;  // per summand ‖core‖_F (plan energies)
+    // First stacked column of summand i in mode j at scol[i*order + j]
+    // (i = 0..count; row `count` holds R_j): the column segments of
+    // ts_krp_sum_segmented.
+    std::vector<std::int64_t> scol;
     int max_shape = 0;
     std::int64_t bytes = 0;
     std::uint64_t id = 0;  // unique per upload (graph-cache key; never reused)
@@ -529,8 +533,8 @@ void kron_stage_b(const ts_batch* b, double* const* Z, const std::int64_t* ow, d
 // for given projections P_n (q_n × R_n, ld q_n).  Order 3 fuses the chain per
 // core slice (ttm3.cu); other orders run a per-atom grouped GEMM chain.  The sum
 // over atoms is the K dimension of the final GEMM (deterministic split-K).
-double* project_core(ts_ctx* ctx, const ts_batch* b, double* const* P, const std::int64_t* q, const double* d_w,
-                     const double* weights, CallScratch& sc, std::int64_t* hsize) {
+double* project_core_f1(ts_ctx* ctx, const ts_batch* b, double* const* P, const std::int64_t* q, const double* d_w,
+                        const double* weights, CallScratch& sc) {
     const int d = b->order;
     // ---- Stage F1: per-atom multi-TTM over modes 0..d-2 into T_stack (Q' × R_{d-1})
     std::int64_t Qp = 1;
@@ -616,6 +620,15 @@ double* project_core(ts_ctx* ctx, const ts_batch* b, double* const* P, const std
             std::swap(cur, nxt);
         }
     }
+    return Tstack;
+}
+
+double* project_core(ts_ctx* ctx, const ts_batch* b, double* const* P, const std::int64_t* q, const double* d_w,
+                     const double* weights, CallScratch& sc, std::int64_t* hsize) {
+    const int d = b->order;
+    std::int64_t Qp = 1;
+    for (int j = 0; j < d - 1; ++j) Qp *= q[j];
+    double* Tstack = project_core_f1(ctx, b, P, q, d_w, weights, sc);
     mark(ctx, 7);
     // ---- Stage F2: h (Q' × q_{d-1}) = T_stack · P_{d-1}ᵀ
     *hsize = Qp * q[d - 1];
@@ -1453,6 +1466,536 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     return res.release();
 }
 
+// Segmented KRP sums (one round_sum per NDG node with a
+// shared plan, src/ndg.cpp:401-462; many GMRES sums, src/cookie.cpp:389-421).
+// S independent krp_sum calls whose summands are the consecutive segments
+// [seg[s], seg[s+1]) of ONE uploaded batch share the plan widths; every stage
+// runs as one launch over all sums — grouped DMMA GEMMs over the (sum, mode)
+// problems, the stage-B and stage-F1 kernels over all atoms, one Cholesky CTA
+// and one eigensolver CTA per (sum, mode) — so S small sums cost about what one
+// does instead of S times its latency.  Sum s computes exactly what
+// ts_krp_sum(batch of its summands, its weights, widths, seeds[s], …) computes
+// (same kernels per problem, so the same numbers up to the split-K choices of
+// the grouped launches).
+std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int64_t S, const std::int64_t* seg,
+                                       const double* weights, const std::int64_t* widths, const std::uint64_t* seeds,
+                                       const std::uint64_t* streams, double eps, const std::int64_t* max_rank,
+                                       bool allow_spec) {
+    if (b == nullptr || b->count < 1 || S < 1 || seg == nullptr || weights == nullptr || seeds == nullptr ||
+        streams == nullptr)
+        invalid("sum request needs matching, nonempty summands and weights");
+    if (b->ctx->device != ctx->device) invalid("batch was uploaded to another device than this context's");
+    if (seg[0] != 0 || seg[S] != b->count) invalid("segments must partition the batch's summands");
+    for (std::int64_t s = 0; s < S; ++s)
+        if (seg[s + 1] <= seg[s]) invalid("sum request needs matching, nonempty summands and weights");
+    if (!(eps >= 0.0)) invalid("tolerance must be nonnegative");
+    const int d = b->order;
+    if (d < 2) invalid("sketched summation needs order >= 2");
+    if (widths == nullptr) invalid("plan order does not match summand order");
+    for (int n = 0; n < d; ++n)
+        if (widths[n] < 1) invalid("plan sketch widths must be positive");
+    if (sharded(ctx)) throw ts::Error(TS_UNSUPPORTED, "segmented sums do not shard: use a context without NCCL");
+    if (b->scol.empty()) throw ts::Error(TS_UNSUPPORTED, "segmented sums need a batch from ts_batch_upload*");
+    for (std::int64_t i = 0; i < b->count; ++i)
+        if (!std::isfinite(weights[i])) invalid("weights must be finite");
+    const std::int64_t sw = *std::max_element(widths, widths + d);
+    if (sw > ts::max_tsqr_cols())
+        throw ts::Error(TS_UNSUPPORTED, "sketch width " + std::to_string(sw) + " exceeds the supported maximum of " +
+                                            std::to_string(ts::max_tsqr_cols()));
+    TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+    ctx->stage.reset();
+    cudaStream_t st = ctx->stream;
+    CallScratch sc(st, ctx->stage);
+    const std::int64_t* dims = b->dims;
+    auto col = [&](std::int64_t s, int n) { return b->scol[static_cast<size_t>(seg[s] * d + n)]; };
+    auto rsn = [&](std::int64_t s, int n) { return col(s + 1, n) - col(s, n); };
+    const size_t SD = static_cast<size_t>(S) * static_cast<size_t>(d);
+    auto sn = [&](std::int64_t s, int n) { return static_cast<size_t>(s) * static_cast<size_t>(d) + static_cast<size_t>(n); };
+    std::int64_t q[TS_MAX_ORDER], ow[TS_MAX_ORDER], ooff[TS_MAX_ORDER], yoff[TS_MAX_ORDER];
+    std::int64_t ysum = 0, oacc = 0;
+    for (int n = 0; n < d; ++n) {
+        ow[n] = sw;
+        q[n] = std::min(dims[n], sw);
+        ooff[n] = oacc;
+        oacc += dims[n] * sw;
+        yoff[n] = ysum;
+        ysum += dims[n] * sw;
+    }
+    std::vector<double*> om(static_cast<size_t>(S));
+    for (std::int64_t s = 0; s < S; ++s) om[static_cast<size_t>(s)] = omega_get(ctx, d, dims, ow, seeds[s], streams[s]);
+    auto* d_w = static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
+
+    // ---- A: Z_n[:, cols_s] = Ω_{s,n}ᵀ F_n[:, cols_s]
+    double* Z[TS_MAX_ORDER];
+    {
+        std::vector<GemmProblem> ps;
+        for (int n = 0; n < d; ++n) Z[n] = sc.alloc_n<double>(static_cast<size_t>(sw * b->R[n]));
+        for (std::int64_t s = 0; s < S; ++s)
+            for (int n = 0; n < d; ++n) {
+                GemmProblem p{};
+                p.A = om[static_cast<size_t>(s)] + ooff[n];
+                p.lda = dims[n];
+                p.B = b->F[n] + col(s, n) * dims[n];
+                p.ldb = dims[n];
+                p.C = Z[n] + col(s, n) * sw;
+                p.ldc = sw;
+                p.M = static_cast<int>(sw);
+                p.N = static_cast<int>(rsn(s, n));
+                p.K = static_cast<int>(dims[n]);
+                ps.push_back(p);
+            }
+        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+    }
+    // ---- B: one launch over all atoms (each atom reads its own sum's Z columns)
+    double* W[TS_MAX_ORDER];
+    {
+        ts::KrpArgs ka{};
+        for (int n = 0; n < d; ++n) {
+            W[n] = sc.alloc_n<double>(static_cast<size_t>(b->R[n] * sw));
+            ka.Z[n] = Z[n];
+            ka.W[n] = W[n];
+            ka.R[n] = b->R[n];
+        }
+        ka.order = d;
+        ka.s = static_cast<int>(sw);
+        ka.natoms = static_cast<int>(b->atoms.size());
+        ka.atoms = b->d_atoms;
+        ka.cores = b->cores;
+        ka.weights = d_w;
+        ts::launch_krp_contract(ka, b->max_shape, sc);
+    }
+    // ---- C: Y_{s,n} = F_n[:, cols_s] · W_n[cols_s, :]
+    double* Y = sc.alloc_n<double>(static_cast<size_t>(S * ysum));
+    auto ypos = [&](std::int64_t s, int n) { return Y + s * ysum + yoff[n]; };
+    {
+        std::vector<GemmProblem> ps;
+        for (std::int64_t s = 0; s < S; ++s)
+            for (int n = 0; n < d; ++n) {
+                GemmProblem p{};
+                p.A = b->F[n] + col(s, n) * dims[n];
+                p.lda = dims[n];
+                p.B = W[n] + col(s, n) * sw;
+                p.ldb = sw;
+                p.C = ypos(s, n);
+                p.ldc = dims[n];
+                p.M = static_cast<int>(dims[n]);
+                p.N = static_cast<int>(sw);
+                p.K = static_cast<int>(rsn(s, n));
+                ps.push_back(p);
+            }
+        ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+    }
+    const bool spec = allow_spec && ctx->spec_ok;
+    int* dflags = nullptr;
+    int* gflags = nullptr;
+    // ---- D: CholeskyQR2 R form per (sum, mode) where dims ≥ 2s, Householder TSQR otherwise / on rejection
+    std::vector<int> rform(SD, 0);
+    std::vector<double*> Rinv(SD, nullptr), Uh(SD, nullptr);
+    {
+        int* flags = sc.alloc_n<int>(SD);
+        TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * SD, st));
+        std::vector<GemmProblem> g1, q1, g2, rr;
+        std::vector<const double*> hG1, hG2;
+        std::vector<double*> hR1, hR2, hRi;
+        std::vector<int*> hF;
+        for (std::int64_t s = 0; s < S; ++s)
+            for (int n = 0; n < d; ++n) {
+                if (dims[n] < 2 * sw) continue;
+                const size_t i = sn(s, n);
+                rform[i] = 1;
+                const std::int64_t c = sw;
+                double* G1 = sc.alloc_n<double>(static_cast<size_t>(c * c));
+                double* G2 = sc.alloc_n<double>(static_cast<size_t>(c * c));
+                double* Ri1 = sc.alloc_n<double>(static_cast<size_t>(c * c));
+                double* Ri2 = sc.alloc_n<double>(static_cast<size_t>(c * c));
+                double* Q1 = sc.alloc_n<double>(static_cast<size_t>(dims[n] * c));
+                Rinv[i] = sc.alloc_n<double>(static_cast<size_t>(c * c));
+                GemmProblem p{};
+                p.M = p.N = static_cast<int>(c);
+                p.K = static_cast<int>(dims[n]);
+                p.A = p.B = ypos(s, n);
+                p.lda = p.ldb = dims[n];
+                p.C = G1;
+                p.ldc = c;
+                g1.push_back(p);
+                p.A = p.B = Q1;
+                p.C = G2;
+                g2.push_back(p);
+                GemmProblem m{};
+                m.M = static_cast<int>(dims[n]);
+                m.N = m.K = static_cast<int>(c);
+                m.A = ypos(s, n);
+                m.lda = dims[n];
+                m.B = Ri1;
+                m.ldb = c;
+                m.C = Q1;
+                m.ldc = dims[n];
+                q1.push_back(m);
+                GemmProblem r{};
+                r.M = r.N = r.K = static_cast<int>(c);
+                r.A = Ri1;
+                r.lda = c;
+                r.B = Ri2;
+                r.ldb = c;
+                r.C = Rinv[i];
+                r.ldc = c;
+                rr.push_back(r);
+                hG1.push_back(G1);
+                hG2.push_back(G2);
+                hR1.push_back(Ri1);
+                hR2.push_back(Ri2);
+                hRi.push_back(Rinv[i]);
+                hF.push_back(flags + i);
+            }
+        const int nb = static_cast<int>(hG1.size());
+        if (nb > 0) {
+            auto up = [&](const void* src, size_t bytes) { return sc.upload(src, bytes); };
+            ts::CholBatch c1{}, c2{}, cr{};
+            c1.Gd = static_cast<const double* const*>(up(hG1.data(), sizeof(double*) * hG1.size()));
+            c1.Rd = static_cast<double* const*>(up(hR1.data(), sizeof(double*) * hR1.size()));
+            c1.Fd = static_cast<int* const*>(up(hF.data(), sizeof(int*) * hF.size()));
+            c2 = c1;
+            c2.Gd = static_cast<const double* const*>(up(hG2.data(), sizeof(double*) * hG2.size()));
+            c2.Rd = static_cast<double* const*>(up(hR2.data(), sizeof(double*) * hR2.size()));
+            cr = c1;
+            cr.Rd = static_cast<double* const*>(up(hRi.data(), sizeof(double*) * hRi.size()));
+            for (ts::CholBatch* cb : {&c1, &c2, &cr}) {
+                cb->ldg = cb->ldri = sw;
+                cb->n = static_cast<int>(sw);
+            }
+            c2.check_identity = 1;
+            ts::launch_grouped_gemm(Layout::TN, g1, sc, ctx->num_sms);
+            ts::launch_chol_inv(c1, nb, sc);
+            ts::launch_grouped_gemm(Layout::NN, q1, sc, ctx->num_sms);
+            ts::launch_grouped_gemm(Layout::TN, g2, sc, ctx->num_sms);
+            ts::launch_chol_inv(c2, nb, sc);
+            ts::launch_grouped_gemm(Layout::NN, rr, sc, ctx->num_sms);
+            ts::launch_rform_check(cr, nb, sc);
+            if (spec) {
+                dflags = flags;
+            } else {
+                std::vector<int> hf(SD, 0);
+                TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), flags, sizeof(int) * SD, cudaMemcpyDeviceToHost, st));
+                TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                for (size_t i = 0; i < SD; ++i)
+                    if (hf[i] != 0) rform[i] = 0;
+            }
+        }
+        std::vector<ts::TsqrPlan> plans(SD);
+        std::vector<ts::TsqrPlan*> pp;
+        for (std::int64_t s = 0; s < S; ++s)
+            for (int n = 0; n < d; ++n) {
+                const size_t i = sn(s, n);
+                if (rform[i]) continue;
+                Uh[i] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+                plans[i] = ts::plan_tsqr(ypos(s, n), dims[n], dims[n], sw, Uh[i], dims[n], sc);
+                pp.push_back(&plans[i]);
+            }
+        if (!pp.empty()) ts::run_tsqr(pp, sc, true);
+        ctx->last_qr_fallbacks = static_cast<int>(pp.size());
+    }
+    // ---- E: P_n[:, cols_s] = Û_{s,n}ᵀ F_n[:, cols_s]  (R form: R⁻ᵀ (Y_{s,n}ᵀ F_n[:, cols_s]))
+    double* P[TS_MAX_ORDER];
+    {
+        for (int n = 0; n < d; ++n) P[n] = sc.alloc_n<double>(static_cast<size_t>(q[n] * b->R[n]));
+        std::vector<GemmProblem> ps, pr;
+        for (std::int64_t s = 0; s < S; ++s)
+            for (int n = 0; n < d; ++n) {
+                const size_t i = sn(s, n);
+                const bool rf = rform[i] != 0;
+                double* Pt = rf ? sc.alloc_n<double>(static_cast<size_t>(q[n] * rsn(s, n))) : nullptr;
+                GemmProblem p{};
+                p.A = rf ? ypos(s, n) : Uh[i];
+                p.lda = dims[n];
+                p.B = b->F[n] + col(s, n) * dims[n];
+                p.ldb = dims[n];
+                p.C = rf ? Pt : P[n] + col(s, n) * q[n];
+                p.ldc = q[n];
+                p.M = static_cast<int>(q[n]);
+                p.N = static_cast<int>(rsn(s, n));
+                p.K = static_cast<int>(dims[n]);
+                ps.push_back(p);
+                if (rf) {
+                    GemmProblem r{};
+                    r.A = Rinv[i];
+                    r.lda = q[n];
+                    r.B = Pt;
+                    r.ldb = q[n];
+                    r.C = P[n] + col(s, n) * q[n];
+                    r.ldc = q[n];
+                    r.M = static_cast<int>(q[n]);
+                    r.N = static_cast<int>(rsn(s, n));
+                    r.K = static_cast<int>(q[n]);
+                    pr.push_back(r);
+                }
+            }
+        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        if (!pr.empty()) ts::launch_grouped_gemm(Layout::TN, pr, sc, ctx->num_sms);
+    }
+    // ---- F: T_stack over all atoms, then h_s = T_stack[:, cols_s] · P_{d-1}[:, cols_s]ᵀ
+    std::int64_t Qp = 1;
+    for (int j = 0; j < d - 1; ++j) Qp *= q[j];
+    const std::int64_t hsz = Qp * q[d - 1];
+    double* Tstack = project_core_f1(ctx, b, P, q, d_w, weights, sc);
+    double* H = sc.alloc_n<double>(static_cast<size_t>(S * hsz));
+    {
+        std::vector<GemmProblem> ps;
+        for (std::int64_t s = 0; s < S; ++s) {
+            GemmProblem p{};
+            p.A = Tstack + col(s, d - 1) * Qp;
+            p.lda = Qp;
+            p.B = P[d - 1] + col(s, d - 1) * q[d - 1];
+            p.ldb = q[d - 1];
+            p.C = H + s * hsz;
+            p.ldc = Qp;
+            p.M = static_cast<int>(Qp);
+            p.N = static_cast<int>(q[d - 1]);
+            p.K = static_cast<int>(rsn(s, d - 1));
+            ps.push_back(p);
+        }
+        ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+    }
+    // ---- G: ST-HOSVD of every h_s, one mode step at a time for all sums
+    std::vector<std::array<std::int64_t, TS_MAX_ORDER>> shp(static_cast<size_t>(S));
+    std::vector<std::array<std::int64_t, TS_MAX_ORDER>> rank(static_cast<size_t>(S));
+    std::vector<std::array<double*, TS_MAX_ORDER>> Pk(static_cast<size_t>(S));
+    std::vector<double*> g(static_cast<size_t>(S));
+    for (std::int64_t s = 0; s < S; ++s) {
+        for (int n = 0; n < d; ++n) shp[static_cast<size_t>(s)][static_cast<size_t>(n)] = q[n];
+        g[static_cast<size_t>(s)] = H + s * hsz;
+    }
+    const bool spec_g = spec && eps == 0.0;
+    if (spec_g) {
+        gflags = sc.alloc_n<int>(SD);
+        TS_CUDA_CHECK(cudaMemsetAsync(gflags, 0, sizeof(int) * SD, st));
+    }
+    std::vector<double> theta(static_cast<size_t>(S), 0.0);
+    if (eps != 0.0) {  // θ_s = ε²‖h_s‖²/d
+        double* d_ss = sc.alloc_n<double>(static_cast<size_t>(S));
+        for (std::int64_t s = 0; s < S; ++s) ts::launch_sumsq(H + s * hsz, hsz, d_ss + s, sc);
+        std::vector<double> hs(static_cast<size_t>(S));
+        TS_CUDA_CHECK(cudaMemcpyAsync(hs.data(), d_ss, sizeof(double) * static_cast<size_t>(S), cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (std::int64_t s = 0; s < S; ++s) theta[static_cast<size_t>(s)] = eps * eps * hs[static_cast<size_t>(s)] / static_cast<double>(d);
+    }
+    ctx->last_svd_fallbacks = 0;
+    ctx->last_eig_fallbacks = 0;
+    std::vector<int> mode_order(static_cast<size_t>(d));
+    std::iota(mode_order.begin(), mode_order.end(), 0);
+    std::stable_sort(mode_order.begin(), mode_order.end(), [&](int x, int y) { return q[x] < q[y]; });
+    for (int k : mode_order) {
+        const std::int64_t qk = q[k];  // mode k is untouched until its step: q_k for every sum
+        double* Call = sc.alloc_n<double>(static_cast<size_t>(S * qk * qk));
+        double* Lall = sc.alloc_n<double>(static_cast<size_t>(S * qk));
+        double* Vall = sc.alloc_n<double>(static_cast<size_t>(S * qk * qk));
+        std::vector<double*> X(static_cast<size_t>(S), nullptr);
+        std::vector<std::int64_t> rest(static_cast<size_t>(S), 1);
+        std::vector<GemmProblem> gnt, gtn;
+        for (std::int64_t s = 0; s < S; ++s) {
+            auto& cs = shp[static_cast<size_t>(s)];
+            for (int j = 0; j < d; ++j)
+                if (j != k) rest[static_cast<size_t>(s)] *= cs[static_cast<size_t>(j)];
+            Pk[static_cast<size_t>(s)][static_cast<size_t>(k)] = Vall + s * qk * qk;
+            GemmProblem p{};
+            p.M = p.N = static_cast<int>(qk);
+            p.K = static_cast<int>(rest[static_cast<size_t>(s)]);
+            p.C = Call + s * qk * qk;
+            p.ldc = qk;
+            if (k == 0) {
+                p.A = p.B = g[static_cast<size_t>(s)];
+                p.lda = p.ldb = qk;
+                gnt.push_back(p);
+            } else {
+                if (k != d - 1) {
+                    X[static_cast<size_t>(s)] = sc.alloc_n<double>(static_cast<size_t>(rest[static_cast<size_t>(s)] * qk));
+                    ts::launch_unfold_t(g[static_cast<size_t>(s)], d, cs.data(), k, X[static_cast<size_t>(s)], sc);
+                }
+                p.A = p.B = k == d - 1 ? g[static_cast<size_t>(s)] : X[static_cast<size_t>(s)];
+                p.lda = p.ldb = rest[static_cast<size_t>(s)];
+                gtn.push_back(p);
+            }
+        }
+        if (!gnt.empty()) ts::launch_grouped_gemm(Layout::NT, gnt, sc, ctx->num_sms);
+        if (!gtn.empty()) ts::launch_grouped_gemm(Layout::TN, gtn, sc, ctx->num_sms);
+        const std::int64_t capk = max_rank ? max_rank[k] : 0;
+        // speculative: the eigensolver's rejections and the Gram checks of this
+        // mode step land in gflags[k·S + s] directly
+        int* tflags = spec_g ? gflags + static_cast<size_t>(k) * static_cast<size_t>(S) : sc.alloc_n<int>(static_cast<size_t>(S));
+        if (!spec_g) TS_CUDA_CHECK(cudaMemsetAsync(tflags, 0, sizeof(int) * static_cast<size_t>(S), st));
+        double* res = sc.alloc_n<double>(static_cast<size_t>(S));
+        const bool trd = qk <= 64 && !ts::jacobi_eig_forced();
+        if (trd) {
+            ts::launch_sym_trd(Call, qk, static_cast<int>(qk), Lall, Vall, tflags, res, sc, static_cast<int>(S), qk * qk,
+                               qk, qk * qk);
+        } else {
+            for (std::int64_t s = 0; s < S; ++s)
+                ts::launch_sym_jacobi(Call + s * qk * qk, qk, static_cast<int>(qk), Lall + s * qk, Vall + s * qk * qk, sc);
+        }
+        std::vector<std::int64_t> rk(static_cast<size_t>(S), 0);
+        if (spec_g) {
+            for (std::int64_t s = 0; s < S; ++s) rk[static_cast<size_t>(s)] = (capk > 0 && capk < qk) ? capk : qk;
+            ts::launch_gram_check(Lall, static_cast<int>(qk), static_cast<int>(capk), trd ? res : nullptr, tflags, sc,
+                                  static_cast<int>(S), qk);
+        } else {
+            std::vector<double> lv(static_cast<size_t>(S * qk)), hres(static_cast<size_t>(S), -1.0);
+            std::vector<int> htf(static_cast<size_t>(S), 0);
+            TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), Lall, sizeof(double) * lv.size(), cudaMemcpyDeviceToHost, st));
+            TS_CUDA_CHECK(cudaMemcpyAsync(htf.data(), tflags, sizeof(int) * htf.size(), cudaMemcpyDeviceToHost, st));
+            if (trd) TS_CUDA_CHECK(cudaMemcpyAsync(hres.data(), res, sizeof(double) * hres.size(), cudaMemcpyDeviceToHost, st));
+            TS_CUDA_CHECK(cudaStreamSynchronize(st));
+            for (std::int64_t s = 0; s < S; ++s) {
+                const size_t si = static_cast<size_t>(s);
+                double* Cs = Call + s * qk * qk;
+                double* Ls = Lall + s * qk;
+                double* Vs = Vall + s * qk * qk;
+                std::vector<double> lam(lv.begin() + static_cast<std::ptrdiff_t>(s * qk),
+                                        lv.begin() + static_cast<std::ptrdiff_t>((s + 1) * qk));
+                double rres = trd ? hres[si] : -1.0;
+                if (trd && htf[si]) {  // the tridiagonalisation solver rejected its own result
+                    ts::launch_sym_jacobi(Cs, qk, static_cast<int>(qk), Ls, Vs, sc);
+                    TS_CUDA_CHECK(cudaMemcpyAsync(lam.data(), Ls, sizeof(double) * static_cast<size_t>(qk),
+                                                  cudaMemcpyDeviceToHost, st));
+                    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                    rres = -1.0;
+                    ++ctx->last_eig_fallbacks;
+                }
+                bool ok = false;
+                rk[si] = gram_rank(lam, eps, theta[si], capk, rres, &ok);
+                if (!ok) {  // accurate path: TSQR (R only) of h_(k)ᵀ + one-sided Jacobi SVD
+                    double* Xs = sc.alloc_n<double>(static_cast<size_t>(rest[si] * qk));
+                    ts::launch_unfold_t(g[si], d, shp[si].data(), k, Xs, sc);
+                    double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
+                    unfolding_svd_accurate(Xs, rest[si], qk, sigma, Vs, sc);
+                    std::vector<double> sig(static_cast<size_t>(qk));
+                    TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
+                                                  cudaMemcpyDeviceToHost, st));
+                    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+                    rk[si] = hosvd_rank(sig, eps, theta[si], capk);
+                    ++ctx->last_svd_fallbacks;
+                }
+            }
+        }
+        // g_s ← g_s ×_k P_kᵀ (first rank columns)
+        std::vector<GemmProblem> t0, t1;
+        for (std::int64_t s = 0; s < S; ++s) {
+            const size_t si = static_cast<size_t>(s);
+            auto& cs = shp[si];
+            std::int64_t left = 1, right = 1, total_out = rk[si];
+            for (int j = 0; j < d; ++j) {
+                if (j < k) left *= cs[static_cast<size_t>(j)];
+                if (j > k) right *= cs[static_cast<size_t>(j)];
+                if (j != k) total_out *= cs[static_cast<size_t>(j)];
+            }
+            double* gn = sc.alloc_n<double>(static_cast<size_t>(total_out));
+            GemmProblem p{};
+            if (k == 0) {
+                p.A = Pk[si][static_cast<size_t>(k)];
+                p.lda = qk;
+                p.B = g[si];
+                p.ldb = qk;
+                p.C = gn;
+                p.ldc = rk[si];
+                p.M = static_cast<int>(rk[si]);
+                p.N = static_cast<int>(right);
+                p.K = static_cast<int>(qk);
+                t0.push_back(p);
+            } else {
+                p.A = g[si];
+                p.lda = left;
+                p.sA = left * qk;
+                p.B = Pk[si][static_cast<size_t>(k)];
+                p.ldb = qk;
+                p.C = gn;
+                p.ldc = left;
+                p.sC = left * rk[si];
+                p.M = static_cast<int>(left);
+                p.N = static_cast<int>(rk[si]);
+                p.K = static_cast<int>(qk);
+                p.batch = static_cast<int>(right);
+                t1.push_back(p);
+            }
+            g[si] = gn;
+            cs[static_cast<size_t>(k)] = rk[si];
+            rank[si][static_cast<size_t>(k)] = rk[si];
+        }
+        if (!t0.empty()) ts::launch_grouped_gemm(Layout::TN, t0, sc, ctx->num_sms);
+        if (!t1.empty()) ts::launch_grouped_gemm(Layout::NN, t1, sc, ctx->num_sms);
+    }
+    // ---- H: Ũ_{s,n} = Y_{s,n}(R⁻¹P_k) or Û_{s,n}P_k; results
+    std::vector<std::unique_ptr<ts_result>> out(static_cast<size_t>(S));
+    {
+        std::vector<GemmProblem> tp, up;
+        for (std::int64_t s = 0; s < S; ++s) {
+            const size_t si = static_cast<size_t>(s);
+            out[si] = std::make_unique<ts_result>();
+            ts_result* r = out[si].get();
+            r->device = ctx->device;
+            r->stream = st;
+            r->order = d;
+            std::int64_t csize = 1;
+            for (int n = 0; n < d; ++n) {
+                const size_t i = sn(s, n);
+                const std::int64_t rkn = rank[si][static_cast<size_t>(n)];
+                r->dims[n] = dims[n];
+                r->ranks[n] = rkn;
+                csize *= rkn;
+                TS_CUDA_CHECK(cudaMallocAsync(&r->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rkn), st));
+                const double* Bm = Pk[si][static_cast<size_t>(n)];
+                if (rform[i]) {
+                    double* T = sc.alloc_n<double>(static_cast<size_t>(q[n] * rkn));
+                    GemmProblem p{};
+                    p.A = Rinv[i];
+                    p.lda = q[n];
+                    p.B = Pk[si][static_cast<size_t>(n)];
+                    p.ldb = q[n];
+                    p.C = T;
+                    p.ldc = q[n];
+                    p.M = static_cast<int>(q[n]);
+                    p.N = static_cast<int>(rkn);
+                    p.K = static_cast<int>(q[n]);
+                    tp.push_back(p);
+                    Bm = T;
+                }
+                GemmProblem p{};
+                p.A = rform[i] ? ypos(s, n) : Uh[i];
+                p.lda = dims[n];
+                p.B = Bm;
+                p.ldb = q[n];
+                p.C = r->factors[n];
+                p.ldc = dims[n];
+                p.M = static_cast<int>(dims[n]);
+                p.N = static_cast<int>(rkn);
+                p.K = static_cast<int>(q[n]);
+                up.push_back(p);
+            }
+            TS_CUDA_CHECK(cudaMallocAsync(&r->core, sizeof(double) * static_cast<size_t>(csize), st));
+            TS_CUDA_CHECK(cudaMemcpyAsync(r->core, g[si], sizeof(double) * static_cast<size_t>(csize),
+                                          cudaMemcpyDeviceToDevice, st));
+        }
+        if (!tp.empty()) ts::launch_grouped_gemm(Layout::NN, tp, sc, ctx->num_sms);
+        ts::launch_grouped_gemm(Layout::NN, up, sc, ctx->num_sms);
+    }
+    ctx->launches += sc.launches;
+    if (spec) {
+        std::vector<int> hf(2 * SD, 0);
+        if (dflags) TS_CUDA_CHECK(cudaMemcpyAsync(hf.data(), dflags, sizeof(int) * SD, cudaMemcpyDeviceToHost, st));
+        if (gflags) TS_CUDA_CHECK(cudaMemcpyAsync(hf.data() + SD, gflags, sizeof(int) * SD, cudaMemcpyDeviceToHost, st));
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int x : hf)
+            if (x != 0) {  // speculation rejected: redo every sum on the synchronous path
+                ctx->spec_ok = false;
+                out.clear();
+                return segmented_impl(ctx, b, S, seg, weights, widths, seeds, streams, eps, max_rank, false);
+            }
+    } else {
+        ctx->spec_ok = ctx->last_qr_fallbacks == 0 && ctx->last_svd_fallbacks == 0;
+    }
+    TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::vector<ts_result*> res(static_cast<size_t>(S));
+    for (std::int64_t s = 0; s < S; ++s) res[static_cast<size_t>(s)] = out[static_cast<size_t>(s)].release();
+    return res;
+}
+
 // Entry of ts_krp_sum / ts_kron_sum / ts_lazy_sum.  A call that repeats an
 // earlier one exactly (same batch upload, method, widths, cap, seed, ε) is
 // captured into a CUDA graph the second time and replayed from then on (at
@@ -1749,6 +2292,10 @@ int ts_batch_upload(ts_ctx* ctx, const ts_tucker_view* xs, int64_t count, ts_bat
                 if (cursor[j] != x.ranks[j]) invalid("TuckerTensor: blocks must span the full rank box");
             for (int j = 0; j < d; ++j) b->R[j] += x.ranks[j];
         }
+        b->scol.assign(static_cast<size_t>((count + 1) * d), 0);
+        for (std::int64_t i = 0; i < count; ++i)
+            for (int j = 0; j < d; ++j)
+                b->scol[static_cast<size_t>((i + 1) * d + j)] = b->scol[static_cast<size_t>(i * d + j)] + xs[i].ranks[j];
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
         cudaStream_t st = ctx->stream;
         std::int64_t bytes = 0;
@@ -1847,6 +2394,7 @@ int ts_batch_upload_stacked(ts_ctx* ctx, int64_t order, const int64_t* dims, int
             if (factors[j] == nullptr) invalid("TuckerTensor: one factor matrix per mode required");
             b->dims[j] = dims[j];
         }
+        b->scol.assign(static_cast<size_t>((count + 1) * d), 0);
         for (std::int64_t i = 0; i < count; ++i) {
             ts::Atom& at = b->atoms[static_cast<size_t>(i)];
             at.summand = static_cast<int>(i);
@@ -1854,6 +2402,7 @@ int ts_batch_upload_stacked(ts_ctx* ctx, int64_t order, const int64_t* dims, int
             std::int64_t e = 1;
             for (int j = 0; j < d; ++j) {
                 const std::int64_t r = ranks[i * d + j];
+                b->scol[static_cast<size_t>((i + 1) * d + j)] = b->scol[static_cast<size_t>(i * d + j)] + std::max<std::int64_t>(r, 0);
                 if (r < 1) invalid("TuckerTensor: dims and ranks must be positive");
                 at.col[j] = static_cast<int>(b->R[j]);
                 at.shape[j] = static_cast<int>(r);
@@ -1940,6 +2489,18 @@ int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const
     return guarded([&] {
         if (!ctx || !out) invalid("ts_kron_sum: null argument");
         *out = run_sum(ctx, batch, weights, widths, seed, stream, eps, max_rank, Method::Kron);
+    });
+}
+
+int ts_krp_sum_segmented(ts_ctx* ctx, const ts_batch* batch, int64_t nsums, const int64_t* segments,
+                         const double* weights, const int64_t* widths, const uint64_t* seeds, const uint64_t* streams,
+                         double eps, const int64_t* max_rank, ts_result** out) {
+    return guarded([&] {
+        if (!ctx || !out || !segments) invalid("ts_krp_sum_segmented: null argument");
+        for (int64_t i = 0; i < nsums; ++i) out[i] = nullptr;
+        std::vector<ts_result*> r =
+            segmented_impl(ctx, batch, nsums, segments, weights, widths, seeds, streams, eps, max_rank, true);
+        for (int64_t i = 0; i < nsums; ++i) out[i] = r[static_cast<size_t>(i)];
     });
 }
 

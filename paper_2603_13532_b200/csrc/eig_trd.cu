@@ -42,7 +42,8 @@ namespace ts {
 namespace {
 
 constexpr int kEN = 64;               // largest n
-constexpr int kEThreads = 1024;       // 32 warps
+constexpr int kEThreads = 256;        // 8 warps: row r = tid/4 owns 16 columns per thread
+constexpr int kEWarps = kEThreads / 32;
 constexpr int kLZ = kEN + 1;          // row stride of the [row][col] smem matrices
 constexpr double kEps = 1.1102230246251565e-16;
 
@@ -52,7 +53,7 @@ struct TrdSmem {
     double W[kEN * kLZ];      // scratch: C (original), DMMA outputs
     double Lm[kEN * kLZ];     // inverse iteration: L_i of eigenvalue j at [i*kEN + j]; later E = ZᵀZ − I
     double Dinv[kEN * kLZ];   //                    1/D_i at [i*kEN + j]; later Z·E
-    double tau[kEN], d[kEN], e[kEN], ds[kEN], e2s[kEN], es[kEN], lam[kEN], p[kEN], pv[kEN];
+    double tau[kEN], d[kEN], e[kEN], ds[kEN], e2s[kEN], es[kEN], lam[kEN], p[kEN], pw[kEWarps];
     double red[32];
     double misc[8];
     int flag;
@@ -87,9 +88,7 @@ template <bool TransA>
 __device__ __forceinline__ void dmma_64(const double* A, const double* B, double* Cout, int n) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int tile = 2 * warp + u;
+    for (int tile = warp; tile < 64; tile += kEWarps) {
         const int r0 = 8 * (tile & 7), c0 = 8 * (tile >> 3);
         double c_0 = 0.0, c_1 = 0.0;
         for (int k0 = 0; k0 < n; k0 += 4) {
@@ -106,22 +105,33 @@ __device__ __forceinline__ void dmma_64(const double* A, const double* B, double
 __global__ void __launch_bounds__(kEThreads, 1)
     trd_eig_kernel(const double* __restrict__ Cin, int64_t ldc, int n, double* __restrict__ lambda_out,
                    double* __restrict__ V_out, int* __restrict__ flag_out, double* __restrict__ resid_out,
-                   unsigned long long* __restrict__ prof) {
+                   unsigned long long* __restrict__ prof, int64_t strideC, int64_t strideL, int64_t strideV) {
+    // Batched launches (segmented sums): CTA b solves problem b.
+    {
+        const int64_t b = blockIdx.x;
+        Cin += b * strideC;
+        lambda_out += b * strideL;
+        V_out += b * strideV;
+        flag_out += b;
+        if (resid_out) resid_out += b;
+        if (b > 0) prof = nullptr;
+    }
     extern __shared__ __align__(16) unsigned char smraw[];
     TrdSmem& S = *reinterpret_cast<TrdSmem*>(smraw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int ra = 2 * warp;  // own rows ra, ra+1; own columns lane, lane+32
+    // Tridiagonalisation layout: thread t owns row r = t/4, columns c0..c0+15
+    // (c0 = 16·(t%4)) — a row is one 4-lane group, a warp 8 rows.
+    const int r = tid >> 2, c0 = 16 * (tid & 3);
+    const unsigned gmask4 = 0xfu << (lane & 28);
 
-    // ---- load + symmetrise into registers: a[s][h] = A[ra+s][lane+32h]
-    double a[2][2];
+    // ---- load + symmetrise into registers
+    double a[16];
 #pragma unroll
-    for (int s = 0; s < 2; ++s)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int i = ra + s, j = lane + 32 * h;
-            a[s][h] = (i < n && j < n) ? 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc])
-                                       : 0.0;
-        }
+    for (int u = 0; u < 16; ++u) {
+        const int j = c0 + u;
+        a[u] = (r < n && j < n) ? 0.5 * (Cin[r + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(r) * ldc])
+                                : 0.0;
+    }
     if (tid == 0) S.flag = 0;
     // Optional phase clocks (TS_EIG_PROFILE): prof[10 + phase] = cycles.
     long long tmark = clock64();
@@ -132,34 +142,48 @@ __global__ void __launch_bounds__(kEThreads, 1)
             tmark = now;
         }
     };
+    // Element (r, col) of the owning group, summed over the group (one nonzero).
+    auto group_pick = [&](int col, unsigned mask) {
+        double v = 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v = (c0 + u == col) ? a[u] : v;
+        v += __shfl_xor_sync(mask, v, 1);
+        v += __shfl_xor_sync(mask, v, 2);
+        return v;
+    };
 
-    // ---- 1. tridiagonalisation
+    // ---- 1. tridiagonalisation (two CTA barriers per reflector)
     for (int k = 0; k + 2 < n; ++k) {
         const int r0 = k + 1;
-        if (warp == (k >> 1)) {
-            // the owned row k, selected without dynamic register indexing
-            const double rlo = (k & 1) ? a[1][0] : a[0][0], rhi = (k & 1) ? a[1][1] : a[0][1];
-            const double xl = (lane > r0) ? rlo : 0.0;   // x_j, j > r0 (entries ≥ n are 0)
-            const double xh = (lane + 32 > r0) ? rhi : 0.0;
-            const double ss = warp_sum(fma(xl, xl, xh * xh));
-            const double x0 = __shfl_sync(0xffffffffu, r0 < 32 ? rlo : rhi, r0 & 31);
-            const double akk = __shfl_sync(0xffffffffu, k < 32 ? rlo : rhi, k & 31);
+        if (r == k) {  // the 4 threads owning row k form the reflector (dlarfg)
+            double ss = 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) ss = (c0 + u > r0) ? fma(a[u], a[u], ss) : ss;  // entries ≥ n are 0
+            ss += __shfl_xor_sync(gmask4, ss, 1);
+            ss += __shfl_xor_sync(gmask4, ss, 2);
+            const double x0 = group_pick(r0, gmask4);
+            const double akk = group_pick(k, gmask4);
             double tau = 0.0, beta = x0, scale = 0.0;
-            if (ss > 0.0) {  // dlarfg with refined MUFU sqrt / reciprocals (no IEEE slow paths)
+            if (ss > 0.0) {  // refined MUFU sqrt / reciprocals (no IEEE slow paths)
                 const double nn = fma(x0, x0, ss);
-                double r;
-                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(nn));
-                r = r * fma(-0.5 * nn, r * r, 1.5);
-                r = r * fma(-0.5 * nn, r * r, 1.5);
-                double sq = nn * r;
-                sq = fma(0.5 * r, fma(-sq, sq, nn), sq);  // one more correction of √nn
+                double rs;
+                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(nn));
+                rs = rs * fma(-0.5 * nn, rs * rs, 1.5);
+                rs = rs * fma(-0.5 * nn, rs * rs, 1.5);
+                double sq = nn * rs;
+                sq = fma(0.5 * rs, fma(-sq, sq, nn), sq);  // one more correction of √nn
                 beta = -copysign(sq, x0);
                 tau = fma(-x0, rcp_refined(beta), 1.0);
                 scale = rcp_refined(x0 - beta);
             }
-            S.V[k * kEN + lane] = lane == r0 ? 1.0 : xl * scale;
-            S.V[k * kEN + lane + 32] = lane + 32 == r0 ? 1.0 : xh * scale;
-            if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+                const int j = c0 + u;
+                const double v0 = j == r0 ? 1.0 : (j > r0 ? a[u] * scale : 0.0);
+                const double v1 = j + 1 == r0 ? 1.0 : (j + 1 > r0 ? a[u + 1] * scale : 0.0);
+                *reinterpret_cast<double2*>(&S.V[k * kEN + j]) = make_double2(v0, v1);
+            }
+            if ((tid & 3) == 0) {
                 S.tau[k] = tau;
                 S.d[k] = akk;
                 S.e[k] = beta;
@@ -167,47 +191,58 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
         __syncthreads();
         const double tk = S.tau[k];
-        const double vl = S.V[k * kEN + lane], vh = S.V[k * kEN + lane + 32];
-        const double vr0 = S.V[k * kEN + ra], vr1 = S.V[k * kEN + ra + 1];
-        double p0 = fma(a[0][0], vl, a[0][1] * vh), p1 = fma(a[1][0], vl, a[1][1] * vh);
+        double v[16];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            p0 += __shfl_xor_sync(0xffffffffu, p0, o);
-            p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+        for (int u = 0; u < 16; u += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(&S.V[k * kEN + c0 + u]);
+            v[u] = t2.x;
+            v[u + 1] = t2.y;
         }
-        p0 = ra > k ? tk * p0 : 0.0;  // rows ≤ k are finished (stale values there)
-        p1 = ra + 1 > k ? tk * p1 : 0.0;
-        if (lane == 0) {
-            S.p[ra] = p0;
-            S.p[ra + 1] = p1;
-            S.pv[ra] = p0 * vr0;
-            S.pv[ra + 1] = p1 * vr1;
+        const double vr = S.V[k * kEN + r];
+        // p_r = τ (A v)_r over the group, then Σ_r p_r v_r over the warp's 8 rows
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+            acc0 = fma(a[u], v[u], acc0);
+            acc1 = fma(a[u + 1], v[u + 1], acc1);
         }
+        double pr = acc0 + acc1;
+        pr += __shfl_xor_sync(0xffffffffu, pr, 1);
+        pr += __shfl_xor_sync(0xffffffffu, pr, 2);
+        pr = r > k ? tk * pr : 0.0;  // rows ≤ k are finished (stale values there)
+        double pvw = pr * vr;
+        pvw += __shfl_xor_sync(0xffffffffu, pvw, 4);
+        pvw += __shfl_xor_sync(0xffffffffu, pvw, 8);
+        pvw += __shfl_xor_sync(0xffffffffu, pvw, 16);
+        if ((tid & 3) == 0) S.p[r] = pr;
+        if (lane == 0) S.pw[warp] = pvw;
         __syncthreads();
-        const double K = 0.5 * tk * warp_sum(S.pv[lane] + S.pv[lane + 32]);
-        const double wl = fma(-K, vl, S.p[lane]), wh = fma(-K, vh, S.p[lane + 32]);
-        const double w0 = fma(-K, vr0, p0), w1 = fma(-K, vr1, p1);
+        double pvs = 0.0;
+#pragma unroll
+        for (int w = 0; w < kEWarps; w += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(&S.pw[w]);
+            pvs += t2.x + t2.y;
+        }
+        const double K = 0.5 * tk * pvs;
+        const double wr = fma(-K, vr, pr);
         // A -= v wᵀ + w vᵀ (zero outside the trailing block: v, w vanish there)
-        a[0][0] -= fma(vr0, wl, w0 * vl);
-        a[0][1] -= fma(vr0, wh, w0 * vh);
-        a[1][0] -= fma(vr1, wl, w1 * vl);
-        a[1][1] -= fma(vr1, wh, w1 * vh);
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+            const double2 p2 = *reinterpret_cast<const double2*>(&S.p[c0 + u]);
+            const double w0 = fma(-K, v[u], p2.x), w1 = fma(-K, v[u + 1], p2.y);
+            a[u] -= fma(vr, w0, wr * v[u]);
+            a[u + 1] -= fma(vr, w1, wr * v[u + 1]);
+        }
     }
     // trailing 2×2 (or the whole matrix when n ≤ 2)
     {
         const int k0 = n >= 2 ? n - 2 : 0;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            const int i = ra + s;
-            const double rlo = s ? a[1][0] : a[0][0], rhi = s ? a[1][1] : a[0][1];
-            if (i >= k0 && i < n) {
-                const double dii = __shfl_sync(0xffffffffu, i < 32 ? rlo : rhi, i & 31);
-                const double nxt = (i + 1 < n) ? __shfl_sync(0xffffffffu, i + 1 < 32 ? rlo : rhi, (i + 1) & 31) : 0.0;
-                if (lane == 0) {
-                    S.d[i] = dii;
-                    if (i + 1 < n) S.e[i] = nxt;
-                }
-            }
+        const bool mine = r >= k0 && r < n;
+        const double dii = group_pick(r, 0xffffffffu);
+        const double nxt = group_pick(r + 1, 0xffffffffu);
+        if (mine && (tid & 3) == 0) {
+            S.d[r] = dii;
+            if (r + 1 < n) S.e[r] = nxt;
         }
     }
     __syncthreads();
@@ -369,39 +404,38 @@ __global__ void __launch_bounds__(kEThreads, 1)
     __syncthreads();
     phase(2);
 
-    // ---- 4. back-transformation: 16 lanes per eigenvector (column), rows
-    // lane16 + 16u; Z ← H_k Z for k = n-3 … 0.  No CTA barrier.
+    // ---- 4. back-transformation: 4 lanes per eigenvector (column), 16 rows
+    // each; Z ← H_k Z for k = n-3 … 0.  No CTA barrier.
     {
-        const int col = tid >> 4, t = lane & 15;
-        double z[4];
+        const int col = tid >> 2;
+        double z[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) z[u] = (col < n && t + 16 * u < n) ? S.Z[(t + 16 * u) * kLZ + col] : 0.0;
-        double v[4], tk = 0.0;
-        if (n >= 3) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = S.V[(n - 3) * kEN + t + 16 * u];
-            tk = S.tau[n - 3];
-        }
+        for (int u = 0; u < 16; ++u) z[u] = (col < n && c0 + u < n) ? S.Z[(c0 + u) * kLZ + col] : 0.0;
         for (int k = n - 3; k >= 0; --k) {
-            // prefetch reflector k-1 (independent of z)
-            double vn[4], tn1 = 0.0;
-            const int kn = k > 0 ? k - 1 : 0;
+            double v[16];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) vn[u] = S.V[kn * kEN + t + 16 * u];
-            tn1 = S.tau[kn];
-            double s = fma(v[0], z[0], v[1] * z[1]) + fma(v[2], z[2], v[3] * z[3]);
-            s = hsum16(s) * tk;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                z[u] = fma(-s, v[u], z[u]);
-                v[u] = vn[u];
+            for (int u = 0; u < 16; u += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(&S.V[k * kEN + c0 + u]);
+                v[u] = t2.x;
+                v[u + 1] = t2.y;
             }
-            tk = tn1;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+                s0 = fma(v[u], z[u], s0);
+                s1 = fma(v[u + 1], z[u + 1], s1);
+            }
+            double sv = s0 + s1;
+            sv += __shfl_xor_sync(0xffffffffu, sv, 1);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 2);
+            sv *= S.tau[k];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) z[u] = fma(-sv, v[u], z[u]);
         }
         if (col < n) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (t + 16 * u < n) S.Z[(t + 16 * u) * kLZ + col] = z[u];
+            for (int u = 0; u < 16; ++u)
+                if (c0 + u < n) S.Z[(c0 + u) * kLZ + col] = z[u];
         }
         // the original (symmetrised) C into W for the residual check
         for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
@@ -420,10 +454,17 @@ __global__ void __launch_bounds__(kEThreads, 1)
     __syncthreads();
 
     phase(3);
-    // ---- 5. Löwdin re-orthonormalisation, at most 3 first-order steps:
-    // E = ZᵀZ − I, Z ← Z − ½·Z·E (the orthogonality defect squares each step).
+    // ---- 5. re-orthonormalisation.  E = ZᵀZ − I (DMMA).  Small defects (close
+    // but separated eigenvalues): Löwdin steps Z ← Z − ½·Z·E, the defect squares
+    // each step.  Large defects (tight clusters, e.g. the zero eigenvalues of a
+    // rank-deficient Gram, whose inverse-iteration vectors come out nearly
+    // parallel): modified Gram-Schmidt in DESCENDING eigenvalue order, which
+    // keeps the span of every leading set of columns (the kept subspace) and
+    // completes a collapsed cluster column by the unit vector with the largest
+    // component outside the columns already fixed.
     double* E = S.Lm;
     double* P = S.Dinv;
+    bool mgs = false;
     for (int itl = 0; itl < 3; ++itl) {
         dmma_64<true>(S.Z, S.Z, E, n);
         __syncthreads();
@@ -439,10 +480,10 @@ __global__ void __launch_bounds__(kEThreads, 1)
         if (lane == 0) S.red[warp] = emax;
         __syncthreads();
         emax = 0.0;
-        for (int w = 0; w < 32; ++w) emax = fmax(emax, S.red[w]);
+        for (int w = 0; w < kEWarps; ++w) emax = fmax(emax, S.red[w]);
         if (emax <= 4.0 * kEps * n) break;  // uniform: orthonormal to working precision
-        if (!(emax <= 0.25) || itl == 2) {  // nearly parallel vectors: leave it to Jacobi
-            if (tid == 0) S.flag = 1;
+        if (!(emax <= 1e-3) || itl == 2) {
+            mgs = true;
             break;
         }
         dmma_64<false>(S.Z, E, P, n);
@@ -453,6 +494,93 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
         __syncthreads();
     }
+    if (mgs) {  // uniform
+        // thread t: column ci = t/4, rows c0..c0+15 (c0 = 16·(t%4)); rowfill[m] =
+        // Σ over fixed columns of z[m]² (P is free scratch)
+        double* rowfill = P;
+        const int ci = tid >> 2;
+        if (tid < kEN) rowfill[tid] = 0.0;
+        __syncthreads();
+        for (int jp = n - 1; jp >= 0; --jp) {
+            // 1. norm of the pivot column (all threads of its group; others idle)
+            double nrm2 = 0.0;
+            if (ci == jp) {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const double z = c0 + u < n ? S.Z[(c0 + u) * kLZ + jp] : 0.0;
+                    nrm2 = fma(z, z, nrm2);
+                }
+                nrm2 += __shfl_xor_sync(gmask4, nrm2, 1);
+                nrm2 += __shfl_xor_sync(gmask4, nrm2, 2);
+                if ((tid & 3) == 0) S.misc[5] = nrm2;
+            }
+            __syncthreads();
+            nrm2 = S.misc[5];
+            if (!(nrm2 > 1e-4)) {  // collapsed (< 1% left): replace by e_m ⟂ the fixed columns
+                if (warp == 0) {
+                    double best = -1.0;
+                    int bm = 0;
+                    for (int m = lane; m < n; m += 32) {
+                        const double room = 1.0 - rowfill[m];
+                        if (room > best) {
+                            best = room;
+                            bm = m;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                        const int om = __shfl_xor_sync(0xffffffffu, bm, o);
+                        if (ob > best || (ob == best && om < bm)) {
+                            best = ob;
+                            bm = om;
+                        }
+                    }
+                    if (lane == 0) S.misc[6] = static_cast<double>(bm);
+                }
+                __syncthreads();
+                const int m = static_cast<int>(S.misc[6]);
+                // v_r = δ_rm − Σ_{f > jp, fixed} z_f[m] z_f[r]   (thread per row r < n)
+                if (tid < n) {
+                    double v = tid == m ? 1.0 : 0.0;
+                    for (int f = jp + 1; f < n; ++f) v = fma(-S.Z[m * kLZ + f], S.Z[tid * kLZ + f], v);
+                    S.p[tid] = v;
+                }
+                __syncthreads();
+                if (tid < n) S.Z[tid * kLZ + jp] = S.p[tid];
+                if (warp == 0) {
+                    double ss = 0.0;
+                    for (int r2 = lane; r2 < n; r2 += 32) ss = fma(S.p[r2], S.p[r2], ss);
+                    ss = warp_sum(ss);
+                    if (lane == 0) S.misc[5] = ss;
+                }
+                __syncthreads();
+                nrm2 = S.misc[5];
+                if (!(nrm2 > 1e-16) && tid == 0) S.flag = 1;  // cannot complete: leave it to Jacobi
+            }
+            const double inv = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
+            // 2. normalise the pivot, record its row weights
+            if (tid < n) {
+                const double z = S.Z[tid * kLZ + jp] * inv;
+                S.Z[tid * kLZ + jp] = z;
+                rowfill[tid] = fma(z, z, rowfill[tid]);
+            }
+            __syncthreads();
+            // 3. project the pivot out of the remaining columns ci < jp (group per column)
+            if (ci < jp) {
+                double dz = 0.0;
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (c0 + u < n) dz = fma(S.Z[(c0 + u) * kLZ + jp], S.Z[(c0 + u) * kLZ + ci], dz);
+                dz += __shfl_xor_sync(gmask4, dz, 1);
+                dz += __shfl_xor_sync(gmask4, dz, 2);
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (c0 + u < n) S.Z[(c0 + u) * kLZ + ci] = fma(-dz, S.Z[(c0 + u) * kLZ + jp], S.Z[(c0 + u) * kLZ + ci]);
+            }
+            __syncthreads();
+        }
+    }
     __syncthreads();
 
     phase(4);
@@ -460,9 +588,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
     {
         const int g = lane >> 2, t = lane & 3;
         double r2 = 0.0;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int tile = 2 * warp + u;
+        for (int tile = warp; tile < 64; tile += kEWarps) {
             const int r0 = 8 * (tile & 7), c0 = 8 * (tile >> 3);
             double c_0 = 0.0, c_1 = 0.0;
             for (int k0 = 0; k0 < n; k0 += 4) {
@@ -489,7 +615,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
     __syncthreads();
     if (tid == 0) {
         double r2 = 0.0;
-        for (int w = 0; w < 32; ++w) r2 += S.red[w];
+        for (int w = 0; w < kEWarps; ++w) r2 += S.red[w];
         const double res = sqrt(r2);
         // Backward-stable methods leave ~n·ε‖C‖; far more means a failure.
         if (!(res <= 1e-12 * tn)) S.flag = 1;
@@ -516,11 +642,12 @@ bool jacobi_eig_forced() {
 }
 
 bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, double* resid,
-                    CallScratch& sc) {
+                    CallScratch& sc, int count, int64_t strideC, int64_t strideL, int64_t strideV) {
     if (n < 1 || n > kEN) return false;
+    if (count < 1) return true;
     set_max_smem(trd_eig_kernel, static_cast<int>(sizeof(TrdSmem)));
-    trd_eig_kernel<<<1, kEThreads, sizeof(TrdSmem), sc.stream()>>>(C, ldc, n, lambda, V, flag, resid,
-                                                                   eig_probe_buffer());
+    trd_eig_kernel<<<count, kEThreads, sizeof(TrdSmem), sc.stream()>>>(C, ldc, n, lambda, V, flag, resid,
+                                                                       eig_probe_buffer(), strideC, strideL, strideV);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
     return true;

@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(4 * NC) chol_inv_kernel(CholBatch cb) {
     constexpr int LD = NC + 1;   // odd stride: the column-major store below is conflict-free
     const int b = blockIdx.x;
     const int n = cb.n;
-    const double* __restrict__ G = cb.G[b];
+    const double* __restrict__ G = cb.Gd ? cb.Gd[b] : cb.G[b];
     extern __shared__ __align__(16) double sm[];
     double* U = sm;           // n × LD: published rows of U
     double* X = U + n * LD;   // n × LD: rows of R⁻¹
@@ -774,13 +774,13 @@ __global__ void __launch_bounds__(4 * NC) chol_inv_kernel(CholBatch cb) {
     }
     __syncthreads();
     CHOL_T(2)
-    double* Rinv = cb.Rinv[b];
+    double* Rinv = cb.Rd ? cb.Rd[b] : cb.Rinv[b];
     for (int idx = tid; idx < n * n; idx += 4 * NC) {
         const int i = idx % n, c = idx / n;
         Rinv[i + static_cast<int64_t>(c) * cb.ldri] = X[i * LD + c];
     }
     CHOL_T(4)
-    if (tid == 0 && bad) atomicOr(cb.flag[b], bad);
+    if (tid == 0 && bad) atomicOr(cb.Fd ? cb.Fd[b] : cb.flag[b], bad);
 }
 
 // ------------------------------------------------------------------ misc
@@ -795,8 +795,14 @@ __device__ __forceinline__ double resid_abs(const double* resid, double l1) {
 }
 
 __global__ void gram_check_kernel(const double* __restrict__ lam, int q, int cap, const double* __restrict__ resid,
-                                  int* __restrict__ flag) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+                                  int* __restrict__ flag, int64_t strideL) {
+    if (threadIdx.x != 0) return;
+    {  // batched: CTA b checks problem b
+        const int64_t b = blockIdx.x;
+        lam += b * strideL;
+        if (resid) resid += b;
+        flag += b;
+    }
     const double l1 = lam[0];
     bool ok = l1 > 0.0;
     if (ok) {
@@ -1131,8 +1137,10 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
     sc.launches += 1;
 }
 
-void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc) {
-    gram_check_kernel<<<1, 32, 0, sc.stream()>>>(lam, q, cap, resid, flag);
+void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc, int count,
+                       int64_t strideL) {
+    if (count < 1) return;
+    gram_check_kernel<<<count, 32, 0, sc.stream()>>>(lam, q, cap, resid, flag, strideL);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
@@ -1152,15 +1160,17 @@ __global__ void rform_check_kernel(CholBatch cb) {
     __shared__ double part[32];
     const int b = blockIdx.x, n = cb.n;
     double tr = 0.0, fr = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) tr += cb.G[b][i + static_cast<int64_t>(i) * cb.ldg];
+    const double* G = cb.Gd ? cb.Gd[b] : cb.G[b];
+    const double* Ri = cb.Rd ? cb.Rd[b] : cb.Rinv[b];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) tr += G[i + static_cast<int64_t>(i) * cb.ldg];
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-        const double v = cb.Rinv[b][e % n + static_cast<int64_t>(e / n) * cb.ldri];
+        const double v = Ri[e % n + static_cast<int64_t>(e / n) * cb.ldri];
         fr = fma(v, v, fr);
     }
     tr = block_sum(tr, part);
     __syncthreads();
     fr = block_sum(fr, part);
-    if (threadIdx.x == 0 && !(tr * fr <= 1e8)) atomicOr(cb.flag[b], 4);
+    if (threadIdx.x == 0 && !(tr * fr <= 1e8)) atomicOr(cb.Fd ? cb.Fd[b] : cb.flag[b], 4);
 }
 
 void launch_rform_check(const CholBatch& cb, int count, CallScratch& sc) {

@@ -114,6 +114,11 @@ struct CholBatch {
     const double* G[kMaxOrder];
     double* Rinv[kMaxOrder];
     int* flag[kMaxOrder];
+    // Device arrays of the same pointers for batches larger than kMaxOrder
+    // (segmented sums); when set they replace G / Rinv / flag.
+    const double* const* Gd = nullptr;
+    double* const* Rd = nullptr;
+    int* const* Fd = nullptr;
     int64_t ldg, ldri;
     int n;
     int check_identity;
@@ -123,7 +128,8 @@ void launch_chol_inv(const CholBatch& cb, int count, CallScratch& sc);
 // trace(G)·‖R⁻¹‖_F² > 1e8 (κ_F(Y) > 1e4).
 void launch_rform_check(const CholBatch& cb, int count, CallScratch& sc);
 // Device check of the ε = 0 Gram fast path (twin of capi.cu gram_rank): *flag |= 1 on rejection.
-void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc);
+void launch_gram_check(const double* lam, int q, int cap, const double* resid, int* flag, CallScratch& sc,
+                       int count = 1, int64_t strideL = 0);
 // Device check of the ε > 0 Gram fast path with a known output rank `expect`
 // (twin of capi.cu gram_rank, θ from the device ‖h‖² *hss): *flag |= 1 on rejection.
 void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int order, const double* hss,
@@ -133,8 +139,10 @@ void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int o
 // re-orthonormalisation, all in one CTA.  lambda descending, V (n × n) the
 // matching columns; *resid = ‖C V − V Λ‖_F (measured); *flag |= 1 when the
 // result is not acceptable (then use launch_sym_jacobi).  False if n > 64.
+// count > 1: `count` independent problems, problem b at C + b·strideC,
+// lambda + b·strideL, V + b·strideV, flag + b, resid + b (one CTA each).
 bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, double* resid,
-                    CallScratch& sc);
+                    CallScratch& sc, int count = 1, int64_t strideC = 0, int64_t strideL = 0, int64_t strideV = 0);
 
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);

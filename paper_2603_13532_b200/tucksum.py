@@ -51,7 +51,7 @@ EXPORTED_SYMBOLS = [
     "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
     "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked", "ts_ctx_comm_info",
-    "ts_ctx_set_host_allreduce",
+    "ts_ctx_set_host_allreduce", "ts_krp_sum_segmented",
 ]
 
 HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
@@ -118,6 +118,8 @@ def lib():
         L.ts_batch_upload.argtypes = [C.c_void_p, C.POINTER(TsTuckerView), i64, C.POINTER(C.c_void_p)]
         L.ts_omega_prepare.argtypes = [C.c_void_p, i64, i64p, i64, u64, u64]
         L.ts_ctx_set_host_allreduce.argtypes = [C.c_void_p, HOST_ALLREDUCE_FN, C.c_void_p, C.c_int, C.c_int]
+        L.ts_krp_sum_segmented.argtypes = [C.c_void_p, C.c_void_p, i64, i64p, dptr, i64p, C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_uint64), C.c_double, i64p, C.POINTER(C.c_void_p)]
         for name in ("ts_result_factor", "ts_result_core", "ts_result_free", "ts_result_dims", "ts_result_ranks",
                      "ts_batch_free", "ts_ctx_destroy", "ts_ctx_set_debug", "ts_ctx_set_timing",
                      "ts_ctx_stage_times", "ts_result_intermediate"):
@@ -773,6 +775,32 @@ class Engine:
                                      C.c_double(eps), cap.ctypes.data_as(i64p) if cap is not None else None,
                                      C.c_int(lanes), out))
         return [DeviceResult(C.c_void_p(out[i]), self) for i in range(n)]
+
+    def krp_sum_segmented(self, batch: DeviceBatch, segments, weights, widths, seeds: Sequence[RngSeed], eps: float,
+                          max_rank=None) -> List[DeviceResult]:
+        """Segmented independent sums (ts_krp_sum_segmented):
+        sum s = the summands [segments[s], segments[s+1]) of `batch`, per-summand
+        `weights`, shared plan `widths` / `max_rank`, own seed; every stage runs as
+        one launch over all sums."""
+        seg = np.ascontiguousarray(np.asarray(segments, dtype=np.int64))
+        nsums = len(seg) - 1
+        if nsums < 1 or len(seeds) != nsums:
+            raise ValueError("krp_sum_segmented needs nsums + 1 segment bounds and one seed per sum")
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        if len(w) != batch.count:
+            raise ValueError("sum request needs matching, nonempty summands and weights")
+        wd = np.ascontiguousarray(np.asarray(widths, dtype=np.int64))
+        if len(wd) != batch.order:
+            raise ValueError("plan order does not match summand order")
+        cap = None if max_rank is None else np.ascontiguousarray(np.asarray(max_rank, dtype=np.int64))
+        sd = np.ascontiguousarray([x.seed for x in seeds], dtype=np.uint64)
+        st = np.ascontiguousarray([x.stream for x in seeds], dtype=np.uint64)
+        out = (C.c_void_p * nsums)()
+        _check(lib().ts_krp_sum_segmented(self.handle, batch.handle, i64(nsums), seg.ctypes.data_as(i64p), _p(w),
+                                          wd.ctypes.data_as(i64p), sd.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                          st.ctypes.data_as(C.POINTER(C.c_uint64)), C.c_double(eps),
+                                          cap.ctypes.data_as(i64p) if cap is not None else None, out))
+        return [DeviceResult(C.c_void_p(out[i]), self) for i in range(nsums)]
 
     def effective_subrank(self, batch: DeviceBatch, weights, eps: float, oversampling, strategy: "Strategy" = None):
         order = batch.order

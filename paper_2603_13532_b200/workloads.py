@@ -104,10 +104,12 @@ def _library_rng() -> Tuple[Gaussian, Substream]:
 
 def make_workload(cfg: int, K: Optional[int] = None, n_override: Optional[List[int]] = None,
                   k_range: Optional[Tuple[int, int]] = None, gaussian: Optional[Gaussian] = None,
-                  substream: Optional[Substream] = None) -> Workload:
+                  substream: Optional[Substream] = None, node: int = 0) -> Workload:
     """Builds BASELINE config `cfg` (1..5).  `K` / `n_override` shrink it for parity tests;
     `k_range` = [begin, end) builds only that shard of the K summands; `gaussian` /
-    `substream` replace the library's host RNG by a bit-identical one (e.g. the oracle's)."""
+    `substream` replace the library's host RNG by a bit-identical one (e.g. the oracle's);
+    `node` > 0 draws an independent instance (base seed S.substream(700000 + node)),
+    e.g. one sum per NDG node."""
     sp = _SPECS[cfg]
     dims = list(n_override or sp["dims"])
     K = int(K or sp["K"])
@@ -119,6 +121,8 @@ def make_workload(cfg: int, K: Optional[int] = None, n_override: Optional[List[i
     r = list(sp["r"])
     d = len(dims)
     S = (2603, cfg)
+    if node:
+        S = substream(S, 700000 + node)
     Kl = ke - kb
     R = [Kl * r[j] for j in range(d)]
     slabs = [np.zeros((dims[j], R[j]), order="F") for j in range(d)]
