@@ -138,20 +138,21 @@ int ts_krp_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const 
                uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
 /* kron_sum with the plan given: Ω_n is
  * dims[n] × widths[n] and the mode-n sketch has C_n = prod_{j != n} widths[j]
- * columns (src/sketch.cpp:91-101,132-140); every C_n must be <= 96.  Other
- * arguments as ts_krp_sum. */
+ * columns (src/sketch.cpp:91-101,132-140), any size (C_n > 96 takes the
+ * generic-width stages of wide.cu).  Other arguments as ts_krp_sum. */
 int ts_kron_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, const int64_t* widths, uint64_t seed,
                 uint64_t stream, double eps, const int64_t* max_rank, ts_result** out);
 /* Lazy rounding of the formal sum (the paper's deterministic baseline):
  * orthogonalize the stacked factors (thin QR of F_n), absorb R_n into the block
  * cores, st_hosvd(eps [, max_rank]) and Q·P — on the device, through the same
- * stage D-H kernels as ts_krp_sum.  Needs sum_k ranks_n^(k) <= 96 per mode and
- * order >= 2; not available with a NCCL communicator. */
+ * stage D-H kernels as ts_krp_sum; stacked ranks sum_k ranks_n^(k) > 96 take
+ * the generic-width stages (wide.cu).  Needs order >= 2; not available with a
+ * NCCL communicator. */
 int ts_lazy_sum(ts_ctx* ctx, const ts_batch* batch, const double* weights, double eps, const int64_t* max_rank,
                 ts_result** out);
 /* ‖Σ_k w_k X_k‖_F by the reference's orthogonalized-core norm (thin QR of every
  * stacked factor, R absorbed into the block cores): accurate for cancelling
- * sums; same size limits as ts_lazy_sum. */
+ * sums; any size (as ts_lazy_sum). */
 int ts_tucker_norm(ts_ctx* ctx, const ts_batch* batch, const double* weights, double* out);
 /* Σ_{a,b} wx_a wy_b <X_a, Y_b> by per-block Gram contractions (the reference's
  * tucker_inner, no densification, any size): one cross-Gram DMMA GEMM per mode
@@ -197,9 +198,10 @@ int ts_effective_subrank_kron(ts_ctx* ctx, const ts_batch* batch, const double* 
                               int64_t* widths);
 
 /* Small symmetric eigensolver used by ST-HOSVD's fast path (reference sym_eig,
- * src/kernels.cpp:70-86): a (n × n, column-major, host), n <= 96 → values
- * (descending) and column eigenvectors (host).  sweeps / ms (nullable) report
- * the Jacobi sweeps and the kernel time. */
+ * src/kernels.cpp:70-86): a (n × n, column-major, host; positive semidefinite
+ * for n > 96) → values (descending) and column eigenvectors (host).  n <= 96:
+ * one-CTA two-sided Jacobi; n > 96: block one-sided Jacobi (wide.cu).  sweeps /
+ * ms (nullable) report the Jacobi sweeps and the time. */
 int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms);
 /* The stage-G default for n <= 64: register-resident Householder
  * tridiagonalisation + multisection + inverse iteration + Löwdin

@@ -375,11 +375,34 @@ std::int64_t hosvd_rank(const std::vector<double>& s, double tau, double theta, 
 // Accurate path: left singular vectors + singular values of the unfolding
 // g_(k) (q_k × rest) from X = g_(k)ᵀ via TSQR (R only) and a one-sided Jacobi SVD
 // of the small triangular factor.  X is overwritten.
-void unfolding_svd_accurate(double* X, std::int64_t rest, std::int64_t qk, double* sigma, double* U, CallScratch& sc) {
+void unfolding_svd_accurate(double* X, std::int64_t rest, std::int64_t qk, double* sigma, double* U, CallScratch& sc,
+                            int num_sms) {
+    if (qk > ts::max_tsqr_cols()) {  // any width: block one-sided Jacobi on X itself (wide.cu)
+        ts::bosj_svd(X, rest, rest, qk, sigma, U, qk, sc, num_sms);
+        return;
+    }
     ts::TsqrPlan plan = ts::plan_tsqr(X, rest, rest, qk, nullptr, 0, sc);
     ts::run_tsqr({&plan}, sc, false);
     ts::launch_jacobi_svd(plan.Rtop, plan.kk, static_cast<int>(plan.kk), static_cast<int>(qk), sigma, U, sc);
 }
+
+// Symmetric eigensolver of the Gram fast paths (reference sym_eig,
+// src/kernels.cpp:70-86) for any n: the one-CTA Jacobi (eig.cu / kernels.cu)
+// up to 96, beyond that the block one-sided Jacobi of the (PSD) Gram itself,
+// whose singular values are its eigenvalues (wide.cu).
+void sym_eig_any(const double* C, std::int64_t n, double* lambda, double* V, CallScratch& sc, int num_sms,
+                 int* sweeps = nullptr) {
+    if (n <= ts::max_tsqr_cols()) {
+        ts::launch_sym_jacobi(C, n, static_cast<int>(n), lambda, V, sc, sweeps);
+        return;
+    }
+    ts::bosj_svd(C, n, n, n, lambda, V, n, sc, num_sms);
+}
+
+// Stage-D thin Q of a mode the CholeskyQR2 fast path does not take, for any
+// width: widths ≤ 96 are planned into one batched Householder TSQR (Y is
+// overwritten), wider ones go through wide.cu's BCGS2 (Y is kept).
+bool qr_wide_mode(std::int64_t cols) { return cols > ts::max_tsqr_cols(); }
 
 // Fast path of the ST-HOSVD rank decision from the eigenvalues lam (descending)
 // of the Gram h_(k)h_(k)ᵀ.  The Gram's eigenvalues carry absolute errors of a few
@@ -778,10 +801,6 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     for (int n = 0; n < d; ++n) {
         ow[n] = lazy ? 0 : krp ? s : widths[n];
         yc[n] = lazy ? b->R[n] : krp ? s : complement_product(widths, d, n);
-        if (yc[n] > ts::max_tsqr_cols())
-            throw ts::Error(TS_UNSUPPORTED, std::string(lazy ? "stacked rank " : "sketch width ") +
-                                                std::to_string(yc[n]) + " exceeds the supported maximum of " +
-                                                std::to_string(ts::max_tsqr_cols()));
     }
     for (std::int64_t i = 0; i < b->count; ++i)
         if (!std::isfinite(weights[i])) invalid("weights must be finite");
@@ -949,14 +968,14 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     double* Rinv[TS_MAX_ORDER] = {};
     std::vector<int> rform(static_cast<size_t>(d), 0);
     bool overlap = spec && !lazy && !ctx->debug && !norm_out;
-    for (int n = 0; n < d && overlap; ++n) overlap = dims[n] >= 2 * yc[n];
+    for (int n = 0; n < d && overlap; ++n) overlap = dims[n] >= 2 * yc[n] && !qr_wide_mode(yc[n]);
     {
         std::vector<int>& chol = rform;
         int* flags = sc.alloc_n<int>(static_cast<size_t>(d));
         TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<size_t>(d), st));
         bool any = false;
         for (int n = 0; n < d; ++n) {
-            chol[static_cast<size_t>(n)] = dims[n] >= 2 * yc[n];
+            chol[static_cast<size_t>(n)] = dims[n] >= 2 * yc[n] && !qr_wide_mode(yc[n]);
             if (!chol[static_cast<size_t>(n)]) continue;
             any = true;
             Rinv[n] = sc.alloc_n<double>(static_cast<size_t>(yc[n] * yc[n]));
@@ -1072,6 +1091,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         for (int n = 0; n < d; ++n) {
             if (chol[static_cast<size_t>(n)]) continue;
             Uh[n] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+            if (qr_wide_mode(yc[n])) {
+                ts::wide_qr(Y + yoff[n], dims[n], dims[n], yc[n], Uh[n], dims[n], sc, ctx->num_sms);
+                continue;
+            }
             plans[static_cast<size_t>(n)] = ts::plan_tsqr(Y + yoff[n], dims[n], dims[n], yc[n], Uh[n], dims[n], sc);
             pp.push_back(&plans[static_cast<size_t>(n)]);
         }
@@ -1167,7 +1190,8 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     // known in advance only for a captured call (the probe run's ranks): then the
     // device re-derives the reference tail rule and flags any difference.
     const std::int64_t* fixed_rank = ge ? ge->ranks : nullptr;
-    const bool spec_g = spec && (eps == 0.0 || fixed_rank != nullptr);
+    bool spec_g = spec && (eps == 0.0 || fixed_rank != nullptr);
+    for (int n = 0; n < d; ++n) spec_g = spec_g && !qr_wide_mode(q[n]);  // wide eigensolves sync anyway
     if (spec_g) {
         gflags = sc.alloc_n<int>(static_cast<size_t>(d));
         TS_CUDA_CHECK(cudaMemsetAsync(gflags, 0, sizeof(int) * static_cast<size_t>(d), st));
@@ -1239,7 +1263,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 // Last time this mode's Gram decision was not provably exact: go
                 // straight to the accurate TSQR + one-sided Jacobi SVD.
                 double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
-                unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc);
+                unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc, ctx->num_sms);
                 std::vector<double> sig(static_cast<size_t>(qk));
                 TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
                                               cudaMemcpyDeviceToHost, st));
@@ -1266,7 +1290,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 d_res = sc.alloc_n<double>(1);
                 ts::launch_sym_trd(C, qk, static_cast<int>(qk), lam, Pk[k], tflag, d_res, sc);
             } else {
-                ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, dsw);
+                sym_eig_any(C, qk, lam, Pk[k], sc, ctx->num_sms, dsw);
             }
             std::int64_t rk = 0;
             if (spec_g && !dsw) {
@@ -1290,7 +1314,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 if (d_res) TS_CUDA_CHECK(cudaMemcpyAsync(&hres, d_res, sizeof(double), cudaMemcpyDeviceToHost, st));
                 TS_CUDA_CHECK(cudaStreamSynchronize(st));
                 if (htf) {  // the tridiagonalisation solver rejected its own result
-                    ts::launch_sym_jacobi(C, qk, static_cast<int>(qk), lam, Pk[k], sc, nullptr);
+                    sym_eig_any(C, qk, lam, Pk[k], sc, ctx->num_sms);
                     TS_CUDA_CHECK(cudaMemcpyAsync(lv.data(), lam, sizeof(double) * static_cast<size_t>(qk),
                                                   cudaMemcpyDeviceToHost, st));
                     TS_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -1304,7 +1328,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 rk = gram_rank(lv, eps, theta, capk, hres, &ok);
                 if (!ok) {
                     double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
-                    unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc);
+                    unfolding_svd_accurate(need_X(), rest, qk, sigma, Pk[k], sc, ctx->num_sms);
                     std::vector<double> sig(static_cast<size_t>(qk));
                     TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
                                                   cudaMemcpyDeviceToHost, st));
@@ -1499,9 +1523,6 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
     for (std::int64_t i = 0; i < b->count; ++i)
         if (!std::isfinite(weights[i])) invalid("weights must be finite");
     const std::int64_t sw = *std::max_element(widths, widths + d);
-    if (sw > ts::max_tsqr_cols())
-        throw ts::Error(TS_UNSUPPORTED, "sketch width " + std::to_string(sw) + " exceeds the supported maximum of " +
-                                            std::to_string(ts::max_tsqr_cols()));
     TS_CUDA_CHECK(cudaSetDevice(ctx->device));
     ctx->stage.reset();
     cudaStream_t st = ctx->stream;
@@ -1600,7 +1621,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         std::vector<int*> hF;
         for (std::int64_t s = 0; s < S; ++s)
             for (int n = 0; n < d; ++n) {
-                if (dims[n] < 2 * sw) continue;
+                if (dims[n] < 2 * sw || qr_wide_mode(sw)) continue;
                 const size_t i = sn(s, n);
                 rform[i] = 1;
                 const std::int64_t c = sw;
@@ -1688,6 +1709,10 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                 const size_t i = sn(s, n);
                 if (rform[i]) continue;
                 Uh[i] = sc.alloc_n<double>(static_cast<size_t>(dims[n] * q[n]));
+                if (qr_wide_mode(sw)) {
+                    ts::wide_qr(ypos(s, n), dims[n], dims[n], sw, Uh[i], dims[n], sc, ctx->num_sms);
+                    continue;
+                }
                 plans[i] = ts::plan_tsqr(ypos(s, n), dims[n], dims[n], sw, Uh[i], dims[n], sc);
                 pp.push_back(&plans[i]);
             }
@@ -1764,7 +1789,8 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         for (int n = 0; n < d; ++n) shp[static_cast<size_t>(s)][static_cast<size_t>(n)] = q[n];
         g[static_cast<size_t>(s)] = H + s * hsz;
     }
-    const bool spec_g = spec && eps == 0.0;
+    bool spec_g = spec && eps == 0.0;
+    for (int n = 0; n < d; ++n) spec_g = spec_g && !qr_wide_mode(q[n]);  // wide eigensolves sync anyway
     if (spec_g) {
         gflags = sc.alloc_n<int>(SD);
         TS_CUDA_CHECK(cudaMemsetAsync(gflags, 0, sizeof(int) * SD, st));
@@ -1829,7 +1855,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                                qk, qk * qk);
         } else {
             for (std::int64_t s = 0; s < S; ++s)
-                ts::launch_sym_jacobi(Call + s * qk * qk, qk, static_cast<int>(qk), Lall + s * qk, Vall + s * qk * qk, sc);
+                sym_eig_any(Call + s * qk * qk, qk, Lall + s * qk, Vall + s * qk * qk, sc, ctx->num_sms);
         }
         std::vector<std::int64_t> rk(static_cast<size_t>(S), 0);
         if (spec_g) {
@@ -1852,7 +1878,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                                         lv.begin() + static_cast<std::ptrdiff_t>((s + 1) * qk));
                 double rres = trd ? hres[si] : -1.0;
                 if (trd && htf[si]) {  // the tridiagonalisation solver rejected its own result
-                    ts::launch_sym_jacobi(Cs, qk, static_cast<int>(qk), Ls, Vs, sc);
+                    sym_eig_any(Cs, qk, Ls, Vs, sc, ctx->num_sms);
                     TS_CUDA_CHECK(cudaMemcpyAsync(lam.data(), Ls, sizeof(double) * static_cast<size_t>(qk),
                                                   cudaMemcpyDeviceToHost, st));
                     TS_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -1865,7 +1891,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                     double* Xs = sc.alloc_n<double>(static_cast<size_t>(rest[si] * qk));
                     ts::launch_unfold_t(g[si], d, shp[si].data(), k, Xs, sc);
                     double* sigma = sc.alloc_n<double>(static_cast<size_t>(qk));
-                    unfolding_svd_accurate(Xs, rest[si], qk, sigma, Vs, sc);
+                    unfolding_svd_accurate(Xs, rest[si], qk, sigma, Vs, sc, ctx->num_sms);
                     std::vector<double> sig(static_cast<size_t>(qk));
                     TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(qk),
                                                   cudaMemcpyDeviceToHost, st));
@@ -2014,7 +2040,19 @@ ts_result* run_sum(ts_ctx* ctx, const ts_batch* b, const double* weights, const 
     }();
     const bool graphable = !env_off && ctx->graphs && b != nullptr && weights != nullptr && eps >= 0.0 &&
                            !sharded(ctx) && !ctx->debug && !ctx->timing && ctx->spec_ok && ctx->parent == nullptr;
-    if (!graphable)
+    // Generic-width stages (wide.cu) synchronise with the host once per
+    // Jacobi sweep: such calls are never captured.
+    bool wide = false;
+    if (graphable && b->order >= 2) {
+        for (int n = 0; n < b->order; ++n) {
+            const std::int64_t c = method == Method::Lazy ? b->R[n]
+                                   : widths == nullptr    ? 0
+                                   : method == Method::Krp ? *std::max_element(widths, widths + b->order)
+                                                           : complement_product(widths, b->order, n);
+            wide = wide || qr_wide_mode(c);
+        }
+    }
+    if (!graphable || wide)
         return sketched_sum_impl(ctx, b, weights, widths, seed, stream, eps, max_rank, method);
     const int d = b->order;
     GraphKey key{b->id, static_cast<int>(method),
@@ -2643,8 +2681,6 @@ static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, 
         for (int n = 0; n < d; ++n) {
             const std::int64_t rows = b->dims[n], R = b->R[n];
             const std::int64_t small = std::min(rows, R);
-            if (small > ts::max_tsqr_cols())
-                throw ts::Error(TS_UNSUPPORTED, "effective_subrank: min(n, sum of ranks) exceeds the device eigen-solver size");
             // Per-column energy scale.
             std::vector<double> cscale(static_cast<size_t>(R));
             // Column ranges per summand follow the stacking order.
@@ -2660,11 +2696,15 @@ static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, 
             double* V = sc.alloc_n<double>(static_cast<size_t>(rows * R));
             ts::launch_scale_columns(b->F[n], rows, R, d_scale, V, !tall, sc);
             const std::int64_t m = tall ? rows : R, cols = tall ? R : rows;
-            ts::TsqrPlan plan = ts::plan_tsqr(V, m, m, cols, nullptr, 0, sc);
-            ts::run_tsqr({&plan}, sc, false);
             double* sigma = sc.alloc_n<double>(static_cast<size_t>(cols));
-            double* U = sc.alloc_n<double>(static_cast<size_t>(cols * cols));
-            ts::launch_jacobi_svd(plan.Rtop, plan.kk, static_cast<int>(plan.kk), static_cast<int>(cols), sigma, U, sc);
+            if (qr_wide_mode(cols)) {  // any width: block one-sided Jacobi on V itself (wide.cu)
+                ts::bosj_svd(V, m, m, cols, sigma, nullptr, 0, sc, ctx->num_sms);
+            } else {
+                ts::TsqrPlan plan = ts::plan_tsqr(V, m, m, cols, nullptr, 0, sc);
+                ts::run_tsqr({&plan}, sc, false);
+                double* U = sc.alloc_n<double>(static_cast<size_t>(cols * cols));
+                ts::launch_jacobi_svd(plan.Rtop, plan.kk, static_cast<int>(plan.kk), static_cast<int>(cols), sigma, U, sc);
+            }
             std::vector<double> sig(static_cast<size_t>(cols));
             TS_CUDA_CHECK(cudaMemcpyAsync(sig.data(), sigma, sizeof(double) * static_cast<size_t>(cols),
                                           cudaMemcpyDeviceToHost, ctx->stream));
@@ -2776,7 +2816,7 @@ int ts_debug_eig_profile(long long* out17) {
 // src/kernels.cpp:70-86): host in / host out; also reports sweeps and kernel ms.
 int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* sweeps, double* ms) {
     return guarded([&] {
-        if (!ctx || n < 1 || n > ts::max_tsqr_cols()) invalid("ts_sym_eig: need 1 <= n <= 96");
+        if (!ctx || n < 1) invalid("ts_sym_eig: need n >= 1");
         TS_CUDA_CHECK(cudaSetDevice(ctx->device));
         ctx->stage.reset();
         CallScratch sc(ctx->stream, ctx->stage);
@@ -2788,9 +2828,15 @@ int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* 
         TS_CUDA_CHECK(cudaEventCreate(&e0));
         TS_CUDA_CHECK(cudaEventCreate(&e1));
         TS_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
-        ts::launch_sym_jacobi(dA, n, static_cast<int>(n), dl, dV, sc, dsw);
-        TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
         int hs = 0;
+        if (qr_wide_mode(n)) {  // block one-sided Jacobi of the (PSD) matrix (wide.cu)
+            hs = ts::bosj_svd(dA, n, n, n, dl, dV, n, sc, ctx->num_sms);
+            TS_CUDA_CHECK(cudaMemsetAsync(dsw, 0, sizeof(int), ctx->stream));
+        } else {
+            ts::launch_sym_jacobi(dA, n, static_cast<int>(n), dl, dV, sc, dsw);
+        }
+        TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        const int bosj_sweeps = hs;
         TS_CUDA_CHECK(cudaMemcpyAsync(values, dl, sizeof(double) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, ctx->stream));
         TS_CUDA_CHECK(cudaMemcpyAsync(vectors, dV, sizeof(double) * static_cast<size_t>(n * n), cudaMemcpyDeviceToHost, ctx->stream));
         TS_CUDA_CHECK(cudaMemcpyAsync(&hs, dsw, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -2799,7 +2845,7 @@ int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* 
         TS_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        if (sweeps) *sweeps = hs;
+        if (sweeps) *sweeps = qr_wide_mode(n) ? bosj_sweeps : hs;
         if (ms) *ms = t;
     });
 }

@@ -131,10 +131,17 @@ __device__ __forceinline__ double2 rotation_or_identity(double app, double aqq, 
 __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const double* __restrict__ Cin, int64_t ldc, int n,
                                                                     double2* __restrict__ rot,
                                                                     double* __restrict__ diag_out, int* __restrict__ info,
-                                                                    unsigned long long* __restrict__ prof) {
+                                                                    unsigned long long* __restrict__ prof,
+                                                                    int64_t strideC, int rel_only) {
     extern __shared__ __align__(16) double sm[];
     const int np = n + (n & 1);
     const int k = np / 2;
+    // Batched launches (blockIdx.y = problem): per-problem operands and logs.
+    Cin += blockIdx.y * strideC;
+    rot += static_cast<int64_t>(blockIdx.y) * kMaxSweeps * (np - 1) * k;
+    diag_out += static_cast<int64_t>(blockIdx.y) * np;
+    info += 2 * blockIdx.y;
+    if (blockIdx.y > 0) prof = nullptr;
     const int mat = np * np;
     // Layout: matrix buffers 0/1 (mat doubles each), rotations cs[2][kMaxNp/2],
     // then the rotation log ring (2·(np-1) rounds), flushed to global once per
@@ -168,7 +175,9 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
     __syncthreads();
     // Entries below 1e-15·max|a_ii| sit under the Gram's rounding noise (the fast
     // path needs absolute accuracy only); rotating them only burns sweeps.
-    const double abs_floor = 1e-15 * amax_s;
+    // rel_only (block one-sided Jacobi, wide.cu): only the relative criterion
+    // g² > 1e-30·|a·b| — tiny columns are orthogonalised too.
+    const double abs_floor = rel_only ? 0.0 : 1e-15 * amax_s;
 
     const unsigned sbase = smem_u32(sm);
     const unsigned matb = static_cast<unsigned>(mat) * 8u;
@@ -415,9 +424,14 @@ __global__ void __launch_bounds__(kValThreads, 1) jacobi_values_kernel(const dou
 __global__ void __launch_bounds__(128) jacobi_vectors_kernel(int n, const double2* __restrict__ rot,
                                                              const double* __restrict__ diag_pos,
                                                              const int* __restrict__ info, double* __restrict__ lambda,
-                                                             double* __restrict__ V) {
+                                                             double* __restrict__ V, int64_t strideL, int64_t strideV) {
     const int np = n + (n & 1);
     const int k = np / 2;
+    rot += static_cast<int64_t>(blockIdx.y) * kMaxSweeps * (np - 1) * k;
+    diag_pos += static_cast<int64_t>(blockIdx.y) * np;
+    info += 2 * blockIdx.y;
+    lambda += blockIdx.y * strideL;
+    V += blockIdx.y * strideV;
     const int lane = threadIdx.x & 31;
     const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int rounds = info[0];
@@ -504,15 +518,22 @@ unsigned long long* eig_probe_buffer() {
 
 bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
                           int* sweeps) {
+    return launch_sym_jacobi_batched(C, ldc, n, lambda, V, sc, 1, 0, 0, 0, false, sweeps);
+}
+
+bool launch_sym_jacobi_batched(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
+                               int count, int64_t strideC, int64_t strideL, int64_t strideV, bool rel_only,
+                               int* sweeps) {
     const int np = n + (n & 1);
     if (np > kMaxNp || np < 4) return false;
+    if (count < 1) return true;
     const int k = np / 2;
     const size_t smem = sizeof(double) * (2 * static_cast<size_t>(np) * np + 2 * kMaxNp + 4 * static_cast<size_t>(np - 1) * k + np);
     // Per-device, thread-safe smem attribute (runtime.hpp set_max_smem).
     set_max_smem(jacobi_values_kernel, 200 * 1024);
-    auto* rot = sc.alloc_n<double2>(static_cast<size_t>(kMaxSweeps) * (np - 1) * k);
-    double* dpos = sc.alloc_n<double>(static_cast<size_t>(np));
-    int* info = sc.alloc_n<int>(2);
+    auto* rot = sc.alloc_n<double2>(static_cast<size_t>(count) * kMaxSweeps * (np - 1) * k);
+    double* dpos = sc.alloc_n<double>(static_cast<size_t>(count) * np);
+    int* info = sc.alloc_n<int>(2 * static_cast<size_t>(count));
     // Upper bound on the off-diagonal blocks the workers own (all k(k-1)/2; the
     // pivot warp takes a few of them).  At n = 64 the 15-warp cap is exact.
     const int blocks = k * (k - 1) / 2;
@@ -522,9 +543,11 @@ bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, d
     }();
     int work = std::min(kWorkWarps, std::max(1, (blocks + 31) / 32));
     if (force_warps > 0) work = std::max(work, std::min(force_warps, kWorkWarps));
-    jacobi_values_kernel<<<1, 32 * (work + 1), smem, sc.stream()>>>(C, ldc, n, rot, dpos, info, eig_probe_buffer());
+    jacobi_values_kernel<<<dim3(1, static_cast<unsigned>(count)), 32 * (work + 1), smem, sc.stream()>>>(
+        C, ldc, n, rot, dpos, info, eig_probe_buffer(), strideC, rel_only ? 1 : 0);
     TS_LAUNCH_CHECK();
-    jacobi_vectors_kernel<<<(np + 3) / 4, 128, 0, sc.stream()>>>(n, rot, dpos, info, lambda, V);
+    jacobi_vectors_kernel<<<dim3((np + 3) / 4, static_cast<unsigned>(count)), 128, 0, sc.stream()>>>(
+        n, rot, dpos, info, lambda, V, strideL, strideV);
     TS_LAUNCH_CHECK();
     if (sweeps) TS_CUDA_CHECK(cudaMemcpyAsync(sweeps, info + 1, sizeof(int), cudaMemcpyDeviceToDevice, sc.stream()));
     sc.launches += 2;

@@ -105,6 +105,13 @@ void launch_sym_jacobi(const double* C, int64_t ldc, int n, double* lambda, doub
 // Fixed-address (permuted-layout) variant for n ≤ 64 (eig.cu); false if n > 64.
 bool launch_sym_jacobi_pp(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
                           int* sweeps);
+// `count` independent problems of the same n ≤ 64 (problem b at C + b·strideC,
+// lambda + b·strideL, V + b·strideV), one CTA each.  rel_only: rotate on the
+// relative criterion only (no absolute floor) — the block one-sided Jacobi of
+// wide.cu needs tiny columns orthogonalised too.
+bool launch_sym_jacobi_batched(const double* C, int64_t ldc, int n, double* lambda, double* V, CallScratch& sc,
+                               int count, int64_t strideC, int64_t strideL, int64_t strideV, bool rel_only,
+                               int* sweeps = nullptr);
 // TS_EIG=jacobi: stage G uses the Jacobi solver even for n ≤ 64 (A/B timing).
 bool jacobi_eig_forced();
 // R⁻¹ of the Cholesky factor of small SPD matrices G[b] (n ≤ 96, one CTA each);
@@ -189,6 +196,18 @@ struct Kron3Args {
 bool launch_kron3(const Kron3Args& args, int max_shape, CallScratch& sc);
 
 int max_tsqr_cols();
+
+// ---- wide.cu: generic widths (any column count)
+// Thin Q (rows × min(rows, cols), ld ldq) of Y (rows × cols, ld ldy; not
+// modified): BCGS2 over 64-column TSQR panels for tall Y, the identity for wide Y.
+void wide_qr(const double* Y, int64_t ldy, int64_t rows, int64_t cols, double* Q, int64_t ldq, CallScratch& sc,
+             int num_sms);
+// Block one-sided Jacobi SVD of A (rows × cols, rows ≥ cols, ld lda; not
+// modified), cols ≥ 4: sigma[cols] descending and (if V) the right singular
+// vectors V (cols × cols, ld ldv).  Host-synchronising (one read per sweep).
+// Returns the number of sweeps.
+int bosj_svd(const double* A, int64_t lda, int64_t rows, int64_t cols, double* sigma, double* V, int64_t ldv,
+             CallScratch& sc, int num_sms);
 // Device buffer of the values-kernel phase probe (non-null iff TS_EIG_PROFILE is set).
 unsigned long long* eig_probe_buffer();
 

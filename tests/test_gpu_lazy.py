@@ -121,11 +121,13 @@ def test_eager_cancellation_loses_quiet_components(engine):
     assert max(max(r) for r in stats.eager_rank_trace) > 2 * max(krp.ranks)
 
 
-def test_lazy_rejects_oversized_stack(engine):
-    xs = [random_tucker([200, 200, 200], [10, 10, 10], (90, i)) for i in range(10)]  # stacked rank 100 > 96
+def test_lazy_rejects_bad_tolerance(engine):
+    """Stacked ranks beyond 96 are supported (tests/test_gpu_wide.py); a negative
+    tolerance is still the reference's invalid_argument."""
+    xs = [random_tucker([20, 20, 20], [3, 3, 3], (90, i)) for i in range(3)]
     batch = engine.upload(xs)
     try:
-        with pytest.raises(T.TucksumCudaError):
-            engine.lazy_sum(batch, [1.0] * 10, 1e-8)
+        with pytest.raises(ValueError):
+            engine.lazy_sum(batch, [1.0] * 3, -1.0)
     finally:
         batch.free()
