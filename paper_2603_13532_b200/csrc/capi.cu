@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <atomic>
 #include <set>
@@ -254,7 +255,11 @@ struct ts_result {
     std::vector<double> inter[3][TS_MAX_ORDER];
     std::int64_t inter_rows[3][TS_MAX_ORDER] = {}, inter_cols[3][TS_MAX_ORDER] = {};
     std::vector<double> h;
+    // Results of one segmented call live in one shared device block (one
+    // allocation instead of (order + 1) per sum); freed with the last of them.
+    std::shared_ptr<void> arena;
     ~ts_result() {
+        if (arena) return;
         cudaSetDevice(device);
         for (auto* f : factors)
             if (f) cudaFreeAsync(f, stream);
@@ -1527,6 +1532,15 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
     ctx->stage.reset();
     cudaStream_t st = ctx->stream;
     CallScratch sc(st, ctx->stage);
+    static const bool dbg_seg = std::getenv("TS_DEBUG_SEG") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto tick = [&](const char* what) {
+        if (!dbg_seg) return;
+        TS_CUDA_CHECK(cudaStreamSynchronize(st));
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[seg] %-8s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const std::int64_t* dims = b->dims;
     auto col = [&](std::int64_t s, int n) { return b->scol[static_cast<size_t>(seg[s] * d + n)]; };
     auto rsn = [&](std::int64_t s, int n) { return col(s + 1, n) - col(s, n); };
@@ -1546,6 +1560,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
     for (std::int64_t s = 0; s < S; ++s) om[static_cast<size_t>(s)] = omega_get(ctx, d, dims, ow, seeds[s], streams[s]);
     auto* d_w = static_cast<double*>(sc.upload(weights, sizeof(double) * static_cast<size_t>(b->count)));
 
+    tick("setup");
     // ---- A: Z_n[:, cols_s] = Ω_{s,n}ᵀ F_n[:, cols_s]
     double* Z[TS_MAX_ORDER];
     {
@@ -1567,6 +1582,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
             }
         ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
     }
+    tick("A");
     // ---- B: one launch over all atoms (each atom reads its own sum's Z columns)
     double* W[TS_MAX_ORDER];
     {
@@ -1585,6 +1601,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         ka.weights = d_w;
         ts::launch_krp_contract(ka, b->max_shape, sc);
     }
+    tick("B");
     // ---- C: Y_{s,n} = F_n[:, cols_s] · W_n[cols_s, :]
     double* Y = sc.alloc_n<double>(static_cast<size_t>(S * ysum));
     auto ypos = [&](std::int64_t s, int n) { return Y + s * ysum + yoff[n]; };
@@ -1609,6 +1626,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
     const bool spec = allow_spec && ctx->spec_ok;
     int* dflags = nullptr;
     int* gflags = nullptr;
+    tick("C");
     // ---- D: CholeskyQR2 R form per (sum, mode) where dims ≥ 2s, Householder TSQR otherwise / on rejection
     std::vector<int> rform(SD, 0);
     std::vector<double*> Rinv(SD, nullptr), Uh(SD, nullptr);
@@ -1719,6 +1737,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         if (!pp.empty()) ts::run_tsqr(pp, sc, true);
         ctx->last_qr_fallbacks = static_cast<int>(pp.size());
     }
+    tick("D");
     // ---- E: P_n[:, cols_s] = Û_{s,n}ᵀ F_n[:, cols_s]  (R form: R⁻ᵀ (Y_{s,n}ᵀ F_n[:, cols_s]))
     double* P[TS_MAX_ORDER];
     {
@@ -1757,6 +1776,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
         if (!pr.empty()) ts::launch_grouped_gemm(Layout::TN, pr, sc, ctx->num_sms);
     }
+    tick("E");
     // ---- F: T_stack over all atoms, then h_s = T_stack[:, cols_s] · P_{d-1}[:, cols_s]ᵀ
     std::int64_t Qp = 1;
     for (int j = 0; j < d - 1; ++j) Qp *= q[j];
@@ -1780,6 +1800,7 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         }
         ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
     }
+    tick("F");
     // ---- G: ST-HOSVD of every h_s, one mode step at a time for all sums
     std::vector<std::array<std::int64_t, TS_MAX_ORDER>> shp(static_cast<size_t>(S));
     std::vector<std::array<std::int64_t, TS_MAX_ORDER>> rank(static_cast<size_t>(S));
@@ -1832,13 +1853,29 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                 p.lda = p.ldb = qk;
                 gnt.push_back(p);
             } else {
-                if (k != d - 1) {
+                if (k != d - 1)
                     X[static_cast<size_t>(s)] = sc.alloc_n<double>(static_cast<size_t>(rest[static_cast<size_t>(s)] * qk));
-                    ts::launch_unfold_t(g[static_cast<size_t>(s)], d, cs.data(), k, X[static_cast<size_t>(s)], sc);
-                }
                 p.A = p.B = k == d - 1 ? g[static_cast<size_t>(s)] : X[static_cast<size_t>(s)];
                 p.lda = p.ldb = rest[static_cast<size_t>(s)];
                 gtn.push_back(p);
+            }
+        }
+        if (k != 0 && k != d - 1) {  // X_s = g_s,(k)ᵀ: one launch per group of sums with the same current shape
+            std::vector<bool> done(static_cast<size_t>(S), false);
+            for (std::int64_t s0 = 0; s0 < S; ++s0) {
+                if (done[static_cast<size_t>(s0)]) continue;
+                std::vector<const double*> gsrc;
+                std::vector<double*> xdst;
+                for (std::int64_t s = s0; s < S; ++s)
+                    if (!done[static_cast<size_t>(s)] && shp[static_cast<size_t>(s)] == shp[static_cast<size_t>(s0)]) {
+                        done[static_cast<size_t>(s)] = true;
+                        gsrc.push_back(g[static_cast<size_t>(s)]);
+                        xdst.push_back(X[static_cast<size_t>(s)]);
+                    }
+                auto* dg = static_cast<const double* const*>(sc.upload(gsrc.data(), sizeof(double*) * gsrc.size()));
+                auto* dx = static_cast<double* const*>(sc.upload(xdst.data(), sizeof(double*) * xdst.size()));
+                ts::launch_unfold_t_batched(dg, dx, static_cast<int>(gsrc.size()), d, shp[static_cast<size_t>(s0)].data(), k,
+                                            sc);
             }
         }
         if (!gnt.empty()) ts::launch_grouped_gemm(Layout::NT, gnt, sc, ctx->num_sms);
@@ -1947,9 +1984,28 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
         if (!t0.empty()) ts::launch_grouped_gemm(Layout::TN, t0, sc, ctx->num_sms);
         if (!t1.empty()) ts::launch_grouped_gemm(Layout::NN, t1, sc, ctx->num_sms);
     }
+    tick("G");
     // ---- H: Ũ_{s,n} = Y_{s,n}(R⁻¹P_k) or Û_{s,n}P_k; results
     std::vector<std::unique_ptr<ts_result>> out(static_cast<size_t>(S));
     {
+        std::int64_t total = 0;
+        for (std::int64_t s = 0; s < S; ++s) {
+            std::int64_t csize = 1;
+            for (int n = 0; n < d; ++n) {
+                const std::int64_t rkn = rank[static_cast<size_t>(s)][static_cast<size_t>(n)];
+                total += (dims[n] * rkn + 31) / 32 * 32;
+                csize *= rkn;
+            }
+            total += (csize + 31) / 32 * 32;
+        }
+        double* block = nullptr;
+        TS_CUDA_CHECK(cudaMallocAsync(&block, sizeof(double) * static_cast<size_t>(std::max<std::int64_t>(total, 1)), st));
+        const int dev = ctx->device;
+        std::shared_ptr<void> arena(block, [dev, st](void* p) {
+            cudaSetDevice(dev);
+            cudaFreeAsync(p, st);
+        });
+        double* bump = block;
         std::vector<GemmProblem> tp, up;
         for (std::int64_t s = 0; s < S; ++s) {
             const size_t si = static_cast<size_t>(s);
@@ -1965,7 +2021,8 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                 r->dims[n] = dims[n];
                 r->ranks[n] = rkn;
                 csize *= rkn;
-                TS_CUDA_CHECK(cudaMallocAsync(&r->factors[n], sizeof(double) * static_cast<size_t>(dims[n] * rkn), st));
+                r->factors[n] = bump;
+                bump += (dims[n] * rkn + 31) / 32 * 32;
                 const double* Bm = Pk[si][static_cast<size_t>(n)];
                 if (rform[i]) {
                     double* T = sc.alloc_n<double>(static_cast<size_t>(q[n] * rkn));
@@ -1994,13 +2051,16 @@ std::vector<ts_result*> segmented_impl(ts_ctx* ctx, const ts_batch* b, std::int6
                 p.K = static_cast<int>(q[n]);
                 up.push_back(p);
             }
-            TS_CUDA_CHECK(cudaMallocAsync(&r->core, sizeof(double) * static_cast<size_t>(csize), st));
+            r->core = bump;
+            bump += (csize + 31) / 32 * 32;
+            r->arena = arena;
             TS_CUDA_CHECK(cudaMemcpyAsync(r->core, g[si], sizeof(double) * static_cast<size_t>(csize),
                                           cudaMemcpyDeviceToDevice, st));
         }
         if (!tp.empty()) ts::launch_grouped_gemm(Layout::NN, tp, sc, ctx->num_sms);
         ts::launch_grouped_gemm(Layout::NN, up, sc, ctx->num_sms);
     }
+    tick("H");
     ctx->launches += sc.launches;
     if (spec) {
         std::vector<int> hf(2 * SD, 0);

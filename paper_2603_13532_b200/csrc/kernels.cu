@@ -882,6 +882,26 @@ __global__ void unfold_t_kernel(const double* __restrict__ g, UnfoldArgs a, doub
     }
 }
 
+// Batched: problem blockIdx.y reads gs[y] and writes Xs[y] (same shape).
+__global__ void unfold_t_batched_kernel(const double* const* __restrict__ gs, UnfoldArgs a, double* const* __restrict__ Xs,
+                                        int64_t total) {
+    int64_t left = 1, right = 1;
+    for (int j = 0; j < a.order; ++j) {
+        if (j < a.mode) left *= a.shape[j];
+        else if (j > a.mode) right *= a.shape[j];
+    }
+    const int64_t qk = a.shape[a.mode], rest = left * right;
+    const double* __restrict__ g = gs[blockIdx.y];
+    double* __restrict__ X = Xs[blockIdx.y];
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t l = e % left;
+        const int64_t i = (e / left) % qk;
+        const int64_t r = e / (left * qk);
+        X[(l + left * r) + i * rest] = g[e];
+    }
+}
+
 // Σ x_i² in two deterministic passes: fixed contiguous chunks per CTA, then the
 // per-CTA partials summed in order by one CTA.
 constexpr int kSumsqBlocks = 128;
@@ -1216,6 +1236,25 @@ void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode,
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 2048);
     unfold_t_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), threads, 0, sc.stream()>>>(g, a, X, total);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
+void launch_unfold_t_batched(const double* const* gs, double* const* Xs, int count, int order, const int64_t* shape,
+                             int mode, CallScratch& sc) {
+    if (count < 1) return;
+    UnfoldArgs a{};
+    int64_t total = 1;
+    for (int j = 0; j < order; ++j) {
+        a.shape[j] = shape[j];
+        total *= shape[j];
+    }
+    a.order = order;
+    a.mode = mode;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 1024);
+    unfold_t_batched_kernel<<<dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(count)), threads,
+                              0, sc.stream()>>>(gs, a, Xs, total);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }

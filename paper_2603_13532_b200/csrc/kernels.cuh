@@ -153,6 +153,9 @@ bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double*
 
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);
+// Same for `count` tensors of one shape: device pointer arrays gs[count] → Xs[count].
+void launch_unfold_t_batched(const double* const* gs, double* const* Xs, int count, int order, const int64_t* shape,
+                             int mode, CallScratch& sc);
 // out[0] = Σ x_i² (single-CTA, deterministic).
 void launch_sumsq(const double* x, int64_t n, double* out, CallScratch& sc);
 

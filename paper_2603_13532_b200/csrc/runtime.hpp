@@ -86,6 +86,8 @@ private:
     cudaStream_t stream_;
     HostStage& stage_;
     std::vector<void*> ptrs_;
+    char* cur_ = nullptr;  // bump pointer into the current chunk
+    char* end_ = nullptr;
 };
 
 }  // namespace ts

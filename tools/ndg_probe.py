@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--sums", type=int, default=64)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--once", action="store_true")
 a = ap.parse_args()
 wls = [make_workload(a.config, node=i + 1) for i in range(a.sums)]
 widths, cap = wls[0].widths, wls[0].cap
@@ -59,12 +60,16 @@ def timed(fn):
 seq = timed(lambda: [eng.krp_sum(b, w.weights, widths, w.seed, 0.0, cap) for b, w in zip(singles, wls)])
 many = timed(lambda: eng.krp_sum_many(singles, [w.weights for w in wls], widths, seeds, 0.0, cap, lanes=8))
 segd = timed(lambda: eng.krp_sum_segmented(big, seg, ws, widths, seeds, 0.0, cap))
+seg_paths = eng.last_paths()
+if a.once:  # one extra segmented call (ncu target)
+    for r in eng.krp_sum_segmented(big, seg, ws, widths, seeds, 0.0, cap):
+        r.free()
 line = {"pattern": "NDG: independent sums with a shared plan (src/ndg.cpp:401-462)", "config": a.config,
         "sums": a.sums, "summands_per_sum": wls[0].K, "eps": 0.0, "cap": cap, "widths": widths,
         "sequential_ms": seq[0], "sequential_wall_ms": seq[1], "many_lanes_ms": many[0], "many_lanes_wall_ms": many[1],
         "segmented_ms": segd[0], "segmented_wall_ms": segd[1],
         "sums_per_s": {"sequential": a.sums / (seq[1] / 1000), "many_lanes": a.sums / (many[1] / 1000),
                        "segmented": a.sums / (segd[1] / 1000)},
-        "speedup_segmented_vs_sequential": seq[1] / segd[1]}
+        "speedup_segmented_vs_sequential": seq[1] / segd[1], "segmented_last_paths": list(seg_paths)}
 print(json.dumps(line), flush=True)
 eng.close()
