@@ -2868,7 +2868,7 @@ int ts_kron_sketch_dims(int64_t order, const int64_t* targets, const int64_t* di
 
 void tsi_read_eig_profile(long long* out);
 // Debug: phase clock totals of the last n ≤ 64 values-kernel run (TS_EIG_PROFILE=1).
-int ts_debug_eig_profile(long long* out17) {
+int ts_debug_eig_profile(long long* out17) {  // 18 entries
     return guarded([&] { tsi_read_eig_profile(out17); });
 }
 

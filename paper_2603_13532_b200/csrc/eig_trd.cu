@@ -1,37 +1,38 @@
 // eig_trd.cu — the symmetric eigensolver of ST-HOSVD's Gram fast path (stage G)
-// for n ≤ 64, in ONE kernel on one CTA of 1024 threads.
+// for n ≤ 64: ONE kernel, one CTA of 512 threads per problem (batched over
+// blockIdx.x for segmented sums).
 //
 // Reference semantics: sym_eig (src/kernels.cpp:70-86) — symmetrise,
-// eigendecompose, eigenpairs in descending order.  A Jacobi eigensolver needs
-// ~8 sweeps × 63 rounds, each round streaming the matrix through shared memory
-// (eig.cu: ~780 cycles a round, ~210 µs at n = 64).  This kernel replaces the
-// rounds by a fixed number of short steps:
+// eigendecompose, eigenpairs in descending order.  Stage G runs one of these
+// per mode on the serial tail of every call, so the kernel is built for
+// latency: every phase is either a short chain per step with all 16 warps busy,
+// or independent per-eigenvector chains with no CTA barrier.
 //
-//  1. Householder tridiagonalisation QᵀCQ = T (dsytd2 order).  The matrix stays
-//     in REGISTERS (warp w owns rows 2w, 2w+1, lane l columns l, l+32); a step
-//     is one warp forming the reflector from the row it owns, a CTA barrier, the
-//     matrix-vector product as two warp reductions per warp, a barrier, and the
-//     rank-2 update in registers — two barriers per reflector.
-//  2. All eigenvalues of T by multisection: a half-warp per eigenvalue, 16
-//     shifts per round (17× narrowing), 13 rounds.  The Sturm count uses the
-//     product form of the characteristic-polynomial recurrence
+//  1. Householder tridiagonalisation QᵀCQ = T (dsytd2 order, lower).  The
+//     matrix lives in REGISTERS: thread (i = tid/8, t = tid%8) owns row i,
+//     columns t + 8u (shared memory only carries v, p and one partial per
+//     warp, so a step is not bound by the shared-memory pipe).  Per reflector:
+//     p = τ·A v (8-lane row sums), the rank-2 update A −= v wᵀ + w vᵀ, and the
+//     8 lanes of the next row form the next reflector from their registers
+//     (one 8-lane reduction, MUFU rsqrt/rcp + Newton) — two CTA barriers per
+//     step; warps whose rows are finished skip the step.
+//  2. Eigenvalues of T to ~2^-44 of its Gershgorin width by multisection: 8
+//     lanes per eigenvalue, 8 shifts per round (9× narrowing), 14 rounds, Sturm
+//     counts from the sign bits of the product-form recurrence
 //     p_i = (d_i − x)p_{i−1} − e²_{i−1}p_{i−2} (one dependent FMA per step,
-//     exact power-of-two rescaling every 8 steps) instead of the ratio form's
-//     division per step.
+//     power-of-two rescaling every 8 steps).  Full accuracy comes from step 5.
 //  3. Eigenvectors of T by inverse iteration on the LDLᵀ factorisation of
 //     T − λI (thread per eigenvalue, two iterations).
-//  4. Back-transformation Z ← H_0 ⋯ H_{n−3} Z, 16 lanes per eigenvector, no
-//     CTA barrier.
-//  5. Löwdin re-orthonormalisation Z ← Z(I − E/2), E = ZᵀZ − I (DMMA): inverse
-//     iteration leaves vectors of close eigenvalues slightly non-orthogonal;
-//     the first-order correction mixes z_i and z_j in proportion to their
-//     overlap, which is of the order of the subspace error ε‖C‖/|λ_i − λ_j| the
-//     problem itself has, and leaves an O(‖E‖²) orthogonality defect.
-//  6. Acceptance on the ORIGINAL matrix (DMMA): the Frobenius norm of the
-//     residual C Z − ZΛ is written to *resid (the rank checks use the measured
-//     value, not an assumed one); a non-finite or too large residual, or an
-//     orthogonality defect E beyond 1e-4, sets *flag and the caller recomputes
-//     with the Jacobi solver (eig.cu).
+//  4. Back-transformation Z ← H_0 ⋯ H_{n−3} Z: 8 lanes per eigenvector, its
+//     rows in registers, no CTA barrier.
+//  5. Orthonormality: E = ZᵀZ − I (DMMA); Löwdin steps Z ← Z − ½ZE for small
+//     defects (close eigenvalues), modified Gram-Schmidt with completion for
+//     collapsed clusters (e.g. the zero eigenvalues of a rank-deficient Gram).
+//     Then R = C Z (DMMA, C re-read from global), λ_j = z_jᵀ(Cz_j) (Rayleigh
+//     quotients: accurate to O(ε‖C‖ + ‖r_j‖²/gap)), the measured residual
+//     ‖C Z − ZΛ‖_F (written to *resid; the rank checks use it), and the
+//     descending sort.  A non-finite or too large residual sets *flag and the
+//     caller recomputes with the Jacobi solver (eig.cu).
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -42,20 +43,23 @@ namespace ts {
 namespace {
 
 constexpr int kEN = 64;               // largest n
-constexpr int kEThreads = 256;        // 8 warps: row r = tid/4 owns 16 columns per thread
+constexpr int kEThreads = 512;        // 16 warps
 constexpr int kEWarps = kEThreads / 32;
-constexpr int kLZ = kEN + 1;          // row stride of the [row][col] smem matrices
+constexpr int kLA = 72;               // row stride of the [row][col] smem matrices
 constexpr double kEps = 1.1102230246251565e-16;
 
 struct TrdSmem {
-    double V[kEN * kEN];      // reflector k at V[k*kEN + i]; v_i = 0 for i ≤ k, v_{k+1} = 1
-    double Z[kEN * kLZ];      // eigenvectors [row][col]
-    double W[kEN * kLZ];      // scratch: C (original), DMMA outputs
-    double Lm[kEN * kLZ];     // inverse iteration: L_i of eigenvalue j at [i*kEN + j]; later E = ZᵀZ − I
-    double Dinv[kEN * kLZ];   //                    1/D_i at [i*kEN + j]; later Z·E
-    double tau[kEN], d[kEN], e[kEN], ds[kEN], e2s[kEN], es[kEN], lam[kEN], p[kEN], pw[kEWarps];
-    double red[32];
+    double A[kEN * kLA];      // matrix during (1); later C for the residual; later R = C Z
+    double Z[kEN * kLA];      // eigenvectors [row][col]
+    double Lm[kEN * kEN];     // inverse iteration: L_i of eigenvalue j at [i*kEN + j]; later E, Z·E
+    double Dinv[kEN * kEN];   //                    1/D_i at [i*kEN + j]
+    double V[kEN * kEN];      // reflector k at V[k*kEN + i]: v_i = 0 for i ≤ k, v_{k+1} = 1
+    double2 de2[kEN];         // multisection operands (d_i, e²_{i−1}), scaled
+    double lamb[kEN];         // multisection eigenvalues (scaled, ascending)
+    double tau[kEN], d[kEN], e[kEN], ds[kEN], e2s[kEN], es[kEN], lam[kEN], p[kEN], rowfill[kEN];
+    double red[kEWarps];
     double misc[8];
+    int rank[kEN];
     int flag;
 };
 
@@ -67,10 +71,13 @@ __device__ __forceinline__ double rcp_refined(double x) {  // ≈ correctly roun
     return fma(y, fma(-x, y, 1.0), y);
 }
 
-__device__ __forceinline__ double hsum16(double v) {  // sum over the 16 lanes of a half-warp
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+__device__ __forceinline__ double sqrt_refined(double x) {  // x > 0
+    double rs;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(x));
+    rs = rs * fma(-0.5 * x, rs * rs, 1.5);
+    rs = rs * fma(-0.5 * x, rs * rs, 1.5);
+    const double sq = x * rs;
+    return fma(0.5 * rs, fma(-sq, sq, x), sq);
 }
 
 // 2^-(exponent of m) for m > 0, exactly representable (rescales a pair of
@@ -81,11 +88,11 @@ __device__ __forceinline__ double inv_pow2_of(double m) {
     return __hiloint2double((2046 - ex) << 20, 0);
 }
 
-// C(64×64) = op(A)·B over kLZ-strided smem operands with DMMA.8x8x4 (inner
-// dimension n, zero beyond); warp w computes output tiles 2w, 2w+1 (8×8 each,
-// tile t → rows 8(t&7), cols 8(t>>3)).  TransA: op(A)(i,k) = A[k][i].
-template <bool TransA>
-__device__ __forceinline__ void dmma_64(const double* A, const double* B, double* Cout, int n) {
+// Out(64×64) = op(X)·Y over kLA-strided smem operands with DMMA.8x8x4 (inner
+// dimension n, zero beyond); warp w computes the 8×8 output tiles w, w+16, ….
+// TransX: op(X)(i,k) = X[k][i].  Out may be given a different stride.
+template <bool TransX>
+__device__ __forceinline__ void dmma_64(const double* X, const double* Y, double* Out, int ldo, int n) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     for (int tile = warp; tile < 64; tile += kEWarps) {
@@ -93,21 +100,31 @@ __device__ __forceinline__ void dmma_64(const double* A, const double* B, double
         double c_0 = 0.0, c_1 = 0.0;
         for (int k0 = 0; k0 < n; k0 += 4) {
             const int kk = k0 + t;
-            const double a = kk < n ? (TransA ? A[kk * kLZ + r0 + g] : A[(r0 + g) * kLZ + kk]) : 0.0;
-            const double b = kk < n ? B[kk * kLZ + c0 + g] : 0.0;
+            const double a = kk < n ? (TransX ? X[kk * kLA + r0 + g] : X[(r0 + g) * kLA + kk]) : 0.0;
+            const double b = kk < n ? Y[kk * kLA + c0 + g] : 0.0;
             dmma884(c_0, c_1, a, b);
         }
-        Cout[(r0 + g) * kLZ + c0 + 2 * t] = c_0;
-        Cout[(r0 + g) * kLZ + c0 + 2 * t + 1] = c_1;
+        Out[(r0 + g) * ldo + c0 + 2 * t] = c_0;
+        Out[(r0 + g) * ldo + c0 + 2 * t + 1] = c_1;
     }
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = 0.0;
+#pragma unroll
+    for (int w = 0; w < kEWarps; ++w) v = fmax(v, red[w]);
+    __syncthreads();
+    return v;
 }
 
 __global__ void __launch_bounds__(kEThreads, 1)
     trd_eig_kernel(const double* __restrict__ Cin, int64_t ldc, int n, double* __restrict__ lambda_out,
                    double* __restrict__ V_out, int* __restrict__ flag_out, double* __restrict__ resid_out,
                    unsigned long long* __restrict__ prof, int64_t strideC, int64_t strideL, int64_t strideV) {
-    // Batched launches (segmented sums): CTA b solves problem b.
-    {
+    {  // batched launches (segmented sums): CTA b solves problem b
         const int64_t b = blockIdx.x;
         Cin += b * strideC;
         lambda_out += b * strideL;
@@ -119,136 +136,170 @@ __global__ void __launch_bounds__(kEThreads, 1)
     extern __shared__ __align__(16) unsigned char smraw[];
     TrdSmem& S = *reinterpret_cast<TrdSmem*>(smraw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // Tridiagonalisation layout: thread t owns row r = t/4, columns c0..c0+15
-    // (c0 = 16·(t%4)) — a row is one 4-lane group, a warp 8 rows.
-    const int r = tid >> 2, c0 = 16 * (tid & 3);
-    const unsigned gmask4 = 0xfu << (lane & 28);
-
-    // ---- load + symmetrise into registers
-    double a[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-        const int j = c0 + u;
-        a[u] = (r < n && j < n) ? 0.5 * (Cin[r + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(r) * ldc])
-                                : 0.0;
-    }
-    if (tid == 0) S.flag = 0;
-    // Optional phase clocks (TS_EIG_PROFILE): prof[10 + phase] = cycles.
+    const int ri = tid >> 3, rt = tid & 7;  // row ri, columns rt + 8u
     long long tmark = clock64();
-    auto phase = [&](int ph) {
+    auto phase = [&](int ph) {  // optional phase clocks (TS_EIG_PROFILE): prof[10 + phase]
         if (prof != nullptr && tid == 0) {
             const long long now = clock64();
             prof[10 + ph] = static_cast<unsigned long long>(now - tmark);
             tmark = now;
         }
     };
-    // Element (r, col) of the owning group, summed over the group (one nonzero).
-    auto group_pick = [&](int col, unsigned mask) {
-        double v = 0.0;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v = (c0 + u == col) ? a[u] : v;
-        v += __shfl_xor_sync(mask, v, 1);
-        v += __shfl_xor_sync(mask, v, 2);
-        return v;
-    };
 
-    // ---- 1. tridiagonalisation (two CTA barriers per reflector)
+    // ---- load + symmetrise; zero the padding and the reflector store
+    for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
+        const int i = idx & 63, j = idx >> 6;
+        S.A[i * kLA + j] = (i < n && j < n) ? 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc])
+                                            : 0.0;
+        S.V[idx] = 0.0;
+    }
+    if (tid == 0) S.flag = 0;
+    if (tid < kEN) {
+        S.tau[tid] = 0.0;
+        S.e[tid] = 0.0;
+        S.d[tid] = 0.0;
+    }
+    __syncthreads();
+    if (n == 1) {
+        if (tid == 0) {
+            const double c = S.A[0];
+            lambda_out[0] = c;
+            V_out[0] = 1.0;
+            if (resid_out) *resid_out = 0.0;
+            if (!isfinite(c)) atomicOr(flag_out, 1);
+        }
+        return;
+    }
+
+    // ---- 1. tridiagonalisation.  A in registers: thread (ri, rt) holds
+    // a[u] = A[ri][rt + 8u]; the full symmetric matrix is updated, so row k is
+    // column k.  Step k: [row k's 8 lanes form reflector k] → barrier →
+    // p = τ·A v (rows > k) → barrier → A −= v wᵀ + w vᵀ, and row k+1's lanes
+    // form reflector k+1 straight from their updated registers.
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = S.A[ri * kLA + rt + 8 * u];
+    const int gbase = lane & 24;
+    const unsigned gm8 = 0xffu << gbase;
+    auto reflector = [&](int k) {  // the 8 lanes of row k (ri == k)
+        double ss = 0.0, xa = 0.0, xd = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = rt + 8 * u;
+            ss = (j > k + 1) ? fma(a[u], a[u], ss) : ss;
+            xa = (j == k + 1) ? a[u] : xa;
+            xd = (j == k) ? a[u] : xd;
+        }
+        ss += __shfl_xor_sync(gm8, ss, 1);
+        ss += __shfl_xor_sync(gm8, ss, 2);
+        ss += __shfl_xor_sync(gm8, ss, 4);
+        const double alpha = __shfl_sync(gm8, xa, gbase + ((k + 1) & 7));
+        const double dkk = __shfl_sync(gm8, xd, gbase + (k & 7));
+        double tau = 0.0, beta = alpha, scale = 0.0;
+        if (ss > 0.0) {
+            beta = -copysign(sqrt_refined(fma(alpha, alpha, ss)), alpha);
+            tau = fma(-alpha, rcp_refined(beta), 1.0);  // (β − α)/β
+            scale = rcp_refined(alpha - beta);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = rt + 8 * u;
+            S.V[k * kEN + j] = j == k + 1 ? 1.0 : (j > k + 1 ? a[u] * scale : 0.0);
+        }
+        if (rt == 0) {
+            S.tau[k] = tau;
+            S.d[k] = dkk;
+            S.e[k] = beta;
+        }
+    };
+    long long c_refl = 0, c_mv = 0, c_up = 0, c0_ = 0;
+    if (prof && tid == 0) prof[9] = static_cast<unsigned long long>(clock64() - tmark);
+    if (n > 2 && ri == 0) reflector(0);
+    __syncthreads();
+    if (prof && tid == 0) prof[17] = static_cast<unsigned long long>(clock64() - tmark);
     for (int k = 0; k + 2 < n; ++k) {
-        const int r0 = k + 1;
-        if (r == k) {  // the 4 threads owning row k form the reflector (dlarfg)
-            double ss = 0.0;
-#pragma unroll
-            for (int u = 0; u < 16; ++u) ss = (c0 + u > r0) ? fma(a[u], a[u], ss) : ss;  // entries ≥ n are 0
-            ss += __shfl_xor_sync(gmask4, ss, 1);
-            ss += __shfl_xor_sync(gmask4, ss, 2);
-            const double x0 = group_pick(r0, gmask4);
-            const double akk = group_pick(k, gmask4);
-            double tau = 0.0, beta = x0, scale = 0.0;
-            if (ss > 0.0) {  // refined MUFU sqrt / reciprocals (no IEEE slow paths)
-                const double nn = fma(x0, x0, ss);
-                double rs;
-                asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(nn));
-                rs = rs * fma(-0.5 * nn, rs * rs, 1.5);
-                rs = rs * fma(-0.5 * nn, rs * rs, 1.5);
-                double sq = nn * rs;
-                sq = fma(0.5 * rs, fma(-sq, sq, nn), sq);  // one more correction of √nn
-                beta = -copysign(sq, x0);
-                tau = fma(-x0, rcp_refined(beta), 1.0);
-                scale = rcp_refined(x0 - beta);
-            }
-#pragma unroll
-            for (int u = 0; u < 16; u += 2) {
-                const int j = c0 + u;
-                const double v0 = j == r0 ? 1.0 : (j > r0 ? a[u] * scale : 0.0);
-                const double v1 = j + 1 == r0 ? 1.0 : (j + 1 > r0 ? a[u + 1] * scale : 0.0);
-                *reinterpret_cast<double2*>(&S.V[k * kEN + j]) = make_double2(v0, v1);
-            }
-            if ((tid & 3) == 0) {
-                S.tau[k] = tau;
-                S.d[k] = akk;
-                S.e[k] = beta;
-            }
-        }
-        __syncthreads();
+        if (prof) c0_ = clock64();
         const double tk = S.tau[k];
-        double v[16];
+        const double* vk = S.V + k * kEN;
+        const bool wact = 4 * warp + 3 > k && 4 * warp < n;  // warp-uniform: any row in (k, n)
+        double pr = 0.0, vi = 0.0;
+        if (wact) {
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-            const double2 t2 = *reinterpret_cast<const double2*>(&S.V[k * kEN + c0 + u]);
-            v[u] = t2.x;
-            v[u + 1] = t2.y;
+            for (int u = 0; u < 8; u += 2) {
+                s0 = fma(a[u], vk[rt + 8 * u], s0);
+                s1 = fma(a[u + 1], vk[rt + 8 * u + 8], s1);
+            }
+            pr = s0 + s1;
+            pr += __shfl_xor_sync(0xffffffffu, pr, 1);
+            pr += __shfl_xor_sync(0xffffffffu, pr, 2);
+            pr += __shfl_xor_sync(0xffffffffu, pr, 4);
+            vi = vk[ri];
+            pr = ri > k ? tk * pr : 0.0;
+            double pv = pr * vi;  // Σ over the warp's 4 rows
+            pv += __shfl_xor_sync(0xffffffffu, pv, 8);
+            pv += __shfl_xor_sync(0xffffffffu, pv, 16);
+            if (lane == 0) S.red[warp] = pv;
+        } else if (lane == 0) {
+            S.red[warp] = 0.0;
         }
-        const double vr = S.V[k * kEN + r];
-        // p_r = τ (A v)_r over the group, then Σ_r p_r v_r over the warp's 8 rows
-        double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-            acc0 = fma(a[u], v[u], acc0);
-            acc1 = fma(a[u + 1], v[u + 1], acc1);
-        }
-        double pr = acc0 + acc1;
-        pr += __shfl_xor_sync(0xffffffffu, pr, 1);
-        pr += __shfl_xor_sync(0xffffffffu, pr, 2);
-        pr = r > k ? tk * pr : 0.0;  // rows ≤ k are finished (stale values there)
-        double pvw = pr * vr;
-        pvw += __shfl_xor_sync(0xffffffffu, pvw, 4);
-        pvw += __shfl_xor_sync(0xffffffffu, pvw, 8);
-        pvw += __shfl_xor_sync(0xffffffffu, pvw, 16);
-        if ((tid & 3) == 0) S.p[r] = pr;
-        if (lane == 0) S.pw[warp] = pvw;
+        if (rt == 0) S.p[ri] = pr;
         __syncthreads();
-        double pvs = 0.0;
-#pragma unroll
-        for (int w = 0; w < kEWarps; w += 2) {
-            const double2 t2 = *reinterpret_cast<const double2*>(&S.pw[w]);
-            pvs += t2.x + t2.y;
+        if (prof) {
+            const long long c1_ = clock64();
+            c_mv += c1_ - c0_;
+            c0_ = c1_;
         }
-        const double K = 0.5 * tk * pvs;
-        const double wr = fma(-K, vr, pr);
-        // A -= v wᵀ + w vᵀ (zero outside the trailing block: v, w vanish there)
+        if (wact) {
+            double pv2[kEWarps];
 #pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-            const double2 p2 = *reinterpret_cast<const double2*>(&S.p[c0 + u]);
-            const double w0 = fma(-K, v[u], p2.x), w1 = fma(-K, v[u + 1], p2.y);
-            a[u] -= fma(vr, w0, wr * v[u]);
-            a[u + 1] -= fma(vr, w1, wr * v[u + 1]);
+            for (int w = 0; w < kEWarps; w += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(&S.red[w]);
+                pv2[w] = t2.x;
+                pv2[w + 1] = t2.y;
+            }
+#pragma unroll
+            for (int h = kEWarps / 2; h > 0; h >>= 1)
+#pragma unroll
+                for (int w = 0; w < h; ++w) pv2[w] += pv2[w + h];
+            const double K = 0.5 * tk * pv2[0];
+            const double wi = fma(-K, vi, pr);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = rt + 8 * u;
+                const double vj = vk[j];
+                const double wj = fma(-K, vj, S.p[j]);
+                a[u] -= fma(vi, wj, wi * vj);
+            }
+        }
+        if (prof) {
+            const long long c1_ = clock64();
+            c_up += c1_ - c0_;
+            c0_ = c1_;
+        }
+        if (k + 3 < n && ri == k + 1) reflector(k + 1);
+        __syncthreads();
+        if (prof) c_refl += clock64() - c0_;
+    }
+    if (prof && tid == 0) prof[16] = static_cast<unsigned long long>(clock64() - tmark);
+    {  // trailing 2×2 from the registers of rows n-2, n-1
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = rt + 8 * u;
+            if (ri == n - 2 && j == n - 2) S.d[n - 2] = a[u];
+            if (ri == n - 1 && j == n - 1) S.d[n - 1] = a[u];
+            if (ri == n - 1 && j == n - 2) S.e[n - 2] = a[u];
         }
     }
-    // trailing 2×2 (or the whole matrix when n ≤ 2)
-    {
-        const int k0 = n >= 2 ? n - 2 : 0;
-        const bool mine = r >= k0 && r < n;
-        const double dii = group_pick(r, 0xffffffffu);
-        const double nxt = group_pick(r + 1, 0xffffffffu);
-        if (mine && (tid & 3) == 0) {
-            S.d[r] = dii;
-            if (r + 1 < n) S.e[r] = nxt;
-        }
+    if (prof && tid == 0) {
+        prof[5] = static_cast<unsigned long long>(c_refl);
+        prof[6] = static_cast<unsigned long long>(c_mv);
+        prof[8] = static_cast<unsigned long long>(c_up);
     }
     __syncthreads();
     phase(0);
 
-    // ---- 2. eigenvalues (multisection on the power-of-two-scaled T)
+    // ---- 2. eigenvalues of T (power-of-two scaled), multisection
     if (warp == 0) {
         double lo = 1e300, hi = -1e300;
         for (int i = lane; i < n; i += 32) {
@@ -263,22 +314,17 @@ __global__ void __launch_bounds__(kEThreads, 1)
         const double tn = fmax(fabs(lo), fabs(hi));
         const double sc = tn > 0.0 ? inv_pow2_of(tn) : 1.0;  // tn·sc in [1, 2)
         for (int i = lane; i < kEN; i += 32) {
-            if (i >= n) {
-                S.ds[i] = 0.0;
-                S.es[i] = 0.0;
-                S.e2s[i] = 0.0;
-                continue;
-            }
-            S.ds[i] = S.d[i] * sc;
-            const double es = i + 1 < n ? S.e[i] * sc : 0.0;
+            const double es = (i + 1 < n) ? S.e[i] * sc : 0.0;
+            S.ds[i] = i < n ? S.d[i] * sc : 0.0;
             S.es[i] = es;
             S.e2s[i] = es * es;
+            const double ep = (i >= 1 && i < n) ? S.e[i - 1] * sc : 0.0;
+            S.de2[i] = make_double2(i < n ? S.d[i] * sc : 0.0, ep * ep);  // (d_i, e²_{i−1})
         }
         if (lane == 0) {
             const double pad = 8.0 * kEps * n;
             S.misc[0] = lo * sc - pad;
             S.misc[1] = hi * sc + pad;
-            S.misc[2] = sc;
             S.misc[3] = tn;
             S.misc[4] = 1.0 / sc;  // exact: sc is a power of two
         }
@@ -286,46 +332,37 @@ __global__ void __launch_bounds__(kEThreads, 1)
     __syncthreads();
     const double tn = S.misc[3];
     const double isc = S.misc[4];
-    if (tn == 0.0) {  // zero matrix: λ = 0, V = I
+    if (!(tn > 0.0) || !isfinite(tn)) {  // zero matrix (λ = 0, V = I) or non-finite input (flagged)
         for (int idx = tid; idx < n * n; idx += kEThreads) {
             const int i = idx % n, r = idx / n;
             V_out[i + static_cast<int64_t>(r) * n] = i == r ? 1.0 : 0.0;
         }
         if (tid < n) lambda_out[tid] = 0.0;
-        if (tid == 0 && resid_out) *resid_out = 0.0;
+        if (tid == 0) {
+            if (resid_out) *resid_out = 0.0;
+            if (!(tn == 0.0)) atomicOr(flag_out, 1);
+        }
         return;
     }
-    if (tid < 4 * kEN) {
-        // Eigenvalue j (ascending) by a group of 4 lanes, 4 shifts per round
-        // (×5 narrowing), 23 rounds (2^-53 of the scaled Gershgorin width).
-        // Lanes tid ≥ 256 are idle here: the rounds are latency-bound chains,
-        // and fewer shifts per eigenvalue means less total work.
-        const int j = tid >> 2;
-        const int t = lane & 3, gbase = lane & 28;
-        const unsigned gmask = 0xfu << gbase;
-        double lo_b = S.misc[0], hi_b = S.misc[1];
+    {
+        const int j = ri;                      // eigenvalue j (ascending)
         const int jj = j < n ? j : n - 1;
-        for (int it = 0; it < 23; ++it) {
-            const double x = lo_b + (hi_b - lo_b) * (static_cast<double>(t + 1) * 0.2);
-            // number of eigenvalues < x: sign changes of (1, p_1, …, p_n), from
-            // the sign bits (integer ops; an exact +0 counts as positive)
+        const unsigned gbase = lane & 24u;     // the 8 lanes of this eigenvalue
+        double lo_b = S.misc[0], hi_b = S.misc[1];
+        for (int it = 0; it < 14; ++it) {  // 9^14 ≈ 2^44
+            const double x = lo_b + (hi_b - lo_b) * (static_cast<double>(rt + 1) * (1.0 / 9.0));
+            // number of eigenvalues < x = sign changes of (1, p_1, …, p_n)
             double pm = 1.0, pc = S.ds[0] - x;
             unsigned sg = static_cast<unsigned>(__double2hiint(pc)) >> 31;
             int cnt = static_cast<int>(sg);
-            // Blocks of 8 steps, unrolled (the shared-memory loads of a block are
-            // independent of the recurrence and issue ahead of it); steps ≥ n are
-            // masked.
             for (int i0 = 1; i0 < n; i0 += 8) {
-                double dv[8], ev[8];
+                double2 q[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    dv[u] = S.ds[min(i0 + u, kEN - 1)] - x;
-                    ev[u] = S.e2s[min(i0 + u - 1, kEN - 1)];
-                }
+                for (int u = 0; u < 8; ++u) q[u] = S.de2[min(i0 + u, kEN - 1)];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     if (i0 + u < n) {
-                        const double pn = fma(dv[u], pc, -ev[u] * pm);
+                        const double pn = fma(q[u].x - x, pc, -q[u].y * pm);
                         pm = pc;
                         pc = pn;
                         const unsigned sn = static_cast<unsigned>(__double2hiint(pc)) >> 31;
@@ -340,19 +377,20 @@ __global__ void __launch_bounds__(kEThreads, 1)
                     pm *= f;
                 }
             }
-            const unsigned above = __ballot_sync(0xffffffffu, cnt > jj) & gmask;
-            const int first = above ? __ffs(above) - 1 - gbase : 4;  // first shift with > jj below it
-            const double x_hi = __shfl_sync(0xffffffffu, x, gbase + min(first, 3));
+            const unsigned above = (__ballot_sync(0xffffffffu, cnt > jj) >> gbase) & 0xffu;
+            const int first = above ? __ffs(above) - 1 : 8;  // first shift with > jj eigenvalues below it
+            const double x_hi = __shfl_sync(0xffffffffu, x, gbase + min(first, 7));
             const double x_lo = __shfl_sync(0xffffffffu, x, gbase + max(first - 1, 0));
-            if (first < 4) hi_b = x_hi;
+            if (first < 8) hi_b = x_hi;
             if (first > 0) lo_b = x_lo;
         }
-        if (t == 0 && j < n) S.lam[j] = 0.5 * (lo_b + hi_b);  // scaled
+        if (rt == 0 && j < n) S.lam[j] = 0.5 * (lo_b + hi_b);  // scaled
+        if (rt == 0 && j < n) S.lamb[j] = 0.5 * (lo_b + hi_b);  // kept: the output if the vectors are rejected
     }
     __syncthreads();
     phase(1);
 
-    // ---- 3. eigenvectors of T (scaled): inverse iteration, thread j
+    // ---- 3. eigenvectors of T: inverse iteration, thread j
     if (tid < n) {
         const int j = tid;
         const double sig = S.lam[j];
@@ -361,7 +399,6 @@ __global__ void __launch_bounds__(kEThreads, 1)
         if (fabs(Dp) < pivtol) Dp = Dp < 0.0 ? -pivtol : pivtol;
         double Di = rcp_refined(Dp);
         S.Dinv[j] = Di;
-#pragma unroll 4
         for (int i = 0; i + 1 < n; ++i) {
             const double l = S.es[i] * Di;
             S.Lm[i * kEN + j] = l;
@@ -372,156 +409,135 @@ __global__ void __launch_bounds__(kEThreads, 1)
         }
         for (int i = 0; i < n; ++i) {  // deterministic start vector, distinct per eigenvalue
             const unsigned h = (static_cast<unsigned>(i) * 2654435761u) ^ (static_cast<unsigned>(j + 1) * 40503u);
-            S.Z[i * kLZ + j] = 1.0 + 0.5 * (static_cast<double>(h & 0xffffu) * (1.0 / 65535.0) - 0.5);
+            S.Z[i * kLA + j] = 1.0 + 0.5 * (static_cast<double>(h & 0xffffu) * (1.0 / 65535.0) - 0.5);
         }
         for (int itr = 0; itr < 2; ++itr) {
             double y = S.Z[j];
-#pragma unroll 4
             for (int i = 1; i < n; ++i) {
-                y = fma(-S.Lm[(i - 1) * kEN + j], y, S.Z[i * kLZ + j]);
-                S.Z[i * kLZ + j] = y;
+                y = fma(-S.Lm[(i - 1) * kEN + j], y, S.Z[i * kLA + j]);
+                S.Z[i * kLA + j] = y;
             }
             double x = y * S.Dinv[(n - 1) * kEN + j];
-            S.Z[(n - 1) * kLZ + j] = x;
+            S.Z[(n - 1) * kLA + j] = x;
             double m = fabs(x);
-#pragma unroll 4
             for (int i = n - 2; i >= 0; --i) {
-                x = fma(S.Z[i * kLZ + j], S.Dinv[i * kEN + j], -S.Lm[i * kEN + j] * x);
-                S.Z[i * kLZ + j] = x;
+                x = fma(S.Z[i * kLA + j], S.Dinv[i * kEN + j], -S.Lm[i * kEN + j] * x);
+                S.Z[i * kLA + j] = x;
                 m = fmax(m, fabs(x));
             }
             // normalise (∞-norm first so the 2-norm cannot overflow)
             const double im = m > 0.0 ? rcp_refined(m) : 0.0;
             double nrm = 0.0;
             for (int i = 0; i < n; ++i) {
-                const double z = S.Z[i * kLZ + j] * im;
+                const double z = S.Z[i * kLA + j] * im;
                 nrm = fma(z, z, nrm);
             }
             const double inv = nrm > 0.0 ? im * rsqrt(nrm) : 0.0;
-            for (int i = 0; i < n; ++i) S.Z[i * kLZ + j] *= inv;
+            for (int i = 0; i < n; ++i) S.Z[i * kLA + j] *= inv;
         }
     }
     __syncthreads();
     phase(2);
 
-    // ---- 4. back-transformation: 4 lanes per eigenvector (column), 16 rows
-    // each; Z ← H_k Z for k = n-3 … 0.  No CTA barrier.
+    // ---- 4. back-transformation: column ri (eigenvector), rows rt + 8u in registers
     {
-        const int col = tid >> 2;
-        double z[16];
+        const int col = ri;
+        double z[8];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) z[u] = (col < n && c0 + u < n) ? S.Z[(c0 + u) * kLZ + col] : 0.0;
+        for (int u = 0; u < 8; ++u) {
+            const int i = rt + 8 * u;
+            z[u] = (col < n && i < n) ? S.Z[i * kLA + col] : 0.0;
+        }
         for (int k = n - 3; k >= 0; --k) {
-            double v[16];
+            const double* vk = S.V + k * kEN + rt;
+            double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int u = 0; u < 16; u += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(&S.V[k * kEN + c0 + u]);
-                v[u] = t2.x;
-                v[u + 1] = t2.y;
+            for (int u = 0; u < 8; u += 2) {
+                a0 = fma(vk[8 * u], z[u], a0);
+                a1 = fma(vk[8 * u + 8], z[u + 1], a1);
             }
-            double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int u = 0; u < 16; u += 2) {
-                s0 = fma(v[u], z[u], s0);
-                s1 = fma(v[u + 1], z[u + 1], s1);
-            }
-            double sv = s0 + s1;
+            double sv = a0 + a1;
             sv += __shfl_xor_sync(0xffffffffu, sv, 1);
             sv += __shfl_xor_sync(0xffffffffu, sv, 2);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 4);
             sv *= S.tau[k];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) z[u] = fma(-sv, v[u], z[u]);
+            for (int u = 0; u < 8; ++u) z[u] = fma(-sv, vk[8 * u], z[u]);
         }
-        if (col < n) {
+        __syncthreads();  // every column read its inverse-iteration vector
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
-                if (c0 + u < n) S.Z[(c0 + u) * kLZ + col] = z[u];
-        }
-        // the original (symmetrised) C into W for the residual check
-        for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
-            const int i = idx & 63, jx = idx >> 6;
-            S.W[i * kLZ + jx] = (i < n && jx < n)
-                                    ? 0.5 * (Cin[i + static_cast<int64_t>(jx) * ldc] + Cin[jx + static_cast<int64_t>(i) * ldc])
-                                    : 0.0;
-        }
-        if (tid >= n && tid < kEN) S.lam[tid] = 0.0;
-        // zero the padding rows/columns of Z (rows ≥ n are 0 already by construction)
-        for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
-            const int i = idx & 63, jx = idx >> 6;
-            if (i >= n || jx >= n) S.Z[i * kLZ + jx] = 0.0;
+        for (int u = 0; u < 8; ++u) {
+            const int i = rt + 8 * u;
+            S.Z[i * kLA + col] = (col < n && i < n) ? z[u] : 0.0;
         }
     }
     __syncthreads();
-
     phase(3);
-    // ---- 5. re-orthonormalisation.  E = ZᵀZ − I (DMMA).  Small defects (close
-    // but separated eigenvalues): Löwdin steps Z ← Z − ½·Z·E, the defect squares
-    // each step.  Large defects (tight clusters, e.g. the zero eigenvalues of a
-    // rank-deficient Gram, whose inverse-iteration vectors come out nearly
-    // parallel): modified Gram-Schmidt in DESCENDING eigenvalue order, which
-    // keeps the span of every leading set of columns (the kept subspace) and
-    // completes a collapsed cluster column by the unit vector with the largest
-    // component outside the columns already fixed.
-    double* E = S.Lm;
+
+    // ---- 5a. re-orthonormalisation (E = ZᵀZ − I)
+    double* E = S.Lm;     // kEN-strided scratch below: use kLA layout inside Lm/Dinv (2·4096 ≥ 64·72)
     double* P = S.Dinv;
     bool mgs = false;
     for (int itl = 0; itl < 3; ++itl) {
-        dmma_64<true>(S.Z, S.Z, E, n);
+        dmma_64<true>(S.Z, S.Z, E, kEN, n);
         __syncthreads();
         double emax = 0.0;
         for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
             const int i = idx & 63, jx = idx >> 6;
-            double v = (i < n && jx < n) ? E[i * kLZ + jx] - (i == jx ? 1.0 : 0.0) : 0.0;
-            E[i * kLZ + jx] = v;
+            const double v = (i < n && jx < n) ? E[i * kEN + jx] - (i == jx ? 1.0 : 0.0) : 0.0;
+            E[i * kEN + jx] = v;
             emax = fmax(emax, fabs(v));
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-        if (lane == 0) S.red[warp] = emax;
-        __syncthreads();
-        emax = 0.0;
-        for (int w = 0; w < kEWarps; ++w) emax = fmax(emax, S.red[w]);
+        emax = block_max(emax, S.red);
         if (emax <= 4.0 * kEps * n) break;  // uniform: orthonormal to working precision
         if (!(emax <= 1e-3) || itl == 2) {
             mgs = true;
             break;
         }
-        dmma_64<false>(S.Z, E, P, n);
+        // P = Z·E (Z rows × E), then Z −= ½P
+        {
+            const int g = lane >> 2, t = lane & 3;
+            for (int tile = warp; tile < 64; tile += kEWarps) {
+                const int r0 = 8 * (tile & 7), c0 = 8 * (tile >> 3);
+                double c_0 = 0.0, c_1 = 0.0;
+                for (int k0 = 0; k0 < n; k0 += 4) {
+                    const int kk = k0 + t;
+                    const double a = kk < n ? S.Z[(r0 + g) * kLA + kk] : 0.0;
+                    const double b = kk < n ? E[kk * kEN + c0 + g] : 0.0;
+                    dmma884(c_0, c_1, a, b);
+                }
+                P[(r0 + g) * kEN + c0 + 2 * t] = c_0;
+                P[(r0 + g) * kEN + c0 + 2 * t + 1] = c_1;
+            }
+        }
         __syncthreads();
         for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
             const int i = idx & 63, jx = idx >> 6;
-            if (i < n && jx < n) S.Z[i * kLZ + jx] = fma(-0.5, P[i * kLZ + jx], S.Z[i * kLZ + jx]);
+            if (i < n && jx < n) S.Z[i * kLA + jx] = fma(-0.5, P[i * kEN + jx], S.Z[i * kLA + jx]);
         }
         __syncthreads();
     }
-    if (mgs) {  // uniform
-        // thread t: column ci = t/4, rows c0..c0+15 (c0 = 16·(t%4)); rowfill[m] =
-        // Σ over fixed columns of z[m]² (P is free scratch)
-        double* rowfill = P;
-        const int ci = tid >> 2;
-        if (tid < kEN) rowfill[tid] = 0.0;
+    if (mgs) {  // uniform.  Modified Gram-Schmidt in DESCENDING eigenvalue order (the
+                // kept subspace's leading columns keep their span); a collapsed column is
+                // completed by the unit vector with the most room outside the fixed ones.
+        const int ci = ri;  // group of 8 lanes per column, rows rt + 8u
+        if (tid < kEN) S.rowfill[tid] = 0.0;
         __syncthreads();
         for (int jp = n - 1; jp >= 0; --jp) {
-            // 1. norm of the pivot column (all threads of its group; others idle)
-            double nrm2 = 0.0;
-            if (ci == jp) {
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const double z = c0 + u < n ? S.Z[(c0 + u) * kLZ + jp] : 0.0;
-                    nrm2 = fma(z, z, nrm2);
-                }
-                nrm2 += __shfl_xor_sync(gmask4, nrm2, 1);
-                nrm2 += __shfl_xor_sync(gmask4, nrm2, 2);
-                if ((tid & 3) == 0) S.misc[5] = nrm2;
+            if (warp == 0) {
+                double ss = 0.0;
+                for (int r2 = lane; r2 < n; r2 += 32) ss = fma(S.Z[r2 * kLA + jp], S.Z[r2 * kLA + jp], ss);
+                ss = warp_sum(ss);
+                if (lane == 0) S.misc[5] = ss;
             }
             __syncthreads();
-            nrm2 = S.misc[5];
-            if (!(nrm2 > 1e-4)) {  // collapsed (< 1% left): replace by e_m ⟂ the fixed columns
+            double nrm2 = S.misc[5];
+            if (!(nrm2 > 1e-4)) {  // collapsed (< 1% left)
                 if (warp == 0) {
                     double best = -1.0;
                     int bm = 0;
                     for (int m = lane; m < n; m += 32) {
-                        const double room = 1.0 - rowfill[m];
+                        const double room = 1.0 - S.rowfill[m];
                         if (room > best) {
                             best = room;
                             bm = m;
@@ -540,14 +556,13 @@ __global__ void __launch_bounds__(kEThreads, 1)
                 }
                 __syncthreads();
                 const int m = static_cast<int>(S.misc[6]);
-                // v_r = δ_rm − Σ_{f > jp, fixed} z_f[m] z_f[r]   (thread per row r < n)
-                if (tid < n) {
+                if (tid < n) {  // v_r = δ_rm − Σ_{fixed f > jp} z_f[m] z_f[r]
                     double v = tid == m ? 1.0 : 0.0;
-                    for (int f = jp + 1; f < n; ++f) v = fma(-S.Z[m * kLZ + f], S.Z[tid * kLZ + f], v);
+                    for (int f = jp + 1; f < n; ++f) v = fma(-S.Z[m * kLA + f], S.Z[tid * kLA + f], v);
                     S.p[tid] = v;
                 }
                 __syncthreads();
-                if (tid < n) S.Z[tid * kLZ + jp] = S.p[tid];
+                if (tid < n) S.Z[tid * kLA + jp] = S.p[tid];
                 if (warp == 0) {
                     double ss = 0.0;
                     for (int r2 = lane; r2 < n; r2 += 32) ss = fma(S.p[r2], S.p[r2], ss);
@@ -559,60 +574,93 @@ __global__ void __launch_bounds__(kEThreads, 1)
                 if (!(nrm2 > 1e-16) && tid == 0) S.flag = 1;  // cannot complete: leave it to Jacobi
             }
             const double inv = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
-            // 2. normalise the pivot, record its row weights
             if (tid < n) {
-                const double z = S.Z[tid * kLZ + jp] * inv;
-                S.Z[tid * kLZ + jp] = z;
-                rowfill[tid] = fma(z, z, rowfill[tid]);
+                const double z = S.Z[tid * kLA + jp] * inv;
+                S.Z[tid * kLA + jp] = z;
+                S.rowfill[tid] = fma(z, z, S.rowfill[tid]);
             }
             __syncthreads();
-            // 3. project the pivot out of the remaining columns ci < jp (group per column)
-            if (ci < jp) {
+            if (ci < jp) {  // project the pivot out of the remaining columns
                 double dz = 0.0;
 #pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    if (c0 + u < n) dz = fma(S.Z[(c0 + u) * kLZ + jp], S.Z[(c0 + u) * kLZ + ci], dz);
-                dz += __shfl_xor_sync(gmask4, dz, 1);
-                dz += __shfl_xor_sync(gmask4, dz, 2);
+                for (int u = 0; u < 8; ++u) {
+                    const int i = rt + 8 * u;
+                    if (i < n) dz = fma(S.Z[i * kLA + jp], S.Z[i * kLA + ci], dz);
+                }
+                const unsigned gm8 = 0xffu << (lane & 24);  // this column's 8 lanes (the warp may diverge here)
+                dz += __shfl_xor_sync(gm8, dz, 1);
+                dz += __shfl_xor_sync(gm8, dz, 2);
+                dz += __shfl_xor_sync(gm8, dz, 4);
 #pragma unroll
-                for (int u = 0; u < 16; ++u)
-                    if (c0 + u < n) S.Z[(c0 + u) * kLZ + ci] = fma(-dz, S.Z[(c0 + u) * kLZ + jp], S.Z[(c0 + u) * kLZ + ci]);
+                for (int u = 0; u < 8; ++u) {
+                    const int i = rt + 8 * u;
+                    if (i < n) S.Z[i * kLA + ci] = fma(-dz, S.Z[i * kLA + jp], S.Z[i * kLA + ci]);
+                }
             }
             __syncthreads();
         }
     }
-    __syncthreads();
-
     phase(4);
-    // ---- 6. residual R = C Z − Z Λ (unscaled λ), Frobenius norm
-    {
+
+    // ---- 5b. R = C Z (C re-read, symmetrised, into A), Rayleigh quotients,
+    // residual ‖R − ZΛ‖_F, descending order
+    for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
+        const int i = idx & 63, j = idx >> 6;
+        S.Lm[i * kEN + j] = (i < n && j < n) ? 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc])
+                                             : 0.0;
+    }
+    __syncthreads();
+    {  // A = C·Z with C (kEN-strided) in Lm
         const int g = lane >> 2, t = lane & 3;
-        double r2 = 0.0;
         for (int tile = warp; tile < 64; tile += kEWarps) {
             const int r0 = 8 * (tile & 7), c0 = 8 * (tile >> 3);
             double c_0 = 0.0, c_1 = 0.0;
             for (int k0 = 0; k0 < n; k0 += 4) {
                 const int kk = k0 + t;
-                const double av = kk < n ? S.W[(r0 + g) * kLZ + kk] : 0.0;
-                const double bv = kk < n ? S.Z[kk * kLZ + c0 + g] : 0.0;
-                dmma884(c_0, c_1, av, bv);
+                const double a = kk < n ? S.Lm[(r0 + g) * kEN + kk] : 0.0;
+                const double b = kk < n ? S.Z[kk * kLA + c0 + g] : 0.0;
+                dmma884(c_0, c_1, a, b);
             }
-            const int i = r0 + g, j0 = c0 + 2 * t;
-            if (i < n) {
-                if (j0 < n) {
-                    const double r = fma(-S.lam[j0] * isc, S.Z[i * kLZ + j0], c_0);
-                    r2 = fma(r, r, r2);
-                }
-                if (j0 + 1 < n) {
-                    const double r = fma(-S.lam[j0 + 1] * isc, S.Z[i * kLZ + j0 + 1], c_1);
-                    r2 = fma(r, r, r2);
-                }
-            }
+            S.A[(r0 + g) * kLA + c0 + 2 * t] = c_0;
+            S.A[(r0 + g) * kLA + c0 + 2 * t + 1] = c_1;
         }
-        r2 = warp_sum(r2);
-        if (lane == 0) S.red[warp] = r2;
     }
     __syncthreads();
+    {  // column j: 8 lanes; λ_j = z_jᵀ r_j, residual² = ‖r_j − λ_j z_j‖²
+        const int j = ri;
+        double zr = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = rt + 8 * u;
+            if (i < n && j < n) zr = fma(S.Z[i * kLA + j], S.A[i * kLA + j], zr);
+        }
+        zr += __shfl_xor_sync(0xffffffffu, zr, 1);
+        zr += __shfl_xor_sync(0xffffffffu, zr, 2);
+        zr += __shfl_xor_sync(0xffffffffu, zr, 4);
+        double r2 = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = rt + 8 * u;
+            if (i < n && j < n) {
+                const double r = fma(-zr, S.Z[i * kLA + j], S.A[i * kLA + j]);
+                r2 = fma(r, r, r2);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        if (lane == 0) S.red[warp] = r2;
+        if (rt == 0 && j < n) S.lam[j] = zr;  // unscaled now
+    }
+    __syncthreads();
+    if (tid < n) {  // rank in descending order (ties: lower index first)
+        const double v = S.lam[tid];
+        int rk = 0;
+        for (int i = 0; i < n; ++i) {
+            const double w = S.lam[i];
+            rk += (w > v) || (w == v && i < tid);
+        }
+        S.rank[tid] = rk;
+    }
     if (tid == 0) {
         double r2 = 0.0;
         for (int w = 0; w < kEWarps; ++w) r2 += S.red[w];
@@ -620,14 +668,16 @@ __global__ void __launch_bounds__(kEThreads, 1)
         // Backward-stable methods leave ~n·ε‖C‖; far more means a failure.
         if (!(res <= 1e-12 * tn)) S.flag = 1;
         if (resid_out) *resid_out = res;
-        if (S.flag) atomicOr(flag_out, 1);
     }
-    // ---- output, descending
+    __syncthreads();
+    if (tid == 0 && S.flag) atomicOr(flag_out, 1);
     for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
-        const int i = idx & 63, r = idx >> 6;
-        if (i < n && r < n) V_out[i + static_cast<int64_t>(r) * n] = S.Z[i * kLZ + (n - 1 - r)];
+        const int i = idx & 63, j = idx >> 6;
+        if (i < n && j < n) V_out[i + static_cast<int64_t>(S.rank[j]) * n] = S.Z[i * kLA + j];
     }
-    if (tid < n) lambda_out[tid] = S.lam[n - 1 - tid] * isc;
+    // Rejected vectors (an exactly multiple nonzero eigenvalue, say): their
+    // Rayleigh quotients mean nothing, the multisection values still do.
+    if (tid < n) lambda_out[S.flag ? n - 1 - tid : S.rank[tid]] = S.flag ? S.lamb[tid] * isc : S.lam[tid];
     phase(5);
 }
 
