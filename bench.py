@@ -142,8 +142,11 @@ def config_desc(wl, world, strategy="krp", widths=None, omega="cached on device"
     r = wl.ranks[0]
     plan = {"krp": "given (uniform KRP width)", "kron": f"given (Kron widths {widths} = kron_sketch_dims(targets "
             f"{wl.widths}, dims), src/sketch.cpp:222-270)", "lazy": "none (Lazy: tucker_rounding of the formal sum)"}
+    src = ("the paper's synthetic low-rank sweep point d = 100, Fig. 2 (PAPER.md:505-531; reference "
+           "src/bench.cpp:327-400): rank-1 summands in a shared 10-dim subspace per mode, plan computed inside "
+           "every call (oversampling 2)" if wl.cfg == 6 else f"BASELINE.json configs[{wl.cfg - 1}]")
     return {"workload": f"{wl.name}: d={len(wl.dims)} n={wl.dims} K={wl.K_total} r={r} s={wl.widths[0]} "
-                        f"cap={wl.cap} eps={wl.eps} (BASELINE.json configs[{wl.cfg - 1}])",
+                        f"cap={wl.cap} eps={wl.eps} ({src})",
             "strategy": strategy, "mode": ("BASELINE mode (eps = 0 + rank cap)" if wl.cap else
                                            "reference-exact mode (eps, no rank cap)"),
             "summands_per_gpu": wl.K_total // world, "plan": plan[strategy], "omega": omega,
@@ -300,9 +303,18 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    # Each rank generates (and later pins) only its own contiguous shard.
-    b, e = shard_range(config_spec(args.config)["K"], world, rank)
-    wl = make_workload(args.config, k_range=(b, e))
+    fig2 = args.config == 6  # the paper's synthetic low-rank sweep point d = 100 (Fig. 2)
+    if fig2:
+        from paper_2603_13532_b200.workloads import FIG2, make_fig2_workload
+
+        if world > 1:
+            raise SystemExit("bench.py --config 6 runs on one GPU")
+        b, e = 0, FIG2["d"]
+        wl = make_fig2_workload()
+    else:
+        # Each rank generates (and later pins) only its own contiguous shard.
+        b, e = shard_range(config_spec(args.config)["K"], world, rank)
+        wl = make_workload(args.config, k_range=(b, e))
     apply_mode(wl, args)
     xs, ws = wl.summands, np.ascontiguousarray(wl.weights)
     eng = init_nccl_engine(local if world > 1 else 0, rank, world)
@@ -313,13 +325,16 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream)
     strat = {"krp": T.Strategy.Krp, "kron": T.Strategy.Kron, "lazy": T.Strategy.Lazy}[args.strategy]
     widths = T.kron_sketch_dims(wl.widths, wl.dims) if args.strategy == "kron" else wl.widths
-    if args.strategy == "krp":
+    if args.strategy == "krp" and not fig2:
         eng.prepare_omega(wl.dims, max(wl.widths), wl.seed)
     batch = eng.upload(xs)
 
     def call(bt):
         if args.strategy == "lazy":
             return eng.lazy_sum(bt, ws, wl.eps, wl.cap)
+        if fig2:  # no plan passed: effective_subrank inside the call, as round_sum does (src/sketch.cpp:75-79)
+            _, _, wd = eng.effective_subrank(bt, ws, wl.eps, 2, strat)
+            return eng.krp_sum(bt, ws, wd, wl.seed, wl.eps, wl.cap, strat)
         return eng.krp_sum(bt, ws, widths, wl.seed, wl.eps, wl.cap, strat)
 
     def step():
@@ -366,6 +381,8 @@ def main():
     ms = total_ms / args.steps
     value = wl.K_total / (ms / 1000.0)
     krp = args.strategy == "krp"
+    if fig2 and krp:  # the plan's width (computed inside every call)
+        wl.widths = eng.effective_subrank(batch, ws, wl.eps, 2, strat)[2]
     falg = f_alg(wl.dims, [wl.ranks[0]] * wl.K_total, wl.widths[0]) if krp else None  # SURVEY.md §8(d) F_alg is the KRP count
     gflops = falg / (ms / 1000.0) / 1e9 if krp else None
     peak, peak_src = fp64_peak()
@@ -501,7 +518,7 @@ def main():
     # outside the timed region: the reference times it inside its call
     # (src/sketch.cpp:91-95); here it is generated once and cached on the device.
     omega = None
-    if args.strategy == "krp" and rank == 0:
+    if args.strategy == "krp" and rank == 0 and not fig2:
         t0 = time.perf_counter()
         eng.prepare_omega(wl.dims, max(wl.widths), T.RngSeed(wl.seed.seed + 1, wl.seed.stream))
         om = 1000.0 * (time.perf_counter() - t0)
@@ -510,8 +527,40 @@ def main():
                  "e2e_ms_per_step_if_regenerated": (e2e["ms_per_step"] + om) if e2e else None,
                  "note": "the reference regenerates Ω inside every call; here it is cached per (seed, stream, dims, s)"}
 
+    # Fig. 2 comparison: the same sum by Lazy rounding of the formal sum
+    # (TuckerAxby + TuckerRounding), timed the same way, and the KRP result's
+    # relative error to it (the paper's "error relative to the deterministic
+    # baseline"), on the device.
+    vs_lazy = None
+    if fig2 and krp:
+        lt = []
+        for i in range(max(3, min(args.steps, 5)) + 1):
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0_.record(stream)
+            lr = eng.lazy_sum(batch, ws, wl.eps, wl.cap)
+            e1_.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:
+                lt.append(e0_.elapsed_time(e1_))
+            if i == 0:
+                lazy_t = lr.to_tucker()
+            lr.free()
+        kr = call(batch)
+        lb = eng.upload([lazy_t])
+        rel = eng.rel_error_to_sum(kr, lb, [1.0])
+        kranks = kr.ranks
+        kr.free()
+        lb.free()
+        lms = statistics.median(lt)
+        vs_lazy = {"lazy_ms_per_call": lms, "krp_ms_per_call": ms, "krp_speedup_vs_lazy": lms / ms,
+                   "rel_error_krp_vs_lazy": rel, "ranks_krp": kranks, "ranks_lazy": lazy_t.ranks,
+                   "plan_widths": wl.widths,
+                   "note": "Lazy = ts_lazy_sum (thin QR of the stacked factors, formal-sum core 100^4, st_hosvd); "
+                           "KRP = ts_effective_subrank + ts_krp_sum per call; device CUDA-event times"}
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and krp:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and krp and not fig2:
         cpu = cpu_baseline(wl, args)
 
     if rank == 0:
@@ -524,7 +573,7 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages)),
                 "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]},
-                "accuracy": err, "omega": omega,
+                "accuracy": err, "omega": omega, "vs_lazy": vs_lazy,
                 "comm": {"ncclCommCount": comm_count, "backend": "NCCL all-reduce inside ts_krp_sum" if world > 1
                          else "none (1 GPU)"}}
         print(json.dumps(line), flush=True)

@@ -560,7 +560,7 @@ bool launch_sym_jacobi_batched(const double* C, int64_t ldc, int n, double* lamb
 // TS_EIG_PROFILE is set (see jacobi_values_kernel), else zeros.
 extern "C" void tsi_read_eig_profile(long long* out) {
     unsigned long long* p = ts::eig_probe_buffer();
-    unsigned long long h[18] = {};
+    unsigned long long h[22] = {};
     if (p) TS_CUDA_CHECK(cudaMemcpy(h, p, sizeof(h), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 18; ++i) out[i] = static_cast<long long>(h[i]);
+    for (int i = 0; i < 22; ++i) out[i] = static_cast<long long>(h[i]);
 }

@@ -28,7 +28,7 @@
 //  5. Orthonormality: E = ZᵀZ − I (DMMA); Löwdin steps Z ← Z − ½ZE for small
 //     defects (close eigenvalues), modified Gram-Schmidt with completion for
 //     collapsed clusters (e.g. the zero eigenvalues of a rank-deficient Gram).
-//     Then R = C Z (DMMA, C re-read from global), λ_j = z_jᵀ(Cz_j) (Rayleigh
+//     Then R = C Z (DMMA), λ_j = z_jᵀ(Cz_j) (Rayleigh
 //     quotients: accurate to O(ε‖C‖ + ‖r_j‖²/gap)), the measured residual
 //     ‖C Z − ZΛ‖_F (written to *resid; the rank checks use it), and the
 //     descending sort.  A non-finite or too large residual sets *flag and the
@@ -54,7 +54,7 @@ struct TrdSmem {
     double Lm[kEN * kEN];     // inverse iteration: L_i of eigenvalue j at [i*kEN + j]; later E, Z·E
     double Dinv[kEN * kEN];   //                    1/D_i at [i*kEN + j]
     double V[kEN * kEN];      // reflector k at V[k*kEN + i]: v_i = 0 for i ≤ k, v_{k+1} = 1
-    double2 de2[kEN];         // multisection operands (d_i, e²_{i−1}), scaled
+    double2 de2[kEN + 8];     // multisection operands (d_i, e²_{i−1}), scaled, padded
     double lamb[kEN];         // multisection eigenvalues (scaled, ascending)
     double tau[kEN], d[kEN], e[kEN], ds[kEN], e2s[kEN], es[kEN], lam[kEN], p[kEN], rowfill[kEN];
     double red[kEWarps];
@@ -123,7 +123,8 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 __global__ void __launch_bounds__(kEThreads, 1)
     trd_eig_kernel(const double* __restrict__ Cin, int64_t ldc, int n, double* __restrict__ lambda_out,
                    double* __restrict__ V_out, int* __restrict__ flag_out, double* __restrict__ resid_out,
-                   unsigned long long* __restrict__ prof, int64_t strideC, int64_t strideL, int64_t strideV) {
+                   unsigned long long* __restrict__ prof, int64_t strideC, int64_t strideL, int64_t strideV,
+                   int variant) {
     {  // batched launches (segmented sums): CTA b solves problem b
         const int64_t b = blockIdx.x;
         Cin += b * strideC;
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
         S.V[idx] = 0.0;
     }
     if (tid == 0) S.flag = 0;
+    if (prof && tid == 0) prof[19] = prof[20] = prof[21] = 0;
     if (tid < kEN) {
         S.tau[tid] = 0.0;
         S.e[tid] = 0.0;
@@ -182,6 +184,10 @@ __global__ void __launch_bounds__(kEThreads, 1)
     const int gbase = lane & 24;
     const unsigned gm8 = 0xffu << gbase;
     auto reflector = [&](int k) {  // the 8 lanes of row k (ri == k)
+        if (variant == 1) {  // timing ablation: no reflector arithmetic
+            if (rt == 0) S.tau[k] = 0.0;
+            return;
+        }
         double ss = 0.0, xa = 0.0, xd = 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -223,7 +229,8 @@ __global__ void __launch_bounds__(kEThreads, 1)
         const double* vk = S.V + k * kEN;
         const bool wact = 4 * warp + 3 > k && 4 * warp < n;  // warp-uniform: any row in (k, n)
         double pr = 0.0, vi = 0.0;
-        if (wact) {
+        const long long m0_ = clock64();
+        if (wact && variant != 2) {
             double s0 = 0.0, s1 = 0.0;
 #pragma unroll
             for (int u = 0; u < 8; u += 2) {
@@ -244,13 +251,15 @@ __global__ void __launch_bounds__(kEThreads, 1)
             S.red[warp] = 0.0;
         }
         if (rt == 0) S.p[ri] = pr;
+        if (prof && tid == 480) prof[20] += static_cast<unsigned long long>(clock64() - m0_);
         __syncthreads();
+        const long long u0_ = clock64();
         if (prof) {
             const long long c1_ = clock64();
             c_mv += c1_ - c0_;
             c0_ = c1_;
         }
-        if (wact) {
+        if (wact && variant != 3) {
             double pv2[kEWarps];
 #pragma unroll
             for (int w = 0; w < kEWarps; w += 2) {
@@ -272,12 +281,17 @@ __global__ void __launch_bounds__(kEThreads, 1)
                 a[u] -= fma(vi, wj, wi * vj);
             }
         }
+        if (prof && tid == 480) prof[21] += static_cast<unsigned long long>(clock64() - u0_);
         if (prof) {
             const long long c1_ = clock64();
             c_up += c1_ - c0_;
             c0_ = c1_;
         }
-        if (k + 3 < n && ri == k + 1) reflector(k + 1);
+        if (k + 3 < n && ri == k + 1) {
+            const long long r0_ = clock64();
+            reflector(k + 1);
+            if (prof && rt == 0) prof[19] += static_cast<unsigned long long>(clock64() - r0_);
+        }
         __syncthreads();
         if (prof) c_refl += clock64() - c0_;
     }
@@ -319,8 +333,11 @@ __global__ void __launch_bounds__(kEThreads, 1)
             S.es[i] = es;
             S.e2s[i] = es * es;
             const double ep = (i >= 1 && i < n) ? S.e[i - 1] * sc : 0.0;
-            S.de2[i] = make_double2(i < n ? S.d[i] * sc : 0.0, ep * ep);  // (d_i, e²_{i−1})
+            // (d_i, e²_{i−1}); beyond n a decoupled d = 8 > every shift leaves the
+            // Sturm signs unchanged, so the count loop needs no bound checks
+            S.de2[i] = make_double2(i < n ? S.d[i] * sc : 8.0, ep * ep);
         }
+        if (lane < 8) S.de2[kEN + lane] = make_double2(8.0, 0.0);
         if (lane == 0) {
             const double pad = 8.0 * kEps * n;
             S.misc[0] = lo * sc - pad;
@@ -358,17 +375,15 @@ __global__ void __launch_bounds__(kEThreads, 1)
             for (int i0 = 1; i0 < n; i0 += 8) {
                 double2 q[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) q[u] = S.de2[min(i0 + u, kEN - 1)];
+                for (int u = 0; u < 8; ++u) q[u] = S.de2[i0 + u];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    if (i0 + u < n) {
-                        const double pn = fma(q[u].x - x, pc, -q[u].y * pm);
-                        pm = pc;
-                        pc = pn;
-                        const unsigned sn = static_cast<unsigned>(__double2hiint(pc)) >> 31;
-                        cnt += static_cast<int>(sn ^ sg);
-                        sg = sn;
-                    }
+                    const double pn = fma(q[u].x - x, pc, -q[u].y * pm);
+                    pm = pc;
+                    pc = pn;
+                    const unsigned sn = static_cast<unsigned>(__double2hiint(pc)) >> 31;
+                    cnt += static_cast<int>(sn ^ sg);
+                    sg = sn;
                 }
                 const double m = fmax(fabs(pc), fabs(pm));
                 if (m > 0.0) {
@@ -602,27 +617,22 @@ __global__ void __launch_bounds__(kEThreads, 1)
     }
     phase(4);
 
-    // ---- 5b. R = C Z (C re-read, symmetrised, into A), Rayleigh quotients,
-    // residual ‖R − ZΛ‖_F, descending order
-    for (int idx = tid; idx < kEN * kEN; idx += kEThreads) {
-        const int i = idx & 63, j = idx >> 6;
-        S.Lm[i * kEN + j] = (i < n && j < n) ? 0.5 * (Cin[i + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(i) * ldc])
-                                             : 0.0;
-    }
-    __syncthreads();
-    {  // A = C·Z with C (kEN-strided) in Lm
+    // ---- 5b. R = C Z (C still in A: the tridiagonalisation ran in registers),
+    // Rayleigh quotients, residual ‖R − ZΛ‖_F, descending order
+    double* R = S.Lm;  // kEN-strided
+    {
         const int g = lane >> 2, t = lane & 3;
         for (int tile = warp; tile < 64; tile += kEWarps) {
             const int r0 = 8 * (tile & 7), c0 = 8 * (tile >> 3);
             double c_0 = 0.0, c_1 = 0.0;
             for (int k0 = 0; k0 < n; k0 += 4) {
                 const int kk = k0 + t;
-                const double a = kk < n ? S.Lm[(r0 + g) * kEN + kk] : 0.0;
+                const double a = kk < n ? S.A[(r0 + g) * kLA + kk] : 0.0;
                 const double b = kk < n ? S.Z[kk * kLA + c0 + g] : 0.0;
                 dmma884(c_0, c_1, a, b);
             }
-            S.A[(r0 + g) * kLA + c0 + 2 * t] = c_0;
-            S.A[(r0 + g) * kLA + c0 + 2 * t + 1] = c_1;
+            R[(r0 + g) * kEN + c0 + 2 * t] = c_0;
+            R[(r0 + g) * kEN + c0 + 2 * t + 1] = c_1;
         }
     }
     __syncthreads();
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = rt + 8 * u;
-            if (i < n && j < n) zr = fma(S.Z[i * kLA + j], S.A[i * kLA + j], zr);
+            if (i < n && j < n) zr = fma(S.Z[i * kLA + j], R[i * kEN + j], zr);
         }
         zr += __shfl_xor_sync(0xffffffffu, zr, 1);
         zr += __shfl_xor_sync(0xffffffffu, zr, 2);
@@ -642,7 +652,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
         for (int u = 0; u < 8; ++u) {
             const int i = rt + 8 * u;
             if (i < n && j < n) {
-                const double r = fma(-zr, S.Z[i * kLA + j], S.A[i * kLA + j]);
+                const double r = fma(-zr, S.Z[i * kLA + j], R[i * kEN + j]);
                 r2 = fma(r, r, r2);
             }
         }
@@ -696,8 +706,13 @@ bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double*
     if (n < 1 || n > kEN) return false;
     if (count < 1) return true;
     set_max_smem(trd_eig_kernel, static_cast<int>(sizeof(TrdSmem)));
+    static const int variant = [] {  // timing ablations of the tridiagonalisation (tools/probe_trd.py)
+        const char* e = std::getenv("TS_TRD_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
     trd_eig_kernel<<<count, kEThreads, sizeof(TrdSmem), sc.stream()>>>(C, ldc, n, lambda, V, flag, resid,
-                                                                       eig_probe_buffer(), strideC, strideL, strideV);
+                                                                       eig_probe_buffer(), strideC, strideL, strideV,
+                                                                       variant);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
     return true;

@@ -168,6 +168,39 @@ def make_workload(cfg: int, K: Optional[int] = None, n_override: Optional[List[i
                     slabs=slabs + [core_slab], reps=int(sp.get("reps", 1)), K_total=K, k_begin=kb)
 
 
+# The paper's synthetic low-rank sweep (Fig. 2; reference
+# runner src/bench.cpp:327-400 with shared_subspace_summands :101-122): N = 4
+# modes, n = 4000, d rank-1 summands whose mode-k factors are Q_k·m (Q_k a fixed
+# orthonormal 4000 × 10 basis, m ~ N(0, I_10)), unit cores and weights,
+# eps = 1e-6, oversampling p = 2, the plan computed inside every call.
+FIG2 = dict(name="fig2_synthetic_lowrank", dims=[4000] * 4, d=100, latent=10, eps=1e-6, oversampling=2)
+
+
+def make_fig2_workload(d: int = 100, n: int = 4000, modes: int = 4, latent: int = 10, trial: int = 0,
+                       gaussian: Optional[Gaussian] = None, substream: Optional[Substream] = None) -> Workload:
+    """Reference shared_subspace_summands (src/bench.cpp:101-122): bases
+    Q_k = thin-Q(gaussian(n, latent, tseed.substream(10 + k))), factor
+    U_k^(i) = Q_k · gaussian(latent, 1, tseed.substream(1000 + i·modes + k)),
+    core = 1; trial seed tseed = {2603, 6}.substream(trial), request seed
+    tseed.substream(5000 + d) (src/bench.cpp:352)."""
+    if gaussian is None or substream is None:
+        gaussian, substream = _library_rng()
+    tseed = substream((2603, 6), trial)
+    bases = [_thin_q(gaussian(n, latent, substream(tseed, 10 + k))) for k in range(modes)]
+    slabs = [np.zeros((n, d), order="F") for _ in range(modes)]
+    core_slab = np.ones(d)
+    summands = []
+    for i in range(d):
+        factors = []
+        for k in range(modes):
+            slabs[k][:, i:i + 1] = bases[k] @ gaussian(latent, 1, substream(tseed, 1000 + i * modes + k))
+            factors.append(slabs[k][:, i:i + 1])
+        summands.append(TuckerTensor(core_slab[i:i + 1].reshape([1] * modes, order="F"), factors))
+    return Workload(name=FIG2["name"], cfg=6, dims=[n] * modes, ranks=[[1] * modes for _ in range(d)],
+                    summands=summands, weights=np.ones(d), widths=[latent + 2] * modes, cap=None, eps=FIG2["eps"],
+                    seed=RngSeed(*substream(tseed, 5000 + d)), slabs=slabs + [core_slab], K_total=d)
+
+
 def f_alg(dims, ranks_per_summand, s, q=None) -> float:
     """Algorithmic FLOPs of stages A+B+C+E+F."""
     d = len(dims)

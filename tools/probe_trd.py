@@ -39,10 +39,10 @@ for name, c in cases:
                 rej = False
             else:
                 vals, vecs, rej, ms = eng.sym_eig_tri(c)
-                prof = (C.c_longlong * 18)()
+                prof = (C.c_longlong * 22)()
                 T.lib().ts_debug_eig_profile(prof)
                 row["trd_phase_cycles"] = list(prof)[10:16]
-                row["trd_sub"] = [prof[9], prof[17], prof[16], prof[5], prof[6], prof[8]]
+                row["trd_sub"] = {"load": prof[9], "loop_start": prof[17], "loop_end": prof[16], "refl_group": prof[19], "matvec_w15": prof[20], "update_w15": prof[21]}
             ts.append(ms)
         row[solver] = {"ms": float(np.median(ts)), "rejected": bool(rej),
                        "eig_err_rel": float(np.max(np.abs(vals - ov)) / ov[0]),
