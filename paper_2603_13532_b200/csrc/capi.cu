@@ -2757,7 +2757,22 @@ static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, 
             ts::launch_scale_columns(b->F[n], rows, R, d_scale, V, !tall, sc);
             const std::int64_t m = tall ? rows : R, cols = tall ? R : rows;
             double* sigma = sc.alloc_n<double>(static_cast<size_t>(cols));
-            if (qr_wide_mode(cols)) {  // any width: block one-sided Jacobi on V itself (wide.cu)
+            bool gram_values = false;  // sigma holds Gram eigenvalues (λ = σ²) instead of σ
+            if (qr_wide_mode(cols) && cols <= 128) {
+                // The reference's own formulation (src/sketch.cpp:311): eigenvalues of
+                // the Gram VᵀV (DMMA GEMM) by the one-CTA values-only solver.
+                double* G = sc.alloc_n<double>(static_cast<size_t>(cols * cols));
+                GemmProblem p{};
+                p.A = p.B = V;
+                p.lda = p.ldb = m;
+                p.C = G;
+                p.ldc = cols;
+                p.M = p.N = static_cast<int>(cols);
+                p.K = static_cast<int>(m);
+                ts::launch_grouped_gemm(Layout::TN, {p}, sc, ctx->num_sms);
+                ts::launch_sym_eigvals(G, cols, static_cast<int>(cols), sigma, sc);
+                gram_values = true;
+            } else if (qr_wide_mode(cols)) {  // any width: block one-sided Jacobi on V itself (wide.cu)
                 ts::bosj_svd(V, m, m, cols, sigma, nullptr, 0, sc, ctx->num_sms);
             } else {
                 ts::TsqrPlan plan = ts::plan_tsqr(V, m, m, cols, nullptr, 0, sc);
@@ -2771,7 +2786,9 @@ static void plan_targets(ts_ctx* ctx, const ts_batch* b, const double* weights, 
             TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
             // Eigenvalues of VᵀV (R of them; the R - cols missing ones are zero).
             std::vector<double> lam(static_cast<size_t>(R), 0.0);
-            for (std::int64_t j = 0; j < cols; ++j) lam[static_cast<size_t>(j)] = sig[static_cast<size_t>(j)] * sig[static_cast<size_t>(j)];
+            for (std::int64_t j = 0; j < cols; ++j)
+                lam[static_cast<size_t>(j)] = gram_values ? std::max(sig[static_cast<size_t>(j)], 0.0)  // cwiseMax(0), src/sketch.cpp:312
+                                                          : sig[static_cast<size_t>(j)] * sig[static_cast<size_t>(j)];
             const double lmax = lam.empty() ? 0.0 : lam[0];
             const double floor = static_cast<double>(R) * std::numeric_limits<double>::epsilon() * lmax;
             for (double& l : lam)

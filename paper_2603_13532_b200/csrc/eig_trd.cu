@@ -691,6 +691,200 @@ __global__ void __launch_bounds__(kEThreads, 1)
     phase(5);
 }
 
+// Eigenvalues only, n ≤ NR (plan stage, src/sketch.cpp:311-312: the eigenvalues
+// of the energy-weighted Gram VᵀV; no vectors are needed).  The same register-
+// resident tridiagonalisation as trd_eig_kernel with NR/8 columns per thread
+// (only the current reflector is kept), then multisection to full precision:
+// 16 rounds of 8 shifts (9^16 ≈ 2^51 of the Gershgorin width), λ descending.
+template <int NR>
+__global__ void __launch_bounds__(NR * 8, 1)
+    eigvals_kernel(const double* __restrict__ Cin, int64_t ldc, int n, double* __restrict__ lambda_out) {
+    constexpr int NT = NR * 8, NW = NT / 32, CPT = NR / 8;
+    __shared__ __align__(16) double V[2][NR];
+    __shared__ __align__(16) double P[NR];
+    __shared__ __align__(16) double red[NW];
+    __shared__ double dd[NR], ee[NR], tau[NR];
+    __shared__ __align__(16) double2 de2[NR + 8];
+    __shared__ double misc[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ri = tid >> 3, rt = tid & 7;
+    const int gbase = lane & 24;
+    const unsigned gm8 = 0xffu << gbase;
+    double a[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+        const int j = rt + 8 * u;
+        a[u] = (ri < n && j < n) ? 0.5 * (Cin[ri + static_cast<int64_t>(j) * ldc] + Cin[j + static_cast<int64_t>(ri) * ldc])
+                                 : 0.0;
+    }
+    if (n == 1) {
+        if (tid == 0) lambda_out[0] = a[0];
+        return;
+    }
+    auto reflector = [&](int k) {  // the 8 lanes of row k; writes V[k & 1]
+        double s0 = 0.0, s1 = 0.0, xa = 0.0, xd = 0.0;
+#pragma unroll
+        for (int u = 0; u < CPT; u += 2) {
+            const int j = rt + 8 * u;
+            s0 = (j > k + 1) ? fma(a[u], a[u], s0) : s0;
+            s1 = (j + 8 > k + 1) ? fma(a[u + 1], a[u + 1], s1) : s1;
+            xa = (j == k + 1) ? a[u] : ((j + 8 == k + 1) ? a[u + 1] : xa);
+            xd = (j == k) ? a[u] : ((j + 8 == k) ? a[u + 1] : xd);
+        }
+        double ss = s0 + s1;
+        ss += __shfl_xor_sync(gm8, ss, 1);
+        ss += __shfl_xor_sync(gm8, ss, 2);
+        ss += __shfl_xor_sync(gm8, ss, 4);
+        const double alpha = __shfl_sync(gm8, xa, gbase + ((k + 1) & 7));
+        const double dkk = __shfl_sync(gm8, xd, gbase + (k & 7));
+        double tk = 0.0, beta = alpha, scale = 0.0;
+        if (ss > 0.0) {
+            beta = -copysign(sqrt_refined(fma(alpha, alpha, ss)), alpha);
+            tk = fma(-alpha, rcp_refined(beta), 1.0);
+            scale = rcp_refined(alpha - beta);
+        }
+        double* vb = V[k & 1];
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+            const int j = rt + 8 * u;
+            vb[j] = j == k + 1 ? 1.0 : (j > k + 1 ? a[u] * scale : 0.0);
+        }
+        if (rt == 0) {
+            tau[k] = tk;
+            dd[k] = dkk;
+            ee[k] = beta;
+        }
+    };
+    if (n > 2 && ri == 0) reflector(0);
+    __syncthreads();
+    for (int k = 0; k + 2 < n; ++k) {
+        const double tk = tau[k];
+        const double* vk = V[k & 1];
+        const bool wact = 4 * warp + 3 > k && 4 * warp < n;
+        double pr = 0.0, vi = 0.0;
+        if (wact) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int u = 0; u < CPT; u += 2) {
+                s0 = fma(a[u], vk[rt + 8 * u], s0);
+                s1 = fma(a[u + 1], vk[rt + 8 * u + 8], s1);
+            }
+            pr = s0 + s1;
+            pr += __shfl_xor_sync(0xffffffffu, pr, 1);
+            pr += __shfl_xor_sync(0xffffffffu, pr, 2);
+            pr += __shfl_xor_sync(0xffffffffu, pr, 4);
+            vi = vk[ri];
+            pr = ri > k ? tk * pr : 0.0;
+            double pv = pr * vi;
+            pv += __shfl_xor_sync(0xffffffffu, pv, 8);
+            pv += __shfl_xor_sync(0xffffffffu, pv, 16);
+            if (lane == 0) red[warp] = pv;
+        } else if (lane == 0) {
+            red[warp] = 0.0;
+        }
+        if (rt == 0) P[ri] = pr;
+        __syncthreads();
+        if (wact) {
+            double pv2[NW];
+#pragma unroll
+            for (int w = 0; w < NW; w += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(&red[w]);
+                pv2[w] = t2.x;
+                pv2[w + 1] = t2.y;
+            }
+#pragma unroll
+            for (int h = NW / 2; h > 0; h >>= 1)
+#pragma unroll
+                for (int w = 0; w < h; ++w) pv2[w] += pv2[w + h];
+            const double K = 0.5 * tk * pv2[0];
+            const double wi = fma(-K, vi, pr);
+#pragma unroll
+            for (int u = 0; u < CPT; ++u) {
+                const int j = rt + 8 * u;
+                const double vj = vk[j];
+                a[u] -= fma(vi, fma(-K, vj, P[j]), wi * vj);
+            }
+        }
+        if (k + 3 < n && ri == k + 1) reflector(k + 1);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {  // trailing 2×2
+        const int j = rt + 8 * u;
+        if (ri == n - 2 && j == n - 2) dd[n - 2] = a[u];
+        if (ri == n - 1 && j == n - 1) dd[n - 1] = a[u];
+        if (ri == n - 1 && j == n - 2) ee[n - 2] = a[u];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double lo = 1e300, hi = -1e300;
+        for (int i = lane; i < n; i += 32) {
+            const double off = (i > 0 ? fabs(ee[i - 1]) : 0.0) + (i + 1 < n ? fabs(ee[i]) : 0.0);
+            lo = fmin(lo, dd[i] - off);
+            hi = fmax(hi, dd[i] + off);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        const double tn = fmax(fabs(lo), fabs(hi));
+        const double sc = tn > 0.0 && isfinite(tn) ? inv_pow2_of(tn) : 1.0;
+        for (int i = lane; i < NR + 8; i += 32) {
+            const double ep = (i >= 1 && i < n) ? ee[i - 1] * sc : 0.0;
+            de2[i] = make_double2(i < n ? dd[i] * sc : 8.0, ep * ep);
+        }
+        if (lane == 0) {
+            const double pad = 8.0 * kEps * n;
+            misc[0] = lo * sc - pad;
+            misc[1] = hi * sc + pad;
+            misc[2] = tn;
+            misc[3] = 1.0 / sc;
+        }
+    }
+    __syncthreads();
+    const double tn = misc[2];
+    if (!(tn > 0.0) || !isfinite(tn)) {
+        if (tid < n) lambda_out[tid] = tn == 0.0 ? 0.0 : tn;  // zero matrix, or NaN/Inf passed through
+        return;
+    }
+    const int j = ri;
+    const int jj = j < n ? j : n - 1;
+    double lo_b = misc[0], hi_b = misc[1];
+    for (int it = 0; it < 16; ++it) {
+        const double x = lo_b + (hi_b - lo_b) * (static_cast<double>(rt + 1) * (1.0 / 9.0));
+        double pm = 1.0, pc = de2[0].x - x;
+        unsigned sg = static_cast<unsigned>(__double2hiint(pc)) >> 31;
+        int cnt = static_cast<int>(sg);
+        for (int i0 = 1; i0 < n; i0 += 8) {
+            double2 q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q[u] = de2[i0 + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double pn = fma(q[u].x - x, pc, -q[u].y * pm);
+                pm = pc;
+                pc = pn;
+                const unsigned sn = static_cast<unsigned>(__double2hiint(pc)) >> 31;
+                cnt += static_cast<int>(sn ^ sg);
+                sg = sn;
+            }
+            const double m = fmax(fabs(pc), fabs(pm));
+            if (m > 0.0) {
+                const double f = inv_pow2_of(m);
+                pc *= f;
+                pm *= f;
+            }
+        }
+        const unsigned above = (__ballot_sync(0xffffffffu, cnt > jj) >> gbase) & 0xffu;
+        const int first = above ? __ffs(above) - 1 : 8;
+        const double x_hi = __shfl_sync(0xffffffffu, x, gbase + min(first, 7));
+        const double x_lo = __shfl_sync(0xffffffffu, x, gbase + max(first - 1, 0));
+        if (first < 8) hi_b = x_hi;
+        if (first > 0) lo_b = x_lo;
+    }
+    if (rt == 0 && j < n) lambda_out[n - 1 - j] = 0.5 * (lo_b + hi_b) * misc[3];  // descending, unscaled
+}
+
 }  // namespace
 
 bool jacobi_eig_forced() {
@@ -699,6 +893,15 @@ bool jacobi_eig_forced() {
         return e && std::string(e) == "jacobi";
     }();
     return on;
+}
+
+bool launch_sym_eigvals(const double* C, int64_t ldc, int n, double* lambda, CallScratch& sc) {
+    if (n < 1 || n > 128) return false;
+    if (n <= 64) eigvals_kernel<64><<<1, 512, 0, sc.stream()>>>(C, ldc, n, lambda);
+    else eigvals_kernel<128><<<1, 1024, 0, sc.stream()>>>(C, ldc, n, lambda);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+    return true;
 }
 
 bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, double* resid,

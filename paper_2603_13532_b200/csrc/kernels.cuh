@@ -151,6 +151,11 @@ void launch_gram_rank_check(const double* lam, int q, int cap, double eps, int o
 bool launch_sym_trd(const double* C, int64_t ldc, int n, double* lambda, double* V, int* flag, double* resid,
                     CallScratch& sc, int count = 1, int64_t strideC = 0, int64_t strideL = 0, int64_t strideV = 0);
 
+// Eigenvalues only (descending) of a symmetric n × n matrix, n ≤ 128, one CTA
+// (eig_trd.cu): register-resident tridiagonalisation + full-precision
+// multisection.  The plan stage's Gram eigenvalues.  False if n > 128.
+bool launch_sym_eigvals(const double* C, int64_t ldc, int n, double* lambda, CallScratch& sc);
+
 // X (rest × shape[mode]) = unfold(g, mode)ᵀ for a column-major tensor g.
 void launch_unfold_t(const double* g, int order, const int64_t* shape, int mode, double* X, CallScratch& sc);
 // Same for `count` tensors of one shape: device pointer arrays gs[count] → Xs[count].

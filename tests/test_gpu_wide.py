@@ -169,3 +169,13 @@ def test_plan_tall_stack_n4000(engine):
         eff, tg, wd = O.effective_subrank_krp(xs, ws, eps, p)
         plan = T.effective_subrank(xs, ws, eps, p, T.Strategy.Krp, engine=engine)
         assert plan.effective_ranks == eff and plan.targets == tg and plan.mode_sketch_dims == wd
+
+
+def test_plan_stack_beyond_128(engine):
+    """Plan stage with 150 stacked columns per mode (block one-sided Jacobi on the stack)."""
+    xs = shared_subspace(300, 3, 12, 150, (2603, 11))
+    ws = list(np.random.default_rng(11).uniform(0.5, 1.5, size=150))
+    eff, tg, wd = O.effective_subrank_krp(xs, ws, 1e-6, 2)
+    plan = T.effective_subrank(xs, ws, 1e-6, 2, T.Strategy.Krp, engine=engine)
+    assert plan.effective_ranks == eff == [12] * 3
+    assert plan.targets == tg and plan.mode_sketch_dims == wd
