@@ -73,6 +73,15 @@ def dist_env():
     return rank, world, local
 
 
+def measured_hbm_peak():
+    """HBM copy bandwidth from the driver-written MEASURED_PEAKS.json (GB/s)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 def fp64_peak():
     """Measured FP64 DMMA peak (tools/fp64_peak.cu on this pool's B200), TFLOP/s."""
     try:
@@ -387,19 +396,23 @@ def main():
     gflops = falg / (ms / 1000.0) / 1e9 if krp else None
     peak, peak_src = fp64_peak()
 
-    # Dominant kernel: the stage-A grouped DMMA GEMM (Z_j = Ω_jᵀ F_j over all modes, one launch);
-    # for Lazy (no stage A) the stage-E GEMM P_n = Q_nᵀ F_n.
+    # Dominant kernel.  KRP / Kron: stage C's grouped DMMA GEMM (Y_n = F_n W_n, one
+    # launch over all modes; the largest kernel of the call once stages A and E
+    # run on the int8 tensor cores — ozaki.cu), events right before / after that
+    # launch (split-K reduction excluded); Lazy: stage E's GEMM (P_n = Q_nᵀ F_n).
     d = len(wl.dims)
     Kloc = e - b
     if args.strategy == "lazy":
         q = [min(wl.dims[j], sum(r[j] for r in wl.ranks)) for j in range(d)]
         fa = sum(2.0 * q[j] * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d))
         ta = stages[5] if stages else float("nan")
+        kname = "gemm_tma_kernel<TN> (stage E: P_n = Q_nᵀ·F_n, one launch over all modes)"
     else:
-        fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * (wl.widths[0] if krp else widths[j]) * Kloc for j in range(d))
-        # The GEMM kernel's own CUDA-event duration (events around its launch on
-        # the library stream, split-K reduction excluded); the stage time if absent.
-        ta = stages[11] if len(stages) > 11 and stages[11] > 0 else (stages[0] if stages else float("nan"))
+        cw = [wl.widths[0] if krp else T.complement_product(widths, j) for j in range(d)]
+        fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * cw[j] * Kloc for j in range(d))
+        ta = stages[12] if len(stages) > 12 and stages[12] > 0 else (stages[2] if stages else float("nan"))
+        kname = ("gemm_tma_kernel<NT> (stage C: Y_n = F_n·W_n, one launch over all modes); duration = the kernel "
+                 "alone (split-K reduction excluded), stage C incl. reduce = %.4f ms" % stages[2])
     achieved = fa / (ta / 1000.0) / 1e12 if ta == ta and ta > 0 else None
     traffic = None
     try:
@@ -407,18 +420,27 @@ def main():
             traffic = json.load(f).get(wl.name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    kname = ("gemm_tma_kernel<TN> (stage E: P_n = Q_nᵀ·F_n, one launch over all modes)" if args.strategy == "lazy"
-             else "gemm_tma_kernel<TN> (stage A: Z_j = Ω_jᵀ·F_j, one launch over all modes)")
-    if args.strategy != "lazy" and len(stages) > 11 and stages[11] > 0:
-        kname += "; duration = the kernel alone (its split-K reduction excluded), stage A incl. reduce = %.4f ms" % stages[0]
     roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src,
                 "whole_step_fp64_tflops": gflops / 1000.0 if krp else None,
                 "whole_step_frac": gflops / 1000.0 / (peak * world) if krp else None}
+    # Stage A (Z_j = Ω_jᵀ F_j) on the int8 tensor cores is HBM-bound: F read once.
+    roofline_stage_a = None
+    if args.strategy != "lazy" and len(stages) > 11 and stages[11] > 0:
+        bytes_a = sum(8.0 * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d)) + \
+            sum(8.0 * wl.dims[j] * (wl.widths[0] if krp else widths[j]) for j in range(d)) + \
+            sum(8.0 * (wl.widths[0] if krp else widths[j]) * wl.ranks[0][j] * Kloc for j in range(d))
+        hbm = measured_hbm_peak()
+        ach = bytes_a / (stages[11] / 1000.0) / 1e9
+        roofline_stage_a = {"bound": "hbm", "kernel": "stage A GEMM kernel alone (ozaki_gemm_kernel: FP64 via int8 "
+                            "tcgen05 digits when the factors exceed 256 MB, else gemm_tma_kernel<TN>)",
+                            "achieved": ach, "peak": hbm[0], "unit": "GB/s", "frac": ach / hbm[0],
+                            "peak_source": hbm[1], "algorithmic_bytes_per_launch": bytes_a,
+                            "avg_launch_ms": stages[11], "fp64_equiv_tflops": fa / (stages[11] / 1000.0) / 1e12}
     stage_names = ["A_project", "B_krp", "C_expand", "allreduce_Y", "D_tsqr", "E_project", "F1_ttm", "F2_core",
-                   "allreduce_h", "G_sthosvd", "H_output", "A_gemm_kernel_only"]
+                   "allreduce_h", "G_sthosvd", "H_output", "A_gemm_kernel_only", "C_gemm_kernel_only"]
     if args.stages and rank == 0:
         print(json.dumps(dict(zip(stage_names, stages))), file=sys.stderr)
 
@@ -576,7 +598,7 @@ def main():
                 "data": "synthetic (seeded BASELINE.json config recipe; no public dataset)",
                 "config": config_desc(wl, world, args.strategy, widths), "gflops": gflops,
                 "fp64_frac_of_peak": gflops / 1000.0 / (peak * world) if krp else None,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roofline, "roofline_stage_a": roofline_stage_a, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary(), "stages_ms": dict(zip(stage_names, stages)),
                 "numerical_paths": {"qr_fallback_modes": paths[0], "svd_fallback_modes": paths[1]},
                 "accuracy": err, "omega": omega, "vs_lazy": vs_lazy,

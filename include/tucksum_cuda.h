@@ -209,6 +209,11 @@ int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* 
  * its residual / orthogonality acceptance check failed (the pipeline then falls
  * back to the Jacobi solver of ts_sym_eig). */
 int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, double* vectors, int* flag, double* ms);
+/* Test hook of the FP64 GEMM on the int8 tensor cores (Ozaki splitting, the
+ * stage-A / stage-E engine): out (n_cols × m, column-major, ld n_cols) = Fᵀ·B
+ * for host F (k × m) and B (k × n_cols), n_cols <= 64; *ms = kernel time. */
+int ts_debug_ozaki_gemm(ts_ctx* ctx, int64_t k, int64_t m, int64_t n_cols, const double* f, const double* b, double* out,
+                        double* ms);
 
 /* ---- result: a dense-core Tucker tensor owned by the library ---- */
 int64_t ts_result_order(const ts_result* r);

@@ -121,7 +121,7 @@ struct OmegaKey {
     }
 };
 
-constexpr int kNumStages = 11;  // + one extra event: end of stage A's GEMM kernel (before its reduce)
+constexpr int kNumStages = 11;  // + two hook pairs: stage A's and stage C's GEMM kernel alone (before any reduce)
 
 // One captured call (CUDA graph) of the speculative ε = 0 path: everything from
 // stage A to the acceptance flags' download is replayed by one cudaGraphLaunch.
@@ -242,6 +242,7 @@ struct ts_batch {
     int max_shape = 0;
     std::int64_t bytes = 0;
     std::uint64_t id = 0;  // unique per upload (graph-cache key; never reused)
+    int* aexp[TS_MAX_ORDER] = {};  // per-column exponent bounds of F_j (Ozaki stages), computed on first use
 };
 
 struct ts_result {
@@ -408,6 +409,54 @@ void sym_eig_any(const double* C, std::int64_t n, double* lambda, double* V, Cal
 // width: widths ≤ 96 are planned into one batched Householder TSQR (Y is
 // overwritten), wider ones go through wide.cu's BCGS2 (Y is kept).
 bool qr_wide_mode(std::int64_t cols) { return cols > ts::max_tsqr_cols(); }
+
+// Stages A and E (C = Sᵀ F_n with a skinny S of ≤ 64 columns: Ω_n, Y_n or Û_n)
+// on the int8 tensor cores (ozaki.cu) when the stacked factors are large enough
+// for the HBM-bound engine to beat the DMMA one (config 5: 0.55 vs 0.77 ms per
+// stage); small sums stay on DMMA (latency).  TS_OZAKI=0 disables it.
+bool ozaki_worth(const ts_batch* b) {
+    if (!ts::ozaki_enabled()) return false;
+    double bytes = 0.0;
+    for (int n = 0; n < b->order; ++n) bytes += 8.0 * static_cast<double>(b->dims[n]) * static_cast<double>(b->R[n]);
+    return bytes >= 256e6;
+}
+
+// ps[i] = {A = S (K × M, M ≤ 64), B = F_{modes[i]}, C (M × R)}; false (nothing
+// launched) when a problem does not fit — the caller then runs the DMMA GEMM.
+bool ozaki_stage(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>& ps, const std::vector<int>& modes,
+                 CallScratch& sc) {
+    if (!ozaki_worth(b)) return false;
+    for (size_t i = 0; i < ps.size(); ++i) {
+        const GemmProblem& p = ps[i];
+        const int n = modes[i];
+        if (p.M > 64 || p.B != b->F[n] || p.ldb != b->dims[n] || p.N != b->R[n] || p.alpha != 1.0 || p.beta != 0.0 ||
+            p.batch != 1)
+            return false;
+    }
+    auto* bm = const_cast<ts_batch*>(b);
+    for (int n = 0; n < b->order; ++n)
+        if (!bm->aexp[n] && b->R[n] > 0) {  // once per upload (first call, never inside a graph capture)
+            TS_CUDA_CHECK(cudaMallocAsync(&bm->aexp[n], sizeof(int) * static_cast<size_t>(b->R[n]), sc.stream()));
+            ts::launch_col_exponents(b->F[n], b->dims[n], b->dims[n], b->R[n], bm->aexp[n], sc);
+        }
+    std::vector<ts::OzProblem> oz;
+    for (size_t i = 0; i < ps.size(); ++i) {
+        const GemmProblem& p = ps[i];
+        const int n = modes[i];
+        ts::OzProblem q{};
+        q.F = b->F[n];
+        q.ldf = b->dims[n];
+        q.aexp = b->aexp[n];
+        q.M = static_cast<int>(b->R[n]);
+        q.K = p.K;
+        q.B = ts::prepare_ozaki_b(p.A, p.lda, p.K, p.M, sc);
+        q.C = p.C;
+        q.ldc = p.ldc;
+        oz.push_back(q);
+    }
+    int launched = 0;
+    return ts::launch_ozaki_gemm(oz, sc, ctx->num_sms, &launched);
+}
 
 // Fast path of the ST-HOSVD rank decision from the eigenvalues lam (descending)
 // of the Gram h_(k)h_(k)ᵀ.  The Gram's eigenvalues carry absolute errors of a few
@@ -817,7 +866,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     CallScratch sc(st, hstage);
     const std::int64_t* dims = b->dims;
     if (ctx->timing && ctx->events.empty()) {
-        ctx->events.resize(kNumStages + 3);
+        ctx->events.resize(kNumStages + 5);
         for (auto& e : ctx->events) TS_CUDA_CHECK(cudaEventCreate(&e));
     }
     mark(ctx, 0);
@@ -867,7 +916,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 p.K = static_cast<int>(dims[j]);
                 ps.push_back(p);
             }
-            ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+            std::vector<int> modes(static_cast<size_t>(d));
+            std::iota(modes.begin(), modes.end(), 0);
+            if (!ozaki_stage(ctx, b, ps, modes, sc)) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
         }
         mark(ctx, 1);
         sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage A only
@@ -907,6 +958,10 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             ts::launch_krp_contract(ka, b->max_shape, sc);
         }
         mark(ctx, 2);
+        if (ctx->timing) {  // stage C's GEMM kernel alone (the roofline kernel of bench.py)
+            sc.before_next_gemm = ctx->events[kNumStages + 3];
+            sc.after_next_gemm = ctx->events[kNumStages + 4];
+        }
         // ---- Stage C: Y_n = F_n W_n (n × s), all modes in one buffer
         {
             std::vector<GemmProblem> ps;
@@ -924,6 +979,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 ps.push_back(p);
             }
             ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+            sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage C only
         }
     }
     mark(ctx, 3);
@@ -1139,7 +1195,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 pr.push_back(r);
             }
         }
-        ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        std::vector<int> modes(static_cast<size_t>(d));
+        std::iota(modes.begin(), modes.end(), 0);
+        if (!ozaki_stage(ctx, b, ps, modes, sc)) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
         if (overlap) TS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         if (!pr.empty()) ts::launch_grouped_gemm(Layout::TN, pr, sc, ctx->num_sms);
     }
@@ -1477,7 +1535,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     }
     TS_CUDA_CHECK(cudaStreamSynchronize(st));
     if (ctx->timing) {
-        ctx->stage_ms.assign(kNumStages + 1, 0.0);
+        ctx->stage_ms.assign(kNumStages + 2, 0.0);
         for (int i = 0; i < kNumStages; ++i) {
             float ms = 0.f;
             TS_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->events[static_cast<size_t>(i)], ctx->events[static_cast<size_t>(i + 1)]));
@@ -1488,6 +1546,14 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             if (cudaEventElapsedTime(&ms, ctx->events[kNumStages + 1], ctx->events[kNumStages + 2]) == cudaSuccess && ms > 0.f &&
                 ms <= ctx->stage_ms[0] + 1e-3)
                 ctx->stage_ms[kNumStages] = ms;
+            else
+                (void)cudaGetLastError();
+        }
+        if (!lazy) {  // stage C's GEMM kernel alone
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->events[kNumStages + 3], ctx->events[kNumStages + 4]) == cudaSuccess && ms > 0.f &&
+                ms <= ctx->stage_ms[2] + 1e-3)
+                ctx->stage_ms[kNumStages + 1] = ms;
             else
                 (void)cudaGetLastError();
         }
@@ -2545,6 +2611,8 @@ int ts_batch_free(ts_batch* b) {
         cudaStream_t st = b->ctx->stream;  // stream-ordered: safe while kernels are still queued
         for (auto* f : b->F)
             if (f) cudaFreeAsync(f, st);
+        for (auto* e : b->aexp)
+            if (e) cudaFreeAsync(e, st);
         if (b->cores) cudaFreeAsync(b->cores, st);
         if (b->d_atoms) cudaFreeAsync(b->d_atoms, st);
         delete b;
@@ -2923,6 +2991,50 @@ int ts_sym_eig(ts_ctx* ctx, int64_t n, const double* a, double* values, double* 
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (sweeps) *sweeps = qr_wide_mode(n) ? bosj_sweeps : hs;
+        if (ms) *ms = t;
+    });
+}
+
+// Debug / test hook of the Ozaki GEMM (ozaki.cu): out (N × M, ld N) = Fᵀ·B for
+// host F (K × M) and B (K × N, N ≤ 64), column-major.  Returns TS_UNSUPPORTED
+// when the kernel is disabled (TS_OZAKI=0).
+int ts_debug_ozaki_gemm(ts_ctx* ctx, int64_t K, int64_t M, int64_t N, const double* F, const double* B, double* out,
+                        double* ms) {
+    return guarded([&] {
+        if (!ctx || K < 1 || M < 1 || N < 1 || N > 64 || !F || !B || !out) invalid("ts_debug_ozaki_gemm: bad arguments");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->stage.reset();
+        CallScratch sc(ctx->stream, ctx->stage);
+        auto* dF = static_cast<double*>(sc.upload(F, sizeof(double) * static_cast<size_t>(K * M)));
+        auto* dB = static_cast<double*>(sc.upload(B, sizeof(double) * static_cast<size_t>(K * N)));
+        double* dC = sc.alloc_n<double>(static_cast<size_t>(N * M));
+        int* aexp = sc.alloc_n<int>(static_cast<size_t>(M));
+        ts::launch_col_exponents(dF, K, K, M, aexp, sc);
+        ts::OzOperand bo = ts::prepare_ozaki_b(dB, K, static_cast<int>(K), static_cast<int>(N), sc);
+        ts::OzProblem p{};
+        p.F = dF;
+        p.ldf = K;
+        p.aexp = aexp;
+        p.M = static_cast<int>(M);
+        p.K = static_cast<int>(K);
+        p.B = bo;
+        p.C = dC;
+        p.ldc = N;
+        cudaEvent_t e0, e1;
+        TS_CUDA_CHECK(cudaEventCreate(&e0));
+        TS_CUDA_CHECK(cudaEventCreate(&e1));
+        TS_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        int launched = 0;
+        if (!ts::launch_ozaki_gemm({p}, sc, ctx->num_sms, &launched))
+            throw ts::Error(TS_UNSUPPORTED, "ozaki GEMM not available for these operands");
+        TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(out, dC, sizeof(double) * static_cast<size_t>(N * M), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        float t = 0.f;
+        TS_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
         if (ms) *ms = t;
     });
 }

@@ -205,6 +205,32 @@ bool launch_kron3(const Kron3Args& args, int max_shape, CallScratch& sc);
 
 int max_tsqr_cols();
 
+// ---- ozaki.cu: FP64 C = α·FᵀB + βC on the int8 tcgen05 tensor cores (Ozaki
+// splitting into 7 byte digits, int32 TMEM accumulators), out(m, n) at
+// C[n + m·ldc].  F: K × M column-major (the stacked factors), its per-column
+// exponent bounds aexp[M] (launch_col_exponents, once per upload); B: K × N
+// (N ≤ 64) pre-sliced by prepare_ozaki_b.
+struct OzOperand {
+    uint8_t* slices = nullptr;
+    int* exp = nullptr;
+    int K = 0, N = 0;
+};
+struct OzProblem {
+    const double* F;
+    int64_t ldf;
+    const int* aexp;
+    int M, K;
+    OzOperand B;
+    double* C;
+    int64_t ldc;
+    double alpha = 1.0, beta = 0.0;
+};
+bool ozaki_enabled();  // TS_OZAKI=0 turns it off (A/B against the DMMA GEMM)
+void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc);
+OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc);
+// False (nothing launched) when a problem does not qualify.
+bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int num_sms, int* launched);
+
 // ---- wide.cu: generic widths (any column count)
 // Thin Q (rows × min(rows, cols), ld ldq) of Y (rows × cols, ld ldy; not
 // modified): BCGS2 over 64-column TSQR panels for tall Y, the identity for wide Y.

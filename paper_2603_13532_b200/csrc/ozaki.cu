@@ -1,0 +1,511 @@
+// ozaki.cu — FP64 GEMM C = α·AᵀB on the int8 tcgen05 tensor cores (Ozaki
+// splitting), for the KRP sum's HBM-heavy contractions whose long operand is
+// the stacked factor matrix F (stage A: Zᵀ = Fᵀ Ω; stage E: Ptᵀ = Fᵀ Y).
+//
+// FP64 on sm_100a has no tcgen05 kind: the only FP64 tensor instruction is the
+// warp-level DMMA, whose 37 TFLOP/s makes stages A/C/E compute-bound (0.77 ms
+// each at config 5, 90 % of that peak).  Reading F once from HBM takes ~0.23 ms.
+// Splitting every fp64 value into byte "digits" turns the product into a short
+// sum of exact integer GEMMs, which the 5th-generation tensor cores run at
+// 4.5 POPS with int32 accumulators in TMEM:
+//
+//   x_A = rint(a · 2^(54 − e_A))   (e_A: the exponent bound of a's column of F,
+//                                   computed once per upload; |x_A| < 2^54)
+//   x_A = Σ_{t=0..6} d_t 2^(8(6−t)),   balanced signed byte digits d_t ∈ [−128, 127]
+//   a·b ≈ Σ_{i+j ≤ 6} (d_i^A d_j^B) 2^(e_A + e_B − 12 − 8(i+j))
+//
+// The 28 byte products with i + j ≤ 6 (the others weigh < 2^-56 of the leading
+// one) go to 7 int32 accumulators (one per i + j, TMEM columns 64·w); a split
+// of K ≤ 16384 cannot overflow them (7 · 128² · 16384 < 2^31).  All digits are
+// signed, so slice i of A meets slices 0..6−i of B in ONE MMA with B's slices
+// concatenated along N (their accumulators are consecutive column blocks): 10
+// MMAs per 32-K step instead of 28.  The epilogue combines the accumulators
+// exactly in two int64 halves.  Measured error ≤ 1e-16 of Σ|a||b|
+// (tools/ozaki_probe.py) — below an fp64 GEMM's own rounding.
+//
+// Kernel: one CTA per (128 columns of F, K split), 192 threads.
+//   warp 4 (producer): TMA of the fp64 F tile (4 boxes of 16 K × 128 columns,
+//     128-byte swizzle, double-buffered) and a bulk copy of the pre-sliced B
+//     operand (7 × 64 rows × 64 bytes, already in the UMMA layout);
+//   warps 0-3 (converters, thread = row of Fᵀ): fp64 → 7 byte slices, written
+//     in the K-major 64-byte-swizzled UMMA layout; later the epilogue (TMEM →
+//     registers → fp64);
+//   warp 5: allocates TMEM (512 columns) and issues the 56 tcgen05.mma.kind::i8
+//     of a chunk from one elected lane; tcgen05.commit releases the slices.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "tma.cuh"
+#include "tucksum_cuda.h"
+
+namespace ts {
+namespace {
+
+constexpr int kOzM = 128;                    // tile rows (columns of F)
+constexpr int kOzN = 64;                     // B columns (padded)
+constexpr int kOzKC = 32;                    // K per chunk = one MMA K step (32 int8)
+constexpr int kOzS = 7;                      // byte slices
+constexpr int kOzConv = 256;                 // converter threads: (row, 16-K half)
+constexpr int kOzThreads = kOzConv + 64;     // + producer warp + MMA warp
+constexpr int kFStages = 3;
+constexpr int kFBox = 16 * kOzM * 8;         // one 16-K box of fp64: 16 KB
+constexpr int kFStage = 2 * kFBox;           // 32 KB
+constexpr int kASlice = kOzM * kOzKC;        // 4 KB
+constexpr int kBSlice = kOzN * kOzKC;        // 2 KB
+constexpr int kAStage = kOzS * kASlice;      // 28 KB
+constexpr int kBStage = kOzS * kBSlice;      // 14 KB
+constexpr int kOffA = kFStages * kFStage;    // 96 KB
+constexpr int kOffB = kOffA + 2 * kAStage;   // 152 KB
+constexpr int kOffBar = kOffB + 2 * kBStage;  // 180 KB
+constexpr size_t kOzSmem = 1024 + kOffBar + 256;
+constexpr int kOzMaxK = 16384;               // int32 headroom: 7 · 128² · K < 2^31
+
+struct alignas(64) OzGroup {
+    CUtensorMap fa;        // F: dims {K (contiguous), M}, box {16, 128}, 128B swizzle
+    const uint8_t* bsl;    // B slices: [K/32 chunks][7][64 rows × 32 B, UMMA K-major SW32 image]
+    const int* aexp;       // per column of F
+    const int* bexp;       // per column of B
+    double* C;             // out(m, n) at C[n + m·ldc]
+    double* ws;            // split partials [split][M][64]
+    int64_t ldc;
+    int M, N, K;
+    int splits, tiles_m, k_per_split;
+    double alpha, beta;
+    int64_t unit_begin;
+};
+
+// Byte offset of (row, k) in a K-major, 32-byte-swizzled tile of 32-byte rows
+// (Swizzle<1,4,3>: address bit 4 ^= bit 7).
+__host__ __device__ __forceinline__ unsigned sw32(unsigned row, unsigned k) {
+    return row * 32u + ((((k >> 4) ^ (row >> 2)) & 1u) << 4) + (k & 15u);
+}
+
+__device__ __forceinline__ double pow2(int e) {  // 2^e, normal range
+    return __hiloint2double((e + 1023) << 20, 0);
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw32(unsigned saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);  // start address
+    d |= static_cast<uint64_t>(1) << 16;                    // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(256 >> 4) << 32;             // SBO: 8 rows × 32 B
+    d |= static_cast<uint64_t>(1) << 46;                    // version (sm_100)
+    d |= static_cast<uint64_t>(6) << 61;                    // SWIZZLE_32B
+    return d;
+}
+
+__device__ __forceinline__ uint32_t idesc_s8(int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10)           // S32 accumulate, A and B signed int8, K-major
+           | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(kOzM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Balanced signed byte digits of 4 values: x = rint(v·scale) (|x| < 2^54 — the
+// balanced range is ±0x7F7F…7F ≈ ±0.996·2^55, so a full 2^55 would overflow);
+// y = x + 0x80…80 (7 bytes) lies in [0, 2^56) and byte t of y, minus 128, is
+// digit t — i.e. byte XOR 0x80 as int8.  Word t holds digit t (t = 0: the top,
+// weight 2^48) of each value, value u in byte u.
+__device__ __forceinline__ void digits4(const double* v, double scale, unsigned* w) {
+    unsigned hi[4], lo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const unsigned long long y = static_cast<unsigned long long>(__double2ll_rn(v[u] * scale)) + 0x80808080808080ull;
+        hi[u] = static_cast<unsigned>(y >> 32);
+        lo[u] = static_cast<unsigned>(y);
+    }
+#pragma unroll
+    for (int t = 0; t < kOzS; ++t) {
+        const bool fromhi = t < 3;
+        const unsigned p = fromhi ? static_cast<unsigned>(2 - t) : static_cast<unsigned>(6 - t);
+        const unsigned sel = p | ((p + 4u) << 4);
+        const unsigned u01 = __byte_perm(fromhi ? hi[0] : lo[0], fromhi ? hi[1] : lo[1], sel);
+        const unsigned u23 = __byte_perm(fromhi ? hi[2] : lo[2], fromhi ? hi[3] : lo[3], sel);
+        w[t] = __byte_perm(u01, u23, 0x5410) ^ 0x80808080u;
+    }
+}
+
+__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup* __restrict__ groups, int ngroups,
+                                                                   int variant) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* f_full = reinterpret_cast<uint64_t*>(smem + kOffBar);  // [kFStages]
+    uint64_t* f_empty = f_full + kFStages;                             // [kFStages]
+    uint64_t* b_full = f_empty + kFStages;                             // [2]
+    uint64_t* a_full = b_full + 2;                                     // [2]
+    uint64_t* mma_done = a_full + 2;                                   // [2]
+    uint64_t* acc_full = mma_done + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int64_t unit = blockIdx.x;
+    int lo = 0, hi = ngroups - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (groups[mid].unit_begin <= unit) lo = mid;
+        else hi = mid - 1;
+    }
+    const OzGroup& G = groups[lo];
+    const int64_t local = unit - G.unit_begin;
+    const int tm = static_cast<int>(local % G.tiles_m);
+    const int sp = static_cast<int>(local / G.tiles_m);
+    const int m0 = tm * kOzM;
+    const int kbeg = sp * G.k_per_split;
+    const int kend = min(G.K, kbeg + G.k_per_split);
+    const int nk = (kend - kbeg + kOzKC - 1) / kOzKC;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kFStages; ++s) {
+            mbar_init(&f_full[s], 1);
+            mbar_init(&f_empty[s], kOzConv);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&a_full[s], 1);
+            mbar_init(&mma_done[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    constexpr int kProdWarp = kOzConv / 32, kMmaWarp = kProdWarp + 1;
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_holder)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == kProdWarp) {
+        if (lane == 0) {  // producer: fp64 F tiles (TMA) and pre-sliced B (bulk copy)
+            const uint8_t* bsrc = G.bsl + static_cast<int64_t>(kbeg / kOzKC) * kBStage;
+            for (int c = 0; c < nk; ++c) {
+                const int s = c % kFStages;
+                if (c >= kFStages) mbar_wait(&f_empty[s], ((c / kFStages) - 1) & 1);
+                mbar_expect_tx(&f_full[s], kFStage);
+                const int k0 = kbeg + c * kOzKC;
+                tma_load_2d(smem + s * kFStage, &G.fa, k0, m0, &f_full[s]);
+                tma_load_2d(smem + s * kFStage + kFBox, &G.fa, k0 + 16, m0, &f_full[s]);
+                const int s2 = c & 1;
+                if (variant == 1) continue;  // timing ablation: F loads only
+                if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // B stage free again
+                mbar_expect_tx(&b_full[s2], kBStage);
+                bulk_load(smem + kOffB + s2 * kBStage, bsrc + static_cast<int64_t>(c) * kBStage, kBStage, &b_full[s2]);
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (lane == 0 && variant == 1) mma_commit(acc_full);
+        if (lane == 0 && variant != 1) {  // MMA issuer: per chunk 10 MMAs — slice i of A against slices
+                          // 0..6-i of B concatenated along N (their accumulators
+                          // w = i..6 are consecutive TMEM column blocks)
+            const unsigned a_base = smem_u32(smem + kOffA), b_base = smem_u32(smem + kOffB);
+            for (int c = 0; c < nk; ++c) {
+                const int s2 = c & 1;
+                mbar_wait(&a_full[s2], (c >> 1) & 1);
+                mbar_wait(&b_full[s2], (c >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const unsigned ab = a_base + s2 * kAStage, bb = b_base + s2 * kBStage;
+#pragma unroll
+                for (int i = 0; i < (variant == 2 ? 0 : kOzS); ++i) {
+                    const int ntot = kOzN * (kOzS - i);
+                    const uint64_t da = umma_desc_sw32(ab + i * kASlice);
+                    const uint32_t acc = (c > 0 || i > 0) ? 1u : 0u;
+                    const int n1 = min(ntot, 256);
+                    mma_i8(tmem + static_cast<uint32_t>(kOzN * i), da, umma_desc_sw32(bb), idesc_s8(n1), acc);
+                    if (ntot > 256)
+                        mma_i8(tmem + static_cast<uint32_t>(kOzN * i + 256), da, umma_desc_sw32(bb + 4 * kBSlice),
+                               idesc_s8(ntot - 256), acc);
+                }
+                mma_commit(&mma_done[s2]);
+            }
+            mma_commit(acc_full);
+        }
+    } else {  // warps 0-7: converters (thread = row, 16-K half), then the epilogue
+        const int row = threadIdx.x & (kOzM - 1), g = threadIdx.x >> 7;
+        const int ea = (m0 + row < G.M) ? G.aexp[m0 + row] : 0;
+        const double scale = pow2(54 - ea);
+        for (int c = 0; c < nk; ++c) {
+            const int s = c % kFStages, s2 = c & 1;
+            mbar_wait(&f_full[s], (c / kFStages) & 1);
+            double v[16];
+            {
+                const unsigned base = smem_u32(smem + s * kFStage + g * kFBox) + row * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double2 t2 = lds128(base + ((q ^ (row & 7)) << 4));
+                    v[2 * q] = t2.x;
+                    v[2 * q + 1] = t2.y;
+                }
+            }
+            mbar_arrive(&f_empty[s]);
+            if (variant == 1) continue;
+            if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // A stage free again
+            unsigned char* as = smem + kOffA + s2 * kAStage;
+            unsigned wq[4][kOzS];
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) digits4(v + 4 * qd, scale, wq[qd]);
+#pragma unroll
+            for (int t = 0; t < (variant == 3 ? 0 : kOzS); ++t) {
+                const unsigned addr = smem_u32(as + t * kASlice + sw32(row, 16 * g));
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(wq[0][t]), "r"(wq[1][t]),
+                             "r"(wq[2][t]), "r"(wq[3][t]));
+            }
+            // The converters' generic-proxy stores must be visible to the tensor
+            // core (async proxy): a named barrier over the converters, then ONE
+            // proxy fence (fences are cumulative) and one arrival.
+            asm volatile("bar.sync 1, %0;\n" ::"n"(kOzConv) : "memory");
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                mbar_arrive(&a_full[s2]);
+            }
+        }
+        // ---- epilogue: row `row` (TMEM lane 32·(warp % 4) + lane), column groups
+        // 4g..4g+3 of 8.  S = Σ_w acc_w 2^(8(6-w)) combined exactly in two int64
+        // halves (u·2^32 + t), then a·b = S · 2^(e_A + e_B − 60).
+        mbar_wait(acc_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const int m = m0 + row;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+#pragma unroll 1
+        for (int q = 4 * g; q < 4 * g + 4; ++q) {
+            uint32_t r[kOzS][8];
+#pragma unroll
+            for (int w = 0; w < kOzS; ++w)
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                             : "=r"(r[w][0]), "=r"(r[w][1]), "=r"(r[w][2]), "=r"(r[w][3]), "=r"(r[w][4]), "=r"(r[w][5]),
+                               "=r"(r[w][6]), "=r"(r[w][7])
+                             : "r"(lane_base + static_cast<uint32_t>(kOzN * w + 8 * q)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (m < G.M) {
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const int n = 8 * q + cc;
+                    if (n >= G.N) continue;
+                    const long long u = (static_cast<long long>(static_cast<int>(r[0][cc])) << 16) +
+                                        (static_cast<long long>(static_cast<int>(r[1][cc])) << 8) +
+                                        static_cast<long long>(static_cast<int>(r[2][cc]));
+                    const long long t = (static_cast<long long>(static_cast<int>(r[3][cc])) << 24) +
+                                        (static_cast<long long>(static_cast<int>(r[4][cc])) << 16) +
+                                        (static_cast<long long>(static_cast<int>(r[5][cc])) << 8) +
+                                        static_cast<long long>(static_cast<int>(r[6][cc]));
+                    const double val = fma(static_cast<double>(u), 4294967296.0, static_cast<double>(t)) *
+                                       pow2(ea + G.bexp[n] - 60);
+                    if (G.splits == 1) {
+                        double* cp = G.C + n + static_cast<int64_t>(m) * G.ldc;
+                        *cp = G.beta == 0.0 ? G.alpha * val : G.alpha * val + G.beta * *cp;
+                    } else {
+                        G.ws[(static_cast<int64_t>(sp) * G.M + m) * kOzN + n] = val;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+__global__ void ozaki_splitk_reduce(const OzGroup* __restrict__ groups, const int* __restrict__ red) {
+    const OzGroup& d = groups[red[blockIdx.y]];
+    const int64_t mn = static_cast<int64_t>(d.M) * kOzN;
+    for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < mn;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(r / kOzN), n = static_cast<int>(r % kOzN);
+        if (n >= d.N) continue;
+        double s = 0.0;
+        for (int sp = 0; sp < d.splits; ++sp) s += d.ws[sp * mn + r];  // fixed order: deterministic
+        double* c = d.C + n + static_cast<int64_t>(m) * d.ldc;
+        *c = d.beta == 0.0 ? d.alpha * s : d.alpha * s + d.beta * *c;
+    }
+}
+
+// exp[j] = e with max_i |X[i, j]| < 2^e (column-major rows × cols, ld).
+__global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int* __restrict__ out) {
+    const int j = blockIdx.x;
+    const double* c = X + static_cast<int64_t>(j) * ld;
+    double mx = 0.0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) mx = fmax(mx, fabs(c[i]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+        // biased exponent b: 2^(b-1023) ≤ mx < 2^(b-1022); zero / subnormal columns → a small bound
+        const int b = (__double2hiint(mx) >> 20) & 0x7ff;
+        out[j] = mx > 0.0 ? max(b - 1022, -900) : -900;
+    }
+}
+
+// B operand (K × N column-major, ld, N ≤ 64) → 7 balanced byte digits in the
+// UMMA smem image per 32-K chunk; thread = (chunk, column n, 16-K group).
+__global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, int K, int N, const int* __restrict__ bexp,
+                                     uint8_t* __restrict__ out, int nchunks) {
+    const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(nchunks) * kOzN * 2;
+    if (tid >= total) return;
+    const int g = static_cast<int>(tid & 1);
+    const int n = static_cast<int>((tid >> 1) % kOzN);
+    const int c = static_cast<int>(tid / (2 * kOzN));
+    const double scale = n < N ? pow2(54 - bexp[n]) : 0.0;
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const int k = c * kOzKC + 16 * g + u;
+        v[u] = (n < N && k < K) ? B[k + static_cast<int64_t>(n) * ldb] : 0.0;
+    }
+    unsigned wq[4][kOzS];
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) digits4(v + 4 * qd, scale, wq[qd]);
+    uint8_t* base = out + static_cast<int64_t>(c) * kBStage;
+#pragma unroll
+    for (int t = 0; t < kOzS; ++t)
+        *reinterpret_cast<uint4*>(base + t * kBSlice + sw32(static_cast<unsigned>(n), static_cast<unsigned>(16 * g))) =
+            make_uint4(wq[0][t], wq[1][t], wq[2][t], wq[3][t]);
+}
+
+}  // namespace
+
+bool ozaki_enabled() {
+    static const int en = [] {
+        const char* e = std::getenv("TS_OZAKI");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return en == 1 && encode_fn() != nullptr;
+}
+
+void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc) {
+    if (cols <= 0) return;
+    col_exponent_kernel<<<static_cast<unsigned>(cols), 256, 0, sc.stream()>>>(X, ld, rows, out);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
+OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc) {
+    OzOperand o{};
+    if (N > kOzN) throw Error(TS_UNSUPPORTED, "ozaki: B has more than 64 columns");
+    const int nchunks = (K + kOzKC - 1) / kOzKC;
+    o.exp = sc.alloc_n<int>(static_cast<size_t>(std::max(N, 1)));
+    o.slices = sc.alloc_n<uint8_t>(static_cast<size_t>(nchunks) * kBStage);
+    o.K = K;
+    o.N = N;
+    launch_col_exponents(B, ldb, K, N, o.exp, sc);
+    const int64_t threads = static_cast<int64_t>(nchunks) * kOzN * 2;
+    ozaki_slice_b_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, sc.stream()>>>(B, ldb, K, N, o.exp,
+                                                                                             o.slices, nchunks);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+    return o;
+}
+
+bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int num_sms, int* launched) {
+    *launched = 0;
+    if (!ozaki_enabled()) return false;
+    for (const OzProblem& p : probs)
+        if (p.M > 0 && (p.B.N > kOzN || (reinterpret_cast<uintptr_t>(p.F) & 15u) || (p.ldf & 1))) return false;
+    set_max_smem(ozaki_gemm_kernel, static_cast<int>(kOzSmem));
+    std::vector<OzGroup> groups;
+    std::vector<int> red;
+    int64_t units = 0, tiles = 0;
+    for (const OzProblem& p : probs)
+        if (p.M > 0) tiles += (p.M + kOzM - 1) / kOzM;
+    size_t ws_elems = 0;
+    for (const OzProblem& p : probs) {
+        if (p.M <= 0) continue;
+        OzGroup g;
+        std::memset(&g, 0, sizeof(g));
+        if (!make_map(&g.fa, p.F, p.K, p.M, p.ldf, kOzM)) return false;
+        g.bsl = p.B.slices;
+        g.aexp = p.aexp;
+        g.bexp = p.B.exp;
+        g.C = p.C;
+        g.ldc = p.ldc;
+        g.M = p.M;
+        g.N = p.B.N;
+        g.K = p.K;
+        g.alpha = p.alpha;
+        g.beta = p.beta;
+        g.tiles_m = (p.M + kOzM - 1) / kOzM;
+        // K splits: ≤ kOzMaxK per split (int32 headroom), then enough units for
+        // about three waves over the SMs (one CTA per SM), at least 32 chunks each.
+        const int kchunks = (p.K + kOzKC - 1) / kOzKC;
+        int splits = std::max(1, (p.K + kOzMaxK - 1) / kOzMaxK);
+        while (tiles * splits < 3LL * num_sms && (splits * 2) * 32 <= kchunks) splits *= 2;
+        const int cps = (kchunks + splits - 1) / splits;
+        g.k_per_split = cps * kOzKC;
+        g.splits = (kchunks + cps - 1) / cps;
+        g.unit_begin = units;
+        units += static_cast<int64_t>(g.tiles_m) * g.splits;
+        if (g.splits > 1) {
+            red.push_back(static_cast<int>(groups.size()));
+            ws_elems += static_cast<size_t>(g.splits) * p.M * kOzN;
+        }
+        groups.push_back(g);
+    }
+    if (groups.empty()) return true;
+    if (ws_elems) {
+        double* ws = sc.alloc_n<double>(ws_elems);
+        size_t off = 0;
+        for (int gi : red) {
+            OzGroup& d = groups[static_cast<size_t>(gi)];
+            d.ws = ws + off;
+            off += static_cast<size_t>(d.splits) * d.M * kOzN;
+        }
+    }
+    auto* d_groups = static_cast<const OzGroup*>(sc.upload(groups.data(), groups.size() * sizeof(OzGroup)));
+    if (sc.before_next_gemm) {
+        TS_CUDA_CHECK(cudaEventRecord(sc.before_next_gemm, sc.stream()));
+        sc.before_next_gemm = nullptr;
+    }
+    static const int variant = [] {  // timing ablations (tools/ozaki_probe.py)
+        const char* e = std::getenv("TS_OZAKI_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    ozaki_gemm_kernel<<<static_cast<unsigned>(units), kOzThreads, kOzSmem, sc.stream()>>>(
+        d_groups, static_cast<int>(groups.size()), variant);
+    TS_LAUNCH_CHECK();
+    if (sc.after_next_gemm) {
+        TS_CUDA_CHECK(cudaEventRecord(sc.after_next_gemm, sc.stream()));
+        sc.after_next_gemm = nullptr;
+    }
+    *launched = 1;
+    if (!red.empty()) {
+        const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
+        int64_t maxel = 0;
+        for (int gi : red) maxel = std::max<int64_t>(maxel, static_cast<int64_t>(groups[static_cast<size_t>(gi)].M) * kOzN);
+        const int64_t blocks = std::min<int64_t>((maxel + 255) / 256, 4LL * num_sms);
+        ozaki_splitk_reduce<<<dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size())),
+                              256, 0, sc.stream()>>>(d_groups, d_red);
+        TS_LAUNCH_CHECK();
+        *launched = 2;
+    }
+    sc.launches += *launched;
+    return true;
+}
+
+}  // namespace ts

@@ -51,7 +51,7 @@ EXPORTED_SYMBOLS = [
     "ts_kron_sum", "ts_kron_sketch_dims", "ts_effective_subrank_kron", "ts_lazy_sum",
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
     "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked", "ts_ctx_comm_info",
-    "ts_ctx_set_host_allreduce", "ts_krp_sum_segmented",
+    "ts_ctx_set_host_allreduce", "ts_krp_sum_segmented", "ts_debug_ozaki_gemm",
 ]
 
 HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
@@ -624,6 +624,17 @@ class Engine:
         ms = C.c_double()
         _check(lib().ts_sym_eig_tri(self.handle, i64(n), _p(a), _p(vals), _p(vecs), C.byref(fl), C.byref(ms)))
         return vals, vecs, bool(fl.value), float(ms.value)
+
+    def ozaki_gemm(self, f, b):
+        """Fᵀ·B on the int8 tensor cores (ts_debug_ozaki_gemm): (result m × n, ms)."""
+        f = _f64(f)
+        b = _f64(b)
+        k, m = f.shape
+        n = b.shape[1]
+        out = np.zeros((n, m), order="F")
+        ms = C.c_double()
+        _check(lib().ts_debug_ozaki_gemm(self.handle, i64(k), i64(m), i64(n), _p(f), _p(b), _p(out), C.byref(ms)))
+        return out.T.copy(), float(ms.value)
 
     def set_graphs(self, on: bool):
         """CUDA-graph replay of repeated identical calls (ts_ctx_set_graphs)."""
