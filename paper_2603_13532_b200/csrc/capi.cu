@@ -185,6 +185,9 @@ struct ts_ctx {
     // entries beyond kOmegaMaxEntries / kOmegaMaxBytes are freed (together with
     // the captured graphs that read them).
     std::map<OmegaKey, OmegaEntry> omega;
+    // Ω_j pre-sliced for the int8 stage-A engine (ozaki.cu), keyed by the Ω_j
+    // device pointer; released with its Ω entry.
+    std::map<const double*, ts::OzOperand> oz_cache;
     std::int64_t omega_bytes = 0;
     std::uint64_t omega_clock = 0;
     std::uint64_t omega_pin = ~std::uint64_t(0);  // entries used at clock >= pin are never evicted
@@ -314,6 +317,18 @@ double* omega_get(ts_ctx* ctx, int order, const std::int64_t* dims, const std::i
         for (auto g = ctx->graph_cache.begin(); g != ctx->graph_cache.end();)
             g = (g->first.seed == lru->first.seed && g->first.stream == lru->first.stream) ? ctx->graph_cache.erase(g)
                                                                                          : std::next(g);
+        {  // its pre-sliced copies go with it
+            const double* lo = lru->second.ptr;
+            const double* hi = lo + lru->second.bytes / static_cast<std::int64_t>(sizeof(double));
+            for (auto c = ctx->oz_cache.begin(); c != ctx->oz_cache.end();)
+                if (c->first >= lo && c->first < hi) {
+                    cudaFree(c->second.slices);
+                    cudaFree(c->second.exp);
+                    c = ctx->oz_cache.erase(c);
+                } else {
+                    ++c;
+                }
+        }
         TS_CUDA_CHECK(cudaFree(lru->second.ptr));
         ctx->omega_bytes -= lru->second.bytes;
         ctx->omega.erase(lru);
@@ -424,7 +439,7 @@ bool ozaki_worth(const ts_batch* b) {
 // ps[i] = {A = S (K × M, M ≤ 64), B = F_{modes[i]}, C (M × R)}; false (nothing
 // launched) when a problem does not fit — the caller then runs the DMMA GEMM.
 bool ozaki_stage(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>& ps, const std::vector<int>& modes,
-                 CallScratch& sc) {
+                 CallScratch& sc, bool cached_small = false) {
     if (!ozaki_worth(b)) return false;
     for (size_t i = 0; i < ps.size(); ++i) {
         const GemmProblem& p = ps[i];
@@ -449,7 +464,29 @@ bool ozaki_stage(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>&
         q.aexp = b->aexp[n];
         q.M = static_cast<int>(b->R[n]);
         q.K = p.K;
-        q.B = ts::prepare_ozaki_b(p.A, p.lda, p.K, p.M, sc);
+        if (cached_small) {  // Ω_j: sliced once, kept with the Ω cache
+            ts_ctx* owner = ctx->parent ? ctx->parent : ctx;
+            std::lock_guard<std::mutex> lock(owner->omega_mu);
+            auto it = owner->oz_cache.find(p.A);
+            if (it == owner->oz_cache.end() || it->second.K != p.K || it->second.N != p.M) {
+                if (it != owner->oz_cache.end()) {
+                    TS_CUDA_CHECK(cudaStreamSynchronize(sc.stream()));
+                    cudaFree(it->second.slices);
+                    cudaFree(it->second.exp);
+                    owner->oz_cache.erase(it);
+                }
+                ts::OzOperand o{};
+                o.K = p.K;
+                o.N = p.M;
+                TS_CUDA_CHECK(cudaMalloc(&o.slices, ts::ozaki_b_bytes(p.K)));
+                TS_CUDA_CHECK(cudaMalloc(&o.exp, sizeof(int) * 64));
+                ts::prepare_ozaki_b_into(p.A, p.lda, p.K, p.M, o, sc);
+                it = owner->oz_cache.emplace(p.A, o).first;
+            }
+            q.B = it->second;
+        } else {
+            q.B = ts::prepare_ozaki_b(p.A, p.lda, p.K, p.M, sc);
+        }
         q.C = p.C;
         q.ldc = p.ldc;
         oz.push_back(q);
@@ -918,7 +955,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             }
             std::vector<int> modes(static_cast<size_t>(d));
             std::iota(modes.begin(), modes.end(), 0);
-            if (!ozaki_stage(ctx, b, ps, modes, sc)) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+            if (!ozaki_stage(ctx, b, ps, modes, sc, true)) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
         }
         mark(ctx, 1);
         sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage A only
@@ -2316,6 +2353,10 @@ int ts_ctx_destroy(ts_ctx* ctx) {
         cudaStreamSynchronize(ctx->stream);
         ctx->graph_cache.clear();
         for (auto& kv : ctx->omega) cudaFree(kv.second.ptr);
+        for (auto& kv : ctx->oz_cache) {
+            cudaFree(kv.second.slices);
+            cudaFree(kv.second.exp);
+        }
         for (auto& e : ctx->events) cudaEventDestroy(e);
         if (ctx->comm && nccl_api().CommDestroy) nccl_api().CommDestroy(ctx->comm);
         cudaStreamSynchronize(ctx->side);

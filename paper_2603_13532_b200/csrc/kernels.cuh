@@ -228,6 +228,9 @@ struct OzProblem {
 bool ozaki_enabled();  // TS_OZAKI=0 turns it off (A/B against the DMMA GEMM)
 void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc);
 OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc);
+// Same into caller-owned buffers (slices: ozaki_b_bytes(K) bytes, exp: 64 ints).
+size_t ozaki_b_bytes(int K);
+void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc);
 // False (nothing launched) when a problem does not qualify.
 bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int num_sms, int* launched);
 

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const unsigned ab = a_base + s2 * kAStage, bb = b_base + s2 * kBStage;
 #pragma unroll
-                for (int i = 0; i < (variant == 2 ? 0 : kOzS); ++i) {
+                for (int i = 0; i < (variant == 2 ? 0 : variant == 4 ? 1 : kOzS); ++i) {
                     const int ntot = kOzN * (kOzS - i);
                     const uint64_t da = umma_desc_sw32(ab + i * kASlice);
                     const uint32_t acc = (c > 0 || i > 0) ? 1u : 0u;
@@ -406,21 +406,28 @@ void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t col
     sc.launches += 1;
 }
 
+size_t ozaki_b_bytes(int K) { return static_cast<size_t>((K + kOzKC - 1) / kOzKC) * kBStage; }
+
 OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc) {
     OzOperand o{};
     if (N > kOzN) throw Error(TS_UNSUPPORTED, "ozaki: B has more than 64 columns");
-    const int nchunks = (K + kOzKC - 1) / kOzKC;
-    o.exp = sc.alloc_n<int>(static_cast<size_t>(std::max(N, 1)));
-    o.slices = sc.alloc_n<uint8_t>(static_cast<size_t>(nchunks) * kBStage);
+    o.exp = sc.alloc_n<int>(static_cast<size_t>(kOzN));
+    o.slices = sc.alloc_n<uint8_t>(ozaki_b_bytes(K));
     o.K = K;
     o.N = N;
+    prepare_ozaki_b_into(B, ldb, K, N, o, sc);
+    return o;
+}
+
+void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc) {
+    if (N > kOzN) throw Error(TS_UNSUPPORTED, "ozaki: B has more than 64 columns");
+    const int nchunks = (K + kOzKC - 1) / kOzKC;
     launch_col_exponents(B, ldb, K, N, o.exp, sc);
     const int64_t threads = static_cast<int64_t>(nchunks) * kOzN * 2;
     ozaki_slice_b_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, sc.stream()>>>(B, ldb, K, N, o.exp,
                                                                                              o.slices, nchunks);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
-    return o;
 }
 
 bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int num_sms, int* launched) {
