@@ -322,6 +322,157 @@ __global__ void __launch_bounds__(kThreads) krp3_dmma_kernel(KrpArgs args) {
             }
 }
 
+// Order 4, the krp3 idea one level deeper: for each (a2, a3) core slice G_s
+// (r0 × r1) two DMMA slice GEMMs t0 = G_s·M1 and t1 = G_sᵀ·M0 serve all four
+// modes — V0 += t0·(M2[a2]∘M3[a3]), V1 += t1·(M2[a2]∘M3[a3]) and, with
+// x = Σ_a0 M0∘t0, V2[a2] += x∘M3[a3], V3[a3] += x∘M2[a2] (V2 / V3 accumulate in
+// shared memory, one column per thread) — 4·r0·r1·s flops per slice instead
+// of the generic kernel's 4·(r⁴·s) per atom and mode.  One CTA per (atom, 64
+// sketch columns, a3 range); a3 ranges split the slice loop for few atoms
+// (partials summed by krp_split_reduce, deterministic).
+__global__ void __launch_bounds__(kThreads) krp4_dmma_kernel(KrpArgs args) {
+    const Atom& at = args.atoms[blockIdx.x];
+    const int c0 = blockIdx.y * kCT;
+    const int s = args.s;
+    const int r0 = at.shape[0], r1 = at.shape[1], r2 = at.shape[2], r3 = at.shape[3];
+    const int sp = blockIdx.z;
+    const int per = (r3 + args.splits - 1) / args.splits;
+    const int a3b = sp * per, a3e = min(r3, a3b + per);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int cw = warp * 16;
+
+    extern __shared__ __align__(16) double sm[];
+    double* M0s = sm;                        // 32 × k3MLD
+    double* M1s = M0s + k3Rows * k3MLD;      // 32 × k3MLD
+    double* Gs = M1s + k3Rows * k3MLD;       // 2 × 32 × k3GLD
+    double* M2s = Gs + 2 * k3Rows * k3GLD;   // r2 × kCT
+    double* M3s = M2s + r2 * kCT;            // r3 × kCT
+    double* V2s = M3s + r3 * kCT;            // r2 × kCT
+    double* V3s = V2s + r2 * kCT;            // r3 × kCT
+    for (int idx = tid; idx < k3Rows * kCT; idx += kThreads) {
+        const int a = idx / kCT, c = idx % kCT, cg = c0 + c;
+        M0s[a * k3MLD + c] = (a < r0 && cg < s) ? args.Z[0][cg + static_cast<int64_t>(at.col[0] + a) * s] : 0.0;
+        M1s[a * k3MLD + c] = (a < r1 && cg < s) ? args.Z[1][cg + static_cast<int64_t>(at.col[1] + a) * s] : 0.0;
+    }
+    for (int idx = tid; idx < r2 * kCT; idx += kThreads) {
+        const int a = idx / kCT, c = idx % kCT, cg = c0 + c;
+        M2s[idx] = cg < s ? args.Z[2][cg + static_cast<int64_t>(at.col[2] + a) * s] : 0.0;
+        V2s[idx] = 0.0;
+    }
+    for (int idx = tid; idx < r3 * kCT; idx += kThreads) {
+        const int a = idx / kCT, c = idx % kCT, cg = c0 + c;
+        M3s[idx] = cg < s ? args.Z[3][cg + static_cast<int64_t>(at.col[3] + a) * s] : 0.0;
+        V3s[idx] = 0.0;
+    }
+    for (int idx = tid; idx < 2 * k3Rows * k3GLD; idx += kThreads) Gs[idx] = 0.0;
+    __syncthreads();
+    const double* __restrict__ core = args.cores + at.core_off;
+    const int slice = r0 * r1;
+    const int nsl = (a3e - a3b) * r2;  // slices (a2, a3) of this CTA, a2 fastest
+    auto load_slice = [&](int li, int buf) {
+        const int a2 = li % r2, a3 = a3b + li / r2;
+        double* dst = Gs + buf * k3Rows * k3GLD;
+        const double* src = core + static_cast<int64_t>(a2 + r2 * a3) * slice;
+        for (int idx = tid; idx < slice; idx += kThreads) {
+            const int i = idx % r0, j = idx / r0;
+            cp_async8(dst + i + j * k3GLD, src + idx, 8);
+        }
+    };
+    double v0[4][2][2], v1[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) v0[i][j][0] = v0[i][j][1] = v1[i][j][0] = v1[i][j][1] = 0.0;
+
+    if (nsl > 0) load_slice(0, 0);
+    cp_async_commit();
+    for (int li = 0; li < nsl; ++li) {
+        const int buf = li & 1;
+        const int a2 = li % r2, a3 = a3b + li / r2;
+        if (li + 1 < nsl) load_slice(li + 1, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* G = Gs + buf * k3Rows * k3GLD;
+        double t0[4][2][2], t1[4][2][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) t0[i][j][0] = t0[i][j][1] = t1[i][j][0] = t1[i][j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < k3Rows; kk += 4) {
+            double a0f[4], a1f[4], b1f[2], b0f[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a0f[i] = G[(8 * i + g) + (kk + t) * k3GLD];
+                a1f[i] = G[(kk + t) + (8 * i + g) * k3GLD];
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                b1f[j] = M1s[(kk + t) * k3MLD + cw + 8 * j + g];
+                b0f[j] = M0s[(kk + t) * k3MLD + cw + 8 * j + g];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    dmma884(t0[i][j][0], t0[i][j][1], a0f[i], b1f[j]);
+                    dmma884(t1[i][j][0], t1[i][j][1], a1f[i], b0f[j]);
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = cw + 8 * j + 2 * t + h;
+                const double m2 = M2s[a2 * kCT + c], m3 = M3s[a3 * kCT + c];
+                const double m23 = m2 * m3;
+                double part = 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v0[i][j][h] = fma(t0[i][j][h], m23, v0[i][j][h]);
+                    v1[i][j][h] = fma(t1[i][j][h], m23, v1[i][j][h]);
+                    part = fma(M0s[(8 * i + g) * k3MLD + c], t0[i][j][h], part);
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 4);
+                part += __shfl_xor_sync(0xffffffffu, part, 8);
+                part += __shfl_xor_sync(0xffffffffu, part, 16);
+                if (g == 0) {  // column c belongs to this lane alone
+                    V2s[a2 * kCT + c] = fma(part, m3, V2s[a2 * kCT + c]);
+                    V3s[a3 * kCT + c] = fma(part, m2, V3s[a3 * kCT + c]);
+                }
+            }
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+    const double w = args.weights[at.summand];
+    double* Wout[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+        Wout[n] = args.splits == 1 ? args.W[n] : args.Wpart[n] + static_cast<int64_t>(sp) * args.R[n] * s;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int a = 8 * i + g;
+                const int cg = c0 + cw + 8 * j + 2 * t + h;
+                if (cg >= s) continue;
+                if (a < r0) Wout[0][cg + static_cast<int64_t>(at.col[0] + a) * s] = w * v0[i][j][h];
+                if (a < r1) Wout[1][cg + static_cast<int64_t>(at.col[1] + a) * s] = w * v1[i][j][h];
+            }
+    for (int idx = tid; idx < r2 * kCT; idx += kThreads) {
+        const int a = idx / kCT, cg = c0 + idx % kCT;
+        if (cg < s) Wout[2][cg + static_cast<int64_t>(at.col[2] + a) * s] = w * V2s[idx];
+    }
+    for (int idx = tid; idx < r3 * kCT; idx += kThreads) {
+        const int a = idx / kCT, cg = c0 + idx % kCT;
+        if (cg < s) Wout[3][cg + static_cast<int64_t>(at.col[3] + a) * s] = w * V3s[idx];
+    }
+}
+
 }  // namespace
 
 // Wt_n = Σ_split Wpart[split] in split order (deterministic).
@@ -353,6 +504,27 @@ void launch_krp_contract(const KrpArgs& args_in, int max_shape, CallScratch& sc)
         krp3_dmma_kernel<<<grid, kThreads, smem, sc.stream()>>>(args);
         TS_LAUNCH_CHECK();
         sc.launches += 1;
+        return;
+    }
+    if (use3 && args.order == 4 && max_shape <= k3Rows) {
+        // a3 splits so that few atoms still cover the SMs (about two waves)
+        const int cchunks4 = (args.s + kCT - 1) / kCT;
+        const int64_t base4 = static_cast<int64_t>(args.natoms) * cchunks4;
+        args.splits = static_cast<int>(std::clamp<int64_t>((2 * 148 + base4 - 1) / base4, 1, std::max(1, max_shape)));
+        if (args.splits > 1)
+            for (int n = 0; n < 4; ++n)
+                args.Wpart[n] = sc.alloc_n<double>(static_cast<size_t>(args.splits * args.R[n] * args.s));
+        const size_t smem = sizeof(double) * (2 * k3Rows * k3MLD + 2 * k3Rows * k3GLD + 4 * static_cast<size_t>(max_shape) * kCT);
+        set_max_smem(krp4_dmma_kernel, 160 * 1024);
+        dim3 grid(static_cast<unsigned>(args.natoms), static_cast<unsigned>(cchunks4), static_cast<unsigned>(args.splits));
+        krp4_dmma_kernel<<<grid, kThreads, smem, sc.stream()>>>(args);
+        TS_LAUNCH_CHECK();
+        sc.launches += 1;
+        if (args.splits > 1) {
+            krp_split_reduce<<<dim3(64, 4), 256, 0, sc.stream()>>>(args);
+            TS_LAUNCH_CHECK();
+            sc.launches += 1;
+        }
         return;
     }
     const int RT = max_shape <= 32 ? 32 : 64;
