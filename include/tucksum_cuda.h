@@ -214,6 +214,10 @@ int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, doub
  * for host F (k × m) and B (k × n_cols), n_cols <= 64; *ms = kernel time. */
 int ts_debug_ozaki_gemm(ts_ctx* ctx, int64_t k, int64_t m, int64_t n_cols, const double* f, const double* b, double* out,
                         double* ms);
+/* The same engine in stage C's orientation: out (m × n_cols, column-major) =
+ * A·Btᵀ for host A (m × k, column-major) and Bt (n_cols × k), n_cols <= 64. */
+int ts_debug_ozaki_gemm_nt(ts_ctx* ctx, int64_t m, int64_t k, int64_t n_cols, const double* a, const double* bt,
+                           double* out, double* ms);
 
 /* ---- result: a dense-core Tucker tensor owned by the library ---- */
 int64_t ts_result_order(const ts_result* r);

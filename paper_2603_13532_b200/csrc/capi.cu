@@ -245,7 +245,8 @@ struct ts_batch {
     int max_shape = 0;
     std::int64_t bytes = 0;
     std::uint64_t id = 0;  // unique per upload (graph-cache key; never reused)
-    int* aexp[TS_MAX_ORDER] = {};  // per-column exponent bounds of F_j (Ozaki stages), computed on first use
+    int* aexp[TS_MAX_ORDER] = {};  // per-column exponent bounds of F_j (Ozaki stages A/E), computed on first use
+    int* rexp[TS_MAX_ORDER] = {};  // per-row exponent bounds of F_j (Ozaki stage C), computed on first use
 };
 
 struct ts_result {
@@ -489,6 +490,42 @@ bool ozaki_stage(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>&
         }
         q.C = p.C;
         q.ldc = p.ldc;
+        oz.push_back(q);
+    }
+    int launched = 0;
+    return ts::launch_ozaki_gemm(oz, sc, ctx->num_sms, &launched);
+}
+
+// Stage C (Y_n = F_n W_n with W_n stored transposed, ≤ 64 columns) on the same
+// engine in its M-contiguous orientation: per-row exponent bounds of F_n.
+bool ozaki_stage_c(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>& ps, CallScratch& sc) {
+    if (!ozaki_worth(b)) return false;
+    for (size_t n = 0; n < ps.size(); ++n) {
+        const GemmProblem& p = ps[n];
+        if (p.N > 64 || p.A != b->F[n] || p.lda != b->dims[n] || p.K != b->R[n] || p.alpha != 1.0 || p.beta != 0.0 ||
+            p.batch != 1)
+            return false;
+    }
+    auto* bm = const_cast<ts_batch*>(b);
+    for (int n = 0; n < b->order; ++n)
+        if (!bm->rexp[n] && b->dims[n] > 0) {  // once per upload (first call, never inside a graph capture)
+            TS_CUDA_CHECK(cudaMallocAsync(&bm->rexp[n], sizeof(int) * static_cast<size_t>(b->dims[n]), sc.stream()));
+            ts::launch_row_exponents(b->F[n], b->dims[n], b->dims[n], b->R[n], bm->rexp[n], sc);
+        }
+    std::vector<ts::OzProblem> oz;
+    for (size_t n = 0; n < ps.size(); ++n) {
+        const GemmProblem& p = ps[n];
+        ts::OzProblem q{};
+        q.F = b->F[n];
+        q.ldf = b->dims[n];
+        q.aexp = b->rexp[n];
+        q.M = p.M;
+        q.K = p.K;
+        q.B = ts::prepare_ozaki_b(p.B, p.ldb, p.K, p.N, sc, true);
+        q.C = p.C;
+        q.ldc = p.ldc;
+        q.a_mn = true;
+        q.c_colmajor = true;
         oz.push_back(q);
     }
     int launched = 0;
@@ -1015,7 +1052,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 p.K = static_cast<int>(b->R[n]);
                 ps.push_back(p);
             }
-            ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+            if (!ozaki_stage_c(ctx, b, ps, sc)) ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
             sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage C only
         }
     }
@@ -2654,6 +2691,8 @@ int ts_batch_free(ts_batch* b) {
             if (f) cudaFreeAsync(f, st);
         for (auto* e : b->aexp)
             if (e) cudaFreeAsync(e, st);
+        for (auto* e : b->rexp)
+            if (e) cudaFreeAsync(e, st);
         if (b->cores) cudaFreeAsync(b->cores, st);
         if (b->d_atoms) cudaFreeAsync(b->d_atoms, st);
         delete b;
@@ -3061,6 +3100,51 @@ int ts_debug_ozaki_gemm(ts_ctx* ctx, int64_t K, int64_t M, int64_t N, const doub
         p.B = bo;
         p.C = dC;
         p.ldc = N;
+        cudaEvent_t e0, e1;
+        TS_CUDA_CHECK(cudaEventCreate(&e0));
+        TS_CUDA_CHECK(cudaEventCreate(&e1));
+        TS_CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+        int launched = 0;
+        if (!ts::launch_ozaki_gemm({p}, sc, ctx->num_sms, &launched))
+            throw ts::Error(TS_UNSUPPORTED, "ozaki GEMM not available for these operands");
+        TS_CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+        TS_CUDA_CHECK(cudaMemcpyAsync(out, dC, sizeof(double) * static_cast<size_t>(N * M), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        TS_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        float t = 0.f;
+        TS_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (ms) *ms = t;
+    });
+}
+
+// Same engine in the stage-C orientation: out (M × N, column-major) = A·Btᵀ for
+// host A (M × K, column-major: M contiguous) and Bt (N × K, N ≤ 64).
+int ts_debug_ozaki_gemm_nt(ts_ctx* ctx, int64_t M, int64_t K, int64_t N, const double* A, const double* Bt, double* out,
+                           double* ms) {
+    return guarded([&] {
+        if (!ctx || K < 1 || M < 1 || N < 1 || N > 64 || !A || !Bt || !out) invalid("ts_debug_ozaki_gemm_nt: bad arguments");
+        TS_CUDA_CHECK(cudaSetDevice(ctx->device));
+        ctx->stage.reset();
+        CallScratch sc(ctx->stream, ctx->stage);
+        auto* dA = static_cast<double*>(sc.upload(A, sizeof(double) * static_cast<size_t>(K * M)));
+        auto* dB = static_cast<double*>(sc.upload(Bt, sizeof(double) * static_cast<size_t>(K * N)));
+        double* dC = sc.alloc_n<double>(static_cast<size_t>(N * M));
+        int* aexp = sc.alloc_n<int>(static_cast<size_t>(M));
+        ts::launch_row_exponents(dA, M, M, K, aexp, sc);
+        ts::OzOperand bo = ts::prepare_ozaki_b(dB, N, static_cast<int>(K), static_cast<int>(N), sc, true);
+        ts::OzProblem p{};
+        p.F = dA;
+        p.ldf = M;
+        p.aexp = aexp;
+        p.M = static_cast<int>(M);
+        p.K = static_cast<int>(K);
+        p.B = bo;
+        p.C = dC;
+        p.ldc = M;
+        p.a_mn = true;
+        p.c_colmajor = true;
         cudaEvent_t e0, e1;
         TS_CUDA_CHECK(cudaEventCreate(&e0));
         TS_CUDA_CHECK(cudaEventCreate(&e1));

@@ -218,19 +218,24 @@ struct OzOperand {
 struct OzProblem {
     const double* F;
     int64_t ldf;
-    const int* aexp;
+    const int* aexp;  // per m (a column of F; a row when a_mn)
     int M, K;
     OzOperand B;
     double* C;
     int64_t ldc;
     double alpha = 1.0, beta = 0.0;
+    bool a_mn = false;       // F(k, m) stored at F[m + k·ldf] (M contiguous) instead of F[k + m·ldf]
+    bool c_colmajor = false;  // out(m, n) at C[m + n·ldc]
 };
 bool ozaki_enabled();  // TS_OZAKI=0 turns it off (A/B against the DMMA GEMM)
 void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc);
-OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc);
+// trans: B(k, n) is stored at B[n + k·ldb].
+OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc, bool trans = false);
+void launch_row_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc);
 // Same into caller-owned buffers (slices: ozaki_b_bytes(K) bytes, exp: 64 ints).
 size_t ozaki_b_bytes(int K);
-void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc);
+void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc,
+                          bool trans = false);
 // False (nothing launched) when a problem does not qualify.
 bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int num_sms, int* launched);
 

@@ -77,6 +77,8 @@ struct alignas(64) OzGroup {
     int64_t ldc;
     int M, N, K;
     int splits, tiles_m, k_per_split;
+    int a_mn;              // F stored M-contiguous (stage C: F_n as the n × R left operand)
+    int c_colmajor;        // out(m, n) at C[m + n·ldc] instead of C[n + m·ldc]
     double alpha, beta;
     int64_t unit_begin;
 };
@@ -209,8 +211,13 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                 if (c >= kFStages) mbar_wait(&f_empty[s], ((c / kFStages) - 1) & 1);
                 mbar_expect_tx(&f_full[s], kFStage);
                 const int k0 = kbeg + c * kOzKC;
-                tma_load_2d(smem + s * kFStage, &G.fa, k0, m0, &f_full[s]);
-                tma_load_2d(smem + s * kFStage + kFBox, &G.fa, k0 + 16, m0, &f_full[s]);
+                if (G.a_mn) {  // 8 boxes of 16 m × 32 k (m contiguous)
+                    for (int b = 0; b < 8; ++b)
+                        tma_load_2d(smem + s * kFStage + b * (kFStage / 8), &G.fa, m0 + 16 * b, k0, &f_full[s]);
+                } else {       // 2 boxes of 16 k × 128 m (k contiguous)
+                    tma_load_2d(smem + s * kFStage, &G.fa, k0, m0, &f_full[s]);
+                    tma_load_2d(smem + s * kFStage + kFBox, &G.fa, k0 + 16, m0, &f_full[s]);
+                }
                 const int s2 = c & 1;
                 if (variant == 1) continue;  // timing ablation: F loads only
                 if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // B stage free again
@@ -253,7 +260,15 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
             const int s = c % kFStages, s2 = c & 1;
             mbar_wait(&f_full[s], (c / kFStages) & 1);
             double v[16];
-            {
+            if (G.a_mn) {  // box row/16: line k (32 lines of 128 B), element row%16 in it
+                const unsigned base = smem_u32(smem + s * kFStage + (row >> 4) * (kFStage / 8));
+                const int e = row & 15;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int k = 16 * g + u;
+                    v[u] = lds64(base + k * 128 + ((((e >> 1) ^ (k & 7)) << 4) | ((e & 1) << 3)));
+                }
+            } else {
                 const unsigned base = smem_u32(smem + s * kFStage + g * kFBox) + row * 128;
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -316,7 +331,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                     const double val = fma(static_cast<double>(u), 4294967296.0, static_cast<double>(t)) *
                                        pow2(ea + G.bexp[n] - 60);
                     if (G.splits == 1) {
-                        double* cp = G.C + n + static_cast<int64_t>(m) * G.ldc;
+                        double* cp = G.c_colmajor ? G.C + m + static_cast<int64_t>(n) * G.ldc
+                                                  : G.C + n + static_cast<int64_t>(m) * G.ldc;
                         *cp = G.beta == 0.0 ? G.alpha * val : G.alpha * val + G.beta * *cp;
                     } else {
                         G.ws[(static_cast<int64_t>(sp) * G.M + m) * kOzN + n] = val;
@@ -339,17 +355,20 @@ __global__ void ozaki_splitk_reduce(const OzGroup* __restrict__ groups, const in
         if (n >= d.N) continue;
         double s = 0.0;
         for (int sp = 0; sp < d.splits; ++sp) s += d.ws[sp * mn + r];  // fixed order: deterministic
-        double* c = d.C + n + static_cast<int64_t>(m) * d.ldc;
+        double* c = d.c_colmajor ? d.C + m + static_cast<int64_t>(n) * d.ldc : d.C + n + static_cast<int64_t>(m) * d.ldc;
         *c = d.beta == 0.0 ? d.alpha * s : d.alpha * s + d.beta * *c;
     }
 }
 
-// exp[j] = e with max_i |X[i, j]| < 2^e (column-major rows × cols, ld).
-__global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int* __restrict__ out) {
+// exp[j] = e with max_i |X[j·ld + i·es]| < 2^e: a block per vector j of `rows`
+// elements (es = 1: the columns of a column-major matrix; es = ld of the
+// stored matrix, ld = 1: its rows).
+__global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t es,
+                                    int* __restrict__ out) {
     const int j = blockIdx.x;
     const double* c = X + static_cast<int64_t>(j) * ld;
     double mx = 0.0;
-    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) mx = fmax(mx, fabs(c[i]));
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) mx = fmax(mx, fabs(c[i * es]));
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     __shared__ double red[32];
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -362,10 +381,21 @@ __global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, in
     }
 }
 
+// exp[i] = e with max_j |X[i, j]| < 2^e (column-major rows × cols, ld): thread per row.
+__global__ void row_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t cols,
+                                    int* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= rows) return;
+    double mx = 0.0;
+    for (int64_t j = 0; j < cols; ++j) mx = fmax(mx, fabs(X[i + j * ld]));
+    const int b = (__double2hiint(mx) >> 20) & 0x7ff;
+    out[i] = mx > 0.0 ? max(b - 1022, -900) : -900;
+}
+
 // B operand (K × N column-major, ld, N ≤ 64) → 7 balanced byte digits in the
 // UMMA smem image per 32-K chunk; thread = (chunk, column n, 16-K group).
 __global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, int K, int N, const int* __restrict__ bexp,
-                                     uint8_t* __restrict__ out, int nchunks) {
+                                     uint8_t* __restrict__ out, int nchunks, int trans) {
     const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     const int64_t total = static_cast<int64_t>(nchunks) * kOzN * 2;
     if (tid >= total) return;
@@ -377,7 +407,7 @@ __global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, 
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
         const int k = c * kOzKC + 16 * g + u;
-        v[u] = (n < N && k < K) ? B[k + static_cast<int64_t>(n) * ldb] : 0.0;
+        v[u] = (n < N && k < K) ? (trans ? B[n + static_cast<int64_t>(k) * ldb] : B[k + static_cast<int64_t>(n) * ldb]) : 0.0;
     }
     unsigned wq[4][kOzS];
 #pragma unroll
@@ -399,33 +429,46 @@ bool ozaki_enabled() {
     return en == 1 && encode_fn() != nullptr;
 }
 
+void launch_row_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc) {
+    if (rows <= 0) return;
+    row_exponent_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, sc.stream()>>>(X, ld, rows, cols, out);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
 void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc) {
     if (cols <= 0) return;
-    col_exponent_kernel<<<static_cast<unsigned>(cols), 256, 0, sc.stream()>>>(X, ld, rows, out);
+    col_exponent_kernel<<<static_cast<unsigned>(cols), 256, 0, sc.stream()>>>(X, ld, rows, 1, out);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
 
 size_t ozaki_b_bytes(int K) { return static_cast<size_t>((K + kOzKC - 1) / kOzKC) * kBStage; }
 
-OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc) {
+OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc, bool trans) {
     OzOperand o{};
     if (N > kOzN) throw Error(TS_UNSUPPORTED, "ozaki: B has more than 64 columns");
     o.exp = sc.alloc_n<int>(static_cast<size_t>(kOzN));
     o.slices = sc.alloc_n<uint8_t>(ozaki_b_bytes(K));
     o.K = K;
     o.N = N;
-    prepare_ozaki_b_into(B, ldb, K, N, o, sc);
+    prepare_ozaki_b_into(B, ldb, K, N, o, sc, trans);
     return o;
 }
 
-void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc) {
+void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc, bool trans) {
     if (N > kOzN) throw Error(TS_UNSUPPORTED, "ozaki: B has more than 64 columns");
     const int nchunks = (K + kOzKC - 1) / kOzKC;
-    launch_col_exponents(B, ldb, K, N, o.exp, sc);
+    if (trans) {  // B(k, n) = stored[n + k·ld]: the stored matrix's rows, a block each
+        col_exponent_kernel<<<static_cast<unsigned>(N), 256, 0, sc.stream()>>>(B, 1, K, ldb, o.exp);
+        TS_LAUNCH_CHECK();
+        sc.launches += 1;
+    } else {
+        launch_col_exponents(B, ldb, K, N, o.exp, sc);
+    }
     const int64_t threads = static_cast<int64_t>(nchunks) * kOzN * 2;
     ozaki_slice_b_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, sc.stream()>>>(B, ldb, K, N, o.exp,
-                                                                                             o.slices, nchunks);
+                                                                                             o.slices, nchunks, trans ? 1 : 0);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
@@ -446,7 +489,10 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
         if (p.M <= 0) continue;
         OzGroup g;
         std::memset(&g, 0, sizeof(g));
-        if (!make_map(&g.fa, p.F, p.K, p.M, p.ldf, kOzM)) return false;
+        if (p.a_mn ? !make_map_box(&g.fa, p.F, p.M, p.K, p.ldf, 16, kOzKC) : !make_map(&g.fa, p.F, p.K, p.M, p.ldf, kOzM))
+            return false;
+        g.a_mn = p.a_mn ? 1 : 0;
+        g.c_colmajor = p.c_colmajor ? 1 : 0;
         g.bsl = p.B.slices;
         g.aexp = p.aexp;
         g.bexp = p.B.exp;

@@ -68,5 +68,19 @@ inline bool make_map(CUtensorMap* map, const double* ptr, int64_t dim0, int64_t 
 }
 
 
+// Same with an explicit box {box0 (≤ 16 elements = 128 B), box1}.
+inline bool make_map_box(CUtensorMap* map, const double* ptr, int64_t dim0, int64_t dim1, int64_t ld, int box0, int box1) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t gdim[2] = {static_cast<cuuint64_t>(dim0), static_cast<cuuint64_t>(dim1)};
+    cuuint64_t gstride[1] = {static_cast<cuuint64_t>(ld) * 8};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace
 }  // namespace ts

@@ -52,6 +52,7 @@ EXPORTED_SYMBOLS = [
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
     "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked", "ts_ctx_comm_info",
     "ts_ctx_set_host_allreduce", "ts_krp_sum_segmented", "ts_debug_ozaki_gemm",
+    "ts_debug_ozaki_gemm_nt",
 ]
 
 HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
@@ -635,6 +636,17 @@ class Engine:
         ms = C.c_double()
         _check(lib().ts_debug_ozaki_gemm(self.handle, i64(k), i64(m), i64(n), _p(f), _p(b), _p(out), C.byref(ms)))
         return out.T.copy(), float(ms.value)
+
+    def ozaki_gemm_nt(self, a, bt):
+        """A·Btᵀ on the int8 tensor cores, stage-C orientation (ts_debug_ozaki_gemm_nt): (result, ms)."""
+        a = _f64(a)
+        bt = _f64(bt)
+        m, k = a.shape
+        n = bt.shape[0]
+        out = np.zeros((m, n), order="F")
+        ms = C.c_double()
+        _check(lib().ts_debug_ozaki_gemm_nt(self.handle, i64(m), i64(k), i64(n), _p(a), _p(bt), _p(out), C.byref(ms)))
+        return out, float(ms.value)
 
     def set_graphs(self, on: bool):
         """CUDA-graph replay of repeated identical calls (ts_ctx_set_graphs)."""

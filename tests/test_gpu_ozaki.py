@@ -63,3 +63,17 @@ def test_ozaki_bitwise_repeatable(engine):
     first, _ = engine.ozaki_gemm(f, b)
     for _ in range(5):
         assert np.array_equal(first, engine.ozaki_gemm(f, b)[0])
+
+
+@pytest.mark.parametrize("m,k,n", [(128, 64, 8), (300, 200, 64), (1000, 777, 26), (4096, 1024, 64)])
+def test_ozaki_stage_c_orientation(engine, m, k, n):
+    """Stage C's orientation (Y = F·W with W stored transposed): A M-contiguous,
+    per-row exponents, column-major output."""
+    rng = np.random.default_rng(m + k)
+    a = np.asfortranarray(rng.standard_normal((m, k)))
+    a[5 % m, :] *= 1e-9
+    bt = np.asfortranarray(rng.standard_normal((n, k)))
+    out, _ = engine.ozaki_gemm_nt(a, bt)
+    ref = (a.astype(np.longdouble) @ bt.T.astype(np.longdouble)).astype(np.float64)
+    scale = np.abs(a) @ np.abs(bt).T
+    assert np.all(np.abs(out - ref) <= 2e-15 * np.maximum(scale, 1e-300))
