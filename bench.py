@@ -396,48 +396,63 @@ def main():
     gflops = falg / (ms / 1000.0) / 1e9 if krp else None
     peak, peak_src = fp64_peak()
 
-    # Dominant kernel.  KRP / Kron: stage C's grouped DMMA GEMM (Y_n = F_n W_n, one
-    # launch over all modes; the largest kernel of the call once stages A and E
-    # run on the int8 tensor cores — ozaki.cu), events right before / after that
-    # launch (split-K reduction excluded); Lazy: stage E's GEMM (P_n = Q_nᵀ F_n).
+    # Dominant kernel: stage C's GEMM (Y_n = F_n W_n, one launch over all modes),
+    # events right before / after that launch on the library stream (split-K
+    # reduction excluded).  For large sums stages A, C and E run on the int8
+    # tensor cores (ozaki.cu): each reads F once, so the bound is HBM; otherwise
+    # it is the DMMA GEMM (bound: the FP64 tensor peak).  Lazy: stage E's GEMM.
     d = len(wl.dims)
     Kloc = e - b
-    if args.strategy == "lazy":
-        q = [min(wl.dims[j], sum(r[j] for r in wl.ranks)) for j in range(d)]
-        fa = sum(2.0 * q[j] * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d))
-        ta = stages[5] if stages else float("nan")
-        kname = "gemm_tma_kernel<TN> (stage E: P_n = Q_nᵀ·F_n, one launch over all modes)"
-    else:
-        cw = [wl.widths[0] if krp else T.complement_product(widths, j) for j in range(d)]
-        fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * cw[j] * Kloc for j in range(d))
-        ta = stages[12] if len(stages) > 12 and stages[12] > 0 else (stages[2] if stages else float("nan"))
-        kname = ("gemm_tma_kernel<NT> (stage C: Y_n = F_n·W_n, one launch over all modes); duration = the kernel "
-                 "alone (split-K reduction excluded), stage C incl. reduce = %.4f ms" % stages[2])
-    achieved = fa / (ta / 1000.0) / 1e12 if ta == ta and ta > 0 else None
+    int8 = eng.last_int8_stages()
+    cw = [wl.widths[0] if krp else (T.complement_product(widths, j) if args.strategy == "kron" else 0) for j in range(d)]
+    hbm = measured_hbm_peak()
     traffic = None
     try:
         with open(TRAFFIC_FILE) as f:
             traffic = json.load(f).get(wl.name, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    roofline = {"bound": "tensor", "kernel": kname,
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src,
-                "whole_step_fp64_tflops": gflops / 1000.0 if krp else None,
-                "whole_step_frac": gflops / 1000.0 / (peak * world) if krp else None}
-    # Stage A (Z_j = Ω_jᵀ F_j) on the int8 tensor cores is HBM-bound: F read once.
+    if args.strategy == "lazy":
+        q = [min(wl.dims[j], sum(r[j] for r in wl.ranks)) for j in range(d)]
+        fa = sum(2.0 * q[j] * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d))
+        ta = stages[5] if stages else float("nan")
+        achieved = fa / (ta / 1000.0) / 1e12 if ta == ta and ta > 0 else None
+        roofline = {"bound": "tensor", "kernel": "gemm_tma_kernel<TN> (stage E: P_n = Q_nᵀ·F_n, one launch over all modes)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+                    "traffic": None, "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src}
+    else:
+        fa = sum(2.0 * wl.dims[j] * wl.ranks[0][j] * cw[j] * Kloc for j in range(d))
+        ta = stages[12] if len(stages) > 12 and stages[12] > 0 else (stages[2] if stages else float("nan"))
+        if int8 & 2:
+            bytes_c = sum(8.0 * wl.dims[j] * wl.ranks[0][j] * Kloc + 8.0 * cw[j] * wl.ranks[0][j] * Kloc +
+                          8.0 * wl.dims[j] * cw[j] for j in range(d))
+            ach = bytes_c / (ta / 1000.0) / 1e9
+            roofline = {"bound": "hbm", "kernel": "ozaki_gemm_kernel (stage C: Y_n = F_n·W_n as FP64 from int8 "
+                        "tcgen05 digit products, one launch over all modes); duration = the kernel alone (split-K "
+                        "reduction excluded), stage C incl. operand slicing + reduce = %.4f ms" % stages[2],
+                        "achieved": ach, "peak": hbm[0], "unit": "GB/s", "frac": ach / hbm[0], "traffic": traffic,
+                        "algorithmic_bytes_per_launch": bytes_c, "avg_launch_ms": ta, "peak_source": hbm[1],
+                        "fp64_equiv_tflops": fa / (ta / 1000.0) / 1e12,
+                        "fp64_equiv_frac_of_dmma_peak": fa / (ta / 1000.0) / 1e12 / peak}
+        else:
+            achieved = fa / (ta / 1000.0) / 1e12 if ta == ta and ta > 0 else None
+            roofline = {"bound": "tensor", "kernel": "gemm_tma_kernel<NT> (stage C: Y_n = F_n·W_n, one launch over all "
+                        "modes); duration = the kernel alone (split-K reduction excluded), stage C incl. reduce = %.4f ms"
+                        % stages[2], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                        "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src}
+    roofline["whole_step_fp64_tflops"] = gflops / 1000.0 if krp else None
+    roofline["whole_step_frac_of_dmma_peak"] = gflops / 1000.0 / (peak * world) if krp else None
+    roofline["int8_engine_stages"] = {"A": bool(int8 & 1), "C": bool(int8 & 2), "E": bool(int8 & 4)}
     roofline_stage_a = None
     if args.strategy != "lazy" and len(stages) > 11 and stages[11] > 0:
-        bytes_a = sum(8.0 * wl.dims[j] * wl.ranks[0][j] * Kloc for j in range(d)) + \
-            sum(8.0 * wl.dims[j] * (wl.widths[0] if krp else widths[j]) for j in range(d)) + \
-            sum(8.0 * (wl.widths[0] if krp else widths[j]) * wl.ranks[0][j] * Kloc for j in range(d))
-        hbm = measured_hbm_peak()
+        aw = [wl.widths[0] if krp else widths[j] for j in range(d)]  # Ω_j widths
+        bytes_a = sum(8.0 * wl.dims[j] * wl.ranks[0][j] * Kloc + 8.0 * wl.dims[j] * aw[j] +
+                      8.0 * aw[j] * wl.ranks[0][j] * Kloc for j in range(d))
         ach = bytes_a / (stages[11] / 1000.0) / 1e9
-        roofline_stage_a = {"bound": "hbm", "kernel": "stage A GEMM kernel alone (ozaki_gemm_kernel: FP64 via int8 "
-                            "tcgen05 digits when the factors exceed 256 MB, else gemm_tma_kernel<TN>)",
-                            "achieved": ach, "peak": hbm[0], "unit": "GB/s", "frac": ach / hbm[0],
-                            "peak_source": hbm[1], "algorithmic_bytes_per_launch": bytes_a,
+        roofline_stage_a = {"bound": "hbm" if int8 & 1 else "tensor",
+                            "kernel": "ozaki_gemm_kernel (stage A)" if int8 & 1 else "gemm_tma_kernel<TN> (stage A)",
+                            "achieved_gbs": ach, "hbm_peak_gbs": hbm[0], "frac_of_hbm": ach / hbm[0],
                             "avg_launch_ms": stages[11], "fp64_equiv_tflops": fa / (stages[11] / 1000.0) / 1e12}
     stage_names = ["A_project", "B_krp", "C_expand", "allreduce_Y", "D_tsqr", "E_project", "F1_ttm", "F2_core",
                    "allreduce_h", "G_sthosvd", "H_output", "A_gemm_kernel_only", "C_gemm_kernel_only"]

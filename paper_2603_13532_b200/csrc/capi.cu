@@ -202,6 +202,7 @@ struct ts_ctx {
     std::int64_t launches = 0;
     std::vector<cudaEvent_t> events;
     int last_qr_fallbacks = 0, last_svd_fallbacks = 0;  // accurate-path uses in the last call
+    unsigned last_int8_stages = 0;  // bit 0/1/2: stage A/C/E of the last call ran on the int8 engine (ozaki.cu)
     int last_eig_fallbacks = 0;  // tridiagonal-eigensolver rejections (Jacobi recomputes) in the last call
     // ST-HOSVD modes that needed the accurate path in the last synchronous call
     // with these sketch dims: the next such call goes there directly (a pure
@@ -944,6 +945,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         for (auto& e : ctx->events) TS_CUDA_CHECK(cudaEventCreate(&e));
     }
     mark(ctx, 0);
+    unsigned int8_stages = 0;
 
     double* omega = lazy ? nullptr : omega_get(ctx, d, dims, ow, seed, stream);
     std::int64_t q[TS_MAX_ORDER];
@@ -992,7 +994,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
             }
             std::vector<int> modes(static_cast<size_t>(d));
             std::iota(modes.begin(), modes.end(), 0);
-            if (!ozaki_stage(ctx, b, ps, modes, sc, true)) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+            const bool a8 = ozaki_stage(ctx, b, ps, modes, sc, true);
+            if (!a8) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+            int8_stages |= a8 ? 1u : 0u;
         }
         mark(ctx, 1);
         sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage A only
@@ -1052,7 +1056,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
                 p.K = static_cast<int>(b->R[n]);
                 ps.push_back(p);
             }
-            if (!ozaki_stage_c(ctx, b, ps, sc)) ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+            const bool c8 = ozaki_stage_c(ctx, b, ps, sc);
+            if (!c8) ts::launch_grouped_gemm(Layout::NT, ps, sc, ctx->num_sms);
+            int8_stages |= c8 ? 2u : 0u;
             sc.before_next_gemm = sc.after_next_gemm = nullptr;  // the hooks belong to stage C only
         }
     }
@@ -1271,7 +1277,9 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         }
         std::vector<int> modes(static_cast<size_t>(d));
         std::iota(modes.begin(), modes.end(), 0);
-        if (!ozaki_stage(ctx, b, ps, modes, sc)) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        const bool e8 = ozaki_stage(ctx, b, ps, modes, sc);
+        if (!e8) ts::launch_grouped_gemm(Layout::TN, ps, sc, ctx->num_sms);
+        int8_stages |= e8 ? 4u : 0u;
         if (overlap) TS_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         if (!pr.empty()) ts::launch_grouped_gemm(Layout::TN, pr, sc, ctx->num_sms);
     }
@@ -1608,6 +1616,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         ctx->spec_ok = ctx->last_qr_fallbacks == 0 && ctx->last_svd_fallbacks == 0;
     }
     TS_CUDA_CHECK(cudaStreamSynchronize(st));
+    ctx->last_int8_stages = int8_stages;
     if (ctx->timing) {
         ctx->stage_ms.assign(kNumStages + 2, 0.0);
         for (int i = 0; i < kNumStages; ++i) {
@@ -2460,6 +2469,8 @@ int ts_ctx_last_paths(ts_ctx* ctx, int* qr_fallback_modes, int* svd_fallback_mod
         if (svd_fallback_modes) *svd_fallback_modes = ctx->last_svd_fallbacks;
     });
 }
+
+int ts_ctx_last_int8_stages(ts_ctx* ctx) { return ctx ? static_cast<int>(ctx->last_int8_stages) : 0; }
 
 int ts_ctx_set_debug(ts_ctx* ctx, int enabled) {
     return guarded([&] {

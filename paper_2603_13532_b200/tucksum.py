@@ -52,7 +52,7 @@ EXPORTED_SYMBOLS = [
     "ts_tucker_norm", "ts_tucker_inner", "ts_rel_error_to_sum", "ts_sym_eig_tri",
     "ts_ctx_set_graphs", "ts_ctx_graph_replays", "ts_batch_upload_stacked", "ts_ctx_comm_info",
     "ts_ctx_set_host_allreduce", "ts_krp_sum_segmented", "ts_debug_ozaki_gemm",
-    "ts_debug_ozaki_gemm_nt",
+    "ts_debug_ozaki_gemm_nt", "ts_ctx_last_int8_stages",
 ]
 
 HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
@@ -625,6 +625,10 @@ class Engine:
         ms = C.c_double()
         _check(lib().ts_sym_eig_tri(self.handle, i64(n), _p(a), _p(vals), _p(vecs), C.byref(fl), C.byref(ms)))
         return vals, vecs, bool(fl.value), float(ms.value)
+
+    def last_int8_stages(self) -> int:
+        """Bitmask of the last call's stages A (1), C (2), E (4) run on the int8 engine."""
+        return int(lib().ts_ctx_last_int8_stages(self.handle))
 
     def ozaki_gemm(self, f, b):
         """Fᵀ·B on the int8 tensor cores (ts_debug_ozaki_gemm): (result m × n, ms)."""
