@@ -59,6 +59,14 @@ __global__ void k_lds(int iters, long long* out) {
   if (p == 12345) sink = p;
   if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
 }
+__global__ void k_shfl(int iters, long long* out) {
+  double x = threadIdx.x * 1e-3 + 1.5;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; i++) x += __shfl_xor_sync(0xffffffffu, x, 1);
+  long long t1 = clock64();
+  if (x == 123.0) sink = x;
+  if (threadIdx.x == 0) out[0] = (t1 - t0) / iters;
+}
 int main() {
   long long* d; cudaMalloc(&d, 8); long long h;
   auto run = [&](const char* name, void (*k)(int, long long*), int threads) {
@@ -72,6 +80,7 @@ int main() {
   run("div_f64_latency", k_div, 32);
   run("sqrt_f64_latency", k_sqrt, 32);
   run("lds_latency", k_lds, 32);
-  for (int t : {32, 256, 1024}) run("bar_sync", k_bar, t);
+  run("shfl_f64_plus_dadd_latency", k_shfl, 32);
+  for (int t : {32, 64, 128, 256, 512, 1024}) run("bar_sync", k_bar, t);
   return 0;
 }
