@@ -65,6 +65,14 @@ constexpr int kOffA = kFStages * kFStage;    // 96 KB
 constexpr int kOffB = kOffA + 2 * kAStage;   // 152 KB
 constexpr int kOffBar = kOffB + 2 * kBStage;  // 180 KB
 constexpr size_t kOzSmem = 1024 + kOffBar + 256;
+// TS variant (F digits staged in TMEM, not shared memory): no A stages, so the
+// fp64 ring is 5 deep; TMEM columns 448..503 hold one chunk's 7 digit slices
+// (8 columns of 4 bytes each = 32 K per row).
+constexpr int kFStagesTS = 5;
+constexpr int kOffBTS = kFStagesTS * kFStage;     // 160 KB
+constexpr int kOffBarTS = kOffBTS + 2 * kBStage;  // 188 KB
+constexpr size_t kOzSmemTS = 1024 + kOffBarTS + 256;
+constexpr int kTmemA = kOzS * kOzN;               // first TMEM column of the digit slices
 constexpr int kOzMaxK = 16384;               // int32 headroom: 7 · 128² · K < 2^31
 
 struct alignas(64) OzGroup {
@@ -115,6 +123,20 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, 
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Same with the A operand read from tensor memory (lane = row, 4 K bytes per column).
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, unsigned a, unsigned b, unsigned c, unsigned d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                  : "memory");
@@ -151,8 +173,12 @@ __device__ __forceinline__ void digits4(const double* v, double scale, unsigned*
     }
 }
 
+template <bool kTS>
 __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup* __restrict__ groups, int ngroups,
                                                                    int variant) {
+    constexpr int kFStages = kTS ? kFStagesTS : ts::kFStages;
+    constexpr int kOffB = kTS ? kOffBTS : ts::kOffB;
+    constexpr int kOffBar = kTS ? kOffBarTS : ts::kOffBar;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* f_full = reinterpret_cast<uint64_t*>(smem + kOffBar);  // [kFStages]
@@ -187,7 +213,7 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&a_full[s], 1);
+            mbar_init(&a_full[s], kTS ? kOzConv / 32 : 1);
             mbar_init(&mma_done[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -230,23 +256,33 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
         if (lane == 0 && variant != 1) {  // MMA issuer: per chunk 10 MMAs — slice i of A against slices
                           // 0..6-i of B concatenated along N (their accumulators
                           // w = i..6 are consecutive TMEM column blocks)
-            const unsigned a_base = smem_u32(smem + kOffA), b_base = smem_u32(smem + kOffB);
+            const unsigned a_base = smem_u32(smem + (kTS ? 0 : kOffA)), b_base = smem_u32(smem + kOffB);
             for (int c = 0; c < nk; ++c) {
                 const int s2 = c & 1;
-                mbar_wait(&a_full[s2], (c >> 1) & 1);
+                // TS: one digit stage in TMEM (phase flips every chunk); SS: two in shared memory
+                if (kTS) mbar_wait(&a_full[0], c & 1);
+                else mbar_wait(&a_full[s2], (c >> 1) & 1);
                 mbar_wait(&b_full[s2], (c >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const unsigned ab = a_base + s2 * kAStage, bb = b_base + s2 * kBStage;
 #pragma unroll
                 for (int i = 0; i < (variant == 2 ? 0 : variant == 4 ? 1 : kOzS); ++i) {
                     const int ntot = kOzN * (kOzS - i);
-                    const uint64_t da = umma_desc_sw32(ab + i * kASlice);
                     const uint32_t acc = (c > 0 || i > 0) ? 1u : 0u;
                     const int n1 = min(ntot, 256);
-                    mma_i8(tmem + static_cast<uint32_t>(kOzN * i), da, umma_desc_sw32(bb), idesc_s8(n1), acc);
-                    if (ntot > 256)
-                        mma_i8(tmem + static_cast<uint32_t>(kOzN * i + 256), da, umma_desc_sw32(bb + 4 * kBSlice),
-                               idesc_s8(ntot - 256), acc);
+                    if (kTS) {
+                        const uint32_t ta = tmem + static_cast<uint32_t>(kTmemA + 8 * i);
+                        mma_i8_ts(tmem + static_cast<uint32_t>(kOzN * i), ta, umma_desc_sw32(bb), idesc_s8(n1), acc);
+                        if (ntot > 256)
+                            mma_i8_ts(tmem + static_cast<uint32_t>(kOzN * i + 256), ta, umma_desc_sw32(bb + 4 * kBSlice),
+                                      idesc_s8(ntot - 256), acc);
+                    } else {
+                        const uint64_t da = umma_desc_sw32(ab + i * kASlice);
+                        mma_i8(tmem + static_cast<uint32_t>(kOzN * i), da, umma_desc_sw32(bb), idesc_s8(n1), acc);
+                        if (ntot > 256)
+                            mma_i8(tmem + static_cast<uint32_t>(kOzN * i + 256), da, umma_desc_sw32(bb + 4 * kBSlice),
+                                   idesc_s8(ntot - 256), acc);
+                    }
                 }
                 mma_commit(&mma_done[s2]);
             }
@@ -279,11 +315,27 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
             }
             mbar_arrive(&f_empty[s]);
             if (variant == 1) continue;
-            if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // A stage free again
-            unsigned char* as = smem + kOffA + s2 * kAStage;
             unsigned wq[4][kOzS];
 #pragma unroll
             for (int qd = 0; qd < 4; ++qd) digits4(v + 4 * qd, scale, wq[qd]);
+            if (kTS) {
+                // Digits go straight to tensor memory: this thread's row is TMEM lane
+                // `row`, its 16 K bytes of slice t are columns kTmemA + 8t + 4g .. +3.
+                // The single TMEM stage is free once the previous chunk's MMAs retired.
+                if (c >= 1) mbar_wait(&mma_done[(c - 1) & 1], ((c - 1) >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const uint32_t ta = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(kTmemA + 4 * g);
+#pragma unroll
+                for (int t = 0; t < (variant == 3 ? 0 : kOzS); ++t)
+                    tmem_st4(ta + static_cast<uint32_t>(8 * t), wq[0][t], wq[1][t], wq[2][t], wq[3][t]);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[0]);
+                continue;
+            }
+            if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // A stage free again
+            unsigned char* as = smem + kOffA + s2 * kAStage;
 #pragma unroll
             for (int t = 0; t < (variant == 3 ? 0 : kOzS); ++t) {
                 const unsigned addr = smem_u32(as + t * kASlice + sw32(row, 16 * g));
@@ -381,15 +433,32 @@ __global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, in
     }
 }
 
-// exp[i] = e with max_j |X[i, j]| < 2^e (column-major rows × cols, ld): thread per row.
-__global__ void row_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows, int64_t cols,
-                                    int* __restrict__ out) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= rows) return;
+// exp[i] = e with max_j |X[i, j]| < 2^e (column-major rows × cols, ld): a block
+// per 32 rows, 32 column lanes per row (lane y takes columns y, y + 32, …; a warp
+// reads 32 consecutive rows = 256 contiguous bytes), shared-memory max over lanes.
+__global__ void __launch_bounds__(1024) row_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows,
+                                                            int64_t cols, int* __restrict__ out) {
+    __shared__ double red[32][33];
+    const int64_t i = blockIdx.x * 32LL + threadIdx.x;
     double mx = 0.0;
-    for (int64_t j = 0; j < cols; ++j) mx = fmax(mx, fabs(X[i + j * ld]));
-    const int b = (__double2hiint(mx) >> 20) & 0x7ff;
-    out[i] = mx > 0.0 ? max(b - 1022, -900) : -900;
+    if (i < rows) {
+        const double* x = X + i;
+        int64_t j = threadIdx.y;
+        for (; j + 96 < cols; j += 128) {  // four independent loads in flight
+            const double a = fabs(x[j * ld]), b = fabs(x[(j + 32) * ld]);
+            const double c = fabs(x[(j + 64) * ld]), d = fabs(x[(j + 96) * ld]);
+            mx = fmax(fmax(mx, fmax(a, b)), fmax(c, d));
+        }
+        for (; j < cols; j += 32) mx = fmax(mx, fabs(x[j * ld]));
+    }
+    red[threadIdx.y][threadIdx.x] = mx;
+    __syncthreads();
+    if (threadIdx.y == 0 && i < rows) {
+#pragma unroll
+        for (int y = 1; y < 32; ++y) mx = fmax(mx, red[y][threadIdx.x]);
+        const int b = (__double2hiint(mx) >> 20) & 0x7ff;
+        out[i] = mx > 0.0 ? max(b - 1022, -900) : -900;
+    }
 }
 
 // B operand (K × N column-major, ld, N ≤ 64) → 7 balanced byte digits in the
@@ -421,6 +490,15 @@ __global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, 
 
 }  // namespace
 
+// TS_OZAKI_TS=0: the F digits go through shared memory (SS MMAs) instead of TMEM.
+static bool ozaki_ts() {
+    static const int en = [] {
+        const char* e = std::getenv("TS_OZAKI_TS");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return en == 1;
+}
+
 bool ozaki_enabled() {
     static const int en = [] {
         const char* e = std::getenv("TS_OZAKI");
@@ -431,7 +509,7 @@ bool ozaki_enabled() {
 
 void launch_row_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc) {
     if (rows <= 0) return;
-    row_exponent_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, sc.stream()>>>(X, ld, rows, cols, out);
+    row_exponent_kernel<<<static_cast<unsigned>((rows + 31) / 32), dim3(32, 32), 0, sc.stream()>>>(X, ld, rows, cols, out);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
@@ -473,12 +551,39 @@ void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOp
     sc.launches += 1;
 }
 
+// K splits of a launch with `tiles` 128-column tiles (one CTA per SM): the count
+// (≥ min_splits for the int32 headroom, ≥ 24 chunks each) that wastes the least
+// of the last wave, charging each CTA about four chunk-times of pipeline fill
+// and epilogue.  Config 5 (192 tiles, 256 chunks): 3 splits = 3.89 waves.
+static int pick_splits(int64_t tiles, int kchunks, int min_splits, int num_sms) {
+    static const int forced = [] {
+        const char* e = std::getenv("TS_OZAKI_SPLITS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return std::max(forced, min_splits);
+    int best = min_splits;
+    double best_eff = -1.0;
+    for (int s = min_splits; s <= 16; ++s) {
+        const int cps = (kchunks + s - 1) / s;
+        if (s > min_splits && cps < 24) break;
+        const int64_t units = tiles * ((kchunks + cps - 1) / cps);
+        const int64_t waves = (units + num_sms - 1) / num_sms;
+        const double eff = static_cast<double>(units) / static_cast<double>(waves * num_sms) * cps / (cps + 4.0);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
+}
+
 bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int num_sms, int* launched) {
     *launched = 0;
     if (!ozaki_enabled()) return false;
     for (const OzProblem& p : probs)
         if (p.M > 0 && (p.B.N > kOzN || (reinterpret_cast<uintptr_t>(p.F) & 15u) || (p.ldf & 1))) return false;
-    set_max_smem(ozaki_gemm_kernel, static_cast<int>(kOzSmem));
+    set_max_smem(ozaki_gemm_kernel<false>, static_cast<int>(kOzSmem));
+    set_max_smem(ozaki_gemm_kernel<true>, static_cast<int>(kOzSmemTS));
     std::vector<OzGroup> groups;
     std::vector<int> red;
     int64_t units = 0, tiles = 0;
@@ -507,8 +612,7 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
         // K splits: ≤ kOzMaxK per split (int32 headroom), then enough units for
         // about three waves over the SMs (one CTA per SM), at least 32 chunks each.
         const int kchunks = (p.K + kOzKC - 1) / kOzKC;
-        int splits = std::max(1, (p.K + kOzMaxK - 1) / kOzMaxK);
-        while (tiles * splits < 3LL * num_sms && (splits * 2) * 32 <= kchunks) splits *= 2;
+        const int splits = pick_splits(tiles, kchunks, std::max(1, (p.K + kOzMaxK - 1) / kOzMaxK), num_sms);
         const int cps = (kchunks + splits - 1) / splits;
         g.k_per_split = cps * kOzKC;
         g.splits = (kchunks + cps - 1) / cps;
@@ -539,8 +643,12 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
         const char* e = std::getenv("TS_OZAKI_VARIANT");
         return e ? std::atoi(e) : 0;
     }();
-    ozaki_gemm_kernel<<<static_cast<unsigned>(units), kOzThreads, kOzSmem, sc.stream()>>>(
-        d_groups, static_cast<int>(groups.size()), variant);
+    if (ozaki_ts())
+        ozaki_gemm_kernel<true><<<static_cast<unsigned>(units), kOzThreads, kOzSmemTS, sc.stream()>>>(
+            d_groups, static_cast<int>(groups.size()), variant);
+    else
+        ozaki_gemm_kernel<false><<<static_cast<unsigned>(units), kOzThreads, kOzSmem, sc.stream()>>>(
+            d_groups, static_cast<int>(groups.size()), variant);
     TS_LAUNCH_CHECK();
     if (sc.after_next_gemm) {
         TS_CUDA_CHECK(cudaEventRecord(sc.after_next_gemm, sc.stream()));
