@@ -443,7 +443,8 @@ def main():
                         "algorithmic_flops_per_launch": fa, "avg_launch_ms": ta, "peak_source": peak_src}
     roofline["whole_step_fp64_tflops"] = gflops / 1000.0 if krp else None
     roofline["whole_step_frac_of_dmma_peak"] = gflops / 1000.0 / (peak * world) if krp else None
-    roofline["int8_engine_stages"] = {"A": bool(int8 & 1), "C": bool(int8 & 2), "E": bool(int8 & 4)}
+    roofline["int8_engine_stages"] = {"A": bool(int8 & 1), "C": bool(int8 & 2), "E": bool(int8 & 4),
+                                      "F2": bool(int8 & 8)}
     roofline_stage_a = None
     if args.strategy != "lazy" and len(stages) > 11 and stages[11] > 0:
         aw = [wl.widths[0] if krp else widths[j] for j in range(d)]  # Ω_j widths

@@ -213,7 +213,8 @@ int ts_sym_eig_tri(ts_ctx* ctx, int64_t n, const double* a, double* values, doub
  * stage-A / stage-E engine): out (n_cols × m, column-major, ld n_cols) = Fᵀ·B
  * for host F (k × m) and B (k × n_cols), n_cols <= 64; *ms = kernel time. */
 /* Which of the last call's big contractions ran on the int8 tensor-core engine
- * (ozaki.cu; large sums only): bit 0 stage A, bit 1 stage C, bit 2 stage E. */
+ * (ozaki.cu; large sums only): bit 0 stage A, bit 1 stage C, bit 2 stage E,
+ * bit 3 stage F2. */
 int ts_ctx_last_int8_stages(ts_ctx* ctx);
 int ts_debug_ozaki_gemm(ts_ctx* ctx, int64_t k, int64_t m, int64_t n_cols, const double* f, const double* b, double* out,
                         double* ms);

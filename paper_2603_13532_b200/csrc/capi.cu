@@ -202,7 +202,8 @@ struct ts_ctx {
     std::int64_t launches = 0;
     std::vector<cudaEvent_t> events;
     int last_qr_fallbacks = 0, last_svd_fallbacks = 0;  // accurate-path uses in the last call
-    unsigned last_int8_stages = 0;  // bit 0/1/2: stage A/C/E of the last call ran on the int8 engine (ozaki.cu)
+    unsigned last_int8_stages = 0;  // bit 0/1/2/3: stage A/C/E/F2 of the last call ran on the int8 engine (ozaki.cu)
+    bool f2_int8 = false;           // set by project_core when F2 took the int8 engine
     int last_eig_fallbacks = 0;  // tridiagonal-eigensolver rejections (Jacobi recomputes) in the last call
     // ST-HOSVD modes that needed the accurate path in the last synchronous call
     // with these sketch dims: the next such call goes there directly (a pure
@@ -456,6 +457,12 @@ bool ozaki_stage(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>&
             TS_CUDA_CHECK(cudaMallocAsync(&bm->aexp[n], sizeof(int) * static_cast<size_t>(b->R[n]), sc.stream()));
             ts::launch_col_exponents(b->F[n], b->dims[n], b->dims[n], b->R[n], bm->aexp[n], sc);
         }
+    std::vector<ts::OzOperand> small;
+    if (!cached_small) {  // one launch slices every mode's skinny operand
+        std::vector<ts::OzSmall> reqs;
+        for (const GemmProblem& p : ps) reqs.push_back(ts::OzSmall{p.A, p.lda, p.K, p.M, false});
+        small = ts::prepare_ozaki_b_batch(reqs, sc);
+    }
     std::vector<ts::OzProblem> oz;
     for (size_t i = 0; i < ps.size(); ++i) {
         const GemmProblem& p = ps[i];
@@ -487,7 +494,7 @@ bool ozaki_stage(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem>&
             }
             q.B = it->second;
         } else {
-            q.B = ts::prepare_ozaki_b(p.A, p.lda, p.K, p.M, sc);
+            q.B = small[i];
         }
         q.C = p.C;
         q.ldc = p.ldc;
@@ -513,6 +520,9 @@ bool ozaki_stage_c(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem
             TS_CUDA_CHECK(cudaMallocAsync(&bm->rexp[n], sizeof(int) * static_cast<size_t>(b->dims[n]), sc.stream()));
             ts::launch_row_exponents(b->F[n], b->dims[n], b->dims[n], b->R[n], bm->rexp[n], sc);
         }
+    std::vector<ts::OzSmall> reqs;
+    for (const GemmProblem& p : ps) reqs.push_back(ts::OzSmall{p.B, p.ldb, p.K, p.N, true});
+    const std::vector<ts::OzOperand> small = ts::prepare_ozaki_b_batch(reqs, sc);
     std::vector<ts::OzProblem> oz;
     for (size_t n = 0; n < ps.size(); ++n) {
         const GemmProblem& p = ps[n];
@@ -522,7 +532,7 @@ bool ozaki_stage_c(ts_ctx* ctx, const ts_batch* b, const std::vector<GemmProblem
         q.aexp = b->rexp[n];
         q.M = p.M;
         q.K = p.K;
-        q.B = ts::prepare_ozaki_b(p.B, p.ldb, p.K, p.N, sc, true);
+        q.B = small[n];
         q.C = p.C;
         q.ldc = p.ldc;
         q.a_mn = true;
@@ -686,7 +696,7 @@ void kron_stage_b(const ts_batch* b, double* const* Z, const std::int64_t* ow, d
 // core slice (ttm3.cu); other orders run a per-atom grouped GEMM chain.  The sum
 // over atoms is the K dimension of the final GEMM (deterministic split-K).
 double* project_core_f1(ts_ctx* ctx, const ts_batch* b, double* const* P, const std::int64_t* q, const double* d_w,
-                        const double* weights, CallScratch& sc) {
+                        const double* weights, CallScratch& sc, int** rowexp = nullptr) {
     const int d = b->order;
     // ---- Stage F1: per-atom multi-TTM over modes 0..d-2 into T_stack (Q' × R_{d-1})
     std::int64_t Qp = 1;
@@ -707,7 +717,15 @@ double* project_core_f1(ts_ctx* ctx, const ts_batch* b, double* const* P, const 
         ta.natoms = static_cast<int>(b->atoms.size());
         int max_r2 = 0;
         for (const auto& at : b->atoms) max_r2 = std::max(max_r2, at.shape[2]);
+        if (rowexp) {  // row exponent bounds of T_stack for F2 on the int8 engine
+            ta.rowexp = sc.alloc_n<int>(static_cast<size_t>(Qp * ts::kTtmExpBuckets));
+            ts::launch_fill_exponents(ta.rowexp, Qp * ts::kTtmExpBuckets, sc);
+        }
         f1_done = ts::launch_ttm3(ta, b->max_shape, max_r2, sc);
+        if (rowexp && f1_done) ts::launch_reduce_exponents(ta.rowexp, Qp, ts::kTtmExpBuckets, sc);
+        if (rowexp) *rowexp = f1_done ? ta.rowexp : nullptr;
+    } else if (rowexp) {
+        *rowexp = nullptr;
     }
     if (!f1_done) {
         const size_t na = b->atoms.size();
@@ -780,12 +798,36 @@ double* project_core(ts_ctx* ctx, const ts_batch* b, double* const* P, const std
     const int d = b->order;
     std::int64_t Qp = 1;
     for (int j = 0; j < d - 1; ++j) Qp *= q[j];
-    double* Tstack = project_core_f1(ctx, b, P, q, d_w, weights, sc);
+    // F2 on the int8 engine (ozaki.cu, stage-C orientation: T_stack is M-contiguous)
+    // when T_stack is large enough to be HBM-bound there; F1 then tracks the row
+    // exponent bounds.  Config 5: 268 MB, 0.15 ms on DMMA.
+    ctx->f2_int8 = false;
+    const bool f2_int8 = ts::ozaki_enabled() && q[d - 1] <= 64 && (Qp & 1) == 0 &&
+                         8.0 * static_cast<double>(Qp) * static_cast<double>(b->R[d - 1]) >= 128e6;
+    int* rowexp = nullptr;
+    double* Tstack = project_core_f1(ctx, b, P, q, d_w, weights, sc, f2_int8 ? &rowexp : nullptr);
     mark(ctx, 7);
     // ---- Stage F2: h (Q' × q_{d-1}) = T_stack · P_{d-1}ᵀ
     *hsize = Qp * q[d - 1];
     double* h = sc.alloc_n<double>(static_cast<size_t>(*hsize));
-    {
+    bool f2_done = false;
+    if (rowexp) {
+        ts::OzProblem o{};
+        o.F = Tstack;
+        o.ldf = Qp;
+        o.aexp = rowexp;
+        o.M = static_cast<int>(Qp);
+        o.K = static_cast<int>(b->R[d - 1]);
+        o.B = ts::prepare_ozaki_b_batch({ts::OzSmall{P[d - 1], q[d - 1], o.K, static_cast<int>(q[d - 1]), true}}, sc)[0];
+        o.C = h;
+        o.ldc = Qp;
+        o.a_mn = true;
+        o.c_colmajor = true;
+        int launched = 0;
+        f2_done = ts::launch_ozaki_gemm({o}, sc, ctx->num_sms, &launched);
+        if (f2_done) ctx->f2_int8 = true;
+    }
+    if (!f2_done) {
         GemmProblem p{};
         p.A = Tstack;
         p.lda = Qp;
@@ -1616,7 +1658,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
         ctx->spec_ok = ctx->last_qr_fallbacks == 0 && ctx->last_svd_fallbacks == 0;
     }
     TS_CUDA_CHECK(cudaStreamSynchronize(st));
-    ctx->last_int8_stages = int8_stages;
+    ctx->last_int8_stages = int8_stages | (ctx->f2_int8 ? 8u : 0u);
     if (ctx->timing) {
         ctx->stage_ms.assign(kNumStages + 2, 0.0);
         for (int i = 0; i < kNumStages; ++i) {
@@ -2379,7 +2421,12 @@ int ts_ctx_create(int device, ts_ctx** out) {
         auto ctx = std::make_unique<ts_ctx>();
         ctx->device = device;
         TS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-        TS_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        {   // The side stream carries stage D's short latency-bound chain next to stage E's
+            // machine-filling GEMM: highest priority, so its CTAs are placed first.
+            int lo_prio = 0, hi_prio = 0;
+            TS_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+            TS_CUDA_CHECK(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi_prio));
+        }
         TS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         TS_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         TS_CUDA_CHECK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));

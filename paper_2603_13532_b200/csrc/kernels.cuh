@@ -53,6 +53,11 @@ struct Ttm3Args {
     double* Tstack;  // Qp × R_2
     int64_t Qp;
     int natoms;
+    // Optional: per-row exponent bounds of T_stack (max over all its columns of
+    // |T| < 2^e) for stage F2 on the int8 engine: kTtmExpBuckets × Qp ints
+    // pre-filled with the floor by launch_fill_exponents (bucket = atom mod 16),
+    // folded into the first Qp by launch_reduce_exponents; nullptr = not tracked.
+    int* rowexp = nullptr;
 };
 bool launch_ttm3(const Ttm3Args& args, int max_shape, int max_r2, CallScratch& sc);
 
@@ -232,6 +237,20 @@ void launch_col_exponents(const double* X, int64_t ld, int64_t rows, int64_t col
 // trans: B(k, n) is stored at B[n + k·ldb].
 OzOperand prepare_ozaki_b(const double* B, int64_t ldb, int K, int N, CallScratch& sc, bool trans = false);
 void launch_row_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc);
+// out[0..n) = the exponent floor (−900) that kernels raise with atomicMax (ttm3.cu).
+void launch_fill_exponents(int* out, int64_t n, CallScratch& sc);
+constexpr int kOzExpFloor = -900;
+constexpr int kTtmExpBuckets = 16;
+// e[i] = max_b e[b·n + i] over `buckets` copies.
+void launch_reduce_exponents(int* e, int64_t n, int buckets, CallScratch& sc);
+// Several small operands in one launch (exponents + slices fused; scratch-owned).
+struct OzSmall {
+    const double* B;
+    int64_t ldb;
+    int K, N;
+    bool trans;
+};
+std::vector<OzOperand> prepare_ozaki_b_batch(const std::vector<OzSmall>& reqs, CallScratch& sc);
 // Same into caller-owned buffers (slices: ozaki_b_bytes(K) bytes, exp: 64 ints).
 size_t ozaki_b_bytes(int K);
 void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOperand& o, CallScratch& sc,

@@ -35,6 +35,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -74,6 +75,10 @@ constexpr int kOffBarTS = kOffBTS + 2 * kBStage;  // 188 KB
 constexpr size_t kOzSmemTS = 1024 + kOffBarTS + 256;
 constexpr int kTmemA = kOzS * kOzN;               // first TMEM column of the digit slices
 constexpr int kOzMaxK = 16384;               // int32 headroom: 7 · 128² · K < 2^31
+
+// TS_OZAKI_TRACE=1: clock64 stamps of CTA 0's chunks 8..11 (converter thread 0
+// and the MMA thread), printed by ts_debug_ozaki_gemm (tools/ozaki_stageA.py).
+__device__ long long g_oz_trace[64];
 
 struct alignas(64) OzGroup {
     CUtensorMap fa;        // F: dims {K (contiguous), M}, box {16, 128}, 128B swizzle
@@ -149,12 +154,26 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                  : "memory");
 }
 
-// Balanced signed byte digits of 4 values: x = rint(v·scale) (|x| < 2^54 — the
-// balanced range is ±0x7F7F…7F ≈ ±0.996·2^55, so a full 2^55 would overflow);
-// y = x + 0x80…80 (7 bytes) lies in [0, 2^56) and byte t of y, minus 128, is
-// digit t — i.e. byte XOR 0x80 as int8.  Word t holds digit t (t = 0: the top,
-// weight 2^48) of each value, value u in byte u.
-__device__ __forceinline__ void digits4(const double* v, double scale, unsigned* w) {
+// Balanced signed byte digits of 4 values: x = round(v·2^(54−e)) for the column
+// (row) exponent bound e (|v| < 2^e, so |x| < 2^54 — the balanced range is
+// ±0x7F7F…7F ≈ ±0.996·2^55, a full 2^55 would overflow); y = x + 0x80…80
+// (7 bytes) lies in [0, 2^56) and byte t of y, minus 128, is digit t — i.e. byte
+// XOR 0x80 as int8.  Word t holds digit t (t = 0: the top, weight 2^48) of each
+// value, value u in byte u.
+//
+// INTEGER ONLY.  FP64 instructions (DMUL, DFMA, F2I.S64.F64) issue ~14× slower
+// while tcgen05 MMAs are running on the SM (tools/i8_mma_rate.cu: 2.2 → 30.9
+// cycles per warp instruction per SMSP; integer ALU ops are unaffected), which
+// serialised conversion and MMAs.  With v = ±M·2^(E−1075) (M the 53-bit
+// significand), x = ±((M·4 >> sh) + 1) >> 1 for sh = e + 1022 − E ≥ 0 — round
+// half away from zero; zeros and subnormals (E = 0) shift out (e ≥ −900).
+// cexp = e + 1022.
+__device__ __forceinline__ void transpose_digits(const unsigned* hi, const unsigned* lo, unsigned* w);
+
+// The same digits through the FP64 pipe (DMUL + F2I.S64.F64, round to nearest
+// even): fewer instructions, for code that runs while no MMA is in flight.
+// scale = 2^(54 − e).
+__device__ __forceinline__ void digits4_fp(const double* v, double scale, unsigned* w) {
     unsigned hi[4], lo[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -162,18 +181,45 @@ __device__ __forceinline__ void digits4(const double* v, double scale, unsigned*
         hi[u] = static_cast<unsigned>(y >> 32);
         lo[u] = static_cast<unsigned>(y);
     }
-#pragma unroll
-    for (int t = 0; t < kOzS; ++t) {
-        const bool fromhi = t < 3;
-        const unsigned p = fromhi ? static_cast<unsigned>(2 - t) : static_cast<unsigned>(6 - t);
-        const unsigned sel = p | ((p + 4u) << 4);
-        const unsigned u01 = __byte_perm(fromhi ? hi[0] : lo[0], fromhi ? hi[1] : lo[1], sel);
-        const unsigned u23 = __byte_perm(fromhi ? hi[2] : lo[2], fromhi ? hi[3] : lo[3], sel);
-        w[t] = __byte_perm(u01, u23, 0x5410) ^ 0x80808080u;
-    }
+    transpose_digits(hi, lo, w);
 }
 
-template <bool kTS>
+__device__ __forceinline__ void digits4(const double* v, int cexp, unsigned* w) {
+    unsigned hi[4], lo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const unsigned vh = static_cast<unsigned>(__double2hiint(v[u])), vl = static_cast<unsigned>(__double2loint(v[u]));
+        const unsigned sh = min(static_cast<unsigned>(cexp) - ((vh >> 20) & 0x7ffu), 63u);
+        const unsigned mh = (vh & 0xfffffu) | 0x100000u;
+        const unsigned long long m4 = ((static_cast<unsigned long long>(mh) << 32) | vl) << 2;
+        unsigned long long y = ((m4 >> sh) + 1ull) >> 1;
+        const unsigned long long neg = static_cast<unsigned long long>(static_cast<long long>(static_cast<int>(vh) >> 31));
+        y = ((y ^ neg) - neg) + 0x80808080808080ull;
+        hi[u] = static_cast<unsigned>(y >> 32);
+        lo[u] = static_cast<unsigned>(y);
+    }
+    transpose_digits(hi, lo, w);
+}
+
+// 4 × 7 byte transpose: two PRMT stages (pairs, then quads), then the XOR.
+__device__ __forceinline__ void transpose_digits(const unsigned* hi, const unsigned* lo, unsigned* w) {
+    const unsigned l01a = __byte_perm(lo[0], lo[1], 0x5140), l01b = __byte_perm(lo[0], lo[1], 0x7362);
+    const unsigned l23a = __byte_perm(lo[2], lo[3], 0x5140), l23b = __byte_perm(lo[2], lo[3], 0x7362);
+    const unsigned h01a = __byte_perm(hi[0], hi[1], 0x5140), h01b = __byte_perm(hi[0], hi[1], 0x7362);
+    const unsigned h23a = __byte_perm(hi[2], hi[3], 0x5140), h23b = __byte_perm(hi[2], hi[3], 0x7362);
+    w[0] = __byte_perm(h01b, h23b, 0x5410) ^ 0x80808080u;  // byte 6
+    w[1] = __byte_perm(h01a, h23a, 0x7632) ^ 0x80808080u;  // byte 5
+    w[2] = __byte_perm(h01a, h23a, 0x5410) ^ 0x80808080u;  // byte 4
+    w[3] = __byte_perm(l01b, l23b, 0x7632) ^ 0x80808080u;  // byte 3
+    w[4] = __byte_perm(l01b, l23b, 0x5410) ^ 0x80808080u;  // byte 2
+    w[5] = __byte_perm(l01a, l23a, 0x7632) ^ 0x80808080u;  // byte 1
+    w[6] = __byte_perm(l01a, l23a, 0x5410) ^ 0x80808080u;  // byte 0
+}
+
+// kIntGroups (TS): how many of a thread's four 4-value groups are converted with
+// integer instructions while the previous chunk's MMAs run; the rest go through
+// the FP64 pipe after those MMAs retired (FP64 issue is ~14× slower under MMAs).
+template <bool kTS, int kIntGroups>
 __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup* __restrict__ groups, int ngroups,
                                                                    int variant) {
     constexpr int kFStages = kTS ? kFStagesTS : ts::kFStages;
@@ -244,8 +290,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                     tma_load_2d(smem + s * kFStage, &G.fa, k0, m0, &f_full[s]);
                     tma_load_2d(smem + s * kFStage + kFBox, &G.fa, k0 + 16, m0, &f_full[s]);
                 }
+                // TS: the small operand's slices are fetched by converter thread 0 right
+                // after it saw the previous chunk's MMAs retire, so this warp's fp64
+                // ring runs ahead of the MMAs by its full depth (coupling the two
+                // loads here kept only ~one chunk of F in flight per SM).
+                if (kTS || variant == 1) continue;
                 const int s2 = c & 1;
-                if (variant == 1) continue;  // timing ablation: F loads only
                 if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // B stage free again
                 mbar_expect_tx(&b_full[s2], kBStage);
                 bulk_load(smem + kOffB + s2 * kBStage, bsrc + static_cast<int64_t>(c) * kBStage, kBStage, &b_full[s2]);
@@ -260,9 +310,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
             for (int c = 0; c < nk; ++c) {
                 const int s2 = c & 1;
                 // TS: one digit stage in TMEM (phase flips every chunk); SS: two in shared memory
+                const bool tr = variant == 9 && blockIdx.x == 0 && c >= 8 && c < 12;
                 if (kTS) mbar_wait(&a_full[0], c & 1);
                 else mbar_wait(&a_full[s2], (c >> 1) & 1);
+                if (tr) g_oz_trace[(c - 8) * 16 + 8] = clock64();
                 mbar_wait(&b_full[s2], (c >> 1) & 1);
+                if (tr) g_oz_trace[(c - 8) * 16 + 9] = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const unsigned ab = a_base + s2 * kAStage, bb = b_base + s2 * kBStage;
 #pragma unroll
@@ -285,16 +338,27 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                     }
                 }
                 mma_commit(&mma_done[s2]);
+                if (tr) g_oz_trace[(c - 8) * 16 + 10] = clock64();
             }
             mma_commit(acc_full);
         }
     } else {  // warps 0-7: converters (thread = row, 16-K half), then the epilogue
         const int row = threadIdx.x & (kOzM - 1), g = threadIdx.x >> 7;
         const int ea = (m0 + row < G.M) ? G.aexp[m0 + row] : 0;
+        const int cexp = ea + 1022;
         const double scale = pow2(54 - ea);
+        const uint8_t* bsrc = G.bsl + static_cast<int64_t>(kbeg / kOzKC) * kBStage;
+        auto load_b = [&](int c) {  // pre-sliced small operand of chunk c → B stage c & 1
+            mbar_expect_tx(&b_full[c & 1], kBStage);
+            bulk_load(smem + kOffB + (c & 1) * kBStage, bsrc + static_cast<int64_t>(c) * kBStage, kBStage, &b_full[c & 1]);
+        };
+        if (kTS && threadIdx.x == 0 && variant != 1 && nk > 0) load_b(0);
         for (int c = 0; c < nk; ++c) {
             const int s = c % kFStages, s2 = c & 1;
+            const bool tr = variant == 9 && blockIdx.x == 0 && threadIdx.x == 0 && c >= 8 && c < 12;
+            if (tr) g_oz_trace[(c - 8) * 16 + 0] = clock64();
             mbar_wait(&f_full[s], (c / kFStages) & 1);
+            if (tr) g_oz_trace[(c - 8) * 16 + 1] = clock64();
             double v[16];
             if (G.a_mn) {  // box row/16: line k (32 lines of 128 B), element row%16 in it
                 const unsigned base = smem_u32(smem + s * kFStage + (row >> 4) * (kFStage / 8));
@@ -316,24 +380,42 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
             mbar_arrive(&f_empty[s]);
             if (variant == 1) continue;
             unsigned wq[4][kOzS];
-#pragma unroll
-            for (int qd = 0; qd < 4; ++qd) digits4(v + 4 * qd, scale, wq[qd]);
             if (kTS) {
+                // Integer-converted groups first: they overlap the previous chunk's MMAs.
+#pragma unroll
+                for (int qd = 0; qd < kIntGroups; ++qd) digits4(v + 4 * qd, cexp, wq[qd]);
+                if (tr) g_oz_trace[(c - 8) * 16 + 2] = clock64();
+                // The single TMEM digit stage is free once the previous chunk's MMAs
+                // retired; from here until this chunk's MMAs start the FP64 pipe runs
+                // at full speed, so the remaining groups take the short FP64 route.
+                if (c >= 1) mbar_wait(&mma_done[(c - 1) & 1], ((c - 1) >> 1) & 1);
+                if (tr) g_oz_trace[(c - 8) * 16 + 3] = clock64();
+                if (threadIdx.x == 0 && c + 1 < nk) load_b(c + 1);  // its stage was chunk c−1's
+                __syncwarp();
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+                for (int qd = kIntGroups; qd < 4; ++qd) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) asm volatile("" : "+d"(v[4 * qd + u]));  // keep it after the wait
+                    digits4_fp(v + 4 * qd, scale, wq[qd]);
+                }
                 // Digits go straight to tensor memory: this thread's row is TMEM lane
                 // `row`, its 16 K bytes of slice t are columns kTmemA + 8t + 4g .. +3.
-                // The single TMEM stage is free once the previous chunk's MMAs retired.
-                if (c >= 1) mbar_wait(&mma_done[(c - 1) & 1], ((c - 1) >> 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const uint32_t ta = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(kTmemA + 4 * g);
+                if (tr) g_oz_trace[(c - 8) * 16 + 4] = clock64() + (wq[3][0] & 0);  // after the FP64 groups
 #pragma unroll
                 for (int t = 0; t < (variant == 3 ? 0 : kOzS); ++t)
                     tmem_st4(ta + static_cast<uint32_t>(8 * t), wq[0][t], wq[1][t], wq[2][t], wq[3][t]);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                if (tr) g_oz_trace[(c - 8) * 16 + 5] = clock64();
                 asm volatile("tcgen05.fence::before_thread_sync;\n");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[0]);
+                if (tr) g_oz_trace[(c - 8) * 16 + 6] = clock64();
                 continue;
             }
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) digits4(v + 4 * qd, cexp, wq[qd]);
             if (c >= 2) mbar_wait(&mma_done[s2], ((c >> 1) - 1) & 1);  // A stage free again
             unsigned char* as = smem + kOffA + s2 * kAStage;
 #pragma unroll
@@ -461,6 +543,19 @@ __global__ void __launch_bounds__(1024) row_exponent_kernel(const double* __rest
     }
 }
 
+__global__ void fill_exponent_kernel(int* __restrict__ out, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = kOzExpFloor;
+}
+
+__global__ void reduce_exponent_kernel(int* __restrict__ e, int64_t n, int buckets) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    int m = e[i];
+    for (int b = 1; b < buckets; ++b) m = max(m, e[b * n + i]);
+    e[i] = m;
+}
+
 // B operand (K × N column-major, ld, N ≤ 64) → 7 balanced byte digits in the
 // UMMA smem image per 32-K chunk; thread = (chunk, column n, 16-K group).
 __global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, int K, int N, const int* __restrict__ bexp,
@@ -480,12 +575,65 @@ __global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, 
     }
     unsigned wq[4][kOzS];
 #pragma unroll
-    for (int qd = 0; qd < 4; ++qd) digits4(v + 4 * qd, scale, wq[qd]);
+    for (int qd = 0; qd < 4; ++qd) digits4_fp(v + 4 * qd, scale, wq[qd]);
     uint8_t* base = out + static_cast<int64_t>(c) * kBStage;
 #pragma unroll
     for (int t = 0; t < kOzS; ++t)
         *reinterpret_cast<uint4*>(base + t * kBSlice + sw32(static_cast<unsigned>(n), static_cast<unsigned>(16 * g))) =
             make_uint4(wq[0][t], wq[1][t], wq[2][t], wq[3][t]);
+}
+
+// Exponents + slices of several small operands in ONE launch (stages C, E and F2
+// prepare one per mode on every call): block (n, p) handles column n of operand
+// p — the column's exponent bound by a block reduction, then its 7 digit planes.
+struct OzPrep {
+    const double* B;
+    int64_t ldb;
+    int K, N, trans, nchunks;
+    int* exp;
+    uint8_t* slices;
+};
+
+__global__ void __launch_bounds__(256) ozaki_prepare_b_kernel(const OzPrep* __restrict__ preps) {
+    const OzPrep& P = preps[blockIdx.y];
+    const int n = blockIdx.x;
+    const bool live = n < P.N;
+    const int64_t es = P.trans ? P.ldb : 1;  // element stride along k
+    const double* col = P.B + (P.trans ? static_cast<int64_t>(n) : static_cast<int64_t>(n) * P.ldb);
+    __shared__ double red[8];
+    __shared__ int s_exp;
+    double mx = 0.0;
+    if (live)
+        for (int k = threadIdx.x; k < P.K; k += 256) mx = fmax(mx, fabs(col[k * es]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+        const int b = (__double2hiint(mx) >> 20) & 0x7ff;
+        const int e = mx > 0.0 ? max(b - 1022, kOzExpFloor) : kOzExpFloor;
+        s_exp = e;
+        P.exp[n] = e;
+    }
+    __syncthreads();
+    const double scale = live ? pow2(54 - s_exp) : 0.0;
+    for (int idx = threadIdx.x; idx < 2 * P.nchunks; idx += 256) {
+        const int c = idx >> 1, g = idx & 1;
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int k = c * kOzKC + 16 * g + u;
+            v[u] = (live && k < P.K) ? col[k * es] : 0.0;
+        }
+        unsigned wq[4][kOzS];
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) digits4_fp(v + 4 * qd, scale, wq[qd]);
+        uint8_t* base = P.slices + static_cast<int64_t>(c) * kBStage;
+#pragma unroll
+        for (int t = 0; t < kOzS; ++t)
+            *reinterpret_cast<uint4*>(base + t * kBSlice + sw32(static_cast<unsigned>(n), static_cast<unsigned>(16 * g))) =
+                make_uint4(wq[0][t], wq[1][t], wq[2][t], wq[3][t]);
+    }
 }
 
 }  // namespace
@@ -499,6 +647,15 @@ static bool ozaki_ts() {
     return en == 1;
 }
 
+// TS_OZAKI_INT_GROUPS=0..4: the integer / FP64 split of the in-kernel conversion (default 2).
+static int ozaki_int_groups() {
+    static const int n = [] {
+        const char* e = std::getenv("TS_OZAKI_INT_GROUPS");
+        return e ? std::atoi(e) : 2;
+    }();
+    return n;
+}
+
 bool ozaki_enabled() {
     static const int en = [] {
         const char* e = std::getenv("TS_OZAKI");
@@ -510,6 +667,20 @@ bool ozaki_enabled() {
 void launch_row_exponents(const double* X, int64_t ld, int64_t rows, int64_t cols, int* out, CallScratch& sc) {
     if (rows <= 0) return;
     row_exponent_kernel<<<static_cast<unsigned>((rows + 31) / 32), dim3(32, 32), 0, sc.stream()>>>(X, ld, rows, cols, out);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
+void launch_fill_exponents(int* out, int64_t n, CallScratch& sc) {
+    if (n <= 0) return;
+    fill_exponent_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, sc.stream()>>>(out, n);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+}
+
+void launch_reduce_exponents(int* e, int64_t n, int buckets, CallScratch& sc) {
+    if (n <= 0 || buckets <= 1) return;
+    reduce_exponent_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, sc.stream()>>>(e, n, buckets);
     TS_LAUNCH_CHECK();
     sc.launches += 1;
 }
@@ -551,6 +722,27 @@ void prepare_ozaki_b_into(const double* B, int64_t ldb, int K, int N, const OzOp
     sc.launches += 1;
 }
 
+std::vector<OzOperand> prepare_ozaki_b_batch(const std::vector<OzSmall>& reqs, CallScratch& sc) {
+    std::vector<OzOperand> out(reqs.size());
+    std::vector<OzPrep> preps(reqs.size());
+    for (size_t i = 0; i < reqs.size(); ++i) {
+        const OzSmall& r = reqs[i];
+        if (r.N > kOzN) throw Error(TS_UNSUPPORTED, "ozaki: B has more than 64 columns");
+        OzOperand& o = out[i];
+        o.exp = sc.alloc_n<int>(static_cast<size_t>(kOzN));
+        o.slices = sc.alloc_n<uint8_t>(ozaki_b_bytes(r.K));
+        o.K = r.K;
+        o.N = r.N;
+        preps[i] = OzPrep{r.B, r.ldb, r.K, r.N, r.trans ? 1 : 0, (r.K + kOzKC - 1) / kOzKC, o.exp, o.slices};
+    }
+    if (reqs.empty()) return out;
+    auto* d_preps = static_cast<const OzPrep*>(sc.upload(preps.data(), preps.size() * sizeof(OzPrep)));
+    ozaki_prepare_b_kernel<<<dim3(kOzN, static_cast<unsigned>(reqs.size())), 256, 0, sc.stream()>>>(d_preps);
+    TS_LAUNCH_CHECK();
+    sc.launches += 1;
+    return out;
+}
+
 // K splits of a launch with `tiles` 128-column tiles (one CTA per SM): the count
 // (≥ min_splits for the int32 headroom, ≥ 24 chunks each) that wastes the least
 // of the last wave, charging each CTA about four chunk-times of pipeline fill
@@ -582,8 +774,12 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
     if (!ozaki_enabled()) return false;
     for (const OzProblem& p : probs)
         if (p.M > 0 && (p.B.N > kOzN || (reinterpret_cast<uintptr_t>(p.F) & 15u) || (p.ldf & 1))) return false;
-    set_max_smem(ozaki_gemm_kernel<false>, static_cast<int>(kOzSmem));
-    set_max_smem(ozaki_gemm_kernel<true>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel<false, 4>, static_cast<int>(kOzSmem));
+    set_max_smem(ozaki_gemm_kernel<true, 0>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel<true, 1>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel<true, 2>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel<true, 3>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel<true, 4>, static_cast<int>(kOzSmemTS));
     std::vector<OzGroup> groups;
     std::vector<int> red;
     int64_t units = 0, tiles = 0;
@@ -643,18 +839,39 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
         const char* e = std::getenv("TS_OZAKI_VARIANT");
         return e ? std::atoi(e) : 0;
     }();
-    if (ozaki_ts())
-        ozaki_gemm_kernel<true><<<static_cast<unsigned>(units), kOzThreads, kOzSmemTS, sc.stream()>>>(
-            d_groups, static_cast<int>(groups.size()), variant);
-    else
-        ozaki_gemm_kernel<false><<<static_cast<unsigned>(units), kOzThreads, kOzSmem, sc.stream()>>>(
-            d_groups, static_cast<int>(groups.size()), variant);
+    const unsigned grid = static_cast<unsigned>(units);
+    const int ng = static_cast<int>(groups.size());
+    if (!ozaki_ts()) {
+        ozaki_gemm_kernel<false, 4><<<grid, kOzThreads, kOzSmem, sc.stream()>>>(d_groups, ng, variant);
+    } else {
+        switch (ozaki_int_groups()) {
+            case 0: ozaki_gemm_kernel<true, 0><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
+            case 1: ozaki_gemm_kernel<true, 1><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
+            case 3: ozaki_gemm_kernel<true, 3><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
+            case 4: ozaki_gemm_kernel<true, 4><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
+            default: ozaki_gemm_kernel<true, 2><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
+        }
+    }
     TS_LAUNCH_CHECK();
     if (sc.after_next_gemm) {
         TS_CUDA_CHECK(cudaEventRecord(sc.after_next_gemm, sc.stream()));
         sc.after_next_gemm = nullptr;
     }
     *launched = 1;
+    if (variant == 9) {
+        long long tr[64];
+        TS_CUDA_CHECK(cudaStreamSynchronize(sc.stream()));
+        TS_CUDA_CHECK(cudaMemcpyFromSymbol(tr, g_oz_trace, sizeof(tr)));
+        for (int c = 0; c < 4; ++c) {
+            const long long* r = tr + 16 * c;
+            const long long b0 = tr[0];
+            std::fprintf(stderr,
+                         "oz-trace chunk %d: conv start %lld f_full %lld int %lld mma_done(c-1) %lld fp %lld st %lld arrive %lld | "
+                         "mma: a_full %lld b_full %lld issued %lld\n",
+                         8 + c, r[0] - b0, r[1] - b0, r[2] - b0, r[3] - b0, r[4] - b0, r[5] - b0, r[6] - b0, r[8] - b0,
+                         r[9] - b0, r[10] - b0);
+        }
+    }
     if (!red.empty()) {
         const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
         int64_t maxel = 0;

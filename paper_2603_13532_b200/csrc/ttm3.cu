@@ -61,6 +61,16 @@ __global__ void __launch_bounds__(kThreads) ttm3_kernel(Ttm3Args args) {
     // GEMM 2 tiling: 2×2 warps of 32×32 over T (64×64).
     const int wm2 = warp & 1, wn2 = warp >> 1;
 
+    // Running maxima of |T| per output (i0, i1) over this CTA's slices, as the high
+    // words of the doubles (monotone for non-negative values): the row exponent
+    // bounds stage F2's int8 engine needs, without another pass over T_stack.
+    const bool track = args.rowexp != nullptr;
+    int mxh[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mxh[i][j][0] = mxh[i][j][1] = 0;
+
     load_slice(s_begin, 0);
     cp_async_commit();
     for (int a2 = s_begin; a2 < s_end; ++a2) {
@@ -121,11 +131,31 @@ __global__ void __launch_bounds__(kThreads) ttm3_kernel(Ttm3Args args) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int i0 = wm2 * 32 + i * 8 + g, i1 = wn2 * 32 + j * 8 + 2 * t + h;
-                    if (i0 < q0 && i1 < q1) out[i0 + static_cast<int64_t>(i1) * q0] = w * acc[i][j][h];
+                    const double val = w * acc[i][j][h];
+                    if (i0 < q0 && i1 < q1) out[i0 + static_cast<int64_t>(i1) * q0] = val;
+                    if (track) mxh[i][j][h] = max(mxh[i][j][h], __double2hiint(val) & 0x7fffffff);
                 }
         __syncthreads();  // Xs / slice buffer reuse
     }
     cp_async_wait<0>();
+    if (track) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int i0 = wm2 * 32 + i * 8 + g, i1 = wn2 * 32 + j * 8 + 2 * t + h;
+                    if (i0 >= q0 || i1 >= q1) continue;
+                    // biased exponent b: 2^(b-1023) ≤ max < 2^(b-1022); zero / subnormal → the floor
+                    const int bexp = mxh[i][j][h] >> 20;
+                    const int e = bexp > 0 ? max(bexp - 1022, kOzExpFloor) : kOzExpFloor;
+                    // kTtmExpBuckets copies of the bounds (bucket = atom mod 16) keep the first
+                    // wave's same-address atomics short; launch_reduce_exponents folds them.
+                    int* slot = args.rowexp + (blockIdx.x % kTtmExpBuckets) * args.Qp + i0 + static_cast<int64_t>(i1) * q0;
+                    if (e > *reinterpret_cast<volatile int*>(slot)) atomicMax(slot, e);
+                }
+    }
 }
 
 }  // namespace

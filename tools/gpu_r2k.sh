@@ -1,0 +1,18 @@
+#!/bin/bash
+# Round-2 (k): Ozaki TS engine with decoupled B loads + two-group TMEM hand-over; F2 on the int8 engine.
+O=gpurun_out/${1:-r02k}; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_ozaki.py -x -q > $O/ozaki_tests.log 2>&1; echo rc=$? >> $O/ozaki_tests.log
+timeout 300 python tools/ozaki_stageA.py > $O/stageA.log 2>&1
+for v in 1 2 3; do
+  TS_OZAKI_VARIANT=$v timeout 300 python tools/ozaki_stageA.py > $O/stageA_variant$v.log 2>&1
+done
+for sp in 4 6; do
+TS_OZAKI_SPLITS=$sp timeout 300 python tools/ozaki_stageA.py > $O/stageA_sp$sp.log 2>&1
+done
+timeout 600 python bench.py --config 5 --steps 30 --no-cpu-baseline --no-e2e --stages > $O/bench_cfg5.json 2> $O/bench_cfg5.err
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:ozaki_gemm -s 2 -c 1 -o $O/ncu_ozaki_ts python tools/ozaki_stageA.py > $O/ncu_ozaki.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -k "cfg5 or baseline or reference_semantics" > $O/parity_tests.log 2>&1; echo rc=$? >> $O/parity_tests.log
+for f in $O/*.log; do echo "$f: $(tail -n 1 $f)"; done
+python -c "
+import json
+d=json.loads(open('$O/bench_cfg5.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['stages_ms'], d['roofline'].get('int8_engine_stages'))"
