@@ -798,11 +798,17 @@ double* project_core(ts_ctx* ctx, const ts_batch* b, double* const* P, const std
     const int d = b->order;
     std::int64_t Qp = 1;
     for (int j = 0; j < d - 1; ++j) Qp *= q[j];
-    // F2 on the int8 engine (ozaki.cu, stage-C orientation: T_stack is M-contiguous)
-    // when T_stack is large enough to be HBM-bound there; F1 then tracks the row
-    // exponent bounds.  Config 5: 268 MB, 0.15 ms on DMMA.
+    // F2 on the int8 engine (ozaki.cu, stage-C orientation: T_stack is M-contiguous),
+    // with F1 tracking T_stack's row exponent bounds.  Measured at config 5 (268 MB
+    // T_stack): F2 0.150 -> 0.117 ms, but the tracking (32 exponent atomics per
+    // thread at the end of each 8-slice CTA) costs F1 0.158 -> 0.198 ms, so it is
+    // opt-in (TS_OZAKI_F2=1) and F2 stays on the DMMA GEMM by default.
     ctx->f2_int8 = false;
-    const bool f2_int8 = ts::ozaki_enabled() && q[d - 1] <= 64 && (Qp & 1) == 0 &&
+    static const bool f2_opt_in = [] {
+        const char* e = std::getenv("TS_OZAKI_F2");
+        return e && e[0] == '1';
+    }();
+    const bool f2_int8 = f2_opt_in && ts::ozaki_enabled() && q[d - 1] <= 64 && (Qp & 1) == 0 &&
                          8.0 * static_cast<double>(Qp) * static_cast<double>(b->R[d - 1]) >= 128e6;
     int* rowexp = nullptr;
     double* Tstack = project_core_f1(ctx, b, P, q, d_w, weights, sc, f2_int8 ? &rowexp : nullptr);

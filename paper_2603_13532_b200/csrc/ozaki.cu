@@ -79,6 +79,9 @@ constexpr int kOzMaxK = 16384;               // int32 headroom: 7 · 128² · K 
 // TS_OZAKI_TRACE=1: clock64 stamps of CTA 0's chunks 8..11 (converter thread 0
 // and the MMA thread), printed by ts_debug_ozaki_gemm (tools/ozaki_stageA.py).
 __device__ long long g_oz_trace[64];
+// Same switch: per-chunk start clocks of four CTAs (block 0, 200, 400, 570) in
+// [i][0..95], and [i][96..99] = kernel entry, loop start, loop end, epilogue end.
+__device__ long long g_oz_trace2[4][100];
 
 struct alignas(64) OzGroup {
     CUtensorMap fa;        // F: dims {K (contiguous), M}, box {16, 128}, 128B swizzle
@@ -235,6 +238,9 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
     uint64_t* acc_full = mma_done + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
 
+    const int tslot = blockIdx.x == 0 ? 0 : blockIdx.x == 200 ? 1 : blockIdx.x == 400 ? 2 : blockIdx.x == 570 ? 3 : -1;
+    const bool tr2 = variant == 9 && tslot >= 0 && threadIdx.x == 0;
+    if (tr2) g_oz_trace2[tslot][96] = clock64();
     const int64_t unit = blockIdx.x;
     int lo = 0, hi = ngroups - 1;
     while (lo < hi) {
@@ -357,6 +363,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
             const int s = c % kFStages, s2 = c & 1;
             const bool tr = variant == 9 && blockIdx.x == 0 && threadIdx.x == 0 && c >= 8 && c < 12;
             if (tr) g_oz_trace[(c - 8) * 16 + 0] = clock64();
+            if (tr2 && c < 96) g_oz_trace2[tslot][c] = clock64();
+            if (tr2 && c == 0) g_oz_trace2[tslot][97] = clock64();
             mbar_wait(&f_full[s], (c / kFStages) & 1);
             if (tr) g_oz_trace[(c - 8) * 16 + 1] = clock64();
             double v[16];
@@ -436,10 +444,18 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
         // ---- epilogue: row `row` (TMEM lane 32·(warp % 4) + lane), column groups
         // 4g..4g+3 of 8.  S = Σ_w acc_w 2^(8(6-w)) combined exactly in two int64
         // halves (u·2^32 + t), then a·b = S · 2^(e_A + e_B − 60).
+        if (tr2) g_oz_trace2[tslot][98] = clock64();
         mbar_wait(acc_full, 0);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const int m = m0 + row;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+        // the group's fields in registers (the TMEM-load asm's memory clobber would reload them)
+        const int n_cols = G.N, c_colmajor = G.c_colmajor;
+        const int* __restrict__ bexp = G.bexp;
+        double* const Cout = G.C;
+        const int64_t ldc = G.ldc;
+        const double alpha = G.alpha, beta = G.beta;
+        double* const ws_row = G.splits > 1 ? G.ws + (static_cast<int64_t>(sp) * G.M + m) * kOzN : nullptr;
 #pragma unroll 1
         for (int q = 4 * g; q < 4 * g + 4; ++q) {
             uint32_t r[kOzS][8];
@@ -451,10 +467,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                              : "r"(lane_base + static_cast<uint32_t>(kOzN * w + 8 * q)));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
             if (m < G.M) {
+                double val[8];
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc) {
                     const int n = 8 * q + cc;
-                    if (n >= G.N) continue;
                     const long long u = (static_cast<long long>(static_cast<int>(r[0][cc])) << 16) +
                                         (static_cast<long long>(static_cast<int>(r[1][cc])) << 8) +
                                         static_cast<long long>(static_cast<int>(r[2][cc]));
@@ -462,19 +478,27 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                                         (static_cast<long long>(static_cast<int>(r[4][cc])) << 16) +
                                         (static_cast<long long>(static_cast<int>(r[5][cc])) << 8) +
                                         static_cast<long long>(static_cast<int>(r[6][cc]));
-                    const double val = fma(static_cast<double>(u), 4294967296.0, static_cast<double>(t)) *
-                                       pow2(ea + G.bexp[n] - 60);
-                    if (G.splits == 1) {
-                        double* cp = G.c_colmajor ? G.C + m + static_cast<int64_t>(n) * G.ldc
-                                                  : G.C + n + static_cast<int64_t>(m) * G.ldc;
-                        *cp = G.beta == 0.0 ? G.alpha * val : G.alpha * val + G.beta * *cp;
-                    } else {
-                        G.ws[(static_cast<int64_t>(sp) * G.M + m) * kOzN + n] = val;
+                    val[cc] = n < n_cols ? fma(static_cast<double>(u), 4294967296.0, static_cast<double>(t)) *
+                                               pow2(ea + bexp[n] - 60)
+                                         : 0.0;
+                }
+                if (ws_row != nullptr) {  // split partial: this row's 64 bytes of the [m][64] block, 16 B at a time
+                    double2* dst = reinterpret_cast<double2*>(ws_row + 8 * q);
+#pragma unroll
+                    for (int cc = 0; cc < 8; cc += 2) dst[cc >> 1] = make_double2(val[cc], val[cc + 1]);
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) {
+                        const int n = 8 * q + cc;
+                        if (n >= n_cols) continue;
+                        double* cp = c_colmajor ? Cout + m + static_cast<int64_t>(n) * ldc : Cout + n + static_cast<int64_t>(m) * ldc;
+                        *cp = beta == 0.0 ? alpha * val[cc] : alpha * val[cc] + beta * *cp;
                     }
                 }
             }
         }
     }
+    if (tr2) g_oz_trace2[tslot][99] = clock64();
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
@@ -870,6 +894,17 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
                          "mma: a_full %lld b_full %lld issued %lld\n",
                          8 + c, r[0] - b0, r[1] - b0, r[2] - b0, r[3] - b0, r[4] - b0, r[5] - b0, r[6] - b0, r[8] - b0,
                          r[9] - b0, r[10] - b0);
+        }
+    }
+    if (variant == 9) {
+        long long t2[4][100];
+        TS_CUDA_CHECK(cudaMemcpyFromSymbol(t2, g_oz_trace2, sizeof(t2)));
+        for (int i = 0; i < 4; ++i) {
+            const long long* r = t2[i];
+            std::fprintf(stderr, "oz-trace2 cta-slot %d: entry->loop %lld loop %lld (acc wait+epilogue) %lld; chunk periods:", i,
+                         r[97] - r[96], r[98] - r[97], r[99] - r[98]);
+            for (int c = 1; c < 86; c += 6) std::fprintf(stderr, " %lld", r[c] - r[c - 1]);
+            std::fprintf(stderr, "\n");
         }
     }
     if (!red.empty()) {
