@@ -317,11 +317,12 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                 const int s2 = c & 1;
                 // TS: one digit stage in TMEM (phase flips every chunk); SS: two in shared memory
                 const bool tr = variant == 9 && blockIdx.x == 0 && c >= 8 && c < 12;
+                // B arrived a chunk ago; the digits are the late operand, so wait for them last
+                mbar_wait(&b_full[s2], (c >> 1) & 1);
+                if (tr) g_oz_trace[(c - 8) * 16 + 9] = clock64();
                 if (kTS) mbar_wait(&a_full[0], c & 1);
                 else mbar_wait(&a_full[s2], (c >> 1) & 1);
                 if (tr) g_oz_trace[(c - 8) * 16 + 8] = clock64();
-                mbar_wait(&b_full[s2], (c >> 1) & 1);
-                if (tr) g_oz_trace[(c - 8) * 16 + 9] = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const unsigned ab = a_base + s2 * kAStage, bb = b_base + s2 * kBStage;
 #pragma unroll
@@ -398,8 +399,6 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                 // at full speed, so the remaining groups take the short FP64 route.
                 if (c >= 1) mbar_wait(&mma_done[(c - 1) & 1], ((c - 1) >> 1) & 1);
                 if (tr) g_oz_trace[(c - 8) * 16 + 3] = clock64();
-                if (threadIdx.x == 0 && c + 1 < nk) load_b(c + 1);  // its stage was chunk c−1's
-                __syncwarp();
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll
                 for (int qd = kIntGroups; qd < 4; ++qd) {
@@ -420,6 +419,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[0]);
                 if (tr) g_oz_trace[(c - 8) * 16 + 6] = clock64();
+                // off the critical path: the next chunk's small-operand slices (their
+                // stage was chunk c−1's, whose MMAs retired above)
+                if (threadIdx.x == 0 && c + 1 < nk) load_b(c + 1);
+                __syncwarp();
                 continue;
             }
 #pragma unroll
