@@ -105,6 +105,17 @@ __host__ __device__ __forceinline__ unsigned sw32(unsigned row, unsigned k) {
     return row * 32u + ((((k >> 4) ^ (row >> 2)) & 1u) << 4) + (k & 15u);
 }
 
+// Exponent bound e (max |x| < 2^e) from the largest high word of |x| seen: the
+// floor for zero / subnormal vectors, kOzExpBad when a NaN or Inf was among the
+// values (their high words compare above every finite one), so the products
+// come out NaN like an FP64 GEMM's would instead of as finite garbage.
+constexpr int kOzExpBad = 1 << 20;
+__device__ __forceinline__ int exp_bound_of(int max_hi) {
+    const int b = max_hi >> 20;  // biased exponent: 2^(b-1023) ≤ max < 2^(b-1022)
+    return b == 0 ? kOzExpFloor : (b == 0x7ff ? kOzExpBad : max(b - 1022, kOzExpFloor));
+}
+__device__ __forceinline__ int abs_hi(double x) { return __double2hiint(x) & 0x7fffffff; }
+
 __device__ __forceinline__ double pow2(int e) {  // 2^e, normal range
     return __hiloint2double((e + 1023) << 20, 0);
 }
@@ -351,7 +362,8 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
         }
     } else {  // warps 0-7: converters (thread = row, 16-K half), then the epilogue
         const int row = threadIdx.x & (kOzM - 1), g = threadIdx.x >> 7;
-        const int ea = (m0 + row < G.M) ? G.aexp[m0 + row] : 0;
+        const int ea_raw = (m0 + row < G.M) ? G.aexp[m0 + row] : 0;
+        const int ea = ea_raw == kOzExpBad ? 0 : ea_raw;  // a NaN / Inf row: its outputs are NaN (epilogue)
         const int cexp = ea + 1022;
         const double scale = pow2(54 - ea);
         const uint8_t* bsrc = G.bsl + static_cast<int64_t>(kbeg / kOzKC) * kBStage;
@@ -481,9 +493,10 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
                                         (static_cast<long long>(static_cast<int>(r[4][cc])) << 16) +
                                         (static_cast<long long>(static_cast<int>(r[5][cc])) << 8) +
                                         static_cast<long long>(static_cast<int>(r[6][cc]));
-                    val[cc] = n < n_cols ? fma(static_cast<double>(u), 4294967296.0, static_cast<double>(t)) *
-                                               pow2(ea + bexp[n] - 60)
-                                         : 0.0;
+                    const int be = n < n_cols ? bexp[n] : 0;
+                    const double sc2 = (ea_raw == kOzExpBad || be == kOzExpBad) ? __longlong_as_double(0x7ff8000000000000ll)
+                                                                                : pow2(ea + be - 60);
+                    val[cc] = n < n_cols ? fma(static_cast<double>(u), 4294967296.0, static_cast<double>(t)) * sc2 : 0.0;
                 }
                 if (ws_row != nullptr) {  // split partial: this row's 64 bytes of the [m][64] block, 16 B at a time
                     double2* dst = reinterpret_cast<double2*>(ws_row + 8 * q);
@@ -528,17 +541,15 @@ __global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, in
                                     int* __restrict__ out) {
     const int j = blockIdx.x;
     const double* c = X + static_cast<int64_t>(j) * ld;
-    double mx = 0.0;
-    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) mx = fmax(mx, fabs(c[i * es]));
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    __shared__ double red[32];
+    int mx = 0;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) mx = max(mx, abs_hi(c[i * es]));
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ int red[32];
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
-        // biased exponent b: 2^(b-1023) ≤ mx < 2^(b-1022); zero / subnormal columns → a small bound
-        const int b = (__double2hiint(mx) >> 20) & 0x7ff;
-        out[j] = mx > 0.0 ? max(b - 1022, -900) : -900;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) mx = max(mx, red[w]);
+        out[j] = exp_bound_of(mx);
     }
 }
 
@@ -547,26 +558,25 @@ __global__ void col_exponent_kernel(const double* __restrict__ X, int64_t ld, in
 // reads 32 consecutive rows = 256 contiguous bytes), shared-memory max over lanes.
 __global__ void __launch_bounds__(1024) row_exponent_kernel(const double* __restrict__ X, int64_t ld, int64_t rows,
                                                             int64_t cols, int* __restrict__ out) {
-    __shared__ double red[32][33];
+    __shared__ int red[32][33];
     const int64_t i = blockIdx.x * 32LL + threadIdx.x;
-    double mx = 0.0;
+    int mx = 0;
     if (i < rows) {
         const double* x = X + i;
         int64_t j = threadIdx.y;
         for (; j + 96 < cols; j += 128) {  // four independent loads in flight
-            const double a = fabs(x[j * ld]), b = fabs(x[(j + 32) * ld]);
-            const double c = fabs(x[(j + 64) * ld]), d = fabs(x[(j + 96) * ld]);
-            mx = fmax(fmax(mx, fmax(a, b)), fmax(c, d));
+            const int a = abs_hi(x[j * ld]), b = abs_hi(x[(j + 32) * ld]);
+            const int c = abs_hi(x[(j + 64) * ld]), d = abs_hi(x[(j + 96) * ld]);
+            mx = max(max(mx, max(a, b)), max(c, d));
         }
-        for (; j < cols; j += 32) mx = fmax(mx, fabs(x[j * ld]));
+        for (; j < cols; j += 32) mx = max(mx, abs_hi(x[j * ld]));
     }
     red[threadIdx.y][threadIdx.x] = mx;
     __syncthreads();
     if (threadIdx.y == 0 && i < rows) {
 #pragma unroll
-        for (int y = 1; y < 32; ++y) mx = fmax(mx, red[y][threadIdx.x]);
-        const int b = (__double2hiint(mx) >> 20) & 0x7ff;
-        out[i] = mx > 0.0 ? max(b - 1022, -900) : -900;
+        for (int y = 1; y < 32; ++y) mx = max(mx, red[y][threadIdx.x]);
+        out[i] = exp_bound_of(mx);
     }
 }
 
@@ -593,7 +603,7 @@ __global__ void ozaki_slice_b_kernel(const double* __restrict__ B, int64_t ldb, 
     const int g = static_cast<int>(tid & 1);
     const int n = static_cast<int>((tid >> 1) % kOzN);
     const int c = static_cast<int>(tid / (2 * kOzN));
-    const double scale = n < N ? pow2(54 - bexp[n]) : 0.0;
+    const double scale = (n < N && bexp[n] != kOzExpBad) ? pow2(54 - bexp[n]) : 0.0;
     double v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -627,23 +637,22 @@ __global__ void __launch_bounds__(256) ozaki_prepare_b_kernel(const OzPrep* __re
     const bool live = n < P.N;
     const int64_t es = P.trans ? P.ldb : 1;  // element stride along k
     const double* col = P.B + (P.trans ? static_cast<int64_t>(n) : static_cast<int64_t>(n) * P.ldb);
-    __shared__ double red[8];
+    __shared__ int red[8];
     __shared__ int s_exp;
-    double mx = 0.0;
+    int mx = 0;
     if (live)
-        for (int k = threadIdx.x; k < P.K; k += 256) mx = fmax(mx, fabs(col[k * es]));
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int k = threadIdx.x; k < P.K; k += 256) mx = max(mx, abs_hi(col[k * es]));
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
-        const int b = (__double2hiint(mx) >> 20) & 0x7ff;
-        const int e = mx > 0.0 ? max(b - 1022, kOzExpFloor) : kOzExpFloor;
+        for (int w = 1; w < 8; ++w) mx = max(mx, red[w]);
+        const int e = exp_bound_of(mx);
         s_exp = e;
         P.exp[n] = e;
     }
     __syncthreads();
-    const double scale = live ? pow2(54 - s_exp) : 0.0;
+    const double scale = (live && s_exp != kOzExpBad) ? pow2(54 - s_exp) : 0.0;
     for (int idx = threadIdx.x; idx < 2 * P.nchunks; idx += 256) {
         const int c = idx >> 1, g = idx & 1;
         double v[16];

@@ -77,3 +77,39 @@ def test_ozaki_stage_c_orientation(engine, m, k, n):
     ref = (a.astype(np.longdouble) @ bt.T.astype(np.longdouble)).astype(np.float64)
     scale = np.abs(a) @ np.abs(bt).T
     assert np.all(np.abs(out - ref) <= 2e-15 * np.maximum(scale, 1e-300))
+
+
+def test_ozaki_nonfinite_inputs_give_nan(engine):
+    """A NaN or Inf anywhere in an operand makes the affected outputs NaN (as an
+    FP64 GEMM's would be non-finite) instead of finite garbage from the digit
+    conversion; all other outputs stay exact."""
+    rng = np.random.default_rng(11)
+    k, m, n = 256, 160, 32
+    f = np.asfortranarray(rng.standard_normal((k, m)))
+    b = np.asfortranarray(rng.standard_normal((k, n)))
+    f[17, 5] = np.nan
+    f[100, 131] = np.inf
+    b[3, 7] = -np.inf
+    out, _ = engine.ozaki_gemm(f, b)
+    bad_rows = np.zeros(m, dtype=bool)
+    bad_rows[[5, 131]] = True
+    bad_cols = np.zeros(n, dtype=bool)
+    bad_cols[7] = True
+    bad = bad_rows[:, None] | bad_cols[None, :]
+    assert np.all(np.isnan(out[bad]))
+    good = ~bad
+    fz, bz = np.nan_to_num(f, nan=0.0, posinf=0.0, neginf=0.0), np.nan_to_num(b, nan=0.0, posinf=0.0, neginf=0.0)
+    ref = _ref(fz, bz)
+    scale = np.abs(fz).T @ np.abs(bz)
+    assert np.all(np.abs(out - ref)[good] <= 2e-15 * np.maximum(scale, 1e-300)[good])
+    # stage-C orientation: a non-finite entry of A poisons its row, one of Bt its column
+    a = np.asfortranarray(rng.standard_normal((200, 96)))
+    bt = np.asfortranarray(rng.standard_normal((24, 96)))
+    a[9, 50] = np.nan
+    bt[4, 2] = np.inf
+    out2, _ = engine.ozaki_gemm_nt(a, bt)
+    assert np.all(np.isnan(out2[9, :])) and np.all(np.isnan(out2[:, 4]))
+    mask = np.ones_like(out2, dtype=bool)
+    mask[9, :] = False
+    mask[:, 4] = False
+    assert np.all(np.isfinite(out2[mask]))
