@@ -60,8 +60,18 @@ __device__ __forceinline__ void lds128(unsigned addr, double& x, double& y) {
 }
 __device__ __forceinline__ int chunk_of(int g) { return ((g & 1) << 2) | (g >> 1); }
 
+// Launches of up to kPackGroups groups carry their descriptors (tensor maps
+// included) as a __grid_constant__ kernel parameter instead of a scratch upload:
+// inside a CUDA graph every upload is a memcpy node serialised in front of its
+// kernel (a call has ~30 of them).
+constexpr int kPackGroups = 8;
+struct TmaPack {
+    TmaGroup g[kPackGroups];
+    int red[kPackGroups];
+};
+
 template <bool MN>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const TmaGroup* __restrict__ groups, int ngroups) {
+__device__ __forceinline__ void gemm_tma_body(const TmaGroup* __restrict__ groups, int ngroups) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* tilesA = smem;
@@ -215,7 +225,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const TmaGroup* _
             }
 }
 
+template <bool MN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel(const TmaGroup* __restrict__ groups, int ngroups) {
+    gemm_tma_body<MN>(groups, ngroups);
+}
+template <bool MN>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tma_kernel_pk(const __grid_constant__ TmaPack pk, int ngroups) {
+    gemm_tma_body<MN>(pk.g, ngroups);
+}
+
+__device__ __forceinline__ void tma_splitk_reduce_body(const TmaGroup* __restrict__ groups, const int* __restrict__ red);
 __global__ void tma_splitk_reduce(const TmaGroup* __restrict__ groups, const int* __restrict__ red) {
+    tma_splitk_reduce_body(groups, red);
+}
+__global__ void tma_splitk_reduce_pk(const __grid_constant__ TmaPack pk) { tma_splitk_reduce_body(pk.g, pk.red); }
+
+__device__ __forceinline__ void tma_splitk_reduce_body(const TmaGroup* __restrict__ groups, const int* __restrict__ red) {
     const TmaGroup& d = groups[red[blockIdx.y]];
     const int64_t mn = static_cast<int64_t>(d.M) * d.N;
     for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < mn;
@@ -268,6 +293,8 @@ bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallS
     if (total_tiles == 0) return true;
     set_max_smem(gemm_tma_kernel<false>, static_cast<int>(kSmemBytes));  // per device
     set_max_smem(gemm_tma_kernel<true>, static_cast<int>(kSmemBytes));
+    set_max_smem(gemm_tma_kernel_pk<false>, static_cast<int>(kSmemBytes));
+    set_max_smem(gemm_tma_kernel_pk<true>, static_cast<int>(kSmemBytes));
     static const int occ = [] {  // thread-safe one-time query (same on every B200)
         int o = 0;
         TS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, gemm_tma_kernel<false>, kThreads, kSmemBytes));
@@ -342,14 +369,29 @@ bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallS
             off += static_cast<size_t>(d.M) * d.N * d.splits;
         }
     }
-    auto* d_groups = static_cast<const TmaGroup*>(sc.upload(groups.data(), groups.size() * sizeof(TmaGroup)));
     const int ng = static_cast<int>(groups.size());
+    const bool packed = ng <= kPackGroups;
+    TmaPack pk;
+    const TmaGroup* d_groups = nullptr;
+    if (packed) {
+        std::memset(&pk, 0, sizeof(pk));
+        std::memcpy(pk.g, groups.data(), groups.size() * sizeof(TmaGroup));
+        for (size_t i = 0; i < red.size(); ++i) pk.red[i] = red[i];
+    } else {
+        d_groups = static_cast<const TmaGroup*>(sc.upload(groups.data(), groups.size() * sizeof(TmaGroup)));
+    }
     if (sc.before_next_gemm) {
         TS_CUDA_CHECK(cudaEventRecord(sc.before_next_gemm, sc.stream()));
         sc.before_next_gemm = nullptr;
     }
-    if (mn) gemm_tma_kernel<true><<<static_cast<unsigned>(units), kThreads, kSmemBytes, sc.stream()>>>(d_groups, ng);
-    else gemm_tma_kernel<false><<<static_cast<unsigned>(units), kThreads, kSmemBytes, sc.stream()>>>(d_groups, ng);
+    const unsigned grid = static_cast<unsigned>(units);
+    if (packed) {
+        if (mn) gemm_tma_kernel_pk<true><<<grid, kThreads, kSmemBytes, sc.stream()>>>(pk, ng);
+        else gemm_tma_kernel_pk<false><<<grid, kThreads, kSmemBytes, sc.stream()>>>(pk, ng);
+    } else {
+        if (mn) gemm_tma_kernel<true><<<grid, kThreads, kSmemBytes, sc.stream()>>>(d_groups, ng);
+        else gemm_tma_kernel<false><<<grid, kThreads, kSmemBytes, sc.stream()>>>(d_groups, ng);
+    }
     TS_LAUNCH_CHECK();
     if (sc.after_next_gemm) {
         TS_CUDA_CHECK(cudaEventRecord(sc.after_next_gemm, sc.stream()));
@@ -357,12 +399,16 @@ bool launch_tma_gemm(Layout layout, const std::vector<GemmProblem>& probs, CallS
     }
     *launched = 1;
     if (!red.empty()) {
-        const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
         int64_t maxel = 0;
         for (int gi : red) maxel = std::max<int64_t>(maxel, static_cast<int64_t>(groups[static_cast<size_t>(gi)].M) * groups[static_cast<size_t>(gi)].N);
         const int64_t blocks = std::min<int64_t>((maxel + 255) / 256, 4LL * num_sms);
-        tma_splitk_reduce<<<dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size())), 256, 0,
-                            sc.stream()>>>(d_groups, d_red);
+        const dim3 rgrid(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size()));
+        if (packed) {
+            tma_splitk_reduce_pk<<<rgrid, 256, 0, sc.stream()>>>(pk);
+        } else {
+            const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
+            tma_splitk_reduce<<<rgrid, 256, 0, sc.stream()>>>(d_groups, d_red);
+        }
         TS_LAUNCH_CHECK();
         *launched = 2;
     }

@@ -233,9 +233,16 @@ __device__ __forceinline__ void transpose_digits(const unsigned* hi, const unsig
 // kIntGroups (TS): how many of a thread's four 4-value groups are converted with
 // integer instructions while the previous chunk's MMAs run; the rest go through
 // the FP64 pipe after those MMAs retired (FP64 issue is ~14× slower under MMAs).
+// Up to kOzPack groups travel as a __grid_constant__ kernel parameter (no
+// descriptor upload = no memcpy node in front of the kernel inside a CUDA graph).
+constexpr int kOzPack = 8;
+struct OzPack {
+    OzGroup g[kOzPack];
+    int red[kOzPack];
+};
+
 template <bool kTS, int kIntGroups>
-__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup* __restrict__ groups, int ngroups,
-                                                                   int variant) {
+__device__ __forceinline__ void ozaki_gemm_body(const OzGroup* __restrict__ groups, int ngroups, int variant) {
     constexpr int kFStages = kTS ? kFStagesTS : ts::kFStages;
     constexpr int kOffB = kTS ? kOffBTS : ts::kOffB;
     constexpr int kOffBar = kTS ? kOffBarTS : ts::kOffBar;
@@ -520,7 +527,24 @@ __global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup
     if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+template <bool kTS, int kIntGroups>
+__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel(const OzGroup* __restrict__ groups, int ngroups,
+                                                                   int variant) {
+    ozaki_gemm_body<kTS, kIntGroups>(groups, ngroups, variant);
+}
+template <bool kTS, int kIntGroups>
+__global__ void __launch_bounds__(kOzThreads, 1) ozaki_gemm_kernel_pk(const __grid_constant__ OzPack pk, int ngroups,
+                                                                      int variant) {
+    ozaki_gemm_body<kTS, kIntGroups>(pk.g, ngroups, variant);
+}
+
+__device__ __forceinline__ void ozaki_splitk_reduce_body(const OzGroup* __restrict__ groups, const int* __restrict__ red);
 __global__ void ozaki_splitk_reduce(const OzGroup* __restrict__ groups, const int* __restrict__ red) {
+    ozaki_splitk_reduce_body(groups, red);
+}
+__global__ void ozaki_splitk_reduce_pk(const __grid_constant__ OzPack pk) { ozaki_splitk_reduce_body(pk.g, pk.red); }
+
+__device__ __forceinline__ void ozaki_splitk_reduce_body(const OzGroup* __restrict__ groups, const int* __restrict__ red) {
     const OzGroup& d = groups[red[blockIdx.y]];
     const int64_t mn = static_cast<int64_t>(d.M) * kOzN;
     for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < mn;
@@ -631,8 +655,12 @@ struct OzPrep {
     uint8_t* slices;
 };
 
-__global__ void __launch_bounds__(256) ozaki_prepare_b_kernel(const OzPrep* __restrict__ preps) {
-    const OzPrep& P = preps[blockIdx.y];
+struct OzPrepPack {
+    OzPrep p[kOzPack];
+};
+
+__global__ void __launch_bounds__(256) ozaki_prepare_b_kernel(const __grid_constant__ OzPrepPack preps) {
+    const OzPrep& P = preps.p[blockIdx.y];
     const int n = blockIdx.x;
     const bool live = n < P.N;
     const int64_t es = P.trans ? P.ldb : 1;  // element stride along k
@@ -771,11 +799,15 @@ std::vector<OzOperand> prepare_ozaki_b_batch(const std::vector<OzSmall>& reqs, C
         o.N = r.N;
         preps[i] = OzPrep{r.B, r.ldb, r.K, r.N, r.trans ? 1 : 0, (r.K + kOzKC - 1) / kOzKC, o.exp, o.slices};
     }
-    if (reqs.empty()) return out;
-    auto* d_preps = static_cast<const OzPrep*>(sc.upload(preps.data(), preps.size() * sizeof(OzPrep)));
-    ozaki_prepare_b_kernel<<<dim3(kOzN, static_cast<unsigned>(reqs.size())), 256, 0, sc.stream()>>>(d_preps);
-    TS_LAUNCH_CHECK();
-    sc.launches += 1;
+    for (size_t i0 = 0; i0 < reqs.size(); i0 += kOzPack) {  // descriptors as a kernel parameter, ≤ 8 per launch
+        const size_t cnt = std::min<size_t>(kOzPack, reqs.size() - i0);
+        OzPrepPack pk;
+        std::memset(&pk, 0, sizeof(pk));
+        std::memcpy(pk.p, preps.data() + i0, cnt * sizeof(OzPrep));
+        ozaki_prepare_b_kernel<<<dim3(kOzN, static_cast<unsigned>(cnt)), 256, 0, sc.stream()>>>(pk);
+        TS_LAUNCH_CHECK();
+        sc.launches += 1;
+    }
     return out;
 }
 
@@ -810,6 +842,12 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
     if (!ozaki_enabled()) return false;
     for (const OzProblem& p : probs)
         if (p.M > 0 && (p.B.N > kOzN || (reinterpret_cast<uintptr_t>(p.F) & 15u) || (p.ldf & 1))) return false;
+    set_max_smem(ozaki_gemm_kernel_pk<false, 4>, static_cast<int>(kOzSmem));
+    set_max_smem(ozaki_gemm_kernel_pk<true, 0>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel_pk<true, 1>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel_pk<true, 2>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel_pk<true, 3>, static_cast<int>(kOzSmemTS));
+    set_max_smem(ozaki_gemm_kernel_pk<true, 4>, static_cast<int>(kOzSmemTS));
     set_max_smem(ozaki_gemm_kernel<false, 4>, static_cast<int>(kOzSmem));
     set_max_smem(ozaki_gemm_kernel<true, 0>, static_cast<int>(kOzSmemTS));
     set_max_smem(ozaki_gemm_kernel<true, 1>, static_cast<int>(kOzSmemTS));
@@ -866,7 +904,17 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
             off += static_cast<size_t>(d.splits) * d.M * kOzN;
         }
     }
-    auto* d_groups = static_cast<const OzGroup*>(sc.upload(groups.data(), groups.size() * sizeof(OzGroup)));
+    const int ng = static_cast<int>(groups.size());
+    const bool packed = ng <= kOzPack;
+    OzPack pk;
+    const OzGroup* d_groups = nullptr;
+    if (packed) {
+        std::memset(&pk, 0, sizeof(pk));
+        std::memcpy(pk.g, groups.data(), groups.size() * sizeof(OzGroup));
+        for (size_t i = 0; i < red.size(); ++i) pk.red[i] = red[i];
+    } else {
+        d_groups = static_cast<const OzGroup*>(sc.upload(groups.data(), groups.size() * sizeof(OzGroup)));
+    }
     if (sc.before_next_gemm) {
         TS_CUDA_CHECK(cudaEventRecord(sc.before_next_gemm, sc.stream()));
         sc.before_next_gemm = nullptr;
@@ -876,18 +924,23 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
         return e ? std::atoi(e) : 0;
     }();
     const unsigned grid = static_cast<unsigned>(units);
-    const int ng = static_cast<int>(groups.size());
+#define TS_OZ_LAUNCH(TSF, IG, SMEM)                                                                              \
+    do {                                                                                                         \
+        if (packed) ozaki_gemm_kernel_pk<TSF, IG><<<grid, kOzThreads, SMEM, sc.stream()>>>(pk, ng, variant);       \
+        else ozaki_gemm_kernel<TSF, IG><<<grid, kOzThreads, SMEM, sc.stream()>>>(d_groups, ng, variant);           \
+    } while (0)
     if (!ozaki_ts()) {
-        ozaki_gemm_kernel<false, 4><<<grid, kOzThreads, kOzSmem, sc.stream()>>>(d_groups, ng, variant);
+        TS_OZ_LAUNCH(false, 4, kOzSmem);
     } else {
         switch (ozaki_int_groups()) {
-            case 0: ozaki_gemm_kernel<true, 0><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
-            case 1: ozaki_gemm_kernel<true, 1><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
-            case 3: ozaki_gemm_kernel<true, 3><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
-            case 4: ozaki_gemm_kernel<true, 4><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
-            default: ozaki_gemm_kernel<true, 2><<<grid, kOzThreads, kOzSmemTS, sc.stream()>>>(d_groups, ng, variant); break;
+            case 0: TS_OZ_LAUNCH(true, 0, kOzSmemTS); break;
+            case 1: TS_OZ_LAUNCH(true, 1, kOzSmemTS); break;
+            case 3: TS_OZ_LAUNCH(true, 3, kOzSmemTS); break;
+            case 4: TS_OZ_LAUNCH(true, 4, kOzSmemTS); break;
+            default: TS_OZ_LAUNCH(true, 2, kOzSmemTS); break;
         }
     }
+#undef TS_OZ_LAUNCH
     TS_LAUNCH_CHECK();
     if (sc.after_next_gemm) {
         TS_CUDA_CHECK(cudaEventRecord(sc.after_next_gemm, sc.stream()));
@@ -920,12 +973,16 @@ bool launch_ozaki_gemm(const std::vector<OzProblem>& probs, CallScratch& sc, int
         }
     }
     if (!red.empty()) {
-        const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
         int64_t maxel = 0;
         for (int gi : red) maxel = std::max<int64_t>(maxel, static_cast<int64_t>(groups[static_cast<size_t>(gi)].M) * kOzN);
         const int64_t blocks = std::min<int64_t>((maxel + 255) / 256, 4LL * num_sms);
-        ozaki_splitk_reduce<<<dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size())),
-                              256, 0, sc.stream()>>>(d_groups, d_red);
+        const dim3 rgrid(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size()));
+        if (packed) {
+            ozaki_splitk_reduce_pk<<<rgrid, 256, 0, sc.stream()>>>(pk);
+        } else {
+            const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
+            ozaki_splitk_reduce<<<rgrid, 256, 0, sc.stream()>>>(d_groups, d_red);
+        }
         TS_LAUNCH_CHECK();
         *launched = 2;
     }
