@@ -6,6 +6,7 @@
 // fragment load (8 rows × 4 k, or 4 k × 8 cols) hit 16 distinct 8-byte bank
 // pairs per half-warp, whichever operand dimension is contiguous.
 #include <algorithm>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 
@@ -48,9 +49,17 @@ struct GemmCfg {
     static constexpr size_t kSmemBytes = sizeof(double) * STAGES * (kAStage + kBStage);
 };
 
+// Launches of up to kPackDescs groups carry their descriptors as a
+// __grid_constant__ kernel parameter instead of a scratch upload (inside a CUDA
+// graph every upload is a memcpy node serialised in front of its kernel).
+constexpr int kPackDescs = 16;
+struct GemmPack {
+    GemmDesc d[kPackDescs];
+    int red[kPackDescs];
+};
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>::kThreads)
-    gemm_kernel(const GemmDesc* __restrict__ descs, int ngroups) {
+__device__ __forceinline__ void gemm_body(const GemmDesc* __restrict__ descs, int ngroups) {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
     constexpr int NT = Cfg::kThreads;
     constexpr int ASS = Cfg::kASS, BSS = Cfg::kBSS;
@@ -166,8 +175,24 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>::
     }
 }
 
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>::kThreads)
+    gemm_kernel(const GemmDesc* __restrict__ descs, int ngroups) {
+    gemm_body<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>(descs, ngroups);
+}
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>::kThreads)
+    gemm_kernel_pk(const __grid_constant__ GemmPack pk, int ngroups) {
+    gemm_body<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>(pk.d, ngroups);
+}
+
 // Sums the split-K partials of group red[blockIdx.y] in split order.
+__device__ __forceinline__ void splitk_reduce_body(const GemmDesc* __restrict__ descs, const int* __restrict__ red);
 __global__ void splitk_reduce(const GemmDesc* __restrict__ descs, const int* __restrict__ red) {
+    splitk_reduce_body(descs, red);
+}
+__global__ void splitk_reduce_pk(const __grid_constant__ GemmPack pk) { splitk_reduce_body(pk.d, pk.red); }
+__device__ __forceinline__ void splitk_reduce_body(const GemmDesc* __restrict__ descs, const int* __restrict__ red) {
     const GemmDesc& d = descs[red[blockIdx.y]];
     const int64_t mn = static_cast<int64_t>(d.M) * d.N;
     const int64_t total = mn * d.batch;
@@ -210,11 +235,17 @@ constexpr TileCfg kCfgs[] = {
 constexpr int kNumCfgs = sizeof(kCfgs) / sizeof(kCfgs[0]);
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, int VEC>
-void launch_kernel(const GemmDesc* d_descs, int ngroups, int64_t units, cudaStream_t stream) {
+void launch_kernel(const GemmDesc* d_descs, const GemmPack* pk, int ngroups, int64_t units, cudaStream_t stream) {
     using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM>;
-    auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
-    set_max_smem(kern, static_cast<int>(Cfg::kSmemBytes));
-    kern<<<static_cast<unsigned>(units), Cfg::kThreads, Cfg::kSmemBytes, stream>>>(d_descs, ngroups);
+    if (pk) {
+        auto kern = gemm_kernel_pk<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
+        set_max_smem(kern, static_cast<int>(Cfg::kSmemBytes));
+        kern<<<static_cast<unsigned>(units), Cfg::kThreads, Cfg::kSmemBytes, stream>>>(*pk, ngroups);
+    } else {
+        auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES, AK, BKM, VEC>;
+        set_max_smem(kern, static_cast<int>(Cfg::kSmemBytes));
+        kern<<<static_cast<unsigned>(units), Cfg::kThreads, Cfg::kSmemBytes, stream>>>(d_descs, ngroups);
+    }
     TS_LAUNCH_CHECK();
 }
 
@@ -244,14 +275,14 @@ struct Dispatch {
         }
     }
     template <int VEC>
-    static void launch(int cfg, const GemmDesc* d, int ng, int64_t units, cudaStream_t st) {
+    static void launch(int cfg, const GemmDesc* d, const GemmPack* pk, int ng, int64_t units, cudaStream_t st) {
         switch (cfg) {
-            case 1: return launch_kernel<128, 64, 16, 32, 32, 3, AK, BKM, VEC>(d, ng, units, st);
-            case 2: return launch_kernel<64, 128, 16, 32, 32, 3, AK, BKM, VEC>(d, ng, units, st);
-            case 3: return launch_kernel<64, 64, 32, 32, 32, 3, AK, BKM, VEC>(d, ng, units, st);
-            case 4: return launch_kernel<128, 64, 16, 64, 32, 3, AK, BKM, VEC>(d, ng, units, st);
-            case 5: return launch_kernel<64, 128, 16, 32, 64, 3, AK, BKM, VEC>(d, ng, units, st);
-            default: return launch_kernel<64, 64, 16, 32, 32, 4, AK, BKM, VEC>(d, ng, units, st);
+            case 1: return launch_kernel<128, 64, 16, 32, 32, 3, AK, BKM, VEC>(d, pk, ng, units, st);
+            case 2: return launch_kernel<64, 128, 16, 32, 32, 3, AK, BKM, VEC>(d, pk, ng, units, st);
+            case 3: return launch_kernel<64, 64, 32, 32, 32, 3, AK, BKM, VEC>(d, pk, ng, units, st);
+            case 4: return launch_kernel<128, 64, 16, 64, 32, 3, AK, BKM, VEC>(d, pk, ng, units, st);
+            case 5: return launch_kernel<64, 128, 16, 32, 64, 3, AK, BKM, VEC>(d, pk, ng, units, st);
+            default: return launch_kernel<64, 64, 16, 32, 32, 4, AK, BKM, VEC>(d, pk, ng, units, st);
         }
     }
 };
@@ -372,26 +403,36 @@ int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, Ca
             off += static_cast<size_t>(d.M) * d.N * d.batch * d.splits;
         }
     }
-    const auto* d_descs = static_cast<const GemmDesc*>(sc.upload(descs.data(), descs.size() * sizeof(GemmDesc)));
     const int ng = static_cast<int>(descs.size());
+    const bool packed = ng <= kPackDescs;
+    GemmPack pack;
+    const GemmPack* pk = nullptr;
+    const GemmDesc* d_descs = nullptr;
+    if (packed) {
+        std::memset(&pack, 0, sizeof(pack));
+        std::memcpy(pack.d, descs.data(), descs.size() * sizeof(GemmDesc));
+        for (size_t i = 0; i < red.size(); ++i) pack.red[i] = red[i];
+        pk = &pack;
+    } else {
+        d_descs = static_cast<const GemmDesc*>(sc.upload(descs.data(), descs.size() * sizeof(GemmDesc)));
+    }
     cudaStream_t st = sc.stream();
     switch (layout) {
         case Layout::TN:
-            vec2 ? Dispatch<true, true>::launch<2>(cfg, d_descs, ng, units, st)
-                 : Dispatch<true, true>::launch<1>(cfg, d_descs, ng, units, st);
+            vec2 ? Dispatch<true, true>::launch<2>(cfg, d_descs, pk, ng, units, st)
+                 : Dispatch<true, true>::launch<1>(cfg, d_descs, pk, ng, units, st);
             break;
         case Layout::NN:
-            vec2 ? Dispatch<false, true>::launch<2>(cfg, d_descs, ng, units, st)
-                 : Dispatch<false, true>::launch<1>(cfg, d_descs, ng, units, st);
+            vec2 ? Dispatch<false, true>::launch<2>(cfg, d_descs, pk, ng, units, st)
+                 : Dispatch<false, true>::launch<1>(cfg, d_descs, pk, ng, units, st);
             break;
         case Layout::NT:
-            vec2 ? Dispatch<false, false>::launch<2>(cfg, d_descs, ng, units, st)
-                 : Dispatch<false, false>::launch<1>(cfg, d_descs, ng, units, st);
+            vec2 ? Dispatch<false, false>::launch<2>(cfg, d_descs, pk, ng, units, st)
+                 : Dispatch<false, false>::launch<1>(cfg, d_descs, pk, ng, units, st);
             break;
     }
     int launched = 1;
     if (!red.empty()) {
-        const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
         int64_t maxel = 0;
         for (int gi : red) {
             const GemmDesc& d = descs[static_cast<size_t>(gi)];
@@ -399,8 +440,13 @@ int launch_grouped_gemm(Layout layout, const std::vector<GemmProblem>& probs, Ca
         }
         const int threads = 256;
         const int64_t blocks = std::min<int64_t>((maxel + threads - 1) / threads, 4LL * num_sms);
-        splitk_reduce<<<dim3(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size())),
-                        threads, 0, st>>>(d_descs, d_red);
+        const dim3 rgrid(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(red.size()));
+        if (packed) {
+            splitk_reduce_pk<<<rgrid, threads, 0, st>>>(pack);
+        } else {
+            const int* d_red = static_cast<const int*>(sc.upload(red.data(), red.size() * sizeof(int)));
+            splitk_reduce<<<rgrid, threads, 0, st>>>(d_descs, d_red);
+        }
         TS_LAUNCH_CHECK();
         ++launched;
     }
