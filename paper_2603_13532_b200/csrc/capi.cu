@@ -1136,6 +1136,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     const bool spec = allow_spec && ctx->spec_ok && !ctx->debug;
     int* dflags = nullptr;  // stage-D acceptance (CholQR2 pivots / second Gram)
     int* gflags = nullptr;  // stage-G acceptance (gram_rank checks)
+    int* flags_all = nullptr;
     // ---- Stage D: Û_n = thin Q of Y_n.  Fast path CholeskyQR2 (Gram GEMM, small
     // Cholesky + inverse, GEMM, twice); R = R₂R₁ has a positive diagonal, so Û is
     // the Householder Q with R_ii ≥ 0 of the reference.  Modes whose Y is too
@@ -1160,8 +1161,11 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     for (int n = 0; n < d && overlap; ++n) overlap = dims[n] >= 2 * yc[n] && !qr_wide_mode(yc[n]);
     {
         std::vector<int>& chol = rform;
-        int* flags = sc.alloc_n<int>(static_cast<size_t>(d));
-        TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int) * static_cast<size_t>(d), st));
+        // one block for both acceptance-flag sets (stage D: [0, d), stage G: [d, 2d)):
+        // one memset and one download per call instead of two each
+        int* flags = sc.alloc_n<int>(2 * static_cast<size_t>(d));
+        TS_CUDA_CHECK(cudaMemsetAsync(flags, 0, 2 * sizeof(int) * static_cast<size_t>(d), st));
+        flags_all = flags;
         bool any = false;
         for (int n = 0; n < d; ++n) {
             chol[static_cast<size_t>(n)] = dims[n] >= 2 * yc[n] && !qr_wide_mode(yc[n]);
@@ -1385,10 +1389,7 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     const std::int64_t* fixed_rank = ge ? ge->ranks : nullptr;
     bool spec_g = spec && (eps == 0.0 || fixed_rank != nullptr);
     for (int n = 0; n < d; ++n) spec_g = spec_g && !qr_wide_mode(q[n]);  // wide eigensolves sync anyway
-    if (spec_g) {
-        gflags = sc.alloc_n<int>(static_cast<size_t>(d));
-        TS_CUDA_CHECK(cudaMemsetAsync(gflags, 0, sizeof(int) * static_cast<size_t>(d), st));
-    }
+    if (spec_g) gflags = flags_all + d;  // zeroed with the stage-D flags
     {
         double hss = 0.0;  // θ = ε²‖h‖²/d vanishes at ε = 0
         double* d_hss = nullptr;
@@ -1636,9 +1637,11 @@ ts_result* sketched_sum_impl(ts_ctx* ctx, const ts_batch* b, const double* weigh
     mark(ctx, 11);
     if (ge) {  // end of the captured region: flags to pinned host memory, no sync
         ge->launches = sc.launches;
-        if (dflags)
+        if (dflags && gflags)
+            TS_CUDA_CHECK(cudaMemcpyAsync(ge->h_flags, flags_all, 2 * sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
+        else if (dflags)
             TS_CUDA_CHECK(cudaMemcpyAsync(ge->h_flags, dflags, sizeof(int) * static_cast<size_t>(d), cudaMemcpyDeviceToHost, st));
-        if (gflags)
+        else if (gflags)
             TS_CUDA_CHECK(cudaMemcpyAsync(ge->h_flags + d, gflags, sizeof(int) * static_cast<size_t>(d),
                                           cudaMemcpyDeviceToHost, st));
         for (int n = 0; n < d; ++n) res->factors[n] = nullptr;  // graph-owned, not the result's
