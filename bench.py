@@ -482,6 +482,13 @@ def main():
             return eng.upload_stacked(shard_slabs, shard_cores, rk)
 
         d2h = 0
+        # (0) The PCIe floor of a step: the upload alone (same call, same slabs).
+        up_times = []
+        for i in range(3):
+            t0 = time.perf_counter()
+            upload_step().free()
+            up_times.append(time.perf_counter() - t0)
+        upload_only = min(up_times)
         # (1) Sequential: upload, sum, download, one step after the other.
         seq_times = []
         for i in range(args.e2e_steps + 1):
@@ -540,6 +547,7 @@ def main():
                          f"context/stream overlaps step i's sum + download; {args.e2e_steps} steps) and sequential "
                          f"(upload, sum, download one after the other; mean of {args.e2e_steps} steps after 1 "
                          "warm-up); ts_batch_upload_stacked from the registered host slabs",
+               "upload_only_ms_per_step": 1000.0 * upload_only,
                "pipelined_ms_per_step": 1000.0 * float(te[1].item()),
                "sequential_ms_per_step": 1000.0 * float(te[2].item())}
 
