@@ -30,7 +30,7 @@ def up_step():
 
 
 pool.submit(lambda: up_step()[0].free()).result()
-steps = 6
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 t_all = time.perf_counter()
 nxt = pool.submit(up_step)
 rows = []
